@@ -1,0 +1,163 @@
+/*
+ * nysb200 -- C ABI of the B200 (sm_100a) Nystrom LS-SVM ODE hot path.
+ *
+ * Drop-in boundary for the reference package `nysode` (arXiv 2510.04094,
+ * /root/reference/pkg/src/nysode).  The reference has no FFI layer: its seam is
+ * the Python solver API, so each entry point below replaces the numeric core
+ * of one reference function (cited per entry).  The Python host mirror
+ * (paper_2510_04094_b200/{nystrom,linear,newton}.py) keeps the reference's
+ * signatures, callables and exceptions and binds this ABI through ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument is CUDA device memory owned by the caller
+ *     (torch tensors on the host side), row-major, fp64 unless stated;
+ *   - work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream); nothing synchronises the host;
+ *   - return value is an nys_status (NYS_OK = 0); per-instance numerical
+ *     outcomes go to `info` arrays (NYS_INFO_*), mirroring the reference's
+ *     exceptions (SingularSystemError, FloatingPointError, Newton errors);
+ *   - no allocation: scratch comes from a caller workspace sized by the
+ *     matching *_workspace_bytes() query;
+ *   - re-entrant; no global state beyond cached device attributes.
+ */
+#ifndef NYSB200_H
+#define NYSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NYS_ABI_VERSION 1
+
+enum nys_status {
+  NYS_OK = 0,
+  NYS_EINVAL = 1,      /* argument out of range (reference: ValueError)        */
+  NYS_ECUDA = 2,       /* CUDA launch / runtime error                           */
+  NYS_EWORKSPACE = 3,  /* workspace too small                                   */
+  NYS_EUNSUPPORTED = 4 /* shape outside the compiled kernel variants            */
+};
+
+enum nys_info {
+  NYS_INFO_OK = 0,
+  NYS_INFO_SINGULAR = 1,   /* exact zero pivot   (linear.py:148-151 LinAlgError)  */
+  NYS_INFO_NONFINITE = 2,  /* non-finite result  (linear.py:152-153)              */
+  NYS_INFO_DIVERGED = 3,   /* Newton ||F|| > 1e12 (newton.py:298-299)             */
+  NYS_INFO_MAXITERS = 4,   /* Newton budget hit  (newton.py:345-348)              */
+  NYS_INFO_DEGENERATE = 5  /* landmarks within 1e-12 (nystrom.py:145-146)         */
+};
+
+int nys_abi_version(void);
+const char* nys_status_string(int status);
+/* last CUDA error string seen by this thread (diagnostics only) */
+const char* nys_last_cuda_error(void);
+
+/* ------------------------------------------------------------------------
+ * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map
+ * (nystrom.py:136-160) + NystromFeatureMap._scaled_vectors (nystrom.py:120-121).
+ * Omega = K(L, L); cyclic parallel Jacobi; eigenpairs sorted descending;
+ * keep s > max(drop_tol * s_0, 0).
+ *   eigvals  [m]     descending (entries >= m_eff are the dropped ones)
+ *   eigvecs  [m*m]   column k = eigenvector k (row-major m x m)
+ *   W        [m*m]   W[:, k] = eigvecs[:, k] / sqrt(s_k) for k < m_eff, 0 else
+ *   m_eff    [1]     int32, device
+ *   info     [1]     int32, NYS_INFO_DEGENERATE if two landmarks coincide
+ * ------------------------------------------------------------------------ */
+size_t nys_landmark_eig_workspace_bytes(int m);
+int nys_landmark_eig_f64(const double* landmarks, int m, double sigma2, double drop_tol,
+                         double* eigvals, double* eigvecs, double* W, int* m_eff,
+                         int* info, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Feature rows.  Replaces NystromFeatureMap.feature_matrix (nystrom.py:123-127):
+ *   out[i*ldo + k] = sum_s dK^ell(L_s, pts_i)/dt^ell * W[s*ldw + k],  k < m_eff
+ * ------------------------------------------------------------------------ */
+int nys_feature_matrix_f64(const double* landmarks, int m, const double* W, int ldw,
+                           int m_eff, double sigma2, int ell, const double* pts, int n_pts,
+                           double* out, int ldo, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Batched prediction.  Replaces PrimalModel.predict (linear.py:47-53) for B
+ * models sharing one feature map:
+ *   out[b*ldo + i] = Psi_ell(pts_i) . x[b*ldx + 0 : m_eff]  (+ x[b*ldx+m_eff] if ell == 0)
+ * ------------------------------------------------------------------------ */
+int nys_predict_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                    double sigma2, int ell, const double* pts, int n_pts,
+                    const double* x, int ldx, int B, double* out, int ldo, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (ii-a) Fused feature + Gram, one ODE.  Replaces the numeric core of
+ * linear.assemble (linear.py:103-133): for constraint rows i in
+ * [row_begin, row_end) forms, in registers only,
+ *   D_i = phi^(p)(t_i) - sum_k f_k(t_i) phi^(p-k)(t_i),  g_i = -f_p(t_i),  r_i
+ * and writes the extended Gram  E = [D g r]^T [D g r]  ((m_eff+2)^2, row-major)
+ * so E[:m_eff,:m_eff] = D^T D, E[:m_eff, m_eff] = D^T g, E[:m_eff, m_eff+1] = D^T r,
+ * E[m_eff, m_eff] = g^T g, E[m_eff, m_eff+1] = g^T r.  The n x m feature
+ * matrices never reach memory.  Row ranges make row sharding possible (the
+ * partial E of disjoint ranges sum to the full E).
+ *   coef    [p * n_c]   coef[(k-1)*n_c + i] = f_k(pts_i)
+ *   forcing [n_c]
+ * ------------------------------------------------------------------------ */
+size_t nys_fused_gram_workspace_bytes(int n_c, int m, int m_eff, int p);
+int nys_fused_gram_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                       double sigma2, int p, const double* pts, const double* coef,
+                       const double* forcing, int n_c, int row_begin, int row_end,
+                       double* gram_ext, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * (ii-b) Batched extended Gram for B ODEs sharing grid, landmarks and sigma
+ * (config 2).  Same output as (ii-a) per instance, but the per-order features
+ * Psi_0..Psi_p are formed once (the reference's own per-order order,
+ * linear.py:103-112) and each instance only pays its row combine + Gram.
+ *   coef    [B * p * n_c],  forcing [B * n_c],  gram_ext [B * (m_eff+2)^2]
+ * gram_ext may be NULL when only the packed partials are wanted by
+ * nys_batch_kkt_solve_f64 (they live in the workspace).
+ * ------------------------------------------------------------------------ */
+size_t nys_batch_gram_workspace_bytes(int n_c, int m_eff, int p, int B);
+int nys_batch_gram_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                       double sigma2, int p, const double* pts, int n_c,
+                       const double* coef, const double* forcing, int B,
+                       double* gram_ext, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * (iii) KKT assembly + solve, batched.  Replaces linear.assemble's block
+ * layout (linear.py:123-133) and linear.solve (linear.py:140-158): LU with
+ * partial pivoting + one refinement step, per instance.
+ *   gram_ext [B * (m_eff+2)^2]  (from ii-a / ii-b)
+ *   Ac       [n_cond * m_eff]    condition rows (shared), beta [n_cond]
+ *   values   [B * n_cond]
+ *   x        [B * side], side = m_eff + 1 + n_cond: (omega, b, lambda)
+ *   M, rhs   optional outputs (NULL to skip): [B * side^2], [B * side]
+ *   info     [B] int32
+ * ------------------------------------------------------------------------ */
+int nys_kkt_solve_f64(const double* gram_ext, int m_eff, int n_cond, const double* Ac,
+                      const double* beta, const double* values, double gamma, int B,
+                      double* x, int* info, double* M, double* rhs, void* workspace,
+                      size_t workspace_bytes, void* stream);
+size_t nys_kkt_workspace_bytes(int m_eff, int n_cond, int B);
+
+/* (iii-b) Same, reading the packed Gram partials that nys_batch_gram_f64 left
+ * in `batch_workspace` (saves the dense gram_ext round trip). */
+int nys_batch_kkt_solve_f64(const void* batch_workspace, int n_c, int m_eff, int p,
+                            int n_cond, const double* Ac, const double* beta,
+                            const double* values, double gamma, int B, double* x,
+                            int* info, void* stream);
+
+/* ------------------------------------------------------------------------
+ * KKT certificate pieces (linear.check_kkt, linear.py:161-189) without
+ * materialising D:  e_i = D_i . omega + g_i b - r_i  over rows [0, n_c).
+ * ------------------------------------------------------------------------ */
+int nys_ode_residual_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                         double sigma2, int p, const double* pts, const double* coef,
+                         const double* forcing, int n_c, const double* x, double* e,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NYSB200_H */

@@ -1,0 +1,137 @@
+"""Batched linear solves for B ODEs sharing grid, landmarks and sigma (config 2).
+
+The reference solves one spec per call (``linear.assemble`` + ``linear.solve``,
+linear.py:90-158), recomputing the feature matrices every time.  A batch that
+shares the feature map lets the GPU form Psi_0..Psi_p once and spend the rest
+on per-instance row combines + Gram (``nys_batch_gram_f64``) and B small KKT
+solves (``nys_batch_kkt_solve_f64``) -- one stream, no host round trip.
+
+Entry points:
+* :class:`LinearBatchSolver` -- array API: sampled coefficient rows
+  ``coef[B, p, n_c]``, ``forcing[B, n_c]``, condition values ``values[B, p]``
+  (host or device); returns device ``x[B, side]`` and ``info[B]``.
+* :func:`solve_many` -- reference-style API over lists of ``LinearOdeSpec`` /
+  ``Conditions`` (samples the callables on the host exactly like
+  linear.py:103-116) returning ``PrimalModel`` objects.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .linear import PrimalModel, condition_rows, constraint_points, raise_for_info
+from .nystrom import NystromFeatureMap
+
+
+class LinearBatchSolver:
+    def __init__(self, fmap: NystromFeatureMap, grid, gamma: float, order: int, cond,
+                 max_batch: int):
+        if gamma <= 0:
+            raise ValueError(f"gamma must be positive, got {gamma}")
+        lib, torch = _lib.require_device()
+        self.lib, self.torch = lib, torch
+        self.fmap = fmap
+        self.gamma = float(gamma)
+        self.order = int(order)
+        self.cond = cond
+        grid = np.asarray(grid, dtype=float)
+        self.pts_host = constraint_points(cond, grid)
+        self.n_c = self.pts_host.size
+        dev = fmap.device
+        self.pts = _lib.as_f64(self.pts_host, dev)
+        Ac, beta, _ = condition_rows(cond, fmap)
+        self.n_cond = len(cond.entries)
+        self.Ac = _lib.as_f64(Ac.reshape(self.n_cond, fmap.m_eff), dev)
+        self.beta = _lib.as_f64(beta, dev)
+        self.side = fmap.m_eff + 1 + self.n_cond
+        self.max_batch = int(max_batch)
+        self.ws_bytes = lib.nys_batch_gram_workspace_bytes(self.n_c, fmap.m_eff, self.order,
+                                                          self.max_batch)
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+
+    def solve_device(self, coef, forcing, values, out_x=None, out_info=None):
+        """coef (B, p, n_c), forcing (B, n_c), values (B, n_cond) device float64
+        tensors -> (x (B, side), info (B,)).  Fully stream-ordered, no sync."""
+        torch = self.torch
+        fm = self.fmap
+        B = int(coef.shape[0])
+        if B > self.max_batch:
+            raise ValueError(f"batch {B} exceeds max_batch {self.max_batch}")
+        ws_bytes = self.lib.nys_batch_gram_workspace_bytes(self.n_c, fm.m_eff, self.order, B)
+        x = out_x if out_x is not None else torch.empty((B, self.side), dtype=torch.float64,
+                                                         device=fm.device)
+        info = out_info if out_info is not None else torch.empty(B, dtype=torch.int32,
+                                                                 device=fm.device)
+        st = _lib.stream_ptr()
+        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+                  fm.m_eff, float(fm.kernel.sigma2), self.order, _lib.ptr(self.pts), self.n_c,
+                  _lib.ptr(coef), _lib.ptr(forcing), B, None, _lib.ptr(self.ws), ws_bytes, st)
+        _lib.call("nys_batch_kkt_solve_f64", _lib.ptr(self.ws), self.n_c, fm.m_eff, self.order,
+                  self.n_cond, _lib.ptr(self.Ac), _lib.ptr(self.beta), _lib.ptr(values),
+                  self.gamma, B, _lib.ptr(x), _lib.ptr(info), st)
+        return x, info
+
+    def gram_ext(self, coef, forcing):
+        """Dense extended Grams (B, m_eff+2, m_eff+2) -- for tests / inspection."""
+        torch = self.torch
+        fm = self.fmap
+        B = int(coef.shape[0])
+        ws_bytes = self.lib.nys_batch_gram_workspace_bytes(self.n_c, fm.m_eff, self.order, B)
+        E = torch.empty((B, fm.m_eff + 2, fm.m_eff + 2), dtype=torch.float64, device=fm.device)
+        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+                  fm.m_eff, float(fm.kernel.sigma2), self.order, _lib.ptr(self.pts), self.n_c,
+                  _lib.ptr(coef), _lib.ptr(forcing), B, _lib.ptr(E), _lib.ptr(self.ws), ws_bytes,
+                  _lib.stream_ptr())
+        return E
+
+    def solve(self, coef, forcing, values):
+        dev = self.fmap.device
+        coef = _lib.as_f64(coef, dev)
+        forcing = _lib.as_f64(forcing, dev)
+        values = _lib.as_f64(values, dev).reshape(coef.shape[0], self.n_cond)
+        return self.solve_device(coef, forcing, values)
+
+
+def solve_many(specs: Sequence, conds: Sequence, fmap: NystromFeatureMap, grid,
+               gamma: float) -> list[PrimalModel]:
+    """Reference-style batch: one PrimalModel per (spec, cond), same grid/fmap.
+
+    Condition points and orders must be shared (values may differ)."""
+    if len(specs) != len(conds) or not specs:
+        raise ValueError("need matching, non-empty spec and condition lists")
+    grid = np.asarray(grid, dtype=float)
+    c0 = conds[0]
+    key = [(bc.point, bc.order) for bc in c0.entries]
+    for c in conds:
+        if c.kind != c0.kind or [(bc.point, bc.order) for bc in c.entries] != key:
+            raise ValueError("solve_many needs shared condition points/orders")
+    p = specs[0].order
+    pts = constraint_points(c0, grid)
+    coef = np.empty((len(specs), p, pts.size))
+    forcing = np.empty((len(specs), pts.size))
+    for b, sp in enumerate(specs):
+        if sp.order != p:
+            raise ValueError("solve_many needs a common ODE order")
+        for k, fk in enumerate(sp.coeffs, start=1):
+            v = np.asarray(fk(pts), dtype=float)
+            if not np.all(np.isfinite(v)):
+                raise FloatingPointError(f"coefficient f_{k} non-finite on constraint points")
+            coef[b, k - 1] = v
+        r = np.asarray(sp.forcing(pts), dtype=float)
+        if not np.all(np.isfinite(r)):
+            raise FloatingPointError("forcing non-finite on constraint points")
+        forcing[b] = r
+    values = np.array([[bc.value for bc in c.entries] for c in conds])
+    solver = LinearBatchSolver(fmap, grid, gamma, p, c0, len(specs))
+    x, info = solver.solve(coef, forcing, values)
+    x = x.cpu().numpy()
+    info = info.cpu().numpy()
+    me = fmap.m_eff
+    out = []
+    for b in range(len(specs)):
+        raise_for_info(int(info[b]))
+        out.append(PrimalModel(omega=x[b, :me], bias=float(x[b, me]), multipliers=x[b, me + 1:],
+                               feature_map=fmap))
+    return out

@@ -1,0 +1,222 @@
+// Feature rows Psi_ell(t) = K_ell(L, t)^T W (nystrom.py:123-127), batched
+// prediction (linear.py:47-53), the ODE-residual certificate (linear.py:175-189)
+// and the fragment-native packing of Psi_0..Psi_p used by the batched Gram.
+//
+// These are not the timed hot kernels for the linear configs except
+// psi_pack (once per batch); they are small, L2-resident FP64 GEMV/GEMM-like
+// loops with the RBF values generated on the fly.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kTP = 16;        // points per CTA tile
+constexpr int kFeatThreads = 256;
+
+// out(i, k) for points [i0, i0+kTP): K tile in smem, W read from L2.
+// mode 0: dense out[i*ldo + k]; mode 1: packed fragment layout for the batch Gram.
+__global__ void __launch_bounds__(kFeatThreads)
+    feature_tile_kernel(const double* __restrict__ lm, int m, const double* __restrict__ W,
+                        int ldw, int m_eff, double sigma2, int ell,
+                        const double* __restrict__ pts, int n_pts, double* __restrict__ out,
+                        int ldo, int mode, int n_blocks /*packed: NB*/, int n_orders,
+                        int n_rows_pad) {
+  extern __shared__ double kt[];   // [kTP][m]
+  nys::Hermite H;
+  H.init(sigma2, ell);
+  const int i0 = blockIdx.x * kTP;
+  for (int e = threadIdx.x; e < kTP * m; e += blockDim.x) {
+    int ii = e / m, s = e % m;
+    int i = i0 + ii;
+    double v = 0.0;
+    if (i < n_pts) {
+      double d = lm[s] - pts[i];
+      v = H.poly(ell, d) * nys::rbf(d, sigma2);
+    }
+    kt[e] = v;
+  }
+  __syncthreads();
+  const int ncols = mode == 0 ? m_eff : n_blocks * 8;
+  for (int e = threadIdx.x; e < kTP * ncols; e += blockDim.x) {
+    int ii = e / ncols, k = e % ncols;
+    int i = i0 + ii;
+    double acc = 0.0;
+    if (k < m_eff) {
+      const double* kr = kt + ii * m;
+      for (int s = 0; s < m; ++s) acc += kr[s] * W[(size_t)s * ldw + k];
+    }
+    if (mode == 0) {
+      if (i < n_pts) out[(size_t)i * ldo + k] = acc;
+    } else {
+      // extended column m_eff: Psi_0 := 1 so that D_ext[:, m_eff] = -f_p = g
+      if (k == m_eff && ell == 0 && i < n_pts) acc = 1.0;
+      if (i >= n_pts) acc = 0.0;
+      if (i < n_rows_pad) {
+        int ks = i >> 2, t = i & 3, F = k >> 3, g = k & 7;
+        size_t idx = (((size_t)ks * n_orders + ell) * n_blocks + F) * 32 + g * 4 + t;
+        out[idx] = acc;
+      }
+    }
+  }
+}
+
+// y[b, i] = Psi_ell(pts_i) . x_b (+ bias).  Psi tile for kTP points in smem.
+__global__ void __launch_bounds__(kFeatThreads)
+    predict_kernel(const double* __restrict__ lm, int m, const double* __restrict__ W, int ldw,
+                   int m_eff, double sigma2, int ell, const double* __restrict__ pts, int n_pts,
+                   const double* __restrict__ x, int ldx, int B, double* __restrict__ out,
+                   int ldo) {
+  extern __shared__ double sm[];
+  double* kt = sm;                  // [kTP][m]
+  double* psi = sm + kTP * m;       // [kTP][m_eff]
+  nys::Hermite H;
+  H.init(sigma2, ell);
+  const int i0 = blockIdx.x * kTP;
+  for (int e = threadIdx.x; e < kTP * m; e += blockDim.x) {
+    int ii = e / m, s = e % m, i = i0 + ii;
+    double v = 0.0;
+    if (i < n_pts) {
+      double d = lm[s] - pts[i];
+      v = H.poly(ell, d) * nys::rbf(d, sigma2);
+    }
+    kt[e] = v;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kTP * m_eff; e += blockDim.x) {
+    int ii = e / m_eff, k = e % m_eff;
+    double acc = 0.0;
+    for (int s = 0; s < m; ++s) acc += kt[ii * m + s] * W[(size_t)s * ldw + k];
+    psi[e] = acc;
+  }
+  __syncthreads();
+  const int b0 = blockIdx.y * blockDim.x;
+  for (int b = b0 + threadIdx.x; b < min(B, b0 + (int)blockDim.x); b += blockDim.x) {
+    const double* xb = x + (size_t)b * ldx;
+    double bias = ell == 0 ? xb[m_eff] : 0.0;
+    for (int ii = 0; ii < kTP; ++ii) {
+      int i = i0 + ii;
+      if (i >= n_pts) break;
+      double acc = 0.0;
+      for (int k = 0; k < m_eff; ++k) acc += psi[ii * m_eff + k] * xb[k];
+      out[(size_t)b * ldo + i] = acc + bias;
+    }
+  }
+}
+
+// e_i = sum_s [K_p - sum_k f_k K_{p-k}](s, i) v_s + g_i b - r_i,  v = W omega
+// (the Psi omega = K^T (W omega) reassociation: SURVEY.md A1 "predict as
+// K^T(W omega)" <= 2.3e-8).  v is rebuilt per CTA in shared memory.
+constexpr int kResRowsPerThread = 4;
+__global__ void __launch_bounds__(256)
+    ode_residual_kernel(const double* __restrict__ lm, int m, const double* __restrict__ W,
+                        int ldw, int m_eff, double sigma2, int p,
+                        const double* __restrict__ pts, const double* __restrict__ coef,
+                        const double* __restrict__ forcing, int n_c,
+                        const double* __restrict__ x, double* __restrict__ e) {
+  extern __shared__ double v[];
+  for (int s = threadIdx.x; s < m; s += blockDim.x) {
+    double acc = 0.0;
+    for (int k = 0; k < m_eff; ++k) acc += W[(size_t)s * ldw + k] * x[k];
+    v[s] = acc;
+  }
+  __syncthreads();
+  const double bias = x[m_eff];
+  nys::Hermite H;
+  H.init(sigma2, p);
+  for (int r = 0; r < kResRowsPerThread; ++r) {
+    int i = (blockIdx.x * kResRowsPerThread + r) * blockDim.x + threadIdx.x;
+    if (i >= n_c) return;
+    double f[nys::kMaxOrder + 1];
+#pragma unroll
+    for (int k = 1; k <= nys::kMaxOrder; ++k)
+      f[k] = k <= p ? coef[(size_t)(k - 1) * n_c + i] : 0.0;
+    const double t = pts[i];
+    double acc = 0.0;
+    for (int s = 0; s < m; ++s) {
+      double d = lm[s] - t;
+      double gk = H.poly(p, d);
+      for (int k = 1; k <= p; ++k) gk -= f[k] * H.poly(p - k, d);
+      acc += gk * nys::rbf(d, sigma2) * v[s];
+    }
+    e[i] = acc - f[p] * bias - forcing[i];
+  }
+}
+
+}  // namespace
+
+namespace nys_host {
+int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff, double sigma2,
+                    int p, const double* pts, int n_c, int n_blocks, int n_rows_pad,
+                    double* packed, cudaStream_t st) {
+  size_t sm = (size_t)kTP * m * sizeof(double);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(feature_tile_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return record_cuda(e);
+  }
+  dim3 grid((n_rows_pad + kTP - 1) / kTP);
+  for (int ell = 0; ell <= p; ++ell) {
+    feature_tile_kernel<<<grid, kFeatThreads, sm, st>>>(lm, m, W, ldw, m_eff, sigma2, ell, pts,
+                                                        n_c, packed, 0, 1, n_blocks, p + 1,
+                                                        n_rows_pad);
+  }
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+}  // namespace nys_host
+
+extern "C" int nys_feature_matrix_f64(const double* landmarks, int m, const double* W, int ldw,
+                                      int m_eff, double sigma2, int ell, const double* pts,
+                                      int n_pts, double* out, int ldo, void* stream) {
+  if (m < 1 || m_eff < 0 || m_eff > m || ldw < m_eff || ldo < m_eff || ell < 0 ||
+      ell > nys::kMaxOrder || !(sigma2 > 0.0) || n_pts < 0)
+    return NYS_EINVAL;
+  if (n_pts == 0 || m_eff == 0) return NYS_OK;
+  size_t sm = (size_t)kTP * m * sizeof(double);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(feature_tile_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+  }
+  dim3 grid((n_pts + kTP - 1) / kTP);
+  feature_tile_kernel<<<grid, kFeatThreads, sm, static_cast<cudaStream_t>(stream)>>>(
+      landmarks, m, W, ldw, m_eff, sigma2, ell, pts, n_pts, out, ldo, 0, 0, 0, 0);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" int nys_predict_f64(const double* landmarks, int m, const double* W, int ldw,
+                               int m_eff, double sigma2, int ell, const double* pts, int n_pts,
+                               const double* x, int ldx, int B, double* out, int ldo,
+                               void* stream) {
+  if (m < 1 || m_eff < 1 || m_eff > m || ldw < m_eff || ell < 0 || ell > nys::kMaxOrder ||
+      !(sigma2 > 0.0) || n_pts < 0 || B < 0 || ldx < m_eff + 1 || ldo < n_pts)
+    return NYS_EINVAL;
+  if (n_pts == 0 || B == 0) return NYS_OK;
+  size_t sm = (size_t)kTP * (m + m_eff) * sizeof(double);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(predict_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+  }
+  dim3 grid((n_pts + kTP - 1) / kTP, (B + kFeatThreads - 1) / kFeatThreads);
+  predict_kernel<<<grid, kFeatThreads, sm, static_cast<cudaStream_t>(stream)>>>(
+      landmarks, m, W, ldw, m_eff, sigma2, ell, pts, n_pts, x, ldx, B, out, ldo);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" int nys_ode_residual_f64(const double* landmarks, int m, const double* W, int ldw,
+                                    int m_eff, double sigma2, int p, const double* pts,
+                                    const double* coef, const double* forcing, int n_c,
+                                    const double* x, double* e, void* stream) {
+  if (m < 1 || m_eff < 1 || m_eff > m || p < 1 || p > nys::kMaxOrder || n_c < 0 ||
+      !(sigma2 > 0.0))
+    return NYS_EINVAL;
+  if (n_c == 0) return NYS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rows_per_block = 256 * kResRowsPerThread;
+  ode_residual_kernel<<<(n_c + rows_per_block - 1) / rows_per_block, 256, m * sizeof(double), st>>>(
+      landmarks, m, W, ldw, m_eff, sigma2, p, pts, coef, forcing, n_c, x, e);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}

@@ -1,0 +1,230 @@
+// Batched extended Gram for B linear ODEs that share grid, landmarks and sigma
+// (config 2).  Numeric core of linear.assemble (linear.py:103-133) per
+// instance:
+//     D_b = Psi_p - sum_k f_{b,k} (.) Psi_{p-k},  g_b = -f_{b,p},  r_b
+//     E_b = [D_b g_b r_b]^T [D_b g_b r_b]
+// Psi_0..Psi_p are formed once per batch (the reference's own per-order
+// projection, linear.py:103-112) in a fragment-native packed layout; each warp
+// then owns one instance and streams Psi through shared memory (1-D TMA bulk
+// copies, double buffered on mbarriers), combines the row in registers (FP64
+// FMA) and feeds the SAME register fragment to both operands of DMMA.8x8x4,
+// accumulating only the upper block triangle of E.  Gram and rhs come from
+// one rounding of D (mixing roundings costs up to 5.9e-5).
+// Row splits (grid.y) give whole waves on 148 SMs; their partials are summed in
+// a fixed order by the KKT kernel (deterministic, no FP64 atomics).
+#include <algorithm>
+
+#include "batch_layout.cuh"
+#include "common.cuh"
+
+namespace nys_host {
+int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff, double sigma2,
+                    int p, const double* pts, int n_c, int n_blocks, int n_rows_pad,
+                    double* packed, cudaStream_t st);
+}
+
+namespace {
+
+using nys::BatchLayout;
+
+template <int NB>
+struct Tri {
+  static constexpr int kPairs = NB * (NB + 1) / 2;
+  static constexpr NYS_DEV int idx(int I, int J) { return I * NB - (I * (I - 1)) / 2 + (J - I); }
+};
+
+template <int NB, int NO, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    batch_gram_kernel(const double* __restrict__ psi, const double* __restrict__ coef,
+                      const double* __restrict__ forcing, int n_c, int B, int ks_per_split,
+                      int rcol, double* __restrict__ part) {
+  constexpr int P = NO - 1;                       // ODE order
+  constexpr int CH = nys::kBatchChunkKs;          // k-steps per chunk (32 rows)
+  constexpr int kChunkDoubles = CH * NO * NB * 32;
+  constexpr uint32_t kChunkBytes = kChunkDoubles * sizeof(double);
+  constexpr int NPAIR = Tri<NB>::kPairs;
+
+  extern __shared__ __align__(128) double sm[];   // [2][kChunkDoubles]
+  __shared__ __align__(8) uint64_t bar[2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tig = lane & 3, gid = lane >> 2;
+  const int b = blockIdx.x * WARPS + warp;
+  const int split = blockIdx.y;
+  const int ks0 = split * ks_per_split;
+  const int nchunks = ks_per_split / CH;
+  const bool active = b < B;
+
+  if (threadIdx.x == 0) {
+    nys::mbar_init(&bar[0], 1);
+    nys::mbar_init(&bar[1], 1);
+    nys::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2 && s < nchunks; ++s) {
+      nys::mbar_expect_tx(&bar[s], kChunkBytes);
+      nys::bulk_g2s(sm + s * kChunkDoubles, psi + (size_t)(ks0 + s * CH) * NO * NB * 32,
+                    kChunkBytes, &bar[s]);
+    }
+  }
+
+  double acc[NPAIR][2];
+#pragma unroll
+  for (int q = 0; q < NPAIR; ++q) acc[q][0] = acc[q][1] = 0.0;
+
+  const double* cb = coef + (size_t)(active ? b : 0) * P * n_c;
+  const double* rb = forcing + (size_t)(active ? b : 0) * n_c;
+  // per-lane coefficient row (row0 + lane) of the current / next chunk
+  double fk[P], rr, fk_n[P], rr_n;
+  auto load_rows = [&](int c, double* f, double& r) {
+    int row = (ks0 + c * CH) * 4 + lane;
+    bool ok = active && row < n_c;
+#pragma unroll
+    for (int k = 0; k < P; ++k) f[k] = ok ? __ldg(cb + (size_t)k * n_c + row) : 0.0;
+    r = ok ? __ldg(rb + row) : 0.0;
+  };
+  load_rows(0, fk, rr);
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int stage = c & 1;
+    const uint32_t phase = (c >> 1) & 1;
+    if (c + 1 < nchunks) load_rows(c + 1, fk_n, rr_n);
+    nys::mbar_wait(&bar[stage], phase);
+    const double* Q = sm + stage * kChunkDoubles + lane;
+    if (active) {
+#pragma unroll 2
+      for (int kk = 0; kk < CH; ++kk) {
+        const int src = kk * 4 + tig;
+        double f[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) f[k] = nys::shfl(fk[k], src);
+        const double r = nys::shfl(rr, src);
+        double x[NB];
+#pragma unroll
+        for (int F = 0; F < NB; ++F) {
+          // Q layout per k-step: [order][block][lane]
+          double v = Q[((kk * NO + P) * NB + F) * 32];
+#pragma unroll
+          for (int k = 1; k <= P; ++k) v = fma(-f[k - 1], Q[((kk * NO + (P - k)) * NB + F) * 32], v);
+          x[F] = (F * 8 + gid == rcol) ? r : v;
+        }
+#pragma unroll
+        for (int I = 0; I < NB; ++I)
+#pragma unroll
+          for (int J = I; J < NB; ++J)
+            nys::dmma(acc[Tri<NB>::idx(I, J)][0], acc[Tri<NB>::idx(I, J)][1], x[I], x[J]);
+      }
+    }
+    if (c + 1 < nchunks) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) fk[k] = fk_n[k];
+      rr = rr_n;
+    }
+    __syncthreads();   // every warp is done with this stage
+    if (threadIdx.x == 0 && c + 2 < nchunks) {
+      nys::mbar_expect_tx(&bar[stage], kChunkBytes);
+      nys::bulk_g2s(sm + stage * kChunkDoubles,
+                    psi + (size_t)(ks0 + (c + 2) * CH) * NO * NB * 32, kChunkBytes, &bar[stage]);
+    }
+  }
+
+  if (active) {
+    double* out = part + ((size_t)split * B + b) * NPAIR * 64 + lane * 2;
+#pragma unroll
+    for (int q = 0; q < NPAIR; ++q) {
+      out[q * 64] = acc[q][0];
+      out[q * 64 + 1] = acc[q][1];
+    }
+  }
+}
+
+// partials -> dense E (P x P) per instance, summing splits in fixed order
+__global__ void batch_unpack_kernel(const double* __restrict__ part, int nsplit, int B, int NB,
+                                    int Pe, double* __restrict__ gram) {
+  const int b = blockIdx.x;
+  const int npair = NB * (NB + 1) / 2;
+  for (int e = threadIdx.x; e < npair * 64; e += blockDim.x) {
+    int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
+    int I = 0, rem = q;
+    while (rem >= NB - I) {
+      rem -= NB - I;
+      ++I;
+    }
+    int J = I + rem;
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) s += part[((size_t)sp * B + b) * npair * 64 + e];
+    int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
+    if (r < Pe && c < Pe) {
+      gram[(size_t)b * Pe * Pe + (size_t)r * Pe + c] = s;
+      gram[(size_t)b * Pe * Pe + (size_t)c * Pe + r] = s;
+    }
+  }
+}
+
+template <int NB, int NO>
+int launch_gram(const double* psi, const double* coef, const double* forcing, int n_c, int B,
+                const BatchLayout& L, double* part, cudaStream_t st) {
+  constexpr int WARPS = nys::kBatchWarps;
+  auto kern = batch_gram_kernel<NB, NO, WARPS>;
+  size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return nys_host::record_cuda(e);
+  dim3 grid((B + WARPS - 1) / WARPS, L.nsplit);
+  kern<<<grid, WARPS * 32, smem, st>>>(psi, coef, forcing, n_c, B, L.ks_per_split, L.m_eff + 1,
+                                       part);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+template <int NO>
+int dispatch_nb(int NB, const double* psi, const double* coef, const double* forcing, int n_c,
+                int B, const BatchLayout& L, double* part, cudaStream_t st) {
+  switch (NB) {
+    case 1: return launch_gram<1, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 2: return launch_gram<2, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 3: return launch_gram<3, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 4: return launch_gram<4, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 5: return launch_gram<5, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 6: return launch_gram<6, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 7: return launch_gram<7, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 8: return launch_gram<8, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 9: return launch_gram<9, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    default: return NYS_EUNSUPPORTED;
+  }
+}
+
+}  // namespace
+
+extern "C" size_t nys_batch_gram_workspace_bytes(int n_c, int m_eff, int p, int B) {
+  BatchLayout L = BatchLayout::make(n_c, m_eff, p, B);
+  return L.ws_bytes();
+}
+
+extern "C" int nys_batch_gram_f64(const double* landmarks, int m, const double* W, int ldw,
+                                  int m_eff, double sigma2, int p, const double* pts, int n_c,
+                                  const double* coef, const double* forcing, int B,
+                                  double* gram_ext, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (m < 1 || m_eff < 1 || m_eff > m || ldw < m_eff || p < 1 || p > 2 || n_c < 1 || B < 0 ||
+      !(sigma2 > 0.0))
+    return NYS_EINVAL;
+  if (B == 0) return NYS_OK;
+  BatchLayout L = BatchLayout::make(n_c, m_eff, p, B);
+  if (L.NB > nys::kBatchMaxNB) return NYS_EUNSUPPORTED;
+  if (workspace == nullptr || workspace_bytes < L.ws_bytes()) return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* psi = L.psi(workspace);
+  double* part = L.part(workspace);
+  int rc = nys_host::launch_psi_pack(landmarks, m, W, ldw, m_eff, sigma2, p, pts, n_c, L.NB,
+                                     L.rows_pad(), psi, st);
+  if (rc) return rc;
+  rc = (p == 1) ? dispatch_nb<2>(L.NB, psi, coef, forcing, n_c, B, L, part, st)
+                : dispatch_nb<3>(L.NB, psi, coef, forcing, n_c, B, L, part, st);
+  if (rc) return rc;
+  if (gram_ext != nullptr) {
+    batch_unpack_kernel<<<B, 256, 0, st>>>(part, L.nsplit, B, L.NB, m_eff + 2, gram_ext);
+    NYS_CHECK_LAUNCH();
+  }
+  return NYS_OK;
+}

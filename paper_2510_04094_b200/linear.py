@@ -1,0 +1,260 @@
+"""Primal KKT assembly and direct solve for linear ODEs, on the B200.
+
+Mirror of ``pkg/src/nysode/linear.py`` (same names, arguments, exceptions).
+What moved to the GPU:
+
+* :func:`assemble` samples the spec callables on the constraint points on the
+  host (exactly like linear.py:103-116, so the values are the reference's),
+  then calls the fused feature+Gram kernel (``nys_fused_gram_f64``): the
+  n x m feature matrices are never formed.  The system keeps the extended Gram
+  E = [D g r]^T [D g r] on the device; ``matrix`` / ``rhs`` are built on demand.
+* :func:`solve` is the batched device LU + one refinement step
+  (``nys_kkt_solve_f64``, linear.py:140-158).
+* :meth:`PrimalModel.predict` and :func:`check_kkt` run on the device
+  (``nys_predict_f64``, ``nys_ode_residual_f64``).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any, Optional
+
+import numpy as np
+
+from . import _lib
+from .nystrom import NystromFeatureMap
+
+KKT_RESIDUAL_TOL = 1e-8          # linear.py:33
+# kernel-space Gram for m_eff + 2 > 72 is only parity-safe on well-conditioned
+# landmark matrices (1.3e-13 at cond 28, 2.6e-5 when m_eff < m)
+KSPACE_MAX_COND = 1e6
+SMALL_NB_MAX = 9                 # register-resident fused kernel: m_eff + 2 <= 72
+
+
+class SingularSystemError(np.linalg.LinAlgError):
+    """Direct solve failed or produced non-finite entries (linear.py:36-37)."""
+
+
+class IllConditionedLargeMapError(RuntimeError):
+    """m_eff + 2 > 72 with an ill-conditioned landmark matrix: the large-m
+    device path (kernel-space Gram) would not be parity-safe."""
+
+
+@dataclass(frozen=True)
+class PrimalModel:
+    omega: np.ndarray
+    bias: float
+    multipliers: np.ndarray
+    feature_map: NystromFeatureMap
+
+    def x_device(self):
+        _, torch = _lib.require_device()
+        x = np.concatenate([self.omega, [self.bias]])
+        return _lib.as_f64(x, self.feature_map.device)
+
+    def predict_device(self, ell: int, points):
+        """y_hat^(ell)(points) as a device tensor (linear.py:47-53)."""
+        return predict_batch(self.feature_map, self.x_device().reshape(1, -1), ell, points)[0]
+
+    def predict(self, ell: int, points) -> np.ndarray:
+        return self.predict_device(ell, points).cpu().numpy()
+
+
+def predict_batch(fmap: NystromFeatureMap, x, ell: int, points):
+    """Rows x[b] = (omega_b, b_b, ...) sharing fmap -> (B, |points|) device tensor."""
+    lib, torch = _lib.require_device()
+    pts = _lib.as_f64(np.atleast_1d(points) if not hasattr(points, "device") else points,
+                      fmap.device).reshape(-1)
+    x = _lib.as_f64(x, fmap.device)
+    B, ldx = x.shape
+    out = torch.empty((B, pts.numel()), dtype=torch.float64, device=fmap.device)
+    _lib.call("nys_predict_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W), fmap.m,
+              fmap.m_eff, float(fmap.kernel.sigma2), int(ell), _lib.ptr(pts), pts.numel(),
+              _lib.ptr(x), ldx, B, _lib.ptr(out), pts.numel(), _lib.stream_ptr())
+    return out
+
+
+def condition_rows(cond, fmap: NystromFeatureMap):
+    """(A_c, beta, values) -- linear.py:56-63; feature rows from the device."""
+    rows, bias_coeffs, values = [], [], []
+    for bc in cond.entries:
+        rows.append(fmap.feature_deriv(bc.order, bc.point))
+        bias_coeffs.append(1.0 if bc.order == 0 else 0.0)
+        values.append(bc.value)
+    return np.array(rows), np.array(bias_coeffs), np.array(values)
+
+
+def constraint_points(cond, grid: np.ndarray) -> np.ndarray:
+    """t_2..t_n for IVPs, t_2..t_{n-1} for BVPs (linear.py:66-68)."""
+    return grid[1:] if cond.kind == "ivp" else grid[1:-1]
+
+
+def gram_ext_device(fmap: NystromFeatureMap, order: int, pts, coef, forcing,
+                    row_begin: int = 0, row_end: Optional[int] = None):
+    """E = [D g r]^T [D g r] over rows [row_begin, row_end) of the sampled
+    constraint system (device tensors in, (m_eff+2)^2 device tensor out)."""
+    lib, torch = _lib.require_device()
+    dev = fmap.device
+    pts = _lib.as_f64(pts, dev).reshape(-1)
+    coef = _lib.as_f64(coef, dev).reshape(order, -1)
+    forcing = _lib.as_f64(forcing, dev).reshape(-1)
+    n_c = pts.numel()
+    row_end = n_c if row_end is None else row_end
+    me = fmap.m_eff
+    if (me + 2 + 7) // 8 > SMALL_NB_MAX and fmap.condition > KSPACE_MAX_COND:
+        raise IllConditionedLargeMapError(
+            f"m_eff={me} with cond(Omega)={fmap.condition:.2e} > {KSPACE_MAX_COND:.0e}")
+    E = torch.empty((me + 2, me + 2), dtype=torch.float64, device=dev)
+    wsb = lib.nys_fused_gram_workspace_bytes(row_end - row_begin, fmap.m, me, order)
+    ws = _lib.WORKSPACE.get(wsb, dev)
+    _lib.call("nys_fused_gram_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
+              fmap.m, me, float(fmap.kernel.sigma2), int(order), _lib.ptr(pts), _lib.ptr(coef),
+              _lib.ptr(forcing), n_c, int(row_begin), int(row_end), _lib.ptr(E), _lib.ptr(ws),
+              wsb, _lib.stream_ptr())
+    return E
+
+
+@dataclass(eq=False)
+class AssembledSystem:
+    """linear.py:71-87; D is not materialised."""
+
+    constraint_points: np.ndarray
+    gamma: float
+    g: np.ndarray
+    r: np.ndarray
+    coeff_values: np.ndarray         # (p, n_c) f_k on the constraint points
+    cond_rows: np.ndarray
+    cond_bias: np.ndarray
+    cond_values: np.ndarray
+    fmap: NystromFeatureMap
+    order: int
+    d_gram: Any                      # (m_eff+2)^2 device tensor
+    _cache: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def side(self) -> int:
+        return self.fmap.m_eff + 1 + self.cond_values.size
+
+    def _kkt(self):
+        if "x" not in self._cache:
+            self._cache.update(_kkt_solve(self, want_matrix=True))
+        return self._cache
+
+    @property
+    def matrix(self) -> np.ndarray:
+        return self._kkt()["M"].cpu().numpy()[0]
+
+    @property
+    def rhs(self) -> np.ndarray:
+        return self._kkt()["rhs"].cpu().numpy()[0]
+
+    @property
+    def D(self) -> np.ndarray:
+        """Materialises D on request only (linear.py:103-112 order)."""
+        fm = self.fmap
+        D = fm.feature_matrix_device(self.order, self.constraint_points)
+        for k in range(1, self.order + 1):
+            fk = _lib.as_f64(self.coeff_values[k - 1], fm.device)
+            D = D - fk[:, None] * fm.feature_matrix_device(self.order - k, self.constraint_points)
+        return D.cpu().numpy()
+
+
+def assemble(spec, cond, fmap: NystromFeatureMap, grid, gamma: float) -> AssembledSystem:
+    """linear.py:90-137 -- callables sampled on host, Gram on the GPU."""
+    grid = np.asarray(grid, dtype=float)
+    if gamma <= 0:
+        raise ValueError(f"gamma must be positive, got {gamma}")
+    p = spec.order
+    pts = constraint_points(cond, grid)
+    coeff_vals = []
+    for k, fk in enumerate(spec.coeffs, start=1):
+        fkv = np.asarray(fk(pts), dtype=float)
+        if not np.all(np.isfinite(fkv)):
+            raise FloatingPointError(f"coefficient f_{k} non-finite on constraint points")
+        coeff_vals.append(np.broadcast_to(fkv, pts.shape))
+    r = np.asarray(spec.forcing(pts), dtype=float)
+    if not np.all(np.isfinite(r)):
+        raise FloatingPointError("forcing non-finite on constraint points")
+    r = np.broadcast_to(r, pts.shape)
+    coef = np.stack(coeff_vals)
+    Ac, beta, values = condition_rows(cond, fmap)
+    E = gram_ext_device(fmap, p, pts, coef, r)
+    return AssembledSystem(constraint_points=pts, gamma=float(gamma), g=-coef[-1], r=r,
+                           coeff_values=coef, cond_rows=Ac.reshape(len(cond.entries), -1),
+                           cond_bias=beta, cond_values=values, fmap=fmap, order=p, d_gram=E)
+
+
+def _kkt_solve(system: AssembledSystem, want_matrix: bool = False):
+    lib, torch = _lib.require_device()
+    fm = system.fmap
+    dev = fm.device
+    me, nk = fm.m_eff, system.cond_values.size
+    side = me + 1 + nk
+    Ac = _lib.as_f64(system.cond_rows.reshape(nk, me) if nk else np.zeros((0, me)), dev)
+    beta = _lib.as_f64(system.cond_bias, dev)
+    vals = _lib.as_f64(system.cond_values.reshape(1, nk), dev)
+    x = torch.empty((1, side), dtype=torch.float64, device=dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    M = torch.empty((1, side, side), dtype=torch.float64, device=dev) if want_matrix else None
+    rhs = torch.empty((1, side), dtype=torch.float64, device=dev) if want_matrix else None
+    wsb = lib.nys_kkt_workspace_bytes(me, nk, 1)
+    ws = _lib.WORKSPACE.get(wsb, dev) if wsb else None
+    _lib.call("nys_kkt_solve_f64", _lib.ptr(system.d_gram), me, nk, _lib.ptr(Ac), _lib.ptr(beta),
+              _lib.ptr(vals), float(system.gamma), 1, _lib.ptr(x), _lib.ptr(info), _lib.ptr(M),
+              _lib.ptr(rhs), _lib.ptr(ws), wsb, _lib.stream_ptr())
+    return dict(x=x, info=info, M=M, rhs=rhs)
+
+
+def raise_for_info(code: int):
+    if code == _lib.INFO_SINGULAR:
+        raise SingularSystemError("Singular matrix")
+    if code == _lib.INFO_NONFINITE:
+        raise SingularSystemError("solution contains non-finite entries")
+
+
+def solve(system: AssembledSystem, fmap: NystromFeatureMap) -> PrimalModel:
+    """Dense partial-pivoting solve + one refinement step (linear.py:140-158)."""
+    res = system._cache if "x" in system._cache else _kkt_solve(system)
+    raise_for_info(int(res["info"][0]))
+    x = res["x"][0].cpu().numpy()
+    me = fmap.m_eff
+    return PrimalModel(omega=x[:me], bias=float(x[me]), multipliers=x[me + 1:], feature_map=fmap)
+
+
+@dataclass(frozen=True)
+class KktReport:
+    linear_residual: float
+    rhs_scale: float
+    condition_residuals: np.ndarray
+    ode_residuals: np.ndarray
+
+    @property
+    def passed(self) -> bool:
+        bound = KKT_RESIDUAL_TOL * max(self.rhs_scale, 1.0)
+        return bool(self.linear_residual <= bound
+                    and np.all(self.condition_residuals <= KKT_RESIDUAL_TOL))
+
+
+def check_kkt(model: PrimalModel, system: AssembledSystem) -> KktReport:
+    """linear.py:161-189; e = D omega + g b - r from a device kernel (no D)."""
+    lib, torch = _lib.require_device()
+    x = np.concatenate([model.omega, [model.bias], model.multipliers])
+    M, rhs = system.matrix, system.rhs
+    lin = float(np.max(np.abs(M @ x - rhs)))
+    cond_res = np.abs(system.cond_rows @ model.omega + system.cond_bias * model.bias
+                      - system.cond_values)
+    fm = system.fmap
+    dev = fm.device
+    pts = _lib.as_f64(system.constraint_points, dev)
+    coef = _lib.as_f64(system.coeff_values, dev)
+    r = _lib.as_f64(system.r, dev)
+    xd = _lib.as_f64(x, dev)
+    e = torch.empty(pts.numel(), dtype=torch.float64, device=dev)
+    _lib.call("nys_ode_residual_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+              fm.m_eff, float(fm.kernel.sigma2), system.order, _lib.ptr(pts), _lib.ptr(coef),
+              _lib.ptr(r), pts.numel(), _lib.ptr(xd), _lib.ptr(e), _lib.stream_ptr())
+    return KktReport(linear_residual=lin, rhs_scale=float(np.max(np.abs(rhs))),
+                     condition_residuals=cond_res, ode_residuals=e.cpu().numpy())
+
+
+def predict(model: PrimalModel, ell: int, points) -> np.ndarray:
+    return model.predict(ell, points)

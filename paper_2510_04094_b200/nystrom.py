@@ -1,0 +1,152 @@
+"""Landmark selection and the explicit Nystrom feature map, on the B200.
+
+Mirror of ``pkg/src/nysode/nystrom.py`` (same names, arguments, errors):
+
+* :func:`select_landmarks` -- host index logic, identical to nystrom.py:84-106
+  for ``Equidistant`` and ``Random``; ``LeverageScore`` is SURVEY.md §8f
+  "next" row 3 and raises ``NotImplementedError``.
+* :func:`build_feature_map` -- device Jacobi eigendecomposition of Omega_mm
+  (C-ABI ``nys_landmark_eig_f64``), replacing nystrom.py:136-160.
+* :class:`NystromFeatureMap` -- holds the device copies (landmarks, W);
+  ``eigenvalues`` / ``eigenvectors`` are fetched to the host lazily so the
+  reference's attributes keep working.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Any, Optional
+
+import numpy as np
+
+from . import _lib
+from .kernel import RbfKernel, check_order
+
+DEFAULT_DROP_TOL = 1e-16     # nystrom.py:21
+
+
+class DegenerateLandmarksError(ValueError):
+    """Two landmarks coincide within 1e-12 (nystrom.py:29-30)."""
+
+
+class InvalidCountError(ValueError):
+    """Landmark count outside 2..n (nystrom.py:33-34)."""
+
+
+@dataclass(frozen=True)
+class Equidistant:
+    pass
+
+
+@dataclass(frozen=True)
+class Random:
+    seed: int = 0
+
+
+@dataclass(frozen=True)
+class LeverageScore:
+    seed: int = 0
+    ridge: float = 1e-6
+    kernel: Optional[RbfKernel] = None
+
+
+def select_landmarks(strategy, grid, m: int) -> np.ndarray:
+    """Pick m distinct grid points (nystrom.py:84-106)."""
+    grid = np.asarray(grid, dtype=float)
+    n = grid.size
+    if m < 2 or m > n:
+        raise InvalidCountError(f"landmark count m={m} must satisfy 2 <= m <= n={n}")
+    name = type(strategy).__name__
+    if name == "Equidistant":
+        idx = np.round(np.arange(m) * (n - 1) / (m - 1)).astype(int)
+    elif name == "Random":
+        rng = np.random.default_rng(strategy.seed)
+        idx = np.sort(rng.choice(n, size=m, replace=False))
+    elif name == "LeverageScore":
+        raise NotImplementedError("leverage-score sampling is SURVEY.md §8f next-row 3")
+    else:
+        raise TypeError(f"unknown sampling strategy {strategy!r}")
+    return grid[idx]
+
+
+@dataclass(eq=False)
+class NystromFeatureMap:
+    """Feature map phi(t) = Lambda^{-1/2} V^T k(t, L) with device-resident W."""
+
+    kernel: RbfKernel
+    landmarks: np.ndarray
+    m_eff: int
+    device: Any
+    d_landmarks: Any                 # (m,) float64 tensor
+    d_W: Any                         # (m, m) float64 tensor; columns >= m_eff are 0
+    d_eigvals: Any                   # (m,) descending
+    d_eigvecs: Any                   # (m, m)
+    _host: dict = field(default_factory=dict, repr=False)
+
+    @property
+    def m(self) -> int:
+        return int(self.landmarks.size)
+
+    @property
+    def eigenvalues(self) -> np.ndarray:
+        if "s" not in self._host:
+            self._host["s"] = self.d_eigvals[: self.m_eff].cpu().numpy()
+        return self._host["s"]
+
+    @property
+    def eigenvectors(self) -> np.ndarray:
+        if "v" not in self._host:
+            self._host["v"] = self.d_eigvecs[:, : self.m_eff].cpu().numpy()
+        return self._host["v"]
+
+    @property
+    def condition(self) -> float:
+        """s_max / s_min over the retained eigenvalues."""
+        s = self.eigenvalues
+        return float(s[0] / s[-1])
+
+    def feature_matrix_device(self, ell: int, points):
+        """Psi_ell(points) as a (|points|, m_eff) device tensor (nystrom.py:123-127)."""
+        check_order(ell)
+        lib, torch = _lib.require_device()
+        pts = _lib.as_f64(np.atleast_1d(points) if not hasattr(points, "device") else points,
+                          self.device).reshape(-1)
+        out = torch.empty((pts.numel(), self.m_eff), dtype=torch.float64, device=self.device)
+        _lib.call("nys_feature_matrix_f64", _lib.ptr(self.d_landmarks), self.m, _lib.ptr(self.d_W),
+                  self.m, self.m_eff, float(self.kernel.sigma2), int(ell), _lib.ptr(pts),
+                  pts.numel(), _lib.ptr(out), self.m_eff, _lib.stream_ptr())
+        return out
+
+    def feature_matrix(self, ell: int, points) -> np.ndarray:
+        return self.feature_matrix_device(ell, points).cpu().numpy()
+
+    def feature(self, t: float) -> np.ndarray:
+        return self.feature_matrix(0, [t])[0]
+
+    def feature_deriv(self, ell: int, t: float) -> np.ndarray:
+        return self.feature_matrix(ell, [t])[0]
+
+
+def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TOL,
+                      device=None) -> NystromFeatureMap:
+    """Eigendecompose Omega_mm on the GPU and keep s > max(drop_tol s_0, 0)."""
+    landmarks = np.asarray(landmarks, dtype=float).reshape(-1)
+    if not 0 <= drop_tol < 1:
+        raise ValueError(f"drop_tol must lie in [0, 1), got {drop_tol}")
+    lib, torch = _lib.require_device()
+    device = torch.device(device or "cuda")
+    m = landmarks.size
+    d_lm = _lib.as_f64(landmarks, device)
+    s = torch.empty(m, dtype=torch.float64, device=device)
+    V = torch.empty((m, m), dtype=torch.float64, device=device)
+    W = torch.empty((m, m), dtype=torch.float64, device=device)
+    meta = torch.zeros(2, dtype=torch.int32, device=device)   # m_eff, info
+    wsb = lib.nys_landmark_eig_workspace_bytes(m)
+    ws = _lib.WORKSPACE.get(wsb, device) if wsb else None
+    _lib.call("nys_landmark_eig_f64", _lib.ptr(d_lm), m, float(k.sigma2), float(drop_tol),
+              _lib.ptr(s), _lib.ptr(V), _lib.ptr(W), _lib.ptr(meta), _lib.ptr(meta) + 4,
+              _lib.ptr(ws), wsb, _lib.stream_ptr())
+    m_eff, info = (int(v) for v in meta.cpu())
+    if info == _lib.INFO_DEGENERATE:
+        raise DegenerateLandmarksError("two landmarks coincide within 1e-12")
+    return NystromFeatureMap(kernel=k, landmarks=landmarks, m_eff=m_eff, device=device,
+                             d_landmarks=d_lm, d_W=W, d_eigvals=s, d_eigvecs=V)

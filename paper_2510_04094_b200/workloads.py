@@ -59,18 +59,23 @@ class ConfigSpec:
 
 # sigma choices: c0 and c3 are fixed by BASELINE.json (sigma = 0.1).  c1 and c4
 # are "tuned per seed from [0.05, 0.5]"; c2 needs one shared sigma because the
-# landmarks are shared.  The tuning rule (oracle-side grid search over
-# SIGMA_CANDIDATES minimising relative L2 error vs y*) lives in
-# oracle/tune_sigma.py; its outcome is frozen here and recorded in DESIGN.md.
+# landmarks are shared.  The tuning rule (oracle/tune_sigma.py) is an
+# oracle-side grid search over SIGMA_CANDIDATES minimising the relative L2
+# error vs y*, restricted to sigmas whose oracle error is reproducible: swapping
+# LAPACK's eigensolver driver (dsyevd -> dsyev) must move the error vs y* by
+# < 1e-3 of itself, i.e. 10x inside the north star's 1 % error gate.  Without
+# that guard the 1 % gate is unattainable even for the reference against
+# itself (c2 sigma=0.3: 300 % swing).  Outcome (frozen here):
+# c1 -> 0.4 (m_eff 50), c2 -> 0.1 (m_eff 64 = m), c4 -> 0.5 (m_eff 256).
 SIGMA_CANDIDATES = (0.05, 0.1, 0.15, 0.2, 0.3, 0.4, 0.5)
 
 CONFIGS: dict[int, ConfigSpec] = {
     0: ConfigSpec(0, n=1000, m=20, domain=(0.0, 1.0), order=1, terms=3,
                   gamma=1e8, sigma=0.1),
     1: ConfigSpec(1, n=10_000, m=50, domain=(0.0, 5.0), order=2, terms=5,
-                  gamma=1e9, sigma=0.5),
+                  gamma=1e9, sigma=0.4),
     2: ConfigSpec(2, n=4096, m=64, domain=(0.0, 2.0), order=2, terms=5,
-                  gamma=1e9, sigma=0.3, batch=4096),
+                  gamma=1e9, sigma=0.1, batch=4096),
     3: ConfigSpec(3, n=2000, m=40, domain=(0.0, 1.0), order=1, terms=3,
                   gamma=1e8, sigma=0.1, batch=256, nonlinear=True),
     4: ConfigSpec(4, n=1 << 22, m=256, domain=(0.0, 100.0), order=2, terms=7,
