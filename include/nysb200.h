@@ -54,6 +54,9 @@ int nys_abi_version(void);
 const char* nys_status_string(int status);
 /* last CUDA error string seen by this thread (diagnostics only) */
 const char* nys_last_cuda_error(void);
+/* number of kernels this library has launched in the process (evidence for
+ * benchmark launch counts) */
+unsigned long long nys_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map

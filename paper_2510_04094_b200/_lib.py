@@ -26,6 +26,7 @@ SIGNATURES = {
     "nys_abi_version": (_i, []),
     "nys_status_string": (C.c_char_p, [_i]),
     "nys_last_cuda_error": (C.c_char_p, []),
+    "nys_launch_count": (C.c_ulonglong, []),
     "nys_landmark_eig_workspace_bytes": (_sz, [_i]),
     "nys_landmark_eig_f64": (_i, [_vp, _i, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_feature_matrix_f64": (_i, [_vp, _i, _vp, _i, _i, _d, _i, _vp, _i, _vp, _i, _vp]),
@@ -141,4 +142,7 @@ def as_f64(x, device):
 
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float64).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=device)
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if not a.flags.writeable:
+        a = a.copy()
+    return torch.as_tensor(a, device=device)

@@ -135,3 +135,85 @@ def solve_many(specs: Sequence, conds: Sequence, fmap: NystromFeatureMap, grid,
         out.append(PrimalModel(omega=x[b, :me], bias=float(x[b, me]), multipliers=x[b, me + 1:],
                                feature_map=fmap))
     return out
+
+
+class SharedGridPipeline:
+    """One config-2 step from scratch: landmark eigendecomposition (once per
+    shared landmark set), shared features, per-instance Gram, KKT solves.
+
+    ``run_device`` takes device-resident samples; ``run_host`` takes pinned
+    host arrays, streams them in ``chunks`` on a copy stream overlapped with
+    the compute stream, and returns the solutions in pinned host memory --
+    the end-to-end path a caller with host data uses.
+    """
+
+    def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
+                 max_batch: int, drop_tol: float = 1e-16, device=None):
+        from .kernel import RbfKernel
+        from .nystrom import build_feature_map
+
+        self.landmarks = np.asarray(landmarks, dtype=float)
+        self.kernel = RbfKernel(float(sigma2))
+        self.grid = np.asarray(grid, dtype=float)
+        self.gamma, self.order, self.cond = float(gamma), int(order), cond
+        self.max_batch, self.drop_tol = int(max_batch), drop_tol
+        self._build = build_feature_map
+        self.device = device
+        self.solver = None
+
+    def prepare(self):
+        """Eigendecomposition + solver state (the per-landmark-set work)."""
+        fm = self._build(self.kernel, self.landmarks, self.drop_tol, device=self.device)
+        if self.solver is None or self.solver.fmap.m_eff != fm.m_eff:
+            self.solver = LinearBatchSolver(fm, self.grid, self.gamma, self.order, self.cond,
+                                            self.max_batch)
+        else:   # same shapes: keep the workspace, refresh the feature map state
+            s = self.solver
+            s.fmap = fm
+            Ac, beta, _ = condition_rows(self.cond, fm)
+            s.Ac.copy_(_lib.as_f64(Ac.reshape(s.n_cond, fm.m_eff), fm.device))
+            s.beta.copy_(_lib.as_f64(beta, fm.device))
+        return self.solver
+
+    def run_device(self, coef, forcing, values, out_x=None, out_info=None):
+        solver = self.prepare()
+        return solver.solve_device(coef, forcing, values, out_x, out_info)
+
+    def run_host(self, coef_h, forcing_h, values_h, x_h, info_h, chunks: int = 4,
+                 dev_bufs=None):
+        """Pinned host in -> pinned host out.  dev_bufs: optional preallocated
+        device staging (coef, forcing, values, x, info) for the full batch."""
+        torch = _lib.require_device()[1]
+        solver = self.prepare()
+        dev = solver.fmap.device
+        B = coef_h.shape[0]
+        if dev_bufs is None:
+            dev_bufs = (torch.empty(coef_h.shape, dtype=torch.float64, device=dev),
+                        torch.empty(forcing_h.shape, dtype=torch.float64, device=dev),
+                        torch.empty(values_h.shape, dtype=torch.float64, device=dev),
+                        torch.empty((B, solver.side), dtype=torch.float64, device=dev),
+                        torch.empty(B, dtype=torch.int32, device=dev))
+        dc, df, dv, dx, di = dev_bufs
+        comp = torch.cuda.current_stream()
+        copy = getattr(self, "_copy_stream", None)
+        if copy is None:
+            copy = self._copy_stream = torch.cuda.Stream(device=dev)
+        copy.wait_stream(comp)
+        bounds = np.linspace(0, B, chunks + 1).astype(int)
+        ready = []
+        with torch.cuda.stream(copy):
+            for c in range(chunks):
+                a, b = bounds[c], bounds[c + 1]
+                dc[a:b].copy_(coef_h[a:b], non_blocking=True)
+                df[a:b].copy_(forcing_h[a:b], non_blocking=True)
+                dv[a:b].copy_(values_h[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                ready.append(ev)
+        for c in range(chunks):
+            a, b = bounds[c], bounds[c + 1]
+            comp.wait_event(ready[c])
+            solver.solve_device(dc[a:b], df[a:b], dv[a:b], dx[a:b], di[a:b])
+        x_h.copy_(dx, non_blocking=True)
+        info_h.copy_(di, non_blocking=True)
+        return x_h, info_h

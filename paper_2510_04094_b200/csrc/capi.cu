@@ -1,4 +1,5 @@
 // C-ABI plumbing: status strings, CUDA error capture, cached device attributes.
+#include <atomic>
 #include <cstring>
 
 #include "batch_layout.cuh"
@@ -8,7 +9,13 @@ namespace {
 thread_local char g_last_err[256] = "";
 }
 
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+
 namespace nys_host {
+void count_launches(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+
 int record_cuda(cudaError_t e) {
   if (e == cudaSuccess) return NYS_OK;
   std::strncpy(g_last_err, cudaGetErrorString(e), sizeof(g_last_err) - 1);
@@ -45,3 +52,5 @@ extern "C" const char* nys_status_string(int status) {
 }
 
 extern "C" const char* nys_last_cuda_error(void) { return g_last_err; }
+
+extern "C" unsigned long long nys_launch_count(void) { return g_launches.load(); }

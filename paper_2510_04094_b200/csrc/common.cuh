@@ -99,6 +99,7 @@ NYS_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
 // host-side helpers shared by the translation units
 namespace nys_host {
 int record_cuda(cudaError_t e);   // stores the message, returns NYS_ECUDA or NYS_OK
+void count_launches(int k);       // process-wide kernel launch counter (nys_launch_count)
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace nys_host
 

@@ -200,6 +200,7 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
   int threads = m <= 32 ? 256 : kEigThreads;
   jacobi_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
       landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gV, use_smem);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -158,6 +158,7 @@ int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff
     feature_tile_kernel<<<grid, kFeatThreads, sm, st>>>(lm, m, W, ldw, m_eff, sigma2, ell, pts,
                                                         n_c, packed, 0, 1, n_blocks, p + 1,
                                                         n_rows_pad);
+    nys_host::count_launches(1);
   }
   NYS_CHECK_LAUNCH();
   return NYS_OK;
@@ -180,6 +181,7 @@ extern "C" int nys_feature_matrix_f64(const double* landmarks, int m, const doub
   dim3 grid((n_pts + kTP - 1) / kTP);
   feature_tile_kernel<<<grid, kFeatThreads, sm, static_cast<cudaStream_t>(stream)>>>(
       landmarks, m, W, ldw, m_eff, sigma2, ell, pts, n_pts, out, ldo, 0, 0, 0, 0);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -201,6 +203,7 @@ extern "C" int nys_predict_f64(const double* landmarks, int m, const double* W, 
   dim3 grid((n_pts + kTP - 1) / kTP, (B + kFeatThreads - 1) / kFeatThreads);
   predict_kernel<<<grid, kFeatThreads, sm, static_cast<cudaStream_t>(stream)>>>(
       landmarks, m, W, ldw, m_eff, sigma2, ell, pts, n_pts, x, ldx, B, out, ldo);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -217,6 +220,7 @@ extern "C" int nys_ode_residual_f64(const double* landmarks, int m, const double
   int rows_per_block = 256 * kResRowsPerThread;
   ode_residual_kernel<<<(n_c + rows_per_block - 1) / rows_per_block, 256, m * sizeof(double), st>>>(
       landmarks, m, W, ldw, m_eff, sigma2, p, pts, coef, forcing, n_c, x, e);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

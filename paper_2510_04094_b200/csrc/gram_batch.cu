@@ -173,6 +173,7 @@ int launch_gram(const double* psi, const double* coef, const double* forcing, in
   dim3 grid((B + WARPS - 1) / WARPS, L.nsplit);
   kern<<<grid, WARPS * 32, smem, st>>>(psi, coef, forcing, n_c, B, L.ks_per_split, L.m_eff + 1,
                                        part);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -224,6 +225,7 @@ extern "C" int nys_batch_gram_f64(const double* landmarks, int m, const double* 
   if (rc) return rc;
   if (gram_ext != nullptr) {
     batch_unpack_kernel<<<B, 256, 0, st>>>(part, L.nsplit, B, L.NB, m_eff + 2, gram_ext);
+    nys_host::count_launches(1);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;

@@ -177,6 +177,7 @@ int launch_fused(const FusedPlan& F, const double* lm, int m, const double* W, i
   }
   kern<<<F.nctas, kFusedWarps * 32, F.smem, st>>>(lm, m, W, ldw, m_eff, sigma2, pts, coef, forcing,
                                                   n_c, rb, re, F.MK, part);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -245,6 +246,7 @@ extern "C" int nys_fused_gram_f64(const double* landmarks, int m, const double* 
   if (rc) return rc;
   fused_finalize_kernel<<<(F.npair * 64 + 255) / 256, 256, 0, st>>>(part, F.nctas, F.NB, m_eff + 2,
                                                                     gram_ext);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -272,7 +272,8 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
                                          (int)L.smem);                                             \
     if (e != cudaSuccess) return record_cuda(e);                                                   \
     kern<<<grid, nthreads, L.smem, st>>>(lm, m, sigma2, pts, coef, forcing, n_c, row_begin,        \
-                                         row_end, L.NT, L.ntasks, L.tiles_per_cta, part);          \
+                                         row_end, L.NT, L.ntasks, L.tiles_per_cta, part); \
+    nys_host::count_launches(1);                                                                   \
   } while (0)
   switch (p) {
     case 1: NYS_LARGE(1); break;
@@ -285,9 +286,12 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
   int per = L.ntasks * kRT * kRT * 64;
   large_reduce_kernel<<<(per + 255) / 256, 256, 0, st>>>(part, L.nrr, L.ngroups, L.NT, L.ntasks,
                                                          L.Pe, K);
+  nys_host::count_launches(1);
   const int Pw = m_eff + 2;
   proj_right_kernel<<<(L.Pe * Pw + 127) / 128, 128, 0, st>>>(K, L.Pe, W, ldw, m, m_eff, T);
+  nys_host::count_launches(1);
   proj_left_kernel<<<(Pw * Pw + 127) / 128, 128, 0, st>>>(T, L.Pe, W, ldw, m, m_eff, gram_ext);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -256,6 +256,7 @@ int launch_kkt(Src src, int m_eff, int ncond, const double* Ac, const double* be
   }
   kern<<<B, kKktThreads, dyn, st>>>(src, m_eff, ncond, Ac, beta, values, gamma, B, x, info, M,
                                     rhs, static_cast<double*>(ws), use_smem);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

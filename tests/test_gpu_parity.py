@@ -20,7 +20,7 @@ def test_eigendecomposition_matches_reference(name):
     g = load_golden(name)
     fm = fmap_from_golden(g)
     ref = g["eigvals"]
-    if name.startswith("c"):
+    if not name.startswith("cat"):
         assert fm.m_eff == int(g["m_eff"])
     else:   # catalog problems sit at the 1e-16 drop threshold: allow a small shift
         assert abs(fm.m_eff - int(g["m_eff"])) <= 3
@@ -63,7 +63,7 @@ def test_fused_gram_matches_oracle_same_basis(name):
                      kind=str(g["kind"]))
     Dx = np.column_stack([osy["D"], osy["g"], osy["r"]])
     Eo = Dx.T @ Dx
-    scale = np.abs(Dx).max(axis=0)
+    scale = np.maximum(np.abs(Dx).max(axis=0), 1e-300)
     rel = np.abs(E - Eo) / (np.outer(scale, scale) * Dx.shape[0])
     assert rel.max() <= 1e-9
     # the assembled KKT matrix (linear.py:123-133 layout) equals the oracle's
@@ -71,15 +71,24 @@ def test_fused_gram_matches_oracle_same_basis(name):
     np.testing.assert_allclose(M, osy["M"], rtol=0, atol=1e-9 * np.abs(osy["M"]).max())
 
 
-def test_kkt_solve_matches_lapack():
-    g = load_golden("c1_seed0")
+@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0", "cat_p12", "c4_n16384"])
+def test_kkt_solve_matches_lapack(name):
+    """Device LU + refinement vs LAPACK dgesv on the SAME assembled M: the
+    reference's backward-stability bound (reference tests/test_linear.py:79-86)
+    and identical predictions.  (x itself may differ in its ill-conditioned
+    directions -- cond(M) reaches 1e15 -- without moving y_hat.)"""
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden(name)
     fm = fmap_from_golden(g)
     sy, model = solve_golden_instance(g, fm, 0)
     M, rhs = sy.matrix, sy.rhs
     x_ref = np.linalg.solve(M, rhs)
     x_ref = x_ref + np.linalg.solve(M, rhs - M @ x_ref)
     x = np.concatenate([model.omega, [model.bias], model.multipliers])
-    assert rel_l2(x, x_ref) <= 1e-8
+    assert np.max(np.abs(M @ x - rhs)) <= 1e-8 * max(np.abs(rhs).max(), 1.0)
+    me = fm.m_eff
+    ref_model = L.PrimalModel(x_ref[:me], float(x_ref[me]), x_ref[me + 1:], fm)
+    assert rel_l2(model.predict(0, g["grid"]), ref_model.predict(0, g["grid"])) <= 1e-8
 
 
 def test_check_kkt_certificate():
