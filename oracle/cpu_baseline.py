@@ -18,13 +18,18 @@ import numpy as np
 
 
 def _worker_init():
+    # forked workers inherit an already-initialised OpenBLAS pool: cap it at
+    # runtime (env vars alone would be ignored and oversubscribe the cores)
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+
+    global _LIMITS
+    _LIMITS = threadpool_limits(limits=1)
 
 
 def _solve_range(args):
     cid, seed, first, count, budget_s, cfg_over = args
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     from oracle import nys_port as O
     from paper_2510_04094_b200 import workloads as W
 
