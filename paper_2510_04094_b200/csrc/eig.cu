@@ -6,10 +6,9 @@
 // A1: <= 6.5e-8 on y_hat even when m_eff shifts), and the configs use sigma
 // where the problem is eigensolver-insensitive (workloads.py).
 //
-// One CTA per landmark set.  Round-robin ("circle") ordering gives m/2
-// disjoint rotations per round; a round is (1) rotation parameters,
-// (2) column update of A and V, (3) row update of A.  A and V live in shared
-// memory when 2*m^2*8 B fits, otherwise in the caller's workspace (L2-resident).
+// One CTA per landmark set, one-sided Jacobi (see the kernel comment).  U and
+// V live in shared memory when 2*m^2*8 B fits (m <= 112), otherwise in the
+// caller's workspace (L2-resident).
 #include <cmath>
 
 #include "common.cuh"
@@ -17,39 +16,37 @@
 namespace {
 
 constexpr int kEigThreads = 1024;
-constexpr int kMaxSweeps = 40;
+constexpr int kMaxSweeps = 60;
 
-struct Rot {
-  int p, q;
-  double c, s;
-};
-
+// One-sided (Hestenes) Jacobi on U = Omega (symmetric): rotate column pairs
+// until every pair is orthogonal to 1 ulp; V accumulates the rotations, so
+// U = Omega V with orthogonal columns, i.e. u_i = lambda_i v_i.  lambda_i is
+// read back as the Rayleigh quotient v_i . u_i (signed, absolute accuracy
+// eps ||Omega||, like LAPACK dsyevd).  One warp per column pair, pairs of a
+// round are disjoint (round-robin "circle" order), so a round needs a single
+// __syncthreads.  U and V are column-major (conflict-free lane-per-row access).
 __global__ void __launch_bounds__(kEigThreads, 1)
-    jacobi_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
-                      double* __restrict__ eigvals, double* __restrict__ eigvecs,
-                      double* __restrict__ Wout, int* __restrict__ m_eff_out,
-                      int* __restrict__ info, double* __restrict__ gA, double* __restrict__ gV,
-                      int use_smem) {
+    hestenes_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
+                        double* __restrict__ eigvals, double* __restrict__ eigvecs,
+                        double* __restrict__ Wout, int* __restrict__ m_eff_out,
+                        int* __restrict__ info, double* __restrict__ gU, double* __restrict__ gV,
+                        int use_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  // small bookkeeping lives in static shared memory
-  __shared__ Rot rots[256];
-  __shared__ int changed;
   __shared__ int degenerate;
-  __shared__ double diag[512];
+  __shared__ double lam[512];
   __shared__ int order[512];
 
-  const int M = (m + 1) & ~1;   // even player count; index m (if m odd) is a dummy
-  double* A = use_smem ? reinterpret_cast<double*>(smem_raw) : gA;
+  double* U = use_smem ? reinterpret_cast<double*>(smem_raw) : gU;
   double* V = use_smem ? reinterpret_cast<double*>(smem_raw) + (size_t)m * m : gV;
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
 
   if (tid == 0) degenerate = 0;
   __syncthreads();
-  // Omega and V = I; degenerate-landmark check (nystrom.py:145-146)
-  for (int e = tid; e < m * m; e += nt) {
+  for (int e = tid; e < m * m; e += nt) {   // Omega symmetric: row- = column-major
     int i = e / m, j = e % m;
     double d = lm[i] - lm[j];
-    A[e] = nys::rbf(d, sigma2);
+    U[e] = nys::rbf(d, sigma2);
     V[e] = (i == j) ? 1.0 : 0.0;
     if (i != j && fabs(d) <= 1e-12) degenerate = 1;
   }
@@ -62,13 +59,12 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     return;
   }
 
+  const int M = (m + 1) & ~1;
   const int half = M / 2;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
-    if (tid == 0) changed = 0;
-    __syncthreads();
+    int rotated = 0;
     for (int r = 0; r < M - 1; ++r) {
-      // (1) rotation parameters for the m/2 disjoint pairs of round r
-      for (int k = tid; k < half; k += nt) {
+      for (int k = warp; k < half; k += nwarps) {
         int p, q;
         if (k == 0) {
           p = M - 1;
@@ -82,89 +78,80 @@ __global__ void __launch_bounds__(kEigThreads, 1)
           p = q;
           q = t;
         }
-        double c = 1.0, s = 0.0;
-        if (q < m) {
-          double apq = A[p * m + q];
-          double app = A[p * m + p], aqq = A[q * m + q];
-          if (fabs(apq) > 1e-300 && fabs(apq) > 2.220446049250313e-16 * sqrt(fabs(app * aqq))) {
-            double tau = (aqq - app) / (2.0 * apq);
-            double t;
-            if (fabs(tau) > 1e150)
-              t = 0.5 / tau;
-            else
-              t = copysign(1.0, tau) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-            changed = 1;
-          }
+        if (q >= m) continue;   // dummy player (odd m)
+        double* up = U + (size_t)p * m;
+        double* uq = U + (size_t)q * m;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          double a = up[i], b = uq[i];
+          al = fma(a, a, al);
+          be = fma(b, b, be);
+          ga = fma(a, b, ga);
         }
-        rots[k] = Rot{p, q, c, s};
-      }
-      __syncthreads();
-      // (2) column update A <- A J, V <- V J
-      for (int e = tid; e < half * m; e += nt) {
-        int k = e / m, i = e % m;
-        Rot R = rots[k];
-        if (R.s == 0.0) continue;
-        double ap = A[i * m + R.p], aq = A[i * m + R.q];
-        A[i * m + R.p] = R.c * ap - R.s * aq;
-        A[i * m + R.q] = R.s * ap + R.c * aq;
-        double vp = V[i * m + R.p], vq = V[i * m + R.q];
-        V[i * m + R.p] = R.c * vp - R.s * vq;
-        V[i * m + R.q] = R.s * vp + R.c * vq;
-      }
-      __syncthreads();
-      // (3) row update A <- J^T A
-      for (int e = tid; e < half * m; e += nt) {
-        int k = e / m, j = e % m;
-        Rot R = rots[k];
-        if (R.s == 0.0) continue;
-        double ap = A[R.p * m + j], aq = A[R.q * m + j];
-        A[R.p * m + j] = R.c * ap - R.s * aq;
-        A[R.q * m + j] = R.s * ap + R.c * aq;
-      }
-      __syncthreads();
-      for (int k = tid; k < half; k += nt) {
-        Rot R = rots[k];
-        if (R.s != 0.0) {
-          A[R.p * m + R.q] = 0.0;
-          A[R.q * m + R.p] = 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (fabs(ga) > 1e-300 && fabs(ga) > 2.220446049250313e-16 * sqrt(al * be)) {
+          double zeta = (be - al) / (2.0 * ga);
+          double t = fabs(zeta) > 1e150 ? 0.5 / zeta
+                                        : copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+          double* vp = V + (size_t)p * m;
+          double* vq = V + (size_t)q * m;
+          for (int i = lane; i < m; i += 32) {
+            double a = up[i], b = uq[i];
+            up[i] = c * a - s * b;
+            uq[i] = s * a + c * b;
+            double x = vp[i], y = vq[i];
+            vp[i] = c * x - s * y;
+            vq[i] = s * x + c * y;
+          }
+          rotated = 1;
         }
       }
       __syncthreads();
     }
-    if (!changed) break;
-    __syncthreads();
+    if (!__syncthreads_or(rotated)) break;
   }
 
-  // sort descending (stable on index, like argsort(...)[::-1] up to ties)
-  for (int i = tid; i < m; i += nt) diag[i] = A[i * m + i];
+  // lambda_i = v_i . u_i
+  for (int i = warp; i < m; i += nwarps) {
+    double acc = 0.0;
+    for (int r = lane; r < m; r += 32) acc = fma(V[(size_t)i * m + r], U[(size_t)i * m + r], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) lam[i] = acc;
+  }
   __syncthreads();
+  // descending order; ties: higher index first (argsort(...)[::-1] in nystrom.py:151)
   for (int i = tid; i < m; i += nt) {
-    double di = diag[i];
+    double di = lam[i];
     int rank = 0;
     for (int j = 0; j < m; ++j) {
-      double dj = diag[j];
+      double dj = lam[j];
       rank += (dj > di) || (dj == di && j > i);
     }
     order[rank] = i;
   }
   __syncthreads();
-  const double s0 = diag[order[0]];
+  const double s0 = lam[order[0]];
   const double cut = fmax(drop_tol * s0, 0.0);
-  for (int k = tid; k < m; k += nt) eigvals[k] = diag[order[k]];
+  for (int k = tid; k < m; k += nt) eigvals[k] = lam[order[k]];
   if (tid == 0) {
     int me = 0;
-    while (me < m && diag[order[me]] > cut) ++me;
+    while (me < m && lam[order[me]] > cut) ++me;
     *m_eff_out = me;
     *info = NYS_INFO_OK;
   }
   for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, k = e % m;
+    int i = e / m, k = e % m;   // output row-major: row i, column k
     int src = order[k];
-    double v = V[i * m + src];
+    double v = V[(size_t)src * m + i];
     eigvecs[e] = v;
-    double sk = diag[src];
+    double sk = lam[src];
     Wout[e] = (sk > cut) ? v / sqrt(sk) : 0.0;
   }
 }
@@ -189,7 +176,7 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
   size_t dyn = 0;
   if (use_smem) {
     dyn = need;
-    cudaError_t e = cudaFuncSetAttribute(jacobi_eig_kernel,
+    cudaError_t e = cudaFuncSetAttribute(hestenes_eig_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return nys_host::record_cuda(e);
   } else {
@@ -197,8 +184,10 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
     gA = static_cast<double*>(workspace);
     gV = gA + (size_t)m * m;
   }
-  int threads = m <= 32 ? 256 : kEigThreads;
-  jacobi_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
+  int threads = 32 * ((m + 1) / 2);   // one warp per column pair of a round
+  if (threads > kEigThreads) threads = kEigThreads;
+  if (threads < 64) threads = 64;
+  hestenes_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
       landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gV, use_smem);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();

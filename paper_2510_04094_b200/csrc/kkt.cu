@@ -237,6 +237,170 @@ __global__ void __launch_bounds__(kKktThreads)
   if (tid == 0) info[b] = nonfinite ? NYS_INFO_NONFINITE : NYS_INFO_OK;
 }
 
+// Warp-per-system variant for small sides (configs 0-3: n <= 96).  The LU lives
+// in shared memory (one n x n slice per warp), synchronisation is __syncwarp
+// only, and the refinement residual re-reads M's entries from the Gram source
+// instead of keeping a second copy (twice the systems per SM).
+constexpr int kWarpKktMaxN = 96;
+constexpr int kWarpKktWarps = 1;   // 1 warp per CTA: up to 6 systems per SM at n = 67
+
+template <typename Src>
+NYS_DEV double kkt_entry(const Src& src, int b, int i, int j, int me, double inv_gamma,
+                         const double* Ac, const double* beta) {
+  if (i < me && j < me) {
+    double v = src.E(b, i, j);
+    return i == j ? inv_gamma + v : v;
+  }
+  if (i < me && j == me) return src.E(b, i, me);
+  if (i == me && j < me) return src.E(b, j, me);
+  if (i == me && j == me) return src.E(b, me, me);
+  if (i < me) return Ac[(size_t)(j - me - 1) * me + i];
+  if (j < me) return Ac[(size_t)(i - me - 1) * me + j];
+  if (i == me) return beta[j - me - 1];
+  if (j == me) return beta[i - me - 1];
+  return 0.0;
+}
+
+template <typename Src>
+__global__ void __launch_bounds__(kWarpKktWarps * 32)
+    kkt_warp_kernel(Src src, int m_eff, int ncond, const double* __restrict__ Ac,
+                    const double* __restrict__ beta, const double* __restrict__ values,
+                    double gamma, int B, double* __restrict__ xout, int* __restrict__ info,
+                    double* __restrict__ Mout, double* __restrict__ rhsout) {
+  extern __shared__ __align__(16) double dsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * kWarpKktWarps + warp;
+  if (b >= B) return;
+  const int n = m_eff + 1 + ncond, me = m_eff;
+  const size_t per = (size_t)n * n + 4 * (size_t)n;
+  double* LU = dsm + warp * per;
+  double* rhs0 = LU + (size_t)n * n;
+  double* xs = rhs0 + n;
+  double* rs = xs + n;
+  int* perm = reinterpret_cast<int*>(rs + n);
+  const double inv_gamma = 1.0 / gamma;
+
+  for (int e = lane; e < n * n; e += 32) {
+    int i = e / n, j = e % n;
+    double v = kkt_entry(src, b, i, j, me, inv_gamma, Ac, beta);
+    LU[e] = v;
+    if (Mout) Mout[(size_t)b * n * n + e] = v;
+  }
+  for (int i = lane; i < n; i += 32) {
+    double v = i < me ? src.E(b, i, me + 1)
+                      : (i == me ? src.E(b, me, me + 1) : values[(size_t)b * ncond + (i - me - 1)]);
+    rhs0[i] = v;
+    if (rhsout) rhsout[(size_t)b * n + i] = v;
+  }
+  __syncwarp();
+
+  int bad = 0;
+  for (int k = 0; k < n; ++k) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = k + lane; i < n; i += 32) {
+      double a = fabs(LU[(size_t)i * n + k]);
+      if (a > bv) {
+        bv = a;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (!(bv > 0.0)) {
+      bad = 1;
+      break;
+    }
+    if (lane == 0) perm[k] = bi;
+    if (bi != k)
+      for (int j = lane; j < n; j += 32) {
+        double t = LU[(size_t)k * n + j];
+        LU[(size_t)k * n + j] = LU[(size_t)bi * n + j];
+        LU[(size_t)bi * n + j] = t;
+      }
+    __syncwarp();
+    const double pivot = LU[(size_t)k * n + k];
+    for (int i = k + 1 + lane; i < n; i += 32) LU[(size_t)i * n + k] /= pivot;
+    __syncwarp();
+    // trailing update, lanes over columns; the pivot row stays in registers
+    double urow[(kWarpKktMaxN + 31) / 32];
+#pragma unroll
+    for (int c = 0; c < (kWarpKktMaxN + 31) / 32; ++c) {
+      int j = k + 1 + lane + 32 * c;
+      urow[c] = j < n ? LU[(size_t)k * n + j] : 0.0;
+    }
+    for (int i = k + 1; i < n; ++i) {
+      const double l = LU[(size_t)i * n + k];
+#pragma unroll
+      for (int c = 0; c < (kWarpKktMaxN + 31) / 32; ++c) {
+        int j = k + 1 + lane + 32 * c;
+        if (j < n) LU[(size_t)i * n + j] -= l * urow[c];
+      }
+    }
+    __syncwarp();
+  }
+  if (bad) {
+    if (lane == 0) info[b] = NYS_INFO_SINGULAR;
+    for (int i = lane; i < n; i += 32) xout[(size_t)b * n + i] = NAN;
+    return;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = lane; i < n; i += 32) {
+      double v = rhs0[i];
+      if (pass == 1) {
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) acc += kkt_entry(src, b, i, j, me, inv_gamma, Ac, beta) * xs[j];
+        v = v - acc;
+      }
+      rs[i] = v;
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int k = 0; k < n; ++k) {
+        int pr = perm[k];
+        if (pr != k) {
+          double t = rs[k];
+          rs[k] = rs[pr];
+          rs[pr] = t;
+        }
+      }
+    __syncwarp();
+    for (int i = 1; i < n; ++i) {
+      double acc = 0.0;
+      for (int j = lane; j < i; j += 32) acc += LU[(size_t)i * n + j] * rs[j];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) rs[i] -= acc;
+      __syncwarp();
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int j = i + 1 + lane; j < n; j += 32) acc += LU[(size_t)i * n + j] * rs[j];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) rs[i] = (rs[i] - acc) / LU[(size_t)i * n + i];
+      __syncwarp();
+    }
+    for (int i = lane; i < n; i += 32) xs[i] = pass == 0 ? rs[i] : xs[i] + rs[i];
+    __syncwarp();
+  }
+  int nonfinite = 0;
+  for (int i = lane; i < n; i += 32) {
+    double v = xs[i];
+    if (!isfinite(v)) nonfinite = 1;
+    xout[(size_t)b * n + i] = v;
+  }
+  nonfinite = __any_sync(0xffffffffu, nonfinite);
+  if (lane == 0) info[b] = nonfinite ? NYS_INFO_NONFINITE : NYS_INFO_OK;
+}
+
 size_t kkt_smem_bytes(int n) { return (2 * (size_t)n * n + 4 * (size_t)n) * sizeof(double); }
 constexpr size_t kKktSmemMax = 200 * 1024;
 
@@ -245,6 +409,19 @@ int launch_kkt(Src src, int m_eff, int ncond, const double* Ac, const double* be
                const double* values, double gamma, int B, double* x, int* info, double* M,
                double* rhs, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int n = m_eff + 1 + ncond;
+  if (n <= kWarpKktMaxN) {
+    auto wk = kkt_warp_kernel<Src>;
+    size_t dyn = kWarpKktWarps * ((size_t)n * n + 4 * (size_t)n) * sizeof(double);
+    if (dyn > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(wk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return nys_host::record_cuda(e);
+    }
+    wk<<<(B + kWarpKktWarps - 1) / kWarpKktWarps, kWarpKktWarps * 32, dyn, st>>>(
+        src, m_eff, ncond, Ac, beta, values, gamma, B, x, info, M, rhs);
+    nys_host::count_launches(1);
+    NYS_CHECK_LAUNCH();
+    return NYS_OK;
+  }
   size_t per = kkt_smem_bytes(n);
   int use_smem = per <= kKktSmemMax;
   size_t dyn = use_smem ? per : 0;

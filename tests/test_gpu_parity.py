@@ -63,8 +63,11 @@ def test_fused_gram_matches_oracle_same_basis(name):
                      kind=str(g["kind"]))
     Dx = np.column_stack([osy["D"], osy["g"], osy["r"]])
     Eo = Dx.T @ Dx
-    scale = np.maximum(np.abs(Dx).max(axis=0), 1e-300)
-    rel = np.abs(E - Eo) / (np.outer(scale, scale) * Dx.shape[0])
+    scale = np.abs(Dx).max(axis=0)
+    den = np.outer(scale, scale) * Dx.shape[0]
+    err = np.abs(E - Eo)
+    assert np.all(err[den == 0] == 0)
+    rel = err[den > 0] / den[den > 0]
     assert rel.max() <= 1e-9
     # the assembled KKT matrix (linear.py:123-133 layout) equals the oracle's
     M = sy.matrix
