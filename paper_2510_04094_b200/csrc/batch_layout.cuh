@@ -53,13 +53,19 @@ struct BatchLayout {
   int rows_pad() const { return nks_pad * 4; }
   size_t psi_doubles() const { return (size_t)nks_pad * NO * NB * 32; }
   size_t part_doubles() const { return (size_t)nsplit * B * npair * 64; }
-  size_t ws_bytes() const { return (psi_doubles() + part_doubles()) * sizeof(double) + 256; }
+  int Pe() const { return m_eff + 2; }
+  size_t e_doubles() const { return (size_t)B * Pe() * Pe(); }
+  size_t ws_bytes() const {
+    return (psi_doubles() + part_doubles() + e_doubles()) * sizeof(double) + 256;
+  }
   double* psi(void* ws) const {
     size_t a = (reinterpret_cast<size_t>(ws) + 127) & ~(size_t)127;
     return reinterpret_cast<double*>(a);
   }
   double* part(void* ws) const { return psi(ws) + psi_doubles(); }
   const double* part(const void* ws) const { return psi(const_cast<void*>(ws)) + psi_doubles(); }
+  // dense extended Grams (B x Pe x Pe), filled by the unpack kernel
+  double* dense(void* ws) const { return part(ws) + part_doubles(); }
 };
 
 }  // namespace nys

@@ -61,6 +61,19 @@ __global__ void __launch_bounds__(kEigThreads, 1)
 
   const int M = (m + 1) & ~1;
   const int half = M / 2;
+  // ||Omega||_F^2 (warp 0) for the noise floor
+  __shared__ double fro2_s;
+  if (warp == 0) {
+    double acc = 0.0;
+    for (int e = lane; e < m * m; e += 32) acc = fma(U[e], U[e], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) fro2_s = acc;
+  }
+  __syncthreads();
+  const double eps = 2.220446049250313e-16;
+  const double tol_rel = sqrt((double)m) * eps;
+  const double noise2 = (eps * eps * fro2_s) * (eps * eps * fro2_s);
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < M - 1; ++r) {
@@ -94,7 +107,9 @@ __global__ void __launch_bounds__(kEigThreads, 1)
           be += __shfl_xor_sync(0xffffffffu, be, o);
           ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        if (fabs(ga) > 1e-300 && fabs(ga) > 2.220446049250313e-16 * sqrt(al * be)) {
+        // LAPACK dgesvj-style stopping rule: columns orthogonal to sqrt(m) eps,
+        // and pairs of noise-level columns (norm < eps ||Omega||_F) left alone
+        if (fabs(ga) > tol_rel * sqrt(al * be) && al * be > noise2) {
           double zeta = (be - al) / (2.0 * ga);
           double t = fabs(zeta) > 1e150 ? 0.5 / zeta
                                         : copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));

@@ -162,6 +162,20 @@ __global__ void batch_unpack_kernel(const double* __restrict__ part, int nsplit,
   }
 }
 
+}  // namespace
+
+namespace nys_host {
+int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, double* gram,
+                        cudaStream_t st) {
+  batch_unpack_kernel<<<B, 256, 0, st>>>(part, nsplit, B, NB, Pe, gram);
+  count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+}  // namespace nys_host
+
+namespace {
+
 template <int NB, int NO>
 int launch_gram(const double* psi, const double* coef, const double* forcing, int n_c, int B,
                 const BatchLayout& L, double* part, cudaStream_t st) {
