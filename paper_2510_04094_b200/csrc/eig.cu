@@ -73,9 +73,13 @@ __global__ void __launch_bounds__(kEigThreads, 1)
   __syncthreads();
   const double eps = 2.220446049250313e-16;
   const double tol_rel = sqrt((double)m) * eps;
-  const double noise2 = (eps * eps * fro2_s) * (eps * eps * fro2_s);
+  // noise floor: columns with |u| < m eps ||Omega||_F carry no direction information
+  const double nf = (double)m * eps * sqrt(fro2_s);
+  const double noise2 = (nf * nf) * (nf * nf);
+  int sweeps = 0;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     int rotated = 0;
+    ++sweeps;
     for (int r = 0; r < M - 1; ++r) {
       for (int k = warp; k < half; k += nwarps) {
         int p, q;
@@ -159,7 +163,7 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     int me = 0;
     while (me < m && lam[order[me]] > cut) ++me;
     *m_eff_out = me;
-    *info = NYS_INFO_OK;
+    *info = NYS_INFO_OK | (sweeps << 8);   // bits 8+: Jacobi sweeps (diagnostic)
   }
   for (int e = tid; e < m * m; e += nt) {
     int i = e / m, k = e % m;   // output row-major: row i, column k

@@ -64,12 +64,36 @@ __global__ void __launch_bounds__(32)
   int* perm = reinterpret_cast<int*>(xs + n);
   const double inv_gamma = 1.0 / gamma;
 
-  for (int i = 0; i < n; ++i)
+  // E block (rows/cols 0..me) in batches of 8 rows so 8 loads per lane are in flight
+  for (int i0 = 0; i0 <= me; i0 += 8) {
+    double v[8][kNC];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        int i = i0 + r, j = lane + 32 * c;
+        v[r][c] = (i <= me && j <= me) ? __ldg(E + (size_t)i * Pe + j) : 0.0;
+      }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        int i = i0 + r, j = lane + 32 * c;
+        if (i <= me && j <= me) LU[(size_t)i * n + j] = (i == j && i < me) ? inv_gamma + v[r][c] : v[r][c];
+      }
+  }
+  // condition rows / columns (linear.py:127-130) and the zero block
+  for (int mu = 0; mu < ncond; ++mu) {
+    const int row = me + 1 + mu;
     for (int j = lane; j < n; j += 32) {
-      double v = m_entry(E, Pe, i, j, me, inv_gamma, Ac, beta);
-      LU[(size_t)i * n + j] = v;
-      if (Mout) Mout[(size_t)b * n * n + (size_t)i * n + j] = v;
+      double v = j < me ? Ac[(size_t)mu * me + j] : (j == me ? beta[mu] : 0.0);
+      LU[(size_t)row * n + j] = v;
+      if (j <= me) LU[(size_t)j * n + row] = v;
     }
+  }
+  __syncwarp();
+  if (Mout)
+    for (int e = lane; e < n * n; e += 32) Mout[(size_t)b * n * n + e] = LU[e];
   if (rhsout)
     for (int i = lane; i < n; i += 32) rhsout[(size_t)b * n + i] = rhs_entry(E, Pe, i, me, vals);
   __syncwarp();
@@ -168,16 +192,45 @@ __global__ void __launch_bounds__(32)
     if (pass == 0) {
       for (int i = lane; i < n; i += 32) ys[i] = rhs_entry(E, Pe, i, me, vals);
     } else {
-      // ys = rhs - M x ; M symmetric: column i of M = row i of M
+      // ys = rhs - M x ; M symmetric: column i of M = row i of M (coalesced rows of E)
       double acc[kNC];
 #pragma unroll
       for (int c = 0; c < kNC; ++c) acc[c] = 0.0;
-      for (int j = 0; j < n; ++j) {
-        const double xj = xs[j];
+      for (int j0 = 0; j0 <= me; j0 += 8) {
+        double v[8][kNC], xj[8];
 #pragma unroll
-        for (int c = 0; c < kNC; ++c) {
-          int i = lane + 32 * c;
-          if (i < n) acc[c] += m_entry(E, Pe, j, i, me, inv_gamma, Ac, beta) * xj;
+        for (int r = 0; r < 8; ++r) {
+          int j = j0 + r;
+          xj[r] = j <= me ? xs[j] : 0.0;
+#pragma unroll
+          for (int c = 0; c < kNC; ++c) {
+            int i = lane + 32 * c;
+            v[r][c] = (j <= me && i <= me) ? __ldg(E + (size_t)j * Pe + i) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < kNC; ++c) {
+            int i = lane + 32 * c, j = j0 + r;
+            double mv = (i == j && i < me) ? inv_gamma + v[r][c] : v[r][c];
+            acc[c] += mv * xj[r];
+          }
+      }
+      // condition couplings: rows/cols me+1.. of M
+#pragma unroll
+      for (int c = 0; c < kNC; ++c) {
+        int i = lane + 32 * c;
+        if (i < n) {
+          if (i <= me) {
+            for (int mu = 0; mu < ncond; ++mu)
+              acc[c] += (i < me ? Ac[(size_t)mu * me + i] : beta[mu]) * xs[me + 1 + mu];
+          } else {
+            const int mu = i - me - 1;
+            double a2 = 0.0;
+            for (int j = 0; j < me; ++j) a2 += Ac[(size_t)mu * me + j] * xs[j];
+            acc[c] = a2 + beta[mu] * xs[me];
+          }
         }
       }
 #pragma unroll

@@ -146,7 +146,10 @@ def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TO
               _lib.ptr(s), _lib.ptr(V), _lib.ptr(W), _lib.ptr(meta), _lib.ptr(meta) + 4,
               _lib.ptr(ws), wsb, _lib.stream_ptr())
     m_eff, info = (int(v) for v in meta.cpu())
+    sweeps, info = info >> 8, info & 0xFF      # bits 8+: Jacobi sweeps (diagnostic)
     if info == _lib.INFO_DEGENERATE:
         raise DegenerateLandmarksError("two landmarks coincide within 1e-12")
-    return NystromFeatureMap(kernel=k, landmarks=landmarks, m_eff=m_eff, device=device,
-                             d_landmarks=d_lm, d_W=W, d_eigvals=s, d_eigvecs=V)
+    fm = NystromFeatureMap(kernel=k, landmarks=landmarks, m_eff=m_eff, device=device,
+                           d_landmarks=d_lm, d_W=W, d_eigvals=s, d_eigvecs=V)
+    fm._host["sweeps"] = sweeps
+    return fm
