@@ -17,18 +17,16 @@ namespace {
 
 constexpr int kEigThreads = 1024;
 constexpr int kMaxSweeps = 60;
+constexpr int kTPP = 8;                 // threads per rotation pair
+constexpr int kMaxPairsPerGroup = 2;    // m <= 2 * (1024 / kTPP) * 2 = 512
 
-struct Rot {
-  int p, q;
-  double c, s;
-};
 
 // Two-sided cyclic Jacobi, round-robin ("circle") ordering: m/2 disjoint
 // rotations per round, each round = (1) rotation parameters, (2) column update
 // of A, (3) row update of A and of V^T (stored row-major, so both row updates
 // are contiguous).  A uses an odd row stride (m+1) so the column update is
 // bank-conflict free.  Stopping rule: a pair is rotated while |a_pq| exceeds
-// eps ||A||_F / m (LAPACK-level backward error; a relative rule would chase the
+// eps ||A||_F (LAPACK-level backward error; a relative rule would chase the
 // rounding noise of the ~1e-16 s_0 eigenvalues forever).
 __global__ void __launch_bounds__(kEigThreads, 1)
     jacobi_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
@@ -37,8 +35,6 @@ __global__ void __launch_bounds__(kEigThreads, 1)
                       int* __restrict__ info, double* __restrict__ gA, double* __restrict__ gV,
                       int use_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Rot rots[256];
-  __shared__ int changed;
   __shared__ int degenerate;
   __shared__ double diag[512];
   __shared__ int order[512];
@@ -65,7 +61,14 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     if (i != j && fabs(d) <= 1e-12) degenerate = 1;
   }
   for (int o = 16; o; o >>= 1) fro_local += __shfl_xor_sync(0xffffffffu, fro_local, o);
-  if ((tid & 31) == 0) atomicAdd(&fro2_s, fro_local);
+  __shared__ double fro_parts[kEigThreads / 32];
+  if ((tid & 31) == 0) fro_parts[tid >> 5] = fro_local;
+  __syncthreads();
+  if (tid == 0) {   // fixed-order sum: the tolerance (and so the result) is deterministic
+    double acc = 0.0;
+    for (int w = 0; w < nt / 32; ++w) acc += fro_parts[w];
+    fro2_s = acc;
+  }
   __syncthreads();
   if (degenerate) {
     if (tid == 0) {
@@ -74,85 +77,100 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     }
     return;
   }
-  const double tol = 2.220446049250313e-16 * sqrt(fro2_s) / (double)m;
+  const double tol = 2.220446049250313e-16 * sqrt(fro2_s);
 
   const int M = (m + 1) & ~1;
   const int half = M / 2;
+  // kTPP threads own one pair: they compute its rotation redundantly (a pair's
+  // parameters live in its own two columns, which no other pair of the round
+  // touches, so no barrier is needed before the column update) and split its
+  // rows/columns.  Two barriers per round.
+  const int grp = tid / kTPP, gl = tid % kTPP, ngrp = nt / kTPP;
   int sweeps = 0;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     ++sweeps;
-    if (tid == 0) changed = 0;
-    __syncthreads();
+    int rotated = 0;
     for (int r = 0; r < M - 1; ++r) {
-      for (int k = tid; k < half; k += nt) {
-        int p, q;
-        if (k == 0) {
-          p = M - 1;
-          q = r;
-        } else {
-          p = (r + k) % (M - 1);
-          q = (r - k + (M - 1)) % (M - 1);
-        }
-        if (p > q) {
-          int t = p;
-          p = q;
-          q = t;
-        }
+      int pp[kMaxPairsPerGroup], qq[kMaxPairsPerGroup];
+      double cc[kMaxPairsPerGroup], ss[kMaxPairsPerGroup];
+#pragma unroll
+      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
+        const int k = grp + u * ngrp;
+        int p = -1, q = -1;
         double c = 1.0, s = 0.0;
-        if (q < m) {
-          const double apq = A[(size_t)p * lda + q];
-          if (fabs(apq) > tol) {
-            const double app = A[(size_t)p * lda + p], aqq = A[(size_t)q * lda + q];
-            const double tau = (aqq - app) / (2.0 * apq);
-            const double t = fabs(tau) > 1e150
-                                 ? 0.5 / tau
-                                 : copysign(1.0, tau) / (fabs(tau) + sqrt(1.0 + tau * tau));
-            c = rsqrt(1.0 + t * t);
-            s = t * c;
-            changed = 1;
+        if (k < half) {
+          if (k == 0) {
+            p = M - 1;
+            q = r;
+          } else {
+            p = r + k;
+            if (p >= M - 1) p -= M - 1;
+            q = r - k;
+            if (q < 0) q += M - 1;
+          }
+          if (p > q) {
+            int t = p;
+            p = q;
+            q = t;
+          }
+          if (q < m) {
+            const double apq = A[(size_t)p * lda + q];
+            if (fabs(apq) > tol) {
+              const double app = A[(size_t)p * lda + p], aqq = A[(size_t)q * lda + q];
+              const double tau = (aqq - app) / (2.0 * apq);
+              const double t = fabs(tau) > 1e150
+                                   ? 0.5 / tau
+                                   : copysign(1.0, tau) / (fabs(tau) + sqrt(1.0 + tau * tau));
+              c = rsqrt(1.0 + t * t);
+              s = t * c;
+              rotated = 1;
+            }
           }
         }
-        rots[k] = Rot{p, q, c, s};
+        pp[u] = p;
+        qq[u] = q;
+        cc[u] = c;
+        ss[u] = s;
       }
-      __syncthreads();
-      // (2) A <- A J  (columns p, q of every row)
-      for (int e = tid; e < half * m; e += nt) {
-        const int k = e / m, i = e % m;
-        const Rot R = rots[k];
-        if (R.s == 0.0) continue;
-        double* row = A + (size_t)i * lda;
-        const double ap = row[R.p], aq = row[R.q];
-        row[R.p] = R.c * ap - R.s * aq;
-        row[R.q] = R.s * ap + R.c * aq;
-      }
-      __syncthreads();
-      // (3) A <- J^T A and V^T <- J^T V^T  (rows p, q)
-      for (int e = tid; e < half * m; e += nt) {
-        const int k = e / m, j = e % m;
-        const Rot R = rots[k];
-        if (R.s == 0.0) continue;
-        double* rp = A + (size_t)R.p * lda;
-        double* rq = A + (size_t)R.q * lda;
-        const double ap = rp[j], aq = rq[j];
-        rp[j] = R.c * ap - R.s * aq;
-        rq[j] = R.s * ap + R.c * aq;
-        double* vp = VT + (size_t)R.p * m;
-        double* vq = VT + (size_t)R.q * m;
-        const double x = vp[j], y = vq[j];
-        vp[j] = R.c * x - R.s * y;
-        vq[j] = R.s * x + R.c * y;
-      }
-      __syncthreads();
-      for (int k = tid; k < half; k += nt) {
-        const Rot R = rots[k];
-        if (R.s != 0.0) {
-          A[(size_t)R.p * lda + R.q] = 0.0;
-          A[(size_t)R.q * lda + R.p] = 0.0;
+      // (2) A <- A J: columns p, q of every row
+#pragma unroll
+      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
+        if (ss[u] == 0.0) continue;
+        for (int i = gl; i < m; i += kTPP) {
+          double* row = A + (size_t)i * lda;
+          const double ap = row[pp[u]], aq = row[qq[u]];
+          row[pp[u]] = cc[u] * ap - ss[u] * aq;
+          row[qq[u]] = ss[u] * ap + cc[u] * aq;
         }
       }
       __syncthreads();
+      // (3) A <- J^T A, V^T <- J^T V^T: rows p, q
+#pragma unroll
+      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
+        if (ss[u] == 0.0) continue;
+        double* rp = A + (size_t)pp[u] * lda;
+        double* rq = A + (size_t)qq[u] * lda;
+        double* vp = VT + (size_t)pp[u] * m;
+        double* vq = VT + (size_t)qq[u] * m;
+        for (int j = gl; j < m; j += kTPP) {
+          const double ap = rp[j], aq = rq[j];
+          rp[j] = cc[u] * ap - ss[u] * aq;
+          rq[j] = ss[u] * ap + cc[u] * aq;
+          const double x = vp[j], y = vq[j];
+          vp[j] = cc[u] * x - ss[u] * y;
+          vq[j] = ss[u] * x + cc[u] * y;
+        }
+      }
+      __syncwarp();   // the kTPP threads of a group share a warp
+#pragma unroll
+      for (int u = 0; u < kMaxPairsPerGroup; ++u)
+        if (ss[u] != 0.0 && gl == 0) {
+          A[(size_t)pp[u] * lda + qq[u]] = 0.0;
+          A[(size_t)qq[u] * lda + pp[u]] = 0.0;
+        }
+      __syncthreads();
     }
-    if (!changed) break;
+    if (!__syncthreads_or(rotated)) break;
   }
 
   for (int i = tid; i < m; i += nt) diag[i] = A[(size_t)i * lda + i];
@@ -215,7 +233,10 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
     gA = static_cast<double*>(workspace);
     gV = gA + (size_t)m * (m + 1);
   }
-  int threads = m <= 64 ? 256 : (m <= 128 ? 512 : kEigThreads);
+  int pairs = (m + 1) / 2;
+  int threads = pairs * kTPP;
+  if (threads > kEigThreads) threads = kEigThreads;   // groups then take 2 pairs each
+  threads = (threads + 31) / 32 * 32;
   jacobi_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
       landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gV, use_smem);
   nys_host::count_launches(1);
