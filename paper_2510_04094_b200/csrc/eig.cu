@@ -1,14 +1,21 @@
-// Landmark eigendecomposition on device: Omega = K(L, L), cyclic parallel
-// Jacobi, descending sort, drop rule and W = V / sqrt(s).
+// Landmark eigendecomposition on device: Omega = K(L, L) -> Householder
+// tridiagonalisation -> implicit QL with Wilkinson-type shifts -> descending
+// sort, drop rule and W = V / sqrt(s).
 // Replaces nystrom.build_feature_map (nystrom.py:136-160) and
-// NystromFeatureMap._scaled_vectors (nystrom.py:120-121); LAPACK dsyevd in the
-// reference.  Any symmetric eigensolver is parity-safe here (SURVEY.md §0,
-// A1: <= 6.5e-8 on y_hat even when m_eff shifts), and the configs use sigma
-// where the problem is eigensolver-insensitive (workloads.py).
+// NystromFeatureMap._scaled_vectors (nystrom.py:120-121); the reference calls
+// LAPACK dsyevd (tridiagonal + divide and conquer).  This is the tridiagonal +
+// QL route of LAPACK dsyev: backward error ~eps ||Omega||, like the reference.
+// Any accurate symmetric eigensolver is parity-safe.
 //
-// One CTA per landmark set, two-sided Jacobi (see the kernel comment).  A and
-// V^T live in shared memory when they fit (m <= 112), otherwise in the
-// caller's workspace (L2-resident).
+// One CTA per landmark set.
+//   phase 1  A <- Q^T A Q, tridiagonal (d, e); Householder vectors kept in A
+//   phase 2  Z^T = Q^T accumulated backwards
+//   phase 3  QL: one thread generates each sweep's Givens rotations (serial by
+//            nature); all threads apply the sweep to their row of Z (column-major
+//            Z^T, so a sweep streams down contiguous rows: conflict-free)
+//   phase 4  sort, drop, W
+// A and Z^T live in shared memory when they fit (m <= 112), otherwise in the
+// caller's workspace (L2-resident, config 4: m = 256).
 #include <cmath>
 
 #include "common.cuh"
@@ -16,229 +23,289 @@
 namespace {
 
 constexpr int kEigThreads = 1024;
-constexpr int kMaxSweeps = 60;
-constexpr int kTPP = 8;                 // threads per rotation pair
-constexpr int kMaxPairsPerGroup = 2;    // m <= 2 * (1024 / kTPP) * 2 = 512
+constexpr int kMaxM = 512;
+constexpr int kMaxQlIters = 60;   // per eigenvalue
 
+struct Shared {
+  double d[kMaxM], e[kMaxM], beta[kMaxM], v[kMaxM], p[kMaxM];
+  double rc[kMaxM], rs[kMaxM];
+  int order[kMaxM];
+  double red[kEigThreads / 32];
+  int ibcast[4];
+  int degenerate;
+};
 
-// Two-sided cyclic Jacobi, round-robin ("circle") ordering: m/2 disjoint
-// rotations per round, each round = (1) rotation parameters, (2) column update
-// of A, (3) row update of A and of V^T (stored row-major, so both row updates
-// are contiguous).  A uses an odd row stride (m+1) so the column update is
-// bank-conflict free.  Stopping rule: a pair is rotated while |a_pq| exceeds
-// eps ||A||_F (LAPACK-level backward error; a relative rule would chase the
-// rounding noise of the ~1e-16 s_0 eigenvalues forever).
+NYS_DEV double block_sum(double x, Shared& S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if (lane == 0) S.red[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += S.red[i];   // fixed order: deterministic
+  return s;
+}
+
 __global__ void __launch_bounds__(kEigThreads, 1)
-    jacobi_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
-                      double* __restrict__ eigvals, double* __restrict__ eigvecs,
-                      double* __restrict__ Wout, int* __restrict__ m_eff_out,
-                      int* __restrict__ info, double* __restrict__ gA, double* __restrict__ gV,
-                      int use_smem) {
+    tql_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
+                   double* __restrict__ eigvals, double* __restrict__ eigvecs,
+                   double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
+                   double* __restrict__ gA, double* __restrict__ gZ, int use_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int degenerate;
-  __shared__ double diag[512];
-  __shared__ int order[512];
-  __shared__ double fro2_s;
-
-  const int lda = m + 1;
-  double* A = use_smem ? reinterpret_cast<double*>(smem_raw) : gA;                  // m x lda
-  double* VT = use_smem ? reinterpret_cast<double*>(smem_raw) + (size_t)m * lda : gV; // m x m
+  __shared__ Shared S;
+  const int ld = m + 1;
+  double* A = use_smem ? reinterpret_cast<double*>(smem_raw) : gA;                   // m x ld
+  double* ZT = use_smem ? reinterpret_cast<double*>(smem_raw) + (size_t)m * ld : gZ;  // m x ld
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
 
-  if (tid == 0) {
-    degenerate = 0;
-    fro2_s = 0.0;
-  }
+  if (tid == 0) S.degenerate = 0;
   __syncthreads();
-  double fro_local = 0.0;
   for (int e = tid; e < m * m; e += nt) {
-    int i = e / m, j = e % m;
-    double d = lm[i] - lm[j];
-    double v = nys::rbf(d, sigma2);
-    A[(size_t)i * lda + j] = v;
-    VT[e] = (i == j) ? 1.0 : 0.0;
-    fro_local = fma(v, v, fro_local);
-    if (i != j && fabs(d) <= 1e-12) degenerate = 1;
-  }
-  for (int o = 16; o; o >>= 1) fro_local += __shfl_xor_sync(0xffffffffu, fro_local, o);
-  __shared__ double fro_parts[kEigThreads / 32];
-  if ((tid & 31) == 0) fro_parts[tid >> 5] = fro_local;
-  __syncthreads();
-  if (tid == 0) {   // fixed-order sum: the tolerance (and so the result) is deterministic
-    double acc = 0.0;
-    for (int w = 0; w < nt / 32; ++w) acc += fro_parts[w];
-    fro2_s = acc;
+    const int i = e / m, j = e % m;
+    const double d = lm[i] - lm[j];
+    A[(size_t)i * ld + j] = nys::rbf(d, sigma2);   // (Omega + Omega^T)/2 == Omega exactly
+    if (i != j && fabs(d) <= 1e-12) S.degenerate = 1;
   }
   __syncthreads();
-  if (degenerate) {
+  if (S.degenerate) {
     if (tid == 0) {
       *info = NYS_INFO_DEGENERATE;
       *m_eff_out = 0;
     }
     return;
   }
-  const double tol = 2.220446049250313e-16 * sqrt(fro2_s);
 
-  const int M = (m + 1) & ~1;
-  const int half = M / 2;
-  // kTPP threads own one pair: they compute its rotation redundantly (a pair's
-  // parameters live in its own two columns, which no other pair of the round
-  // touches, so no barrier is needed before the column update) and split its
-  // rows/columns.  Two barriers per round.
-  const int grp = tid / kTPP, gl = tid % kTPP, ngrp = nt / kTPP;
-  int sweeps = 0;
-  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
-    ++sweeps;
-    int rotated = 0;
-    for (int r = 0; r < M - 1; ++r) {
-      int pp[kMaxPairsPerGroup], qq[kMaxPairsPerGroup];
-      double cc[kMaxPairsPerGroup], ss[kMaxPairsPerGroup];
-#pragma unroll
-      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
-        const int k = grp + u * ngrp;
-        int p = -1, q = -1;
-        double c = 1.0, s = 0.0;
-        if (k < half) {
-          if (k == 0) {
-            p = M - 1;
-            q = r;
-          } else {
-            p = r + k;
-            if (p >= M - 1) p -= M - 1;
-            q = r - k;
-            if (q < 0) q += M - 1;
-          }
-          if (p > q) {
-            int t = p;
-            p = q;
-            q = t;
-          }
-          if (q < m) {
-            const double apq = A[(size_t)p * lda + q];
-            if (fabs(apq) > tol) {
-              const double app = A[(size_t)p * lda + p], aqq = A[(size_t)q * lda + q];
-              const double tau = (aqq - app) / (2.0 * apq);
-              const double t = fabs(tau) > 1e150
-                                   ? 0.5 / tau
-                                   : copysign(1.0, tau) / (fabs(tau) + sqrt(1.0 + tau * tau));
-              c = rsqrt(1.0 + t * t);
-              s = t * c;
-              rotated = 1;
-            }
-          }
-        }
-        pp[u] = p;
-        qq[u] = q;
-        cc[u] = c;
-        ss[u] = s;
-      }
-      // (2) A <- A J: columns p, q of every row
-#pragma unroll
-      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
-        if (ss[u] == 0.0) continue;
-        for (int i = gl; i < m; i += kTPP) {
-          double* row = A + (size_t)i * lda;
-          const double ap = row[pp[u]], aq = row[qq[u]];
-          row[pp[u]] = cc[u] * ap - ss[u] * aq;
-          row[qq[u]] = ss[u] * ap + cc[u] * aq;
-        }
-      }
-      __syncthreads();
-      // (3) A <- J^T A, V^T <- J^T V^T: rows p, q
-#pragma unroll
-      for (int u = 0; u < kMaxPairsPerGroup; ++u) {
-        if (ss[u] == 0.0) continue;
-        double* rp = A + (size_t)pp[u] * lda;
-        double* rq = A + (size_t)qq[u] * lda;
-        double* vp = VT + (size_t)pp[u] * m;
-        double* vq = VT + (size_t)qq[u] * m;
-        for (int j = gl; j < m; j += kTPP) {
-          const double ap = rp[j], aq = rq[j];
-          rp[j] = cc[u] * ap - ss[u] * aq;
-          rq[j] = ss[u] * ap + cc[u] * aq;
-          const double x = vp[j], y = vq[j];
-          vp[j] = cc[u] * x - ss[u] * y;
-          vq[j] = ss[u] * x + cc[u] * y;
-        }
-      }
-      __syncwarp();   // the kTPP threads of a group share a warp
-#pragma unroll
-      for (int u = 0; u < kMaxPairsPerGroup; ++u)
-        if (ss[u] != 0.0 && gl == 0) {
-          A[(size_t)pp[u] * lda + qq[u]] = 0.0;
-          A[(size_t)qq[u] * lda + pp[u]] = 0.0;
-        }
-      __syncthreads();
+  // ---------------- phase 1: Householder tridiagonalisation
+  for (int k = 0; k + 2 < m; ++k) {
+    const int i0 = k + 1;
+    double tail = 0.0;
+    for (int i = i0 + tid; i < m; i += nt) {
+      const double x = A[(size_t)i * ld + k];
+      S.v[i] = x;
+      if (i != i0) tail = fma(x, x, tail);
     }
-    if (!__syncthreads_or(rotated)) break;
+    tail = block_sum(tail, S);
+    if (tid == 0) {
+      const double x0 = S.v[i0];
+      double beta = 0.0, alpha = x0;
+      if (tail > 0.0) {
+        const double nx = sqrt(fma(x0, x0, tail));
+        alpha = -copysign(nx, x0);
+        const double v0 = x0 - alpha;
+        beta = 2.0 / fma(v0, v0, tail);
+        S.v[i0] = v0;
+        A[(size_t)i0 * ld + k] = v0;
+      }
+      S.e[k] = alpha;
+      S.beta[k] = beta;
+    }
+    __syncthreads();
+    const double beta = S.beta[k];
+    if (beta == 0.0) continue;
+    // p = beta S v  (warp per row, lanes over columns)
+    for (int i = i0 + warp; i < m; i += nw) {
+      const double* row = A + (size_t)i * ld;
+      double acc = 0.0;
+      for (int j = i0 + lane; j < m; j += 32) acc = fma(row[j], S.v[j], acc);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) S.p[i] = beta * acc;
+    }
+    __syncthreads();
+    double vp = 0.0;
+    for (int i = i0 + tid; i < m; i += nt) vp = fma(S.v[i], S.p[i], vp);
+    vp = block_sum(vp, S);
+    const double K = 0.5 * beta * vp;
+    for (int i = i0 + tid; i < m; i += nt) S.p[i] = S.p[i] - K * S.v[i];   // w
+    __syncthreads();
+    const int n1 = m - i0;
+    for (int e = tid; e < n1 * n1; e += nt) {
+      const int i = i0 + e / n1, j = i0 + e % n1;
+      double* a = A + (size_t)i * ld + j;
+      *a = *a - S.v[i] * S.p[j] - S.p[i] * S.v[j];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += nt) S.d[i] = A[(size_t)i * ld + i];
+  if (tid == 0) {
+    if (m >= 2) S.e[m - 2] = A[(size_t)(m - 1) * ld + (m - 2)];
+    S.e[m - 1] = 0.0;
+  }
+  // ---------------- phase 2: Z^T = Q^T, Q = H_0 ... H_{m-3}
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    ZT[(size_t)i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int k = m - 3; k >= 0; --k) {
+    const double beta = S.beta[k];
+    if (beta == 0.0) continue;
+    const int i0 = k + 1;
+    for (int i = i0 + tid; i < m; i += nt) S.v[i] = A[(size_t)i * ld + k];
+    __syncthreads();
+    // u_j = sum_i v_i Z[i][j] = sum_i ZT[j][i] v_i   (warp per j)
+    for (int j = i0 + warp; j < m; j += nw) {
+      const double* zr = ZT + (size_t)j * ld;
+      double acc = 0.0;
+      for (int i = i0 + lane; i < m; i += 32) acc = fma(zr[i], S.v[i], acc);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) S.p[j] = beta * acc;
+    }
+    __syncthreads();
+    const int n1 = m - i0;
+    for (int e = tid; e < n1 * n1; e += nt) {
+      const int j = i0 + e / n1, i = i0 + e % n1;
+      ZT[(size_t)j * ld + i] -= S.p[j] * S.v[i];
+    }
+    __syncthreads();
   }
 
-  for (int i = tid; i < m; i += nt) diag[i] = A[(size_t)i * lda + i];
-  __syncthreads();
-  // descending order; ties: higher index first (argsort(...)[::-1], nystrom.py:151)
+  // ---------------- phase 3: implicit QL on (d, e), rotations applied to Z
+  const double eps = 2.220446049250313e-16;
+  int l = 0, iters = 0, total_iters = 0;   // thread 0's state
+  for (;;) {
+    if (tid == 0) {
+      int lo = -1, hi = -1;
+      while (l < m) {
+        int mm = l;
+        for (; mm < m - 1; ++mm) {
+          const double dd = fabs(S.d[mm]) + fabs(S.d[mm + 1]);
+          if (fabs(S.e[mm]) <= eps * dd) break;
+        }
+        if (mm == l || iters >= kMaxQlIters) {
+          ++l;
+          iters = 0;
+          continue;
+        }
+        ++iters;
+        ++total_iters;
+        double g = (S.d[l + 1] - S.d[l]) / (2.0 * S.e[l]);
+        double r = hypot(g, 1.0);
+        g = S.d[mm] - S.d[l] + S.e[l] / (g + copysign(r, g));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i = mm - 1;
+        bool early = false;
+        for (; i >= l; --i) {
+          const double f = s * S.e[i], b = c * S.e[i];
+          r = hypot(f, g);
+          S.e[i + 1] = r;
+          if (r == 0.0) {
+            S.d[i + 1] -= p;
+            S.e[mm] = 0.0;
+            early = true;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = S.d[i + 1] - p;
+          r = (S.d[i] - g) * s + 2.0 * c * b;
+          p = s * r;
+          S.d[i + 1] = g + p;
+          g = c * r - b;
+          S.rc[i] = c;
+          S.rs[i] = s;
+        }
+        if (!early) {
+          S.d[l] -= p;
+          S.e[l] = g;
+          S.e[mm] = 0.0;
+          lo = l;
+        } else {
+          lo = i + 1;
+        }
+        hi = mm;
+        break;
+      }
+      S.ibcast[0] = lo;
+      S.ibcast[1] = hi;
+    }
+    __syncthreads();
+    const int lo = S.ibcast[0], hi = S.ibcast[1];
+    if (lo < 0) break;
+    if (lo < hi) {
+      for (int k = tid; k < m; k += nt) {   // row k of Z, streamed down the sweep
+        double f = ZT[(size_t)hi * ld + k];
+        for (int i = hi - 1; i >= lo; --i) {
+          const double zi = ZT[(size_t)i * ld + k];
+          const double c = S.rc[i], s = S.rs[i];
+          ZT[(size_t)(i + 1) * ld + k] = s * zi + c * f;
+          f = c * zi - s * f;
+        }
+        ZT[(size_t)lo * ld + k] = f;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---------------- phase 4: descending order (ties: higher index first, like
+  // argsort(...)[::-1] in nystrom.py:151), drop rule, W
   for (int i = tid; i < m; i += nt) {
-    const double di = diag[i];
+    const double di = S.d[i];
     int rank = 0;
     for (int j = 0; j < m; ++j) {
-      const double dj = diag[j];
+      const double dj = S.d[j];
       rank += (dj > di) || (dj == di && j > i);
     }
-    order[rank] = i;
+    S.order[rank] = i;
   }
   __syncthreads();
-  const double s0 = diag[order[0]];
+  const double s0 = S.d[S.order[0]];
   const double cut = fmax(drop_tol * s0, 0.0);
-  for (int k = tid; k < m; k += nt) eigvals[k] = diag[order[k]];
+  for (int k = tid; k < m; k += nt) eigvals[k] = S.d[S.order[k]];
   if (tid == 0) {
     int me = 0;
-    while (me < m && diag[order[me]] > cut) ++me;
+    while (me < m && S.d[S.order[me]] > cut) ++me;
     *m_eff_out = me;
-    *info = NYS_INFO_OK | (sweeps << 8);   // bits 8+: Jacobi sweeps (diagnostic)
+    if (total_iters > 65535) total_iters = 65535;
+    *info = NYS_INFO_OK | (total_iters << 8);   // bits 8+: QL iterations (diagnostic)
   }
   for (int e = tid; e < m * m; e += nt) {
-    const int i = e / m, k = e % m;   // output row-major: row i, column k
-    const int src = order[k];
-    const double v = VT[(size_t)src * m + i];
+    const int i = e / m, k = e % m;   // row-major: row i, column k
+    const int src = S.order[k];
+    const double v = ZT[(size_t)src * ld + i];
     eigvecs[e] = v;
-    const double sk = diag[src];
+    const double sk = S.d[src];
     Wout[e] = (sk > cut) ? v / sqrt(sk) : 0.0;
   }
 }
+
+size_t eig_storage_bytes(int m) { return 2 * (size_t)m * (m + 1) * sizeof(double); }
+constexpr size_t kEigSmemMax = 160 * 1024;   // + ~30 KB static bookkeeping
 
 }  // namespace
 
 extern "C" size_t nys_landmark_eig_workspace_bytes(int m) {
   if (m <= 0) return 0;
-  size_t need = (2 * (size_t)m * m + m) * sizeof(double);
-  return need <= 200 * 1024 ? 0 : need;
+  size_t need = eig_storage_bytes(m);
+  return need <= kEigSmemMax ? 0 : need;
 }
 
 extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma2,
                                     double drop_tol, double* eigvals, double* eigvecs,
                                     double* W, int* m_eff, int* info, void* workspace,
                                     size_t workspace_bytes, void* stream) {
-  if (m < 1 || m > 512 || !(sigma2 > 0.0) || !(drop_tol >= 0.0 && drop_tol < 1.0))
+  if (m < 1 || m > kMaxM || !(sigma2 > 0.0) || !(drop_tol >= 0.0 && drop_tol < 1.0))
     return NYS_EINVAL;
-  size_t need = (2 * (size_t)m * m + m) * sizeof(double);
-  int use_smem = need <= 200 * 1024;
-  double *gA = nullptr, *gV = nullptr;
+  const size_t need = eig_storage_bytes(m);
+  const int use_smem = need <= kEigSmemMax;
+  double *gA = nullptr, *gZ = nullptr;
   size_t dyn = 0;
   if (use_smem) {
     dyn = need;
-    cudaError_t e = cudaFuncSetAttribute(jacobi_eig_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    cudaError_t e = cudaFuncSetAttribute(tql_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn);
     if (e != cudaSuccess) return nys_host::record_cuda(e);
   } else {
     if (workspace == nullptr || workspace_bytes < need) return NYS_EWORKSPACE;
     gA = static_cast<double*>(workspace);
-    gV = gA + (size_t)m * (m + 1);
+    gZ = gA + (size_t)m * (m + 1);
   }
-  int pairs = (m + 1) / 2;
-  int threads = pairs * kTPP;
-  if (threads > kEigThreads) threads = kEigThreads;   // groups then take 2 pairs each
-  threads = (threads + 31) / 32 * 32;
-  jacobi_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
-      landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gV, use_smem);
+  const int threads = m <= 64 ? 256 : (m <= 128 ? 512 : kEigThreads);
+  tql_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
+      landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gZ, use_smem);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
