@@ -188,25 +188,37 @@ __global__ void __launch_bounds__(kEigThreads, 1)
         double s = 1.0, c = 1.0, p = 0.0;
         int i = mm - 1;
         bool early = false;
+        double ei = S.e[mm - 1], di1 = S.d[mm];
         for (; i >= l; --i) {
-          const double f = s * S.e[i], b = c * S.e[i];
-          r = hypot(f, g);
-          S.e[i + 1] = r;
-          if (r == 0.0) {
+          // prefetch the next rotation's operands off the dependency chain
+          const double ei_next = i > l ? S.e[i - 1] : 0.0;
+          const double di = S.d[i];
+          const double f = s * ei, b = c * ei;
+          const double rr = fma(f, f, g * g);
+          if (rr == 0.0) {
+            S.e[i + 1] = 0.0;
             S.d[i + 1] -= p;
             S.e[mm] = 0.0;
             early = true;
             break;
           }
-          s = f / r;
-          c = g / r;
-          g = S.d[i + 1] - p;
-          r = (S.d[i] - g) * s + 2.0 * c * b;
+          // r = hypot(f, g), s = f / r, c = g / r with one reciprocal square
+          // root instead of hypot + two divisions (shortens the serial chain;
+          // |f|, |g| <= ||Omega|| here, so no over/underflow guard is needed)
+          const double ir = rsqrt(rr);
+          r = rr * ir;
+          S.e[i + 1] = r;
+          s = f * ir;
+          c = g * ir;
+          g = di1 - p;
+          r = (di - g) * s + 2.0 * c * b;
           p = s * r;
           S.d[i + 1] = g + p;
           g = c * r - b;
           S.rc[i] = c;
           S.rs[i] = s;
+          ei = ei_next;
+          di1 = di;
         }
         if (!early) {
           S.d[l] -= p;
