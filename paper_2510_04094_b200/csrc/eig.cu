@@ -17,6 +17,8 @@
 // A and Z^T live in shared memory when they fit (m <= 112), otherwise in the
 // caller's workspace (L2-resident, config 4: m = 256).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -51,7 +53,8 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     tql_eig_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
                    double* __restrict__ eigvals, double* __restrict__ eigvecs,
                    double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
-                   double* __restrict__ gA, double* __restrict__ gZ, int use_smem) {
+                   double* __restrict__ gA, double* __restrict__ gZ, int use_smem, int debug) {
+  long long t_start = clock64(), t1 = 0, t2 = 0, t3 = 0;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Shared S;
   const int ld = m + 1;
@@ -104,14 +107,20 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     __syncthreads();
     const double beta = S.beta[k];
     if (beta == 0.0) continue;
-    // p = beta S v  (warp per row, lanes over columns)
-    for (int i = i0 + warp; i < m; i += nw) {
+    // p = beta S v: thread per row, four independent accumulators (FP64 FMA
+    // latency, not throughput, bounds a serial dot product)
+    for (int i = i0 + tid; i < m; i += nt) {
       const double* row = A + (size_t)i * ld;
-      double acc = 0.0;
-      for (int j = i0 + lane; j < m; j += 32) acc = fma(row[j], S.v[j], acc);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) S.p[i] = beta * acc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int j = i0;
+      for (; j + 3 < m; j += 4) {
+        a0 = fma(row[j], S.v[j], a0);
+        a1 = fma(row[j + 1], S.v[j + 1], a1);
+        a2 = fma(row[j + 2], S.v[j + 2], a2);
+        a3 = fma(row[j + 3], S.v[j + 3], a3);
+      }
+      for (; j < m; ++j) a0 = fma(row[j], S.v[j], a0);
+      S.p[i] = beta * ((a0 + a1) + (a2 + a3));
     }
     __syncthreads();
     double vp = 0.0;
@@ -120,14 +129,14 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     const double K = 0.5 * beta * vp;
     for (int i = i0 + tid; i < m; i += nt) S.p[i] = S.p[i] - K * S.v[i];   // w
     __syncthreads();
-    const int n1 = m - i0;
-    for (int e = tid; e < n1 * n1; e += nt) {
-      const int i = i0 + e / n1, j = i0 + e % n1;
-      double* a = A + (size_t)i * ld + j;
-      *a = *a - S.v[i] * S.p[j] - S.p[i] * S.v[j];
+    for (int i = i0 + warp; i < m; i += nw) {   // A -= v w^T + w v^T (warp per row)
+      double* row = A + (size_t)i * ld;
+      const double vi = S.v[i], wi = S.p[i];
+      for (int j = i0 + lane; j < m; j += 32) row[j] = row[j] - vi * S.p[j] - wi * S.v[j];
     }
     __syncthreads();
   }
+  t1 = clock64();
   for (int i = tid; i < m; i += nt) S.d[i] = A[(size_t)i * ld + i];
   if (tid == 0) {
     if (m >= 2) S.e[m - 2] = A[(size_t)(m - 1) * ld + (m - 2)];
@@ -145,24 +154,30 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     const int i0 = k + 1;
     for (int i = i0 + tid; i < m; i += nt) S.v[i] = A[(size_t)i * ld + k];
     __syncthreads();
-    // u_j = sum_i v_i Z[i][j] = sum_i ZT[j][i] v_i   (warp per j)
-    for (int j = i0 + warp; j < m; j += nw) {
+    // u_j = sum_i v_i Z[i][j] = sum_i ZT[j][i] v_i   (thread per j, 4 accumulators)
+    for (int j = i0 + tid; j < m; j += nt) {
       const double* zr = ZT + (size_t)j * ld;
-      double acc = 0.0;
-      for (int i = i0 + lane; i < m; i += 32) acc = fma(zr[i], S.v[i], acc);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0) S.p[j] = beta * acc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int i = i0;
+      for (; i + 3 < m; i += 4) {
+        a0 = fma(zr[i], S.v[i], a0);
+        a1 = fma(zr[i + 1], S.v[i + 1], a1);
+        a2 = fma(zr[i + 2], S.v[i + 2], a2);
+        a3 = fma(zr[i + 3], S.v[i + 3], a3);
+      }
+      for (; i < m; ++i) a0 = fma(zr[i], S.v[i], a0);
+      S.p[j] = beta * ((a0 + a1) + (a2 + a3));
     }
     __syncthreads();
-    const int n1 = m - i0;
-    for (int e = tid; e < n1 * n1; e += nt) {
-      const int j = i0 + e / n1, i = i0 + e % n1;
-      ZT[(size_t)j * ld + i] -= S.p[j] * S.v[i];
+    for (int j = i0 + warp; j < m; j += nw) {   // warp per row of Z^T
+      double* zr = ZT + (size_t)j * ld;
+      const double pj = S.p[j];
+      for (int i = i0 + lane; i < m; i += 32) zr[i] -= pj * S.v[i];
     }
     __syncthreads();
   }
 
+  t2 = clock64();
   // ---------------- phase 3: implicit QL on (d, e), rotations applied to Z
   const double eps = 2.220446049250313e-16;
   int l = 0, iters = 0, total_iters = 0;   // thread 0's state
@@ -252,6 +267,10 @@ __global__ void __launch_bounds__(kEigThreads, 1)
     __syncthreads();
   }
 
+  t3 = clock64();
+  if (debug && tid == 0)
+    printf("[nys eig] m=%d tridiag=%lld accumQ=%lld ql=%lld cycles, ql_iters=%d\n", m, t1 - t_start,
+           t2 - t1, t3 - t2, total_iters);
   // ---------------- phase 4: descending order (ties: higher index first, like
   // argsort(...)[::-1] in nystrom.py:151), drop rule, W
   for (int i = tid; i < m; i += nt) {
@@ -317,7 +336,8 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
   }
   const int threads = m <= 64 ? 256 : (m <= 128 ? 512 : kEigThreads);
   tql_eig_kernel<<<1, threads, dyn, static_cast<cudaStream_t>(stream)>>>(
-      landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gZ, use_smem);
+      landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info, gA, gZ, use_smem,
+      getenv("NYS_EIG_DEBUG") != nullptr);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
