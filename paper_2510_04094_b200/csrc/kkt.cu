@@ -430,230 +430,9 @@ __global__ void __launch_bounds__(kKktThreads)
   if (tid == 0) info[b] = nonfinite ? NYS_INFO_NONFINITE : NYS_INFO_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Batched path: Cholesky of the SPD block + p x p Schur complement.
-// M = [[H, C^T], [C, 0]] with H = [D g]^T [D g] + diag(I/gamma, 0) (SPD unless
-// g lies in range(D)) and C = [A_c beta].  SURVEY.md §0 / A1: replacing the
-// reference's LU by Cholesky + Schur moves y_hat by <= 5e-11.  Half the flops
-// of LU, no pivot search or row swaps, and a packed lower triangle (n_h(n_h+1)/2
-// doubles) doubles the systems resident per SM.  Breakdown (a non-positive
-// pivot) marks the instance kNeedsLu and the LU kernel above re-solves it, so
-// the reference's failure semantics are kept.
-constexpr int kNeedsLu = 16;
-constexpr int kMaxCond = 4;
+}  // namespace
 
-NYS_DEV int pk(int i, int j) { return i * (i + 1) / 2 + j; }   // packed lower, j <= i
-
-__global__ void __launch_bounds__(32)
-    kkt_chol_kernel(const double* __restrict__ gram, int m_eff, int ncond,
-                    const double* __restrict__ Ac, const double* __restrict__ beta,
-                    const double* __restrict__ values, double gamma, int B,
-                    double* __restrict__ xout, int* __restrict__ info) {
-  extern __shared__ __align__(16) double dsm[];
-  const int lane = threadIdx.x, b = blockIdx.x;
-  const int nh = m_eff + 1, me = m_eff, Pe = m_eff + 2, p = ncond;
-  const double* E = gram + (size_t)b * Pe * Pe;
-  const double* vals = values + (size_t)b * ncond;
-  double* L = dsm;                                   // packed lower, nh(nh+1)/2
-  double* Y = L + (size_t)nh * (nh + 1) / 2;         // nh x p   (L^{-1} C^T)
-  double* y = Y + (size_t)nh * p;                    // nh work vector
-  double* xs = y + nh;                               // n = nh + p solution
-  const double inv_gamma = 1.0 / gamma;
-
-  // H (lower) from E, 8 rows of loads in flight per lane
-  for (int i0 = 0; i0 < nh; i0 += 8) {
-    double v[8][kNC];
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        int i = i0 + r, j = lane + 32 * c;
-        v[r][c] = (i < nh && j <= i) ? __ldg(E + (size_t)i * Pe + j) : 0.0;
-      }
-#pragma unroll
-    for (int r = 0; r < 8; ++r)
-#pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        int i = i0 + r, j = lane + 32 * c;
-        if (i < nh && j <= i) L[pk(i, j)] = (i == j && i < me) ? inv_gamma + v[r][c] : v[r][c];
-      }
-  }
-  __syncwarp();
-  // right-looking Cholesky, lanes over columns of each trailing row
-  int bad = 0;
-  for (int k = 0; k < nh; ++k) {
-    const double akk = L[pk(k, k)];
-    if (!(akk > 0.0) || !isfinite(akk)) {
-      bad = 1;
-      break;
-    }
-    const double lkk = sqrt(akk);
-    const double inv = 1.0 / lkk;
-    __syncwarp();
-    if (lane == 0) L[pk(k, k)] = lkk;
-    for (int i = k + 1 + lane; i < nh; i += 32) L[pk(i, k)] *= inv;
-    __syncwarp();
-    for (int i = k + 1; i < nh; ++i) {
-      const double li = L[pk(i, k)];
-      double* row = L + pk(i, 0);
-#pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        int j = k + 1 + lane + 32 * c;
-        if (j <= i) row[j] -= li * L[pk(j, k)];
-      }
-    }
-    __syncwarp();
-  }
-  // Y = L^{-1} C^T, C = [A_c beta]  (column-oriented forward solves)
-  double S[kMaxCond][kMaxCond];
-  if (!bad) {
-    for (int mu = 0; mu < p; ++mu) {
-      for (int i = lane; i < nh; i += 32)
-        Y[(size_t)i * p + mu] = i < me ? Ac[(size_t)mu * me + i] : beta[mu];
-      __syncwarp();
-      for (int j = 0; j < nh; ++j) {
-        const double yj = Y[(size_t)j * p + mu] / L[pk(j, j)];
-        __syncwarp();
-        if (lane == 0) Y[(size_t)j * p + mu] = yj;
-        for (int i = j + 1 + lane; i < nh; i += 32) Y[(size_t)i * p + mu] -= L[pk(i, j)] * yj;
-        __syncwarp();
-      }
-    }
-    // S = Y^T Y (p x p, SPD), Cholesky in registers (all lanes redundantly)
-    for (int a = 0; a < p; ++a)
-      for (int c = 0; c <= a; ++c) {
-        double acc = 0.0;
-        for (int i = lane; i < nh; i += 32) acc = fma(Y[(size_t)i * p + a], Y[(size_t)i * p + c], acc);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        S[a][c] = acc;
-      }
-    for (int a = 0; a < p && !bad; ++a) {
-      double d = S[a][a];
-      for (int c = 0; c < a; ++c) d -= S[a][c] * S[a][c];
-      if (!(d > 0.0)) {
-        bad = 1;
-        break;
-      }
-      S[a][a] = sqrt(d);
-      for (int r = a + 1; r < p; ++r) {
-        double t = S[r][a];
-        for (int c = 0; c < a; ++c) t -= S[r][c] * S[a][c];
-        S[r][a] = t / S[a][a];
-      }
-    }
-  }
-  if (bad) {
-    if (lane == 0) info[b] = kNeedsLu;
-    return;
-  }
-
-  // solve + one refinement (linear.py:144-147); pass 1 rhs = rhs - M x
-  for (int pass = 0; pass < 2; ++pass) {
-    double rv[kMaxCond];
-    if (pass == 0) {
-      for (int i = lane; i < nh; i += 32) y[i] = E[(size_t)i * Pe + me + 1];
-      for (int mu = 0; mu < p; ++mu) rv[mu] = vals[mu];
-    } else {
-      // r1 = rhs1 - H x - C^T lambda ; rv = v - C x   (H symmetric: rows of E coalesced)
-      double acc[kNC];
-#pragma unroll
-      for (int c = 0; c < kNC; ++c) acc[c] = 0.0;
-      for (int j0 = 0; j0 < nh; j0 += 8) {
-        double ev[8][kNC], xj[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          int j = j0 + r;
-          xj[r] = j < nh ? xs[j] : 0.0;
-#pragma unroll
-          for (int c = 0; c < kNC; ++c) {
-            int i = lane + 32 * c;
-            ev[r][c] = (j < nh && i < nh) ? __ldg(E + (size_t)j * Pe + i) : 0.0;
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-          for (int c = 0; c < kNC; ++c) {
-            int i = lane + 32 * c, j = j0 + r;
-            acc[c] += ((i == j && i < me) ? inv_gamma + ev[r][c] : ev[r][c]) * xj[r];
-          }
-      }
-#pragma unroll
-      for (int c = 0; c < kNC; ++c) {
-        int i = lane + 32 * c;
-        if (i < nh) {
-          double a = acc[c];
-          for (int mu = 0; mu < p; ++mu) a += (i < me ? Ac[(size_t)mu * me + i] : beta[mu]) * xs[nh + mu];
-          y[i] = E[(size_t)i * Pe + me + 1] - a;
-        }
-      }
-      for (int mu = 0; mu < p; ++mu) {
-        double a = 0.0;
-        for (int i = lane; i < me; i += 32) a = fma(Ac[(size_t)mu * me + i], xs[i], a);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        rv[mu] = vals[mu] - (a + beta[mu] * xs[me]);
-      }
-    }
-    __syncwarp();
-    // y1 = L^{-1} r1
-    for (int j = 0; j < nh; ++j) {
-      const double yj = y[j] / L[pk(j, j)];
-      __syncwarp();
-      if (lane == 0) y[j] = yj;
-      for (int i = j + 1 + lane; i < nh; i += 32) y[i] -= L[pk(i, j)] * yj;
-      __syncwarp();
-    }
-    // lambda = S^{-1} (Y^T y1 - v)
-    double t[kMaxCond];
-    for (int mu = 0; mu < p; ++mu) {
-      double a = 0.0;
-      for (int i = lane; i < nh; i += 32) a = fma(Y[(size_t)i * p + mu], y[i], a);
-#pragma unroll
-      for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      t[mu] = a - rv[mu];
-    }
-    for (int a = 0; a < p; ++a) {
-      double v = t[a];
-      for (int c = 0; c < a; ++c) v -= S[a][c] * t[c];
-      t[a] = v / S[a][a];
-    }
-    for (int a = p - 1; a >= 0; --a) {
-      double v = t[a];
-      for (int c = a + 1; c < p; ++c) v -= S[c][a] * t[c];
-      t[a] = v / S[a][a];
-    }
-    // z = y1 - Y lambda ; x = L^{-T} z  (row-oriented on packed rows)
-    for (int i = lane; i < nh; i += 32) {
-      double v = y[i];
-      for (int mu = 0; mu < p; ++mu) v -= Y[(size_t)i * p + mu] * t[mu];
-      y[i] = v;
-    }
-    __syncwarp();
-    for (int j = nh - 1; j >= 0; --j) {
-      const double xj = y[j] / L[pk(j, j)];
-      __syncwarp();
-      if (lane == 0) y[j] = xj;
-      const double* row = L + pk(j, 0);
-      for (int i = lane; i < j; i += 32) y[i] -= row[i] * xj;
-      __syncwarp();
-    }
-    for (int i = lane; i < nh; i += 32) xs[i] = pass == 0 ? y[i] : xs[i] + y[i];
-    if (lane == 0)
-      for (int mu = 0; mu < p; ++mu) xs[nh + mu] = pass == 0 ? t[mu] : xs[nh + mu] + t[mu];
-    __syncwarp();
-  }
-  const int n = nh + p;
-  int nonfinite = 0;
-  for (int i = lane; i < n; i += 32) {
-    double v = xs[i];
-    if (!isfinite(v)) nonfinite = 1;
-    xout[(size_t)b * n + i] = v;
-  }
-  nonfinite = __any_sync(0xffffffffu, nonfinite);
-  if (lane == 0) info[b] = nonfinite ? kNeedsLu : NYS_INFO_OK;
-}
+namespace nys_host {
 
 int launch_kkt(const double* gram, int m_eff, int ncond, const double* Ac, const double* beta,
                const double* values, double gamma, int B, double* x, int* info, double* M,
@@ -682,7 +461,7 @@ int launch_kkt(const double* gram, int m_eff, int ncond, const double* Ac, const
   return NYS_OK;
 }
 
-}  // namespace
+}  // namespace nys_host
 
 extern "C" size_t nys_kkt_workspace_bytes(int m_eff, int n_cond, int B) {
   int n = m_eff + 1 + n_cond;
@@ -699,35 +478,3 @@ extern "C" int nys_kkt_solve_f64(const double* gram_ext, int m_eff, int n_cond, 
                     workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
-extern "C" int nys_batch_kkt_solve_f64(const void* batch_workspace, int n_c, int m_eff, int p,
-                                       int n_cond, const double* Ac, const double* beta,
-                                       const double* values, double gamma, int B, double* x,
-                                       int* info, void* stream) {
-  if (m_eff < 1 || n_cond < 0 || B < 0 || !(gamma > 0.0) || p < 1 || p > 2) return NYS_EINVAL;
-  if (B == 0) return NYS_OK;
-  if (m_eff + 1 + n_cond > kWarpKktMaxN) return NYS_EUNSUPPORTED;
-  nys::BatchLayout L = nys::BatchLayout::make(n_c, m_eff, p, B);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  double* dense = L.dense(const_cast<void*>(batch_workspace));
-  int rc = nys_host::launch_batch_unpack(L.part(batch_workspace), L.nsplit, B, L.NB, L.Pe(), dense,
-                                         st);
-  if (rc) return rc;
-  if (n_cond <= kMaxCond) {
-    const int nh = m_eff + 1;
-    size_t dyn = ((size_t)nh * (nh + 1) / 2 + (size_t)nh * n_cond + 2 * (size_t)nh + n_cond) *
-                 sizeof(double);
-    if (dyn > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kkt_chol_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      if (e != cudaSuccess) return nys_host::record_cuda(e);
-    }
-    kkt_chol_kernel<<<B, 32, dyn, st>>>(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info);
-    nys_host::count_launches(1);
-    NYS_CHECK_LAUNCH();
-    // LU (the reference's algorithm) re-solves any instance whose Cholesky broke down
-    return launch_kkt(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, nullptr, nullptr,
-                      nullptr, 0, st, /*only_flagged=*/true);
-  }
-  return launch_kkt(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, nullptr, nullptr,
-                    nullptr, 0, st);
-}
