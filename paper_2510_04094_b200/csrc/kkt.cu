@@ -474,7 +474,8 @@ extern "C" int nys_kkt_solve_f64(const double* gram_ext, int m_eff, int n_cond, 
                                  size_t workspace_bytes, void* stream) {
   if (m_eff < 1 || n_cond < 0 || B < 0 || !(gamma > 0.0)) return NYS_EINVAL;
   if (B == 0) return NYS_OK;
-  return launch_kkt(gram_ext, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, M, rhs,
-                    workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  return nys_host::launch_kkt(gram_ext, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, M,
+                              rhs, workspace, workspace_bytes, static_cast<cudaStream_t>(stream),
+                              false);
 }
 
