@@ -4,14 +4,16 @@
 //     D_b = Psi_p - sum_k f_{b,k} (.) Psi_{p-k},  g_b = -f_{b,p},  r_b
 //     E_b = [D_b g_b r_b]^T [D_b g_b r_b]
 // Psi_0..Psi_p are formed once per batch (the reference's own per-order
-// projection, linear.py:103-112) in a fragment-native packed layout; each warp
-// then owns one instance and streams Psi through shared memory (1-D TMA bulk
-// copies, double buffered on mbarriers), combines the row in registers (FP64
-// FMA) and feeds the SAME register fragment to both operands of DMMA.8x8x4,
-// accumulating only the upper block triangle of E.  Gram and rhs come from
-// one rounding of D (mixing roundings costs up to 5.9e-5).
-// Row splits (grid.y) give whole waves on 148 SMs; their partials are summed in
-// a fixed order by the KKT kernel (deterministic, no FP64 atomics).
+// projection, linear.py:103-112) in a fragment-native packed layout; the CTA
+// streams them through shared memory (1-D TMA bulk copies, double buffered on
+// mbarriers).  Each instance is owned by SPLIT warps (SPLIT = 2 for wide Grams:
+// each warp holds half of the upper block triangle, so a CTA of 16 warps keeps
+// 4 warps per scheduler to hide FP64 latency).  A warp combines its rows in
+// registers (FP64 FMA) and feeds the SAME register fragment to both operands of
+// DMMA.8x8x4.  Gram and rhs come from one rounding of D (mixing
+// roundings costs up to 5.9e-5).  Row splits (grid.y) give whole waves on 148
+// SMs; their partials are summed in a fixed order (deterministic, no FP64
+// atomics).
 #include <algorithm>
 
 #include "batch_layout.cuh"
@@ -33,53 +35,45 @@ struct Tri {
   static constexpr NYS_DEV int idx(int I, int J) { return I * NB - (I * (I - 1)) / 2 + (J - I); }
 };
 
-template <int NB, int NO, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1)
-    batch_gram_kernel(const double* __restrict__ psi, const double* __restrict__ coef,
-                      const double* __restrict__ forcing, int n_c, int B, int ks_per_split,
-                      int rcol, double* __restrict__ part) {
-  constexpr int P = NO - 1;                       // ODE order
-  constexpr int CH = nys::kBatchChunkKs;          // k-steps per chunk (32 rows)
+// pairs [Lo, Hi) of the I-major upper block triangle
+template <int NB, int Lo, int Hi>
+struct Role {
+  static constexpr int kCount = Hi - Lo;
+  static constexpr NYS_DEV bool has(int I, int J) {
+    return Tri<NB>::idx(I, J) >= Lo && Tri<NB>::idx(I, J) < Hi;
+  }
+  static constexpr NYS_DEV bool needs(int F) {
+    for (int I = 0; I < NB; ++I)
+      for (int J = I; J < NB; ++J)
+        if (has(I, J) && (I == F || J == F)) return true;
+    return false;
+  }
+};
+
+template <int NB, int NO, int WARPS, int SPLIT, int Lo, int Hi>
+NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict__ coef,
+                       const double* __restrict__ forcing, int n_c, int B, int b, int ks0,
+                       int nchunks, int rcol, double* sm, uint64_t* bar,
+                       double* __restrict__ part) {
+  constexpr int P = NO - 1;
+  constexpr int CH = nys::kBatchChunkKs;
   constexpr int kChunkDoubles = CH * NO * NB * 32;
   constexpr uint32_t kChunkBytes = kChunkDoubles * sizeof(double);
   constexpr int NPAIR = Tri<NB>::kPairs;
+  using R = Role<NB, Lo, Hi>;
 
-  extern __shared__ __align__(128) double sm[];   // [2][kChunkDoubles]
-  __shared__ __align__(8) uint64_t bar[2];
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tig = lane & 3, gid = lane >> 2;
-  const int b = blockIdx.x * WARPS + warp;
-  const int split = blockIdx.y;
-  const int ks0 = split * ks_per_split;
-  const int nchunks = ks_per_split / CH;
+  const int lane = threadIdx.x & 31, tig = lane & 3, gid = lane >> 2;
   const bool active = b < B;
-
-  if (threadIdx.x == 0) {
-    nys::mbar_init(&bar[0], 1);
-    nys::mbar_init(&bar[1], 1);
-    nys::fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2 && s < nchunks; ++s) {
-      nys::mbar_expect_tx(&bar[s], kChunkBytes);
-      nys::bulk_g2s(sm + s * kChunkDoubles, psi + (size_t)(ks0 + s * CH) * NO * NB * 32,
-                    kChunkBytes, &bar[s]);
-    }
-  }
-
-  double acc[NPAIR][2];
+  double acc[R::kCount][2];
 #pragma unroll
-  for (int q = 0; q < NPAIR; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int q = 0; q < R::kCount; ++q) acc[q][0] = acc[q][1] = 0.0;
 
   const double* cb = coef + (size_t)(active ? b : 0) * P * n_c;
   const double* rb = forcing + (size_t)(active ? b : 0) * n_c;
-  // per-lane coefficient row (row0 + lane) of the current / next chunk
   double fk[P], rr, fk_n[P], rr_n;
   auto load_rows = [&](int c, double* f, double& r) {
-    int row = (ks0 + c * CH) * 4 + lane;
-    bool ok = active && row < n_c;
+    const int row = (ks0 + c * CH) * 4 + lane;
+    const bool ok = active && row < n_c;
 #pragma unroll
     for (int k = 0; k < P; ++k) f[k] = ok ? __ldg(cb + (size_t)k * n_c + row) : 0.0;
     r = ok ? __ldg(rb + row) : 0.0;
@@ -103,17 +97,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         double x[NB];
 #pragma unroll
         for (int F = 0; F < NB; ++F) {
+          if (!R::needs(F)) {
+            x[F] = 0.0;
+            continue;
+          }
           // Q layout per k-step: [order][block][lane]
           double v = Q[((kk * NO + P) * NB + F) * 32];
 #pragma unroll
-          for (int k = 1; k <= P; ++k) v = fma(-f[k - 1], Q[((kk * NO + (P - k)) * NB + F) * 32], v);
+          for (int k = 1; k <= P; ++k)
+            v = fma(-f[k - 1], Q[((kk * NO + (P - k)) * NB + F) * 32], v);
           x[F] = (F * 8 + gid == rcol) ? r : v;
         }
 #pragma unroll
         for (int I = 0; I < NB; ++I)
 #pragma unroll
           for (int J = I; J < NB; ++J)
-            nys::dmma(acc[Tri<NB>::idx(I, J)][0], acc[Tri<NB>::idx(I, J)][1], x[I], x[J]);
+            if (R::has(I, J)) {
+              constexpr int dummy = 0;
+              (void)dummy;
+              const int q = Tri<NB>::idx(I, J) - Lo;
+              nys::dmma(acc[q][0], acc[q][1], x[I], x[J]);
+            }
       }
     }
     if (c + 1 < nchunks) {
@@ -128,63 +132,95 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
                     psi + (size_t)(ks0 + (c + 2) * CH) * NO * NB * 32, kChunkBytes, &bar[stage]);
     }
   }
-
   if (active) {
-    double* out = part + ((size_t)split * B + b) * NPAIR * 64 + lane * 2;
+    double* out = part + (((size_t)blockIdx.y * B + b) * NPAIR + Lo) * 64 + lane * 2;
 #pragma unroll
-    for (int q = 0; q < NPAIR; ++q) {
+    for (int q = 0; q < R::kCount; ++q) {
       out[q * 64] = acc[q][0];
       out[q * 64 + 1] = acc[q][1];
     }
   }
 }
 
-// partials -> dense E (P x P) per instance, summing splits in fixed order
+template <int NB, int NO, int WARPS, int SPLIT>
+__global__ void __launch_bounds__(WARPS * 32, 1)
+    batch_gram_kernel(const double* __restrict__ psi, const double* __restrict__ coef,
+                      const double* __restrict__ forcing, int n_c, int B, int ks_per_split,
+                      int rcol, double* __restrict__ part) {
+  constexpr int CH = nys::kBatchChunkKs;
+  constexpr int kChunkDoubles = CH * NO * NB * 32;
+  constexpr uint32_t kChunkBytes = kChunkDoubles * sizeof(double);
+  constexpr int NPAIR = Tri<NB>::kPairs;
+  constexpr int H = (NPAIR + 1) / 2;
+
+  extern __shared__ __align__(128) double sm[];   // [2][kChunkDoubles]
+  __shared__ __align__(8) uint64_t bar[2];
+
+  const int warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * (WARPS / SPLIT) + warp / SPLIT;
+  const int ks0 = blockIdx.y * ks_per_split;
+  const int nchunks = ks_per_split / CH;
+
+  if (threadIdx.x == 0) {
+    nys::mbar_init(&bar[0], 1);
+    nys::mbar_init(&bar[1], 1);
+    nys::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2 && s < nchunks; ++s) {
+      nys::mbar_expect_tx(&bar[s], kChunkBytes);
+      nys::bulk_g2s(sm + s * kChunkDoubles, psi + (size_t)(ks0 + s * CH) * NO * NB * 32,
+                    kChunkBytes, &bar[s]);
+    }
+  }
+  if constexpr (SPLIT == 1) {
+    gram_body<NB, NO, WARPS, SPLIT, 0, NPAIR>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol,
+                                              sm, bar, part);
+  } else {
+    if ((warp & 1) == 0)
+      gram_body<NB, NO, WARPS, SPLIT, 0, H>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol, sm,
+                                            bar, part);
+    else
+      gram_body<NB, NO, WARPS, SPLIT, H, NPAIR>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol,
+                                                sm, bar, part);
+  }
+}
+
+// partials -> dense E (Pe x Pe) per instance, summing splits in fixed order
 __global__ void batch_unpack_kernel(const double* __restrict__ part, int nsplit, int B, int NB,
                                     int Pe, double* __restrict__ gram) {
   const int b = blockIdx.x;
   const int npair = NB * (NB + 1) / 2;
   for (int e = threadIdx.x; e < npair * 64; e += blockDim.x) {
-    int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
+    const int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
     int I = 0, rem = q;
     while (rem >= NB - I) {
       rem -= NB - I;
       ++I;
     }
-    int J = I + rem;
+    const int J = I + rem;
     double s = 0.0;
     for (int sp = 0; sp < nsplit; ++sp) s += part[((size_t)sp * B + b) * npair * 64 + e];
-    int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
+    const int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
     if (r < Pe && c < Pe) {
+      if (I == J && r > c) continue;   // diagonal block: each pair once
       gram[(size_t)b * Pe * Pe + (size_t)r * Pe + c] = s;
       gram[(size_t)b * Pe * Pe + (size_t)c * Pe + r] = s;
     }
   }
 }
 
-}  // namespace
-
-namespace nys_host {
-int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, double* gram,
-                        cudaStream_t st) {
-  batch_unpack_kernel<<<B, 256, 0, st>>>(part, nsplit, B, NB, Pe, gram);
-  count_launches(1);
-  NYS_CHECK_LAUNCH();
-  return NYS_OK;
-}
-}  // namespace nys_host
-
-namespace {
-
 template <int NB, int NO>
 int launch_gram(const double* psi, const double* coef, const double* forcing, int n_c, int B,
                 const BatchLayout& L, double* part, cudaStream_t st) {
-  constexpr int WARPS = nys::kBatchWarps;
-  auto kern = batch_gram_kernel<NB, NO, WARPS>;
-  size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
+  constexpr int SPLIT = NB >= 7 ? 2 : 1;
+  constexpr int WARPS = nys::kBatchWarps * SPLIT;
+  auto kern = batch_gram_kernel<NB, NO, WARPS, SPLIT>;
+  const size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return nys_host::record_cuda(e);
-  dim3 grid((B + WARPS - 1) / WARPS, L.nsplit);
+  dim3 grid((B + nys::kBatchWarps - 1) / nys::kBatchWarps, L.nsplit);
   kern<<<grid, WARPS * 32, smem, st>>>(psi, coef, forcing, n_c, B, L.ks_per_split, L.m_eff + 1,
                                        part);
   nys_host::count_launches(1);
@@ -210,6 +246,16 @@ int dispatch_nb(int NB, const double* psi, const double* coef, const double* for
 }
 
 }  // namespace
+
+namespace nys_host {
+int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, double* gram,
+                        cudaStream_t st) {
+  batch_unpack_kernel<<<B, 256, 0, st>>>(part, nsplit, B, NB, Pe, gram);
+  count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+}  // namespace nys_host
 
 extern "C" size_t nys_batch_gram_workspace_bytes(int n_c, int m_eff, int p, int B) {
   BatchLayout L = BatchLayout::make(n_c, m_eff, p, B);
@@ -237,10 +283,7 @@ extern "C" int nys_batch_gram_f64(const double* landmarks, int m, const double* 
   rc = (p == 1) ? dispatch_nb<2>(L.NB, psi, coef, forcing, n_c, B, L, part, st)
                 : dispatch_nb<3>(L.NB, psi, coef, forcing, n_c, B, L, part, st);
   if (rc) return rc;
-  if (gram_ext != nullptr) {
-    batch_unpack_kernel<<<B, 256, 0, st>>>(part, L.nsplit, B, L.NB, m_eff + 2, gram_ext);
-    nys_host::count_launches(1);
-    NYS_CHECK_LAUNCH();
-  }
+  if (gram_ext != nullptr) return nys_host::launch_batch_unpack(part, L.nsplit, B, L.NB, m_eff + 2,
+                                                                gram_ext, st);
   return NYS_OK;
 }
