@@ -214,7 +214,9 @@ __global__ void batch_unpack_kernel(const double* __restrict__ part, int nsplit,
 template <int NB, int NO>
 int launch_gram(const double* psi, const double* coef, const double* forcing, int n_c, int B,
                 const BatchLayout& L, double* part, cudaStream_t st) {
-  constexpr int SPLIT = NB >= 7 ? 2 : 1;
+  // SPLIT = 2 (two warps per instance, 128 registers each) measured slower on
+  // B200 for NB = 9: 4.15 ms vs 3.33 ms (doubled combine + Psi reads, spills)
+  constexpr int SPLIT = 1;
   constexpr int WARPS = nys::kBatchWarps * SPLIT;
   auto kern = batch_gram_kernel<NB, NO, WARPS, SPLIT>;
   const size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
