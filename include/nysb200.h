@@ -160,6 +160,47 @@ int nys_ode_residual_f64(const double* landmarks, int m, const double* W, int ld
                          const double* forcing, int n_c, const double* x, double* e,
                          void* stream);
 
+/* ------------------------------------------------------------------------
+ * (v) Newton-KKT for nonlinear first-order ODEs, batched over instances that
+ * share grid / landmarks (config 3).  Replaces newton._residual
+ * (newton.py:128-147), _jacobian_analytic + np.linalg.solve(J, -F)
+ * (newton.py:160-211, 307) by a Schur complement onto (omega, b, lambda): the
+ * Jacobian's y-block is diagonal (newton.py:210).  The driver loop, damping,
+ * gamma continuation and retry ladder (newton.py:279-412) run on the host
+ * (paper_2510_04094_b200/newton.py) around these stream-ordered calls.
+ * Unknown layout per instance: X[b*ldx + (omega[m_eff], b, lambda[n_cond], y[n_c])].
+ * idx[nb] lists the instances to process (device int32).
+ * Nonlinearity: family mode f = g + alpha y^2 + beta sin y (g [B*n_c],
+ * alpha/beta [B], fy = fyy = NULL) or sampled mode (g = f, fy, fyy [B*n_c]
+ * evaluated by the caller at the current y).
+ * ------------------------------------------------------------------------ */
+int nys_transpose_f64(const double* A, int rows, int cols, double* AT, void* stream);
+size_t nys_newton_pack_doubles(int m_eff, int n_c);
+int nys_newton_pack_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                        double sigma2, const double* pts, int n_c, double* packed, void* stream);
+/* F [B*ldx], norm [B] (= max|F|, NaN when f or e1 is non-finite), aux [B*3*n_c]
+ * (f_y, f_yy e1, 1 + f_y^2 - f_yy e1), work [B*2*n_c] */
+int nys_newton_residual_f64(const double* S0, const double* S1, const double* S0T,
+                            const double* S1T, int m_eff, int n_c, const double* g,
+                            const double* fy, const double* fyy, const double* alpha,
+                            const double* beta, const double* Ac, const double* betac,
+                            const double* vals, int n_cond, const double* gamma,
+                            const double* X, int ldx, const int* idx, int nb, double* F,
+                            double* norm, double* aux, double* work, void* stream);
+/* reduced system K [nb * nz^2], rz [nb * nz], nz = m_eff + 1 + n_cond (DMMA weighted Grams) */
+int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, const double* aux,
+                           const double* F, int ldx, const double* gamma, const double* Ac,
+                           const double* betac, int n_cond, const int* idx, int nb, double* K,
+                           double* rz, void* stream);
+/* batched dense LU (partial pivoting) solve, one system of side n <= 96 per slot */
+int nys_lu_solve_f64(double* M, double* rhs, int n, int nb, double* out, int* info, void* stream);
+/* D[b] = (dz, dy) (compute_delta = 1) and Xc[b] = X[b] + alpha[b] * D[b] */
+int nys_newton_step_f64(const double* S0, const double* S1, int m_eff, int n_c, int n_cond,
+                        const double* aux, const double* F, const double* dz,
+                        const double* gamma, const double* X, double* D, double* Xc,
+                        const double* alpha, int ldx, const int* idx, int nb, int compute_delta,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

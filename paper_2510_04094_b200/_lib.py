@@ -42,6 +42,17 @@ SIGNATURES = {
                                _vp]),
     "nys_batch_kkt_solve_f64": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _d, _i, _vp, _vp, _vp]),
     "nys_ode_residual_f64": (_i, [_vp, _i, _vp, _i, _i, _d, _i, _vp, _vp, _vp, _i, _vp, _vp]),
+    "nys_transpose_f64": (_i, [_vp, _i, _i, _vp, _vp]),
+    "nys_newton_pack_doubles": (_sz, [_i, _i]),
+    "nys_newton_pack_f64": (_i, [_vp, _i, _vp, _i, _i, _d, _vp, _i, _vp, _vp]),
+    "nys_newton_residual_f64": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp,
+                                     _vp, _vp, _i, _vp, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp,
+                                     _vp]),
+    "nys_newton_reduced_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _vp,
+                                    _vp, _vp]),
+    "nys_lu_solve_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp]),
+    "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _i, _vp, _i, _i, _vp]),
 }
 
 

@@ -184,15 +184,13 @@ class SharedGridPipeline:
         """Pinned host in -> pinned host out.  dev_bufs: optional preallocated
         device staging (coef, forcing, values, x, info) for the full batch."""
         torch = _lib.require_device()[1]
-        solver = self.prepare()
-        dev = solver.fmap.device
+        dev = torch.device(self.device or "cuda")
         B = coef_h.shape[0]
         if dev_bufs is None:
             dev_bufs = (torch.empty(coef_h.shape, dtype=torch.float64, device=dev),
                         torch.empty(forcing_h.shape, dtype=torch.float64, device=dev),
                         torch.empty(values_h.shape, dtype=torch.float64, device=dev),
-                        torch.empty((B, solver.side), dtype=torch.float64, device=dev),
-                        torch.empty(B, dtype=torch.int32, device=dev))
+                        None, None)
         dc, df, dv, dx, di = dev_bufs
         comp = torch.cuda.current_stream()
         copy = getattr(self, "_copy_stream", None)
@@ -210,6 +208,14 @@ class SharedGridPipeline:
                 ev = torch.cuda.Event()
                 ev.record(copy)
                 ready.append(ev)
+        # eigendecomposition of the shared landmark set runs while the samples
+        # are still crossing PCIe on the copy stream
+        solver = self.prepare()
+        if dx is None:
+            dx = torch.empty((B, solver.side), dtype=torch.float64, device=dev)
+            di = torch.empty(B, dtype=torch.int32, device=dev)
+        if tuple(dx.shape) != (B, solver.side) or tuple(x_h.shape) != (B, solver.side):
+            raise ValueError(f"solution buffers must be ({B}, {solver.side})")
         for c in range(chunks):
             a, b = bounds[c], bounds[c + 1]
             comp.wait_event(ready[c])

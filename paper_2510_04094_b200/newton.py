@@ -1,0 +1,491 @@
+"""Newton-iterated primal KKT solve for nonlinear first-order ODEs, on the B200.
+
+Mirror of ``pkg/src/nysode/newton.py`` (names, options, exceptions, the
+five-rung retry ladder and its semantics), with the numerics on the device
+(C ABI ``nys_newton_*``):
+
+* residual / gradient of the Lagrangian -- ``nys_newton_residual_f64``
+  (newton.py:128-147);
+* Newton direction -- the Jacobian's y-block is diagonal (newton.py:210), so
+  J delta = -F is solved by a Schur complement onto (omega, b, lambda):
+  DMMA-accumulated reduced system (``nys_newton_reduced_f64``) + batched LU
+  (``nys_lu_solve_f64``) + diagonal back-substitution (``nys_newton_step_f64``)
+  instead of the reference's dense (m_eff+2+n_c)-side LU (newton.py:307);
+* damping, continuation and the ladder (newton.py:279-412) stay on the host,
+  batched: every instance of a rung advances in the same kernel launches and
+  drops out when it converges, diverges, hits a singular step or exhausts the
+  iteration budget.
+
+Two ways to give the nonlinearity f(t, y):
+* :class:`SeparableFamily` -- f = g(t) + alpha y^2 + beta sin(y), evaluated on
+  the device (config 3: y' = -k y^2 + g and y' = sin y + g);
+* a reference ``NonlinearOdeSpec`` (callables) -- evaluated on the host at the
+  current y every residual call (the generic drop-in path; slower).
+
+Only first-order problems (p = 1) run on the device; higher orders are
+SURVEY.md §8f next-row 2 and raise ``NotImplementedError``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .linear import PrimalModel, condition_rows, constraint_points, predict_batch
+from .nystrom import NystromFeatureMap
+
+
+class PartialsMissingError(ValueError):
+    pass
+
+
+class SingularJacobianError(np.linalg.LinAlgError):
+    pass
+
+
+class DivergenceError(RuntimeError):
+    pass
+
+
+class MaxItersExceeded(RuntimeError):
+    def __init__(self, message: str, model: PrimalModel, trace: "NewtonTrace"):
+        super().__init__(message)
+        self.model = model
+        self.trace = trace
+
+
+@dataclass(frozen=True)
+class NewtonOptions:
+    """newton.py:52-61."""
+
+    max_iters: int = 100
+    tol: Optional[float] = None
+    damping: Optional[tuple] = None
+    jacobian: str = "analytic"
+    fd_step: float = 1e-6
+
+    def resolved_tol(self, gamma: float) -> float:
+        return self.tol if self.tol is not None else 1e-10 * (1.0 + gamma)
+
+
+@dataclass
+class NewtonTrace:
+    residual_norms: list = field(default_factory=list)
+    converged: bool = False
+    floor_estimate: float = 0.0
+    final_state: Optional["NewtonState"] = None
+    rung: int = 0
+
+    @property
+    def iterations(self) -> int:
+        return max(len(self.residual_norms) - 1, 0)
+
+
+@dataclass(frozen=True)
+class NewtonState:
+    omega: np.ndarray
+    bias: float
+    multipliers: np.ndarray
+    y_aux: np.ndarray
+    iteration: int = 0
+    residual_norm: float = np.inf
+
+    def pack(self) -> np.ndarray:
+        return np.concatenate([self.omega, [self.bias], self.multipliers, self.y_aux])
+
+
+@dataclass
+class SeparableFamily:
+    """f(t, y) = g(t) + alpha y^2 + beta sin(y), sampled g on the constraint points."""
+
+    g: np.ndarray         # (B, n_c)
+    alpha: np.ndarray     # (B,)
+    beta: np.ndarray      # (B,)
+
+
+# outcome codes of a batched solve_once
+OK, MAXITERS, DIVERGED, SINGULAR = 0, 1, 2, 3
+_CONTINUATION_GAMMAS = (1e0, 1e2, 1e4)     # newton.py:349
+
+
+class NewtonBatch:
+    """Batched Newton-KKT engine for B first-order ODEs sharing grid and fmap."""
+
+    def __init__(self, fmap: NystromFeatureMap, grid, cond, values, gamma: float,
+                 family: Optional[SeparableFamily] = None, specs: Optional[Sequence] = None):
+        lib, torch = _lib.require_device()
+        self.lib, self.torch = lib, torch
+        self.fmap = fmap
+        dev = self.dev = fmap.device
+        self.grid = np.asarray(grid, dtype=float)
+        self.cond = cond
+        self.pts_host = constraint_points(cond, self.grid)
+        self.n_c = self.pts_host.size
+        self.values = np.asarray(values, dtype=float).reshape(-1, len(cond.entries))
+        self.B = self.values.shape[0]
+        self.nk = len(cond.entries)
+        self.me = fmap.m_eff
+        self.nz = self.me + 1 + self.nk
+        self.ldx = self.nz + self.n_c
+        self.gamma_target = float(gamma)
+        if (family is None) == (specs is None):
+            raise ValueError("give exactly one of family / specs")
+        self.family, self.specs = family, specs
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.pts = _lib.as_f64(self.pts_host, dev)
+        st = _lib.stream_ptr()
+        # shared feature rows S0, S1 (dense + transposed) and the DMMA-packed copy
+        self.S0 = fmap.feature_matrix_device(0, self.pts).contiguous()
+        self.S1 = fmap.feature_matrix_device(1, self.pts).contiguous()
+        self.S0T = torch.empty((self.me, self.n_c), **f64)
+        self.S1T = torch.empty((self.me, self.n_c), **f64)
+        _lib.call("nys_transpose_f64", _lib.ptr(self.S0), self.n_c, self.me, _lib.ptr(self.S0T), st)
+        _lib.call("nys_transpose_f64", _lib.ptr(self.S1), self.n_c, self.me, _lib.ptr(self.S1T), st)
+        self.packed = torch.zeros(lib.nys_newton_pack_doubles(self.me, self.n_c), **f64)
+        _lib.call("nys_newton_pack_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
+                  fmap.m, self.me, float(fmap.kernel.sigma2), _lib.ptr(self.pts), self.n_c,
+                  _lib.ptr(self.packed), st)
+        Ac, beta, _ = condition_rows(cond, fmap)
+        self.Ac = _lib.as_f64(Ac.reshape(self.nk, self.me), dev)
+        self.betac = _lib.as_f64(beta, dev)
+        self.vals = _lib.as_f64(self.values, dev)
+        B, ldx = self.B, self.ldx
+        self.X = torch.zeros((B, ldx), **f64)
+        self.Xc = torch.zeros((B, ldx), **f64)
+        self.F = torch.zeros((B, ldx), **f64)
+        self.D = torch.zeros((B, ldx), **f64)
+        self.norm = torch.zeros(B, **f64)
+        self.aux = torch.zeros((B, 3, self.n_c), **f64)
+        self.work = torch.zeros((B, 2, self.n_c), **f64)
+        self.gam = torch.full((B,), self.gamma_target, **f64)
+        self.alpha = torch.ones(B, **f64)
+        self.K = torch.zeros((B, self.nz, self.nz), **f64)
+        self.rz = torch.zeros((B, self.nz), **f64)
+        self.dz = torch.zeros((B, self.nz), **f64)
+        self.info = torch.zeros(B, dtype=torch.int32, device=dev)
+        if family is not None:
+            self.g = _lib.as_f64(family.g, dev)
+            self.fal = _lib.as_f64(family.alpha, dev)
+            self.fbe = _lib.as_f64(family.beta, dev)
+            self.fy = self.fyy = None
+        else:
+            self.g = torch.zeros((B, self.n_c), **f64)
+            self.fy = torch.zeros((B, self.n_c), **f64)
+            self.fyy = torch.zeros((B, self.n_c), **f64)
+            self.fal = self.fbe = None
+            for sp in specs:
+                if sp.order != 1:
+                    raise NotImplementedError("device Newton supports first-order ODEs (p = 1)")
+                tab = sp.rhs_second_partials
+                if tab is None or ((0, 0) not in tab):
+                    raise PartialsMissingError(
+                        "rhs_second_partials required for analytic Jacobian")
+        self.launches = 0
+
+    # -------------------------------------------------------------- kernels
+    def _idx(self, ids):
+        return self.torch.as_tensor(np.asarray(ids, dtype=np.int32), device=self.dev)
+
+    def _sample_host(self, X, ids):
+        """Sampled mode: evaluate the spec callables at the current y (host)."""
+        Y = X[:, self.nz:].cpu().numpy()
+        t = self.pts_host
+        for b in ids:
+            sp = self.specs[b]
+            y = Y[b]
+            self.g[b] = _lib.as_f64(np.asarray(sp.rhs(t, y), dtype=float), self.dev)
+            self.fy[b] = _lib.as_f64(np.asarray(sp.rhs_partials[0](t, y), dtype=float), self.dev)
+            self.fyy[b] = _lib.as_f64(np.asarray(sp.rhs_second_partials[(0, 0)](t, y),
+                                                 dtype=float), self.dev)
+
+    def residual(self, X, ids, idx_t=None) -> np.ndarray:
+        """F(X[b]) for b in ids; returns max|F| per id (NaN = non-finite rhs)."""
+        if self.specs is not None:
+            self._sample_host(X, ids)
+        idx_t = self._idx(ids) if idx_t is None else idx_t
+        _lib.call("nys_newton_residual_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
+                  _lib.ptr(self.S0T), _lib.ptr(self.S1T), self.me, self.n_c, _lib.ptr(self.g),
+                  _lib.ptr(self.fy), _lib.ptr(self.fyy), _lib.ptr(self.fal), _lib.ptr(self.fbe),
+                  _lib.ptr(self.Ac), _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk,
+                  _lib.ptr(self.gam), _lib.ptr(X), self.ldx, _lib.ptr(idx_t), len(ids),
+                  _lib.ptr(self.F), _lib.ptr(self.norm), _lib.ptr(self.aux), _lib.ptr(self.work),
+                  _lib.stream_ptr())
+        return self.norm[idx_t].cpu().numpy()
+
+    def direction(self, ids) -> np.ndarray:
+        """Newton direction D[b] at X[b] (aux/F from the last residual at X);
+        returns LU info per id."""
+        idx_t = self._idx(ids)
+        nb, st = len(ids), _lib.stream_ptr()
+        _lib.call("nys_newton_reduced_f64", _lib.ptr(self.packed), self.me, self.n_c,
+                  _lib.ptr(self.aux), _lib.ptr(self.F), self.ldx, _lib.ptr(self.gam),
+                  _lib.ptr(self.Ac), _lib.ptr(self.betac), self.nk, _lib.ptr(idx_t), nb,
+                  _lib.ptr(self.K), _lib.ptr(self.rz), st)
+        _lib.call("nys_lu_solve_f64", _lib.ptr(self.K), _lib.ptr(self.rz), self.nz, nb,
+                  _lib.ptr(self.dz), _lib.ptr(self.info), st)
+        _lib.call("nys_newton_step_f64", _lib.ptr(self.S0), _lib.ptr(self.S1), self.me, self.n_c,
+                  self.nk, _lib.ptr(self.aux), _lib.ptr(self.F), _lib.ptr(self.dz),
+                  _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
+                  _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), nb, 1, st)
+        info = self.info[:nb].cpu().numpy().copy()
+        D = self.D[idx_t]
+        bad = ~self.torch.isfinite(D).all(dim=1).cpu().numpy()
+        info[bad] = _lib.INFO_NONFINITE
+        return info
+
+    def candidate(self, ids, alphas):
+        """Xc[b] = X[b] + alpha_b D[b]."""
+        idx_t = self._idx(ids)
+        self.alpha[idx_t] = self.torch.as_tensor(np.asarray(alphas, dtype=float), device=self.dev)
+        _lib.call("nys_newton_step_f64", _lib.ptr(self.S0), _lib.ptr(self.S1), self.me, self.n_c,
+                  self.nk, _lib.ptr(self.aux), _lib.ptr(self.F), _lib.ptr(self.dz),
+                  _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
+                  _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), len(ids), 0,
+                  _lib.stream_ptr())
+
+    # -------------------------------------------------------------- states
+    def const_state(self, ids):
+        """omega = 0, b = first order-0 IVP value, y = b (newton.py:226-237)."""
+        j0 = [j for j, bc in enumerate(self.cond.entries) if bc.order == 0]
+        if self.cond.kind == "ivp":
+            b0 = self.values[ids, j0[0]]
+        else:
+            b0 = self.values[ids][:, j0].mean(axis=1)
+        x = np.zeros((len(ids), self.ldx))
+        x[:, self.me] = b0
+        x[:, self.nz:] = b0[:, None]
+        return x
+
+    def model_state(self, ids, x):
+        """(omega, b, 0, S0 omega + b) -- continuation hand-off (newton.py:369-372)."""
+        torch = self.torch
+        xd = _lib.as_f64(x[:, :self.me + 1], self.dev)
+        y = predict_batch(self.fmap, xd, 0, self.pts).cpu().numpy()
+        out = np.zeros((len(ids), self.ldx))
+        out[:, :self.me + 1] = x[:, :self.me + 1]
+        out[:, self.nz:] = y
+        return out
+
+    def linearized_state(self, ids):
+        """Warm start from the ODE linearised about (y = b0) (newton.py:240-276):
+        y' = f(t, b0) + f_y(t, b0) (y - b0), solved by the batched linear path."""
+        from .batch import LinearBatchSolver
+
+        x0 = self.const_state(ids)
+        b0 = x0[:, self.me]
+        t = self.pts_host
+        coef = np.empty((len(ids), 1, self.n_c))
+        forcing = np.empty((len(ids), self.n_c))
+        for r, b in enumerate(ids):
+            yb = np.full_like(t, b0[r])
+            if self.family is not None:
+                a, be = self.family.alpha[b], self.family.beta[b]
+                f0 = self.family.g[b] + a * yb * yb + be * np.sin(yb)
+                fy = 2.0 * a * yb + be * np.cos(yb)
+            else:
+                sp = self.specs[b]
+                f0 = np.asarray(sp.rhs(t, yb), dtype=float)
+                fy = np.asarray(sp.rhs_partials[0](t, yb), dtype=float)
+            coef[r, 0] = fy
+            forcing[r] = f0 - fy * b0[r]
+        solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, 1, self.cond, len(ids))
+        xl, info = solver.solve(coef, forcing, self.values[ids])
+        xl = xl.cpu().numpy()
+        info = info.cpu().numpy()
+        out = self.model_state(ids, xl)
+        return out, info
+
+    # -------------------------------------------------------------- solve_once
+    def solve_once(self, ids, x0, gamma, tol, damping, max_iters, shrink=0.5, halvings=30):
+        """Batched newton._solve_once (newton.py:279-349).
+
+        Returns (status[len(ids)], X rows (np), traces)."""
+        torch = self.torch
+        ids = list(ids)
+        nid = len(ids)
+        idx_all = self._idx(ids)
+        self.X[idx_all] = _lib.as_f64(x0, self.dev)
+        g = np.broadcast_to(np.asarray(gamma, dtype=float), (nid,))
+        self.gam[idx_all] = _lib.as_f64(g, self.dev)
+        tol = np.broadcast_to(np.asarray(tol, dtype=float), (nid,))
+        pos = {b: r for r, b in enumerate(ids)}
+        status = np.full(nid, -1)
+        norm = self.residual(self.X, ids, idx_all)
+        traces = [[float(v)] for v in norm]
+        its = np.zeros(nid, dtype=int)
+        bad0 = ~np.isfinite(norm)
+        status[bad0] = DIVERGED           # _residual raised at the initial state
+        active = [b for b in ids if status[pos[b]] < 0]
+        while active:
+            keep = []
+            for b in active:
+                r = pos[b]
+                if norm[r] <= tol[r]:
+                    status[r] = OK
+                elif its[r] >= max_iters:
+                    status[r] = MAXITERS
+                elif norm[r] > 1e12:
+                    status[r] = DIVERGED
+                else:
+                    keep.append(b)
+            active = keep
+            if not active:
+                break
+            info = self.direction(active)
+            step = []
+            for b, inf in zip(active, info):
+                if inf != _lib.INFO_OK:
+                    status[pos[b]] = SINGULAR
+                else:
+                    step.append(b)
+            active = step
+            if not active:
+                break
+            if damping:
+                alpha = {b: 1.0 for b in active}
+                searching = list(active)
+                for _ in range(halvings):
+                    if not searching:
+                        break
+                    self.candidate(searching, [alpha[b] for b in searching])
+                    cn = self.residual(self.Xc, searching)
+                    nxt = []
+                    for b, v in zip(searching, cn):
+                        if np.isfinite(v) and v <= norm[pos[b]]:
+                            continue            # accepted
+                        alpha[b] *= shrink
+                        nxt.append(b)
+                    searching = nxt
+                self.candidate(active, [alpha[b] for b in active])
+            else:
+                self.candidate(active, [1.0] * len(active))
+            act_t = self._idx(active)
+            self.X[act_t] = self.Xc[act_t]
+            newn = self.residual(self.X, active, act_t)
+            still = []
+            for b, v in zip(active, newn):
+                r = pos[b]
+                its[r] += 1
+                norm[r] = v
+                traces[r].append(float(v))
+                if not np.isfinite(v):
+                    status[r] = DIVERGED        # _residual raised after the update
+                else:
+                    still.append(b)
+            active = still
+        # loop ended: converged check after exhausting iterations (newton.py:331-333)
+        for r in range(nid):
+            if status[r] == MAXITERS and norm[r] <= tol[r]:
+                status[r] = OK
+        Xn = self.X[idx_all].cpu().numpy()
+        return status, Xn, traces
+
+    # -------------------------------------------------------------- ladder
+    def solve(self, max_iters: int = 100, tol: Optional[float] = None):
+        """Retry ladder (newton.py:376-412) for all B instances.
+
+        Returns (status[B], X[B, ldx] np, traces list, rung[B]); status is the
+        outcome of the rung that finished the instance (OK) or of the last rung."""
+        gam = self.gamma_target
+        tol_t = 1e-10 * (1.0 + gam) if tol is None else tol
+        B = self.B
+        status = np.full(B, -1)
+        X = np.zeros((B, self.ldx))
+        traces = [None] * B
+        rung = np.zeros(B, dtype=int)
+
+        def record(ids, st, Xn, tr, r):
+            for k, b in enumerate(ids):
+                status[b] = st[k]
+                X[b] = Xn[k]
+                traces[b] = tr[k]
+                rung[b] = r
+
+        todo = list(range(B))
+        plans = [(1, "const", None), (2, "const", (0.5, 30)), (3, "lin", None),
+                 (4, "lin", (0.5, 30))]
+        for r, init, damp in plans:
+            if not todo:
+                break
+            if init == "const":
+                x0 = self.const_state(todo)
+            else:
+                x0, _ = self.linearized_state(todo)
+            st, Xn, tr = self.solve_once(todo, x0, gam, tol_t, damp is not None, max_iters)
+            record(todo, st, Xn, tr, r)
+            todo = [b for b in todo if status[b] != OK]
+        if todo:
+            # rung 5: gamma continuation (newton.py:352-373)
+            stages = [g for g in _CONTINUATION_GAMMAS if g < gam]
+            x_cur = self.const_state(todo)
+            alive = list(todo)
+            failed = {}
+            for g in stages:
+                if not alive:
+                    break
+                x0 = np.stack([x_cur[todo.index(b)] for b in alive])
+                st, Xn, tr = self.solve_once(alive, x0, g, 1e-8 * (1.0 + g), True, max_iters)
+                nxt = []
+                for k, b in enumerate(alive):
+                    if st[k] in (OK, MAXITERS):            # MaxIters tolerated
+                        nxt.append(b)
+                    else:
+                        failed[b] = (st[k], Xn[k], tr[k])  # Divergence / Singular escape
+                if nxt:
+                    sel = [alive.index(b) for b in nxt]
+                    xs = self.model_state(nxt, Xn[sel])
+                    for k, b in enumerate(nxt):
+                        x_cur[todo.index(b)] = xs[k]
+                alive = nxt
+            if alive:
+                x0 = np.stack([x_cur[todo.index(b)] for b in alive])
+                st, Xn, tr = self.solve_once(alive, x0, gam, tol_t, True, max_iters)
+                record(alive, st, Xn, tr, 5)
+            for b, (s, xb, tb) in failed.items():
+                status[b], X[b], traces[b], rung[b] = s, xb, tb, 5
+        return status, X, traces, rung
+
+    def model(self, xrow) -> PrimalModel:
+        me = self.me
+        return PrimalModel(omega=xrow[:me].copy(), bias=float(xrow[me]),
+                           multipliers=xrow[me + 1:self.nz].copy(), feature_map=self.fmap)
+
+
+def _raise_for(status, msg, model, trace):
+    if status == DIVERGED:
+        raise DivergenceError(msg)
+    if status == SINGULAR:
+        raise SingularJacobianError(msg)
+    if status == MAXITERS:
+        raise MaxItersExceeded(msg, model, trace)
+
+
+def solve_nonlinear(spec, cond, fmap: NystromFeatureMap, grid, gamma: float,
+                    opts: NewtonOptions = NewtonOptions(), x0: Optional[NewtonState] = None):
+    """newton.solve_nonlinear (newton.py:376-412) for one first-order spec."""
+    if spec.order != 1:
+        raise NotImplementedError("device Newton supports first-order ODEs (p = 1)")
+    if opts.jacobian != "analytic":
+        raise NotImplementedError("finite-difference Jacobians are not on the device path")
+    values = np.array([[bc.value for bc in cond.entries]])
+    eng = NewtonBatch(fmap, grid, cond, values, gamma, specs=[spec])
+    tol = opts.resolved_tol(float(gamma))
+    if x0 is not None or opts.damping is not None:
+        xs = x0.pack()[None] if x0 is not None else eng.const_state([0])
+        st, Xn, tr = eng.solve_once([0], xs, gamma, tol, opts.damping is not None, opts.max_iters,
+                                    *(opts.damping or (0.5, 30)))
+        status, xrow, trace_l, rung = st[0], Xn[0], tr[0], 0
+    else:
+        status_a, X, traces, rungs = eng.solve(opts.max_iters, opts.tol)
+        status, xrow, trace_l, rung = status_a[0], X[0], traces[0], rungs[0]
+    model = eng.model(xrow)
+    trace = NewtonTrace(residual_norms=list(trace_l), converged=status == OK, rung=int(rung))
+    trace.final_state = NewtonState(xrow[:eng.me], float(xrow[eng.me]), xrow[eng.me + 1:eng.nz],
+                                    xrow[eng.nz:], iteration=trace.iterations,
+                                    residual_norm=trace_l[-1])
+    if status != OK:
+        _raise_for(status, f"Newton failed (status {status}, residual {trace_l[-1]:.3e})",
+                   model, trace)
+    return model, trace
