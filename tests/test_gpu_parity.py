@@ -128,3 +128,21 @@ def test_batch_config2_matches_reference():
     E1 = sy.d_gram.cpu().numpy()
     scale = np.abs(E1).max()
     np.testing.assert_allclose(E[3].cpu().numpy(), E1, rtol=0, atol=1e-9 * scale)
+
+
+@pytest.mark.parametrize("name", ["c1_seed0", "c4_n16384"])
+def test_row_range_partials_sum_to_full_gram(name):
+    """Row sharding contract of nys_fused_gram_f64 (dist.py): partial extended
+    Grams over disjoint row slabs add up to the full one."""
+    from paper_2510_04094_b200 import dist as D
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden(name)
+    fm = fmap_from_golden(g)
+    dev = fm.device
+    pts = L._lib.as_f64(g["pts"], dev)
+    coef = L._lib.as_f64(g["coef"][0], dev)
+    forc = L._lib.as_f64(g["forcing"][0], dev)
+    full = L.gram_ext_device(fm, int(g["order"]), pts, coef, forc).cpu().numpy()
+    parts = sum(L.gram_ext_device(fm, int(g["order"]), pts, coef, forc, lo, hi).cpu().numpy()
+                for lo, hi in D.row_ranges(g["pts"].size, 3))
+    np.testing.assert_allclose(parts, full, rtol=0, atol=1e-11 * np.abs(full).max())
