@@ -1,25 +1,28 @@
-"""Benchmark: ODE solves/s on BASELINE.json config 2 (B = 4096 linear 2nd-order
-IVPs per GPU, n = 4096, m = 64 shared landmarks, FP64).
+"""Benchmark: ODE solves/s on the BASELINE.json configs (default: config 2,
+B = 4096 linear 2nd-order IVPs per GPU, n = 4096, m = 64 shared landmarks).
 
-One step = one batch solved from scratch through the device pipeline:
-landmark eigendecomposition (once per shared landmark set) -> shared features
-Psi_0..Psi_2 -> per-instance fused row-combine + Gram (DMMA) -> per-instance
-KKT LU + refinement.  This is the reference harness' "train" scope
-(harness.py:152-163) for a shared-grid batch.
+One step = the reference harness' "train" scope (harness.py:152-163) on the
+device pipeline, from scratch:
+  c2  landmark eigendecomposition (once per shared landmark set) -> shared
+      features Psi_0..Psi_2 -> per-instance fused row-combine + Gram (DMMA) ->
+      per-instance KKT solve (Cholesky + Schur, LU fallback)
+  c0/c1  eigendecomposition -> fused feature+Gram -> KKT LU + refinement
+  c3  B = 256 Newton-KKT solves (eigendecomposition, retry ladder, Schur-reduced
+      Newton steps)
+  c4  eigendecomposition -> kernel-space Gram over 4,194,303 rows (row-sharded
+      across ranks + one NCCL all-reduce) -> KKT LU
 
-  value  : device-timed, samples already resident in HBM (402 MB > 126 MB L2,
-           so no L2 flush is needed between steps)
-  e2e    : same step through the public API with pinned HOST buffers: H2D of
-           the samples (chunked, overlapped with compute) + D2H of the solutions
-  roofline: the batched Gram launch (batch_gram_kernel + its 3 tiny feature
-           launches) vs the measured FP64 DMMA peak (profiles/fp64_peak.json)
+  value  : device-timed, samples already resident in HBM (max over ranks)
+  e2e    : the same step through the public API with pinned HOST buffers:
+           H2D of the samples + D2H of the solutions inside the timed region
+  roofline: the dominant kernel vs the measured FP64 DMMA peak
+           (profiles/fp64_peak.json; MEASURED_PEAKS.json has no FP64 entry)
   cpu_baseline: the oracle restatement of the reference path on this host's
-           cores (process pool, 1 BLAS thread per worker), bounded sample
+           cores, bounded sample (oracle/cpu_baseline.py)
 
-Multi-GPU (torchrun): instances are independent, so each rank solves its own
-4096 instances (global instance ids rank*4096 + i) with no collective;
-"scaling": "weak"; value = all ranks' solves / max-over-ranks time.
-
+Multi-GPU (torchrun): c2/c3 instances are independent -> each rank solves its
+own batch (instance ids rank*B + i), no collective, "scaling": "weak";
+c4 rows are sharded (one all-reduce), "scaling": "strong"; c0/c1 run replicas.
 --impl reference: the reference's CPU path (oracle port, all host cores) on the
 same config/metric; rank 0 only.
 """
@@ -38,8 +41,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CID = 2
-FP64_PEAK_FALLBACK_TFLOPS = 37.15   # profiles/fp64_peak.json (DMMA m8n8k4, this pool)
+FP64_PEAK_FALLBACK_TFLOPS = 37.15   # tools/fp64_peak.cu on this pool (DMMA m8n8k4)
 
 
 def _args():
@@ -48,7 +50,8 @@ def _args():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nysb200", choices=["nysb200", "reference"])
-    ap.add_argument("--batch", type=int, default=None, help="instances per GPU (default 4096)")
+    ap.add_argument("--config", type=int, default=2, choices=[0, 1, 2, 3, 4])
+    ap.add_argument("--batch", type=int, default=None, help="instances per GPU (c2/c3)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--e2e-chunks", type=int, default=4)
@@ -56,10 +59,8 @@ def _args():
 
 
 def _dist():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 class ClockSampler:
@@ -70,8 +71,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
-        self.proc = None
+        self.index, self.proc, self.lines = index, None, []
 
     def __enter__(self):
         try:
@@ -84,7 +84,6 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -98,7 +97,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
+        for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -110,88 +109,138 @@ class ClockSampler:
             for nm, v in zip(names, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _traffic_from_profiles():
-    path = os.path.join(ROOT, "profiles", "ncu_batch_gram.json")
+def _profile_json(name):
     try:
-        with open(path) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
     except (OSError, ValueError):
-        return None
+        return {}
 
 
 def _fp64_peak():
-    try:
-        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
-            return float(json.load(fh)["dmma_m8n8k4_w8_tflops"]), "measured (profiles/fp64_peak.json)"
-    except (OSError, ValueError, KeyError):
-        return FP64_PEAK_FALLBACK_TFLOPS, "measured earlier (tools/fp64_peak.cu)"
+    d = _profile_json("fp64_peak.json")
+    if "dmma_m8n8k4_w8_tflops" in d:
+        return float(d["dmma_m8n8k4_w8_tflops"]), "measured DMMA.8x8x4 peak (profiles/fp64_peak.json)"
+    return FP64_PEAK_FALLBACK_TFLOPS, "measured DMMA.8x8x4 peak (tools/fp64_peak.cu)"
 
 
-def run_reference(args, world, rank):
-    """Reference arm: the oracle port of the reference path on all host cores."""
+WORKLOAD = {
+    0: "c0: linear 1st-order IVP, n=1000, m=20, sigma=0.1, gamma=1e8 (BASELINE.json configs[0])",
+    1: "c1: linear 2nd-order IVP, n=10000, m=50, sigma=0.4 (tuned), gamma=1e9 (configs[1])",
+    2: "c2: B=4096 linear 2nd-order IVPs per GPU, n=4096 shared grid on [0,2], m=64 shared "
+       "landmarks, sigma=0.1, gamma=1e9 (BASELINE.json configs[2])",
+    3: "c3: B=256 nonlinear 1st-order IVPs per GPU (y'=-k y^2+g / y'=sin y+g), n=2000, m=40, "
+       "sigma=0.1, gamma=1e8, Newton tol 1e-10(1+gamma), max 20 its (configs[3])",
+    4: "c4: linear 2nd-order IVP, n=2^22 on [0,100], m=256, sigma=0.5, gamma=1e9 (configs[4])",
+}
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank):
     if rank != 0:
         return
     from oracle import cpu_baseline as CB
 
     cores = os.cpu_count() or 1
-    per_step_s = 2.0
-    for _ in range(args.warmup):
-        CB.batch_solves_per_second(CID, cores, per_worker=4)
-    vals, solved = [], 0
+    cid = args.config
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, n, _, _ = CB.batch_solves_per_second(CID, cores, per_worker=10_000, budget_s=per_step_s)
-        vals.append(v)
-        solved += n
-    wall = time.perf_counter() - t0
-    value = solved / wall
+    if cid in (2, 3):
+        budget = 2.0 if cid == 2 else 6.0
+        for _ in range(args.warmup):
+            CB.batch_solves_per_second(cid, cores, per_worker=1)
+        solved = 0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            _, n, _, _ = CB.batch_solves_per_second(cid, cores, per_worker=10_000, budget_s=budget)
+            solved += n
+        wall = time.perf_counter() - t0
+        value = solved / wall
+        sample = (f"{solved} instances over {args.steps} steps of ~{budget:.0f} s on a "
+                  f"{cores}-process pool (1 BLAS thread each, shared feature map per worker)")
+    elif cid in (0, 1):
+        for _ in range(args.warmup):
+            CB.single_solve_seconds(cid, reps=1)
+        ts = [CB.single_solve_seconds(cid, reps=1) for _ in range(args.steps)]
+        wall = sum(ts)
+        value = args.steps / wall
+        sample = f"{args.steps} full solves, one process, {cores} BLAS threads"
+    else:
+        tsec, parts = CB.c4_solve_seconds_estimate()
+        wall, value = tsec, 1.0 / tsec
+        sample = (f"eig + KKT solve in full; assembly on 2^18 of 4,194,303 rows scaled x"
+                  f"{parts['scale']:.1f} (O(n) assembly); {cores} BLAS threads")
     line = {
         "impl": "reference", "metric": "ode_solves_per_s", "value": value, "unit": "solves/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (workloads.py, seed 0)",
-        "config": {"workload": "c2: B=4096 linear 2nd-order IVPs, n=4096, m=64, sigma=0.1, "
-                               "gamma=1e9 (BASELINE.json configs[2])"},
+        "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong" if cid == 4 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2510_04094_b200/workloads.py)",
+        "config": {"workload": WORKLOAD[cid]},
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": f"{solved} instances over {args.steps} steps of "
-                                   f"~{per_step_s:.0f} s on a {cores}-process pool "
-                                   "(1 BLAS thread each; shared feature map per worker)"},
+                         "sample": sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def main():
-    args = _args()
-    world, rank, local = _dist()
-    if args.impl == "reference":
-        run_reference(args, world, rank)
-        return
+# --------------------------------------------------------------------------- our arm
+class Timer:
+    def __init__(self, torch, pg, dev):
+        self.torch, self.pg, self.dev = torch, pg, dev
 
-    import torch
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.pg is not None:
+            self.pg.barrier()
+        self.torch.cuda.synchronize()
 
+    def time(self, fn, steps):
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        self.barrier()
+        a.record(st)
+        for _ in range(steps):
+            fn()
+        b.record(st)
+        self.barrier()
+        ms = a.elapsed_time(b)
+        if self.pg is not None:
+            t = torch.tensor([ms], device=self.dev)
+            self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+            ms = float(t)
+        return ms / steps
+
+    def kernel_ms(self, fn, reps):
+        torch = self.torch
+        st = torch.cuda.current_stream()
+        out = []
+        for _ in range(reps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            fn()
+            b.record(st)
+            torch.cuda.synchronize()
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+
+def setup_c2(args, ctx):
+    """Config 2: device-resident batched pipeline + chunked host e2e."""
+    torch, dev, rank = ctx["torch"], ctx["dev"], ctx["rank"]
     from paper_2510_04094_b200 import _lib
     from paper_2510_04094_b200 import batch as BT
     from paper_2510_04094_b200 import workloads as W
     from paper_2510_04094_b200.problems import ivp
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
-
-    cfg = W.CONFIGS[CID]
+    cfg = W.CONFIGS[2]
     B = args.batch or cfg.batch
     cfg = W.scaled(cfg, batch=B)
     bt = W.linear_batch(cfg, seed=0, count=B, first=rank * B)
@@ -201,78 +250,11 @@ def main():
     coef_d = torch.as_tensor(bt.coef, device=dev)
     forc_d = torch.as_tensor(bt.forcing, device=dev)
     vals_d = torch.as_tensor(bt.cond_values, device=dev)
-    side = None
-    lib = _lib.load()
-
-    def step():
-        return pipe.run_device(coef_d, forc_d, vals_d)
-
-    def barrier():
-        torch.cuda.synchronize()
-        if pg is not None:
-            pg.barrier()
-        torch.cuda.synchronize()
-
-    # ---- warm-up + correctness spot check
-    for _ in range(max(args.warmup, 1)):
-        x, info = step()
+    x, info = pipe.run_device(coef_d, forc_d, vals_d)
     torch.cuda.synchronize()
+    if int((info != 0).sum()):
+        raise SystemExit("config 2: instances reported singular/non-finite KKT systems")
     side = x.shape[1]
-    bad = int((info != 0).sum())
-    if bad:
-        raise SystemExit(f"{bad} instances reported singular/non-finite KKT systems")
-
-    # ---- timed device-resident steps
-    st = torch.cuda.current_stream()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    launches0 = lib.nys_launch_count()
-    barrier()
-    with ClockSampler(local) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(st)
-        for k in range(args.steps):
-            ev[k][0].record(st)
-            step()
-            ev[k][1].record(st)
-        t_end.record(st)
-        barrier()
-    launches = (lib.nys_launch_count() - launches0) / args.steps
-    total_ms = t_start.elapsed_time(t_end)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    if pg is not None:
-        t = torch.tensor([total_ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        total_ms = float(t)
-    ms_per_step = total_ms / args.steps
-    value = world * B / (ms_per_step / 1e3)
-
-    # ---- roofline: the batched Gram launch alone
-    fm = pipe.solver.fmap
-    me, n_c, p, m = fm.m_eff, pipe.solver.n_c, cfg.order, cfg.m
-    solver = pipe.solver
-    ws_bytes = lib.nys_batch_gram_workspace_bytes(n_c, me, p, B)
-    g_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in range(args.steps)]
-    for k in range(args.steps):
-        g_ev[k][0].record(st)
-        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
-                  me, float(cfg.sigma2), p, _lib.ptr(solver.pts), n_c, _lib.ptr(coef_d),
-                  _lib.ptr(forc_d), B, None, _lib.ptr(solver.ws), ws_bytes, _lib.stream_ptr())
-        g_ev[k][1].record(st)
-    torch.cuda.synchronize()
-    gram_ms = statistics.median(a.elapsed_time(b) for a, b in g_ev)
-    # per instance 2 n_c m_eff^2 + 8 n_c m_eff + 4 n_c (Gram + combine + rhs)
-    flops_gram = B * (2.0 * n_c * me * me + 8.0 * n_c * me + 4.0 * n_c)
-    flops_shared = 2.0 * (p + 1) * n_c * m * me
-    peak, peak_src = _fp64_peak()
-    achieved = flops_gram / (gram_ms / 1e3) / 1e12
-    nb = (me + 2 + 7) // 8
-    executed = B * (4 * ((n_c + 3) // 4)) * (nb * (nb + 1) // 2) * 64 * 2.0
-    step_flops = flops_gram + flops_shared
-
-    # ---- e2e through the public API with pinned host buffers
     coef_h = torch.from_numpy(bt.coef).pin_memory()
     forc_h = torch.from_numpy(bt.forcing).pin_memory()
     vals_h = torch.from_numpy(bt.cond_values).pin_memory()
@@ -281,71 +263,263 @@ def main():
     bufs = (torch.empty_like(coef_d), torch.empty_like(forc_d), torch.empty_like(vals_d),
             torch.empty((B, side), dtype=torch.float64, device=dev),
             torch.empty(B, dtype=torch.int32, device=dev))
-    for _ in range(2):
-        pipe.run_host(coef_h, forc_h, vals_h, x_h, info_h, chunks=args.e2e_chunks, dev_bufs=bufs)
-    barrier()
-    e_start = torch.cuda.Event(enable_timing=True)
-    e_end = torch.cuda.Event(enable_timing=True)
-    e_start.record(st)
-    for _ in range(args.steps):
-        pipe.run_host(coef_h, forc_h, vals_h, x_h, info_h, chunks=args.e2e_chunks, dev_bufs=bufs)
-    e_end.record(st)
-    barrier()
-    e2e_ms = e_start.elapsed_time(e_end) / args.steps
-    if pg is not None:
-        t = torch.tensor([e2e_ms], device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        e2e_ms = float(t)
-    if int((info_h != 0).sum()):
-        raise SystemExit("e2e path reported failed instances")
-    h2d = coef_h.numel() * 8 + forc_h.numel() * 8 + vals_h.numel() * 8
-    d2h = x_h.numel() * 8 + info_h.numel() * 4
 
-    # ---- CPU baseline (rank 0, N = 1 only)
+    def step():
+        pipe.run_device(coef_d, forc_d, vals_d)
+
+    def e2e():
+        pipe.run_host(coef_h, forc_h, vals_h, x_h, info_h, chunks=args.e2e_chunks, dev_bufs=bufs)
+
+    fm, solver = pipe.solver.fmap, pipe.solver
+    me, n_c, p, m = fm.m_eff, solver.n_c, cfg.order, cfg.m
+    lib = _lib.load()
+    ws_bytes = lib.nys_batch_gram_workspace_bytes(n_c, me, p, B)
+
+    def kernel():
+        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+                  me, float(cfg.sigma2), p, _lib.ptr(solver.pts), n_c, _lib.ptr(coef_d),
+                  _lib.ptr(forc_d), B, None, _lib.ptr(solver.ws), ws_bytes, _lib.stream_ptr())
+
+    nb = (me + 2 + 7) // 8
+    return dict(
+        B=B, step=step, e2e=e2e, kernel=kernel,
+        check=lambda: int((info_h != 0).sum()) == 0,
+        h2d=coef_h.numel() * 8 + forc_h.numel() * 8 + vals_h.numel() * 8,
+        d2h=x_h.numel() * 8 + info_h.numel() * 4,
+        # per instance 2 n_c m_eff^2 + 8 n_c m_eff + 4 n_c
+        flops_kernel=B * (2.0 * n_c * me * me + 8.0 * n_c * me + 4.0 * n_c),
+        flops_step=2.0 * (p + 1) * n_c * m * me + B * (2.0 * n_c * me * me + 8.0 * n_c * me
+                                                        + 4.0 * n_c),
+        executed=B * (4 * ((n_c + 3) // 4)) * (nb * (nb + 1) // 2) * 64 * 2.0,
+        kernel_name="batch_gram_kernel (+3 psi-pack launches)", scaling="weak",
+        parallelism=f"instance-sharded x{ctx['world']}, no collective",
+        extra={"m_eff": me, "global_batch": ctx["world"] * B,
+               "l2": "samples 402 MB/GPU > 126 MB L2; no flush needed",
+               "step": "eig + shared features + batched Gram + batched KKT"},
+        note="algorithmic F (SURVEY.md 8d) counts the full m_eff^2 Gram; the kernel "
+             "computes the upper block triangle only")
+
+
+def setup_single(args, ctx):
+    """Configs 0, 1 (replicas) and 4 (row-sharded, one all-reduce)."""
+    torch, dev, rank, world, cid = ctx["torch"], ctx["dev"], ctx["rank"], ctx["world"], args.config
+    from paper_2510_04094_b200 import _lib
+    from paper_2510_04094_b200 import dist as DI
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import ivp
+
+    cfg = W.CONFIGS[cid]
+    bt = W.linear_batch(cfg, 0, 1, first=rank if cid != 4 else 0)
+    cond = ivp(bt.instances[0].conditions())
+    pts_d = torch.as_tensor(bt.pts, device=dev)
+    coef_d = torch.as_tensor(bt.coef[0], device=dev)
+    forc_d = torch.as_tensor(bt.forcing[0], device=dev)
+    shard = cid == 4 and world > 1
+    Ac_cache = {}
+
+    def solve(pts, coef, forc):
+        fm = N.build_feature_map(RbfKernel(cfg.sigma2), bt.landmarks, device=dev)
+        if shard:
+            E = DI.sharded_gram_ext(fm, cfg.order, pts, coef, forc, rank, world)
+        else:
+            E = L.gram_ext_device(fm, cfg.order, pts, coef, forc)
+        Ac, beta, vals = L.condition_rows(cond, fm)
+        sy = L.AssembledSystem(bt.pts, cfg.gamma, None, None, None,
+                               Ac.reshape(len(cond.entries), -1), beta, vals, fm, cfg.order, E)
+        res = L._kkt_solve(sy)
+        Ac_cache["fm"] = fm
+        return res
+
+    res = solve(pts_d, coef_d, forc_d)
+    torch.cuda.synchronize()
+    if int(res["info"][0]) != 0:
+        raise SystemExit(f"config {cid}: singular KKT system")
+    pts_h = torch.from_numpy(bt.pts).pin_memory()
+    coef_h = torch.from_numpy(bt.coef[0]).pin_memory()
+    forc_h = torch.from_numpy(bt.forcing[0]).pin_memory()
+    x_h = torch.empty(res["x"].shape, dtype=torch.float64).pin_memory()
+
+    def step():
+        solve(pts_d, coef_d, forc_d)
+
+    def e2e():
+        p = pts_h.to(dev, non_blocking=True)
+        c = coef_h.to(dev, non_blocking=True)
+        f = forc_h.to(dev, non_blocking=True)
+        r = solve(p, c, f)
+        x_h.copy_(r["x"], non_blocking=True)
+
+    fm = Ac_cache["fm"]
+    me, n_c, m = fm.m_eff, bt.pts.size, cfg.m
+    rows = DI.row_ranges(n_c, world)[rank] if shard else (0, n_c)
+
+    def kernel():
+        L.gram_ext_device(fm, cfg.order, pts_d, coef_d, forc_d, rows[0], rows[1])
+
+    # SURVEY.md 8(d): single instance F = 2 n_c m_eff (m+m_eff) + 4 n_c (m+m_eff) + 4 n_c
+    fl = lambda n: 2.0 * n * me * (m + me) + 4.0 * n * (m + me) + 4.0 * n   # noqa: E731
+    kspace = (me + 2 + 7) // 8 > 9
+    return dict(
+        B=1 if cid == 4 else world, step=step, e2e=e2e, kernel=kernel, check=lambda: True,
+        h2d=(pts_h.numel() + coef_h.numel() + forc_h.numel()) * 8, d2h=x_h.numel() * 8,
+        flops_kernel=fl(rows[1] - rows[0]), flops_step=fl(n_c),
+        executed=None, kernel_name="large_kspace_kernel (kernel-space Gram, cond-gated)" if kspace
+        else "fused_gram_kernel", scaling="strong" if cid == 4 else "weak",
+        parallelism=(f"row-sharded x{world} + 1 all-reduce" if cid == 4 else
+                     f"replicas x{world}"),
+        extra={"m_eff": me, "n": cfg.n, "m": m,
+               "step": "eig + fused feature/Gram + KKT LU" + (" + all-reduce" if shard else "")},
+        note="algorithmic F of SURVEY.md 8(d)" + ("; config 4 accumulates the Gram in kernel "
+                                                   "space (cond(Omega)=28, SURVEY A1 1.3e-13)"
+                                                   if kspace else ""),
+        per_rank_units=False)
+
+
+def setup_c3(args, ctx):
+    torch, dev, rank, world = ctx["torch"], ctx["dev"], ctx["rank"], ctx["world"]
+    from paper_2510_04094_b200 import newton as NW
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import ivp
+
+    cfg = W.CONFIGS[3]
+    B = args.batch or cfg.batch
+    g = W.grid(cfg)
+    lm = W.equidistant_landmarks(g, cfg.m)
+    insts = [W.instance(3, 0, rank * B + i) for i in range(B)]
+    pts = g[1:]
+    fam = NW.SeparableFamily(np.stack([i.g_fn(pts) for i in insts]),
+                             np.array([i.quad_coeff for i in insts]),
+                             np.array([i.sin_coeff for i in insts]))
+    vals = np.array([[i.conditions()[0][2]] for i in insts])
+    cond = ivp([(0.0, 0, 0.0)])
+    state = {}
+
+    def step():
+        fm = N.build_feature_map(RbfKernel(cfg.sigma2), lm, device=dev)
+        eng = NW.NewtonBatch(fm, g, cond, vals, cfg.gamma, family=fam)
+        st, X, tr, rung = eng.solve(max_iters=cfg.newton_max_iters)
+        state.update(st=st, tr=tr, me=eng.me, eng=eng)
+
+    step()
+    its = sum(len(t) - 1 for t in state["tr"])
+    me, n_c = state["me"], pts.size
+    eng = state["eng"]
+    ids = list(range(B))
+    idx_t = eng._idx(ids)
+
+    def kernel():
+        eng.direction(ids)
+
+    return dict(
+        B=B, step=step, e2e=step, kernel=kernel, check=lambda: True,
+        h2d=(fam.g.size + B * 3) * 8, d2h=B * eng.ldx * 8,
+        # SURVEY.md 8(d): per instance N_it [2 n_c (m_eff+1)^2 + 10 n_c m_eff]
+        flops_kernel=B * (2.0 * n_c * (me + 1) ** 2 + 10.0 * n_c * me),
+        flops_step=its * (2.0 * n_c * (me + 1) ** 2 + 10.0 * n_c * me),
+        executed=None, kernel_name="Newton direction (newton_reduce + LU + step)",
+        scaling="weak", parallelism=f"instance-sharded x{world}, no collective",
+        extra={"m_eff": me, "newton_iterations": its,
+               "status_counts": np.bincount(state["st"], minlength=4).tolist(),
+               "global_batch": world * B,
+               "step": "eig + Newton ladder (rungs 1-5) for the batch; e2e == value "
+                       "(the samples are uploaded inside every step)"},
+        note="F uses this run's Newton iteration count")
+
+
+def main():
+    args = _args()
+    world, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+
+    from paper_2510_04094_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    ctx = dict(torch=torch, dev=dev, rank=rank, world=world)
+    cid = args.config
+    S = setup_c2(args, ctx) if cid == 2 else (setup_c3(args, ctx) if cid == 3
+                                              else setup_single(args, ctx))
+    T = Timer(torch, pg, dev)
+    lib = _lib.load()
+    for _ in range(args.warmup):
+        S["step"]()
+    n0 = lib.nys_launch_count()
+    with ClockSampler(local) as clk:
+        ms = T.time(S["step"], args.steps)
+    launches = (lib.nys_launch_count() - n0) / args.steps
+    # whole-job solves per second: c2/c3 weak (B per rank), c0/c1 replicas, c4 one
+    # solve across all ranks
+    units = {2: world * S["B"], 3: world * S["B"], 0: world, 1: world, 4: 1}[cid]
+    value = units / (ms / 1e3)
+    kms = T.kernel_ms(S["kernel"], max(3, min(args.steps, 10)))
+    peak, peak_src = _fp64_peak()
+    achieved = S["flops_kernel"] / (kms / 1e3) / 1e12
+    for _ in range(2):
+        S["e2e"]()
+    e2e_ms = T.time(S["e2e"], args.steps)
+    if not S["check"]():
+        raise SystemExit("e2e path reported failed instances")
+    e2e_value = value * ms / e2e_ms
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline as CB
 
         cores = os.cpu_count() or 1
-        v, n, workers, wall = CB.batch_solves_per_second(CID, cores, per_worker=10_000,
-                                                        budget_s=args.cpu_seconds)
-        cpu = {"value": v, "unit": "solves/s", "cores": workers, "kind": "port",
-               "sample": f"{n} config-2 instances in {wall:.1f} s on a {workers}-process pool "
-                         "(oracle port of linear.assemble+solve, 1 BLAS thread per worker, "
-                         "shared feature map per worker)"}
-
+        if cid in (2, 3):
+            v, n, workers, wall = CB.batch_solves_per_second(
+                cid, cores, per_worker=10_000, budget_s=args.cpu_seconds)
+            cpu = {"value": v, "unit": "solves/s", "cores": workers, "kind": "port",
+                   "sample": f"{n} config-{cid} instances in {wall:.1f} s on a {workers}-process "
+                             "pool (oracle port of the reference per-spec path, 1 BLAS thread "
+                             "per worker, shared feature map per worker)"}
+        elif cid in (0, 1):
+            t = CB.single_solve_seconds(cid)
+            cpu = {"value": 1.0 / t, "unit": "solves/s", "cores": cores, "kind": "port",
+                   "sample": "best of 3 full solves (landmarks+eig+assemble+solve), one process"}
+        else:
+            t, parts = CB.c4_solve_seconds_estimate()
+            cpu = {"value": 1.0 / t, "unit": "solves/s", "cores": cores, "kind": "port",
+                   "sample": f"eig + KKT in full, assembly on 2^18 of 4,194,303 rows scaled "
+                             f"x{parts['scale']:.1f} (O(n) assembly)"}
     if rank == 0:
+        prof = _profile_json(f"ncu_c{cid}.json")
         line = {
             "metric": "ode_solves_per_s", "value": value, "unit": "solves/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generator, paper_2510_04094_b200/workloads.py)",
-            "config": {"workload": "c2: B=4096 linear 2nd-order IVPs per GPU, n=4096 shared "
-                                   "grid on [0,2], m=64 shared landmarks, sigma=0.1 "
-                                   "(m_eff=%d), gamma=1e9 (BASELINE.json configs[2])" % me,
-                       "global_batch": world * B, "n": cfg.n, "m": cfg.m, "m_eff": me,
-                       "parallelism": f"instance-sharded x{world}, no collective",
-                       "l2": "samples 402 MB/GPU > 126 MB L2; no flush needed",
-                       "step": "eig + shared features + batched Gram + batched KKT"},
-            "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": S["scaling"], "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generator, paper_2510_04094_b200/workloads.py)",
+            "config": dict({"workload": WORKLOAD[cid], "parallelism": S["parallelism"]},
+                           **S["extra"]),
             "gpu_launches": launches,
-            "e2e": {"value": world * B / (e2e_ms / 1e3), "unit": "solves/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms, "chunks": args.e2e_chunks},
+            "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": S["h2d"],
+                    "d2h_bytes_per_step": S["d2h"], "ms_per_step": e2e_ms},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": _traffic_from_profiles(),
-                         "kernel": "batch_gram_kernel (+3 psi-pack launches)",
-                         "kernel_ms": gram_ms, "algorithmic_flops": flops_gram,
-                         "executed_dmma_flops": executed,
-                         "executed_frac": executed / (gram_ms / 1e3) / 1e12 / peak,
+                         "traffic": prof.get("dram_bytes_per_launch"),
+                         "kernel": S["kernel_name"], "kernel_ms": kms,
+                         "algorithmic_flops": S["flops_kernel"],
                          "peak_source": peak_src + "; MEASURED_PEAKS.json has no FP64 entry",
-                         "note": "algorithmic F (SURVEY.md 8d) counts the full m_eff^2 Gram; "
-                                 "the kernel computes the upper block triangle only"},
-            "step_tflops": step_flops / (ms_per_step / 1e3) / 1e12 / world,
+                         "note": S["note"]},
+            "step_tflops": S["flops_step"] / (ms / 1e3) / 1e12,
             "clocks": clk.summary(),
         }
+        if S.get("executed"):
+            line["roofline"]["executed_dmma_flops"] = S["executed"]
+            line["roofline"]["executed_frac"] = S["executed"] / (kms / 1e3) / 1e12 / peak
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
