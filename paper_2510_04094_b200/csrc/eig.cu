@@ -22,6 +22,12 @@
 
 #include "common.cuh"
 
+namespace nys_host {
+bool jacobi_small_fits(int m);
+int launch_jacobi_small(const double* lm, int m, double sigma2, double drop_tol, double* eigvals,
+                        double* eigvecs, double* W, int* m_eff, int* info, cudaStream_t st);
+}  // namespace nys_host
+
 namespace {
 
 constexpr int kEigThreads = 1024;
@@ -320,6 +326,12 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
                                     size_t workspace_bytes, void* stream) {
   if (m < 1 || m > kMaxM || !(sigma2 > 0.0) || !(drop_tol >= 0.0 && drop_tol < 1.0))
     return NYS_EINVAL;
+  // small landmark sets: shared-memory Jacobi with FP32 angles (eig_jacobi.cu);
+  // NYS_EIG_ALGO=ql forces the tridiagonal QL path (diagnostics / A-B tests)
+  const char* algo = getenv("NYS_EIG_ALGO");
+  if (nys_host::jacobi_small_fits(m) && !(algo && algo[0] == 'q'))
+    return nys_host::launch_jacobi_small(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W,
+                                         m_eff, info, static_cast<cudaStream_t>(stream));
   const size_t need = eig_storage_bytes(m);
   const int use_smem = need <= kEigSmemMax;
   double *gA = nullptr, *gZ = nullptr;
