@@ -21,6 +21,7 @@ namespace {
 constexpr int kJThreads = 512;
 constexpr int kTPP = 8;          // threads per rotation pair (one quarter warp)
 constexpr int kMaxSweeps = 60;
+constexpr int kRows = (112 + kTPP - 1) / kTPP;   // rows (columns) per thread per phase
 
 __global__ void __launch_bounds__(kJThreads, 1)
     jacobi_small_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(kJThreads, 1)
   const double tol = 2.220446049250313e-16 * sqrt(fro2);
 
   const int M = (m + 1) & ~1, half = M / 2;
-  const int grp = tid / kTPP, gl = tid % kTPP, ngrp = nt / kTPP;
+  const int grp = tid / kTPP, gl = tid % kTPP;
   int sweeps = 0;
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     ++sweeps;
@@ -107,26 +108,51 @@ __global__ void __launch_bounds__(kJThreads, 1)
           }
         }
       }
-      if (s != 0.0)
-        for (int i = gl; i < m; i += kTPP) {   // A <- A J (columns p, q)
-          double* row = A + (size_t)i * lda;
-          const double ap = row[p], aq = row[q];
-          row[p] = c * ap - s * aq;
-          row[q] = s * ap + c * aq;
+      // all loads of a phase are issued before any store: the compiler cannot
+      // prove the rows disjoint, so a load/compute/store loop would serialise on
+      // shared-memory + FP64 latency (ncu: short_scoreboard dominated)
+      if (s != 0.0) {   // A <- A J (columns p, q)
+        double ap[kRows], aq[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const int i = gl + u * kTPP;
+          ap[u] = i < m ? A[(size_t)i * lda + p] : 0.0;
+          aq[u] = i < m ? A[(size_t)i * lda + q] : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const int i = gl + u * kTPP;
+          if (i < m) {
+            A[(size_t)i * lda + p] = c * ap[u] - s * aq[u];
+            A[(size_t)i * lda + q] = s * ap[u] + c * aq[u];
+          }
+        }
+      }
       __syncthreads();
-      if (s != 0.0) {
+      if (s != 0.0) {   // A <- J^T A, V^T <- J^T V^T (rows p, q)
         double* rp = A + (size_t)p * lda;
         double* rq = A + (size_t)q * lda;
         double* vp = VT + (size_t)p * m;
         double* vq = VT + (size_t)q * m;
-        for (int j = gl; j < m; j += kTPP) {   // A <- J^T A, V^T <- J^T V^T (rows p, q)
-          const double ap = rp[j], aq = rq[j];
-          rp[j] = c * ap - s * aq;
-          rq[j] = s * ap + c * aq;
-          const double xv = vp[j], yv = vq[j];
-          vp[j] = c * xv - s * yv;
-          vq[j] = s * xv + c * yv;
+        double ap[kRows], aq[kRows], xv[kRows], yv[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const int j = gl + u * kTPP;
+          const bool ok = j < m;
+          ap[u] = ok ? rp[j] : 0.0;
+          aq[u] = ok ? rq[j] : 0.0;
+          xv[u] = ok ? vp[j] : 0.0;
+          yv[u] = ok ? vq[j] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const int j = gl + u * kTPP;
+          if (j < m) {
+            rp[j] = c * ap[u] - s * aq[u];
+            rq[j] = s * ap[u] + c * aq[u];
+            vp[j] = c * xv[u] - s * yv[u];
+            vq[j] = s * xv[u] + c * yv[u];
+          }
         }
       }
       __syncthreads();
