@@ -21,8 +21,7 @@ namespace {
 constexpr int kJThreads = 512;
 constexpr int kTPP = 8;          // threads per rotation pair (one quarter warp)
 constexpr int kMaxSweeps = 60;
-constexpr int kRows = (112 + kTPP - 1) / kTPP;   // rows (columns) per thread per phase
-
+template <int kRows>   // rows (columns) per thread per phase: ceil(m / kTPP)
 __global__ void __launch_bounds__(kJThreads, 1)
     jacobi_small_kernel(const double* __restrict__ lm, int m, double sigma2, double drop_tol,
                         double* __restrict__ eigvals, double* __restrict__ eigvecs,
@@ -201,14 +200,16 @@ bool jacobi_small_fits(int m) {
 int launch_jacobi_small(const double* lm, int m, double sigma2, double drop_tol, double* eigvals,
                         double* eigvecs, double* W, int* m_eff, int* info, cudaStream_t st) {
   const size_t dyn = 2 * (size_t)m * (m + 1) * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(jacobi_small_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  const int rows = (m + kTPP - 1) / kTPP;
+  auto kern = rows <= 3 ? jacobi_small_kernel<3>
+                        : (rows <= 6 ? jacobi_small_kernel<6>
+                                     : (rows <= 8 ? jacobi_small_kernel<8> : jacobi_small_kernel<14>));
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return record_cuda(e);
   int threads = ((m + 1) / 2) * kTPP;
   threads = (threads + 31) / 32 * 32;
   if (threads > kJThreads) threads = kJThreads;
-  jacobi_small_kernel<<<1, threads, dyn, st>>>(lm, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff,
-                                               info);
+  kern<<<1, threads, dyn, st>>>(lm, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info);
   count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
