@@ -328,8 +328,11 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
     return NYS_EINVAL;
   // small landmark sets: shared-memory Jacobi with FP32 angles (eig_jacobi.cu);
   // NYS_EIG_ALGO=ql forces the tridiagonal QL path (diagnostics / A-B tests)
+  // (measured on B200: Jacobi wins at m = 20, 0.25 vs 0.32 ms; QL wins from
+  // m = 50, 0.87 vs 1.05 ms, and at m = 64, 1.27 vs 1.50 ms)
   const char* algo = getenv("NYS_EIG_ALGO");
-  if (nys_host::jacobi_small_fits(m) && !(algo && algo[0] == 'q'))
+  const bool force_ql = algo && algo[0] == 'q', force_jac = algo && algo[0] == 'j';
+  if (nys_host::jacobi_small_fits(m) && !force_ql && (m <= 32 || force_jac))
     return nys_host::launch_jacobi_small(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W,
                                          m_eff, info, static_cast<cudaStream_t>(stream));
   const size_t need = eig_storage_bytes(m);
