@@ -50,6 +50,19 @@ class LinearBatchSolver:
         self.ws_bytes = lib.nys_batch_gram_workspace_bytes(self.n_c, fmap.m_eff, self.order,
                                                           self.max_batch)
         self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.cond_pts = _lib.as_f64([bc.point for bc in cond.entries], dev)
+
+    def refresh_condition_rows(self):
+        """A_c[mu] = phi^(order_mu)(point_mu) written straight into the device
+        buffer (linear.py:56-63), no host round trip; beta depends only on the
+        orders and is unchanged."""
+        fm = self.fmap
+        st = _lib.stream_ptr()
+        for mu, bc in enumerate(self.cond.entries):
+            _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W),
+                      fm.m, fm.m_eff, float(fm.kernel.sigma2), int(bc.order),
+                      _lib.ptr(self.cond_pts) + 8 * mu, 1, _lib.ptr(self.Ac) + 8 * mu * fm.m_eff,
+                      fm.m_eff, st)
 
     def solve_device(self, coef, forcing, values, out_x=None, out_info=None):
         """coef (B, p, n_c), forcing (B, n_c), values (B, n_cond) device float64
@@ -167,12 +180,10 @@ class SharedGridPipeline:
         if self.solver is None or self.solver.fmap.m_eff != fm.m_eff:
             self.solver = LinearBatchSolver(fm, self.grid, self.gamma, self.order, self.cond,
                                             self.max_batch)
-        else:   # same shapes: keep the workspace, refresh the feature map state
+        else:   # same shapes: keep the workspace, refresh the condition rows on device
             s = self.solver
             s.fmap = fm
-            Ac, beta, _ = condition_rows(self.cond, fm)
-            s.Ac.copy_(_lib.as_f64(Ac.reshape(s.n_cond, fm.m_eff), fm.device))
-            s.beta.copy_(_lib.as_f64(beta, fm.device))
+            s.refresh_condition_rows()
         return self.solver
 
     def run_device(self, coef, forcing, values, out_x=None, out_info=None):
