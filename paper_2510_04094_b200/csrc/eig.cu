@@ -23,6 +23,12 @@
 #include "common.cuh"
 
 namespace nys_host {
+size_t dc_buffer_bytes(int n);
+bool dc_fits(int n);
+bool dc_uses_smem(int n);
+int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, double* eigvals,
+                  double* eigvecs, double* W, int* m_eff, int* info, void* ws, size_t ws_bytes,
+                  cudaStream_t st);
 bool jacobi_small_fits(int m);
 int launch_jacobi_small(const double* lm, int m, double sigma2, double drop_tol, double* eigvals,
                         double* eigvecs, double* W, int* m_eff, int* info, cudaStream_t st);
@@ -317,7 +323,9 @@ constexpr size_t kEigSmemMax = 160 * 1024;   // + ~30 KB static bookkeeping
 extern "C" size_t nys_landmark_eig_workspace_bytes(int m) {
   if (m <= 0) return 0;
   size_t need = eig_storage_bytes(m);
-  return need <= kEigSmemMax ? 0 : need;
+  size_t ql = need <= kEigSmemMax ? 0 : need;
+  size_t dc = nys_host::dc_fits(m) && !nys_host::dc_uses_smem(m) ? nys_host::dc_buffer_bytes(m) : 0;
+  return ql > dc ? ql : dc;
 }
 
 extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma2,
@@ -330,11 +338,17 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
   // NYS_EIG_ALGO=ql forces the tridiagonal QL path (diagnostics / A-B tests)
   // (measured on B200: Jacobi wins at m = 20, 0.25 vs 0.32 ms; QL wins from
   // m = 50, 0.87 vs 1.05 ms, and at m = 64, 1.27 vs 1.50 ms)
+  // default: divide and conquer (eig_dc.cu, m <= 256); NYS_EIG_ALGO = ql | jacobi
+  // select the alternatives for diagnostics / A-B tests
   const char* algo = getenv("NYS_EIG_ALGO");
   const bool force_ql = algo && algo[0] == 'q', force_jac = algo && algo[0] == 'j';
-  if (nys_host::jacobi_small_fits(m) && !force_ql && (m <= 32 || force_jac))
+  if (force_jac && nys_host::jacobi_small_fits(m))
     return nys_host::launch_jacobi_small(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W,
                                          m_eff, info, static_cast<cudaStream_t>(stream));
+  if (!force_ql && !force_jac && nys_host::dc_fits(m))
+    return nys_host::launch_dc_eig(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff,
+                                   info, workspace, workspace_bytes,
+                                   static_cast<cudaStream_t>(stream));
   const size_t need = eig_storage_bytes(m);
   const int use_smem = need <= kEigSmemMax;
   double *gA = nullptr, *gZ = nullptr;

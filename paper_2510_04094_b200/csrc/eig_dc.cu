@@ -1,0 +1,603 @@
+// Landmark eigendecomposition, divide and conquer (the route of the
+// reference's LAPACK dsyevd, nystrom.py:150): Householder tridiagonalisation,
+// Cuppen tears at every multiple of kLeaf, leaves by implicit QL (one thread
+// each, in parallel), then log2(m / kLeaf) merge levels, each a rank-one
+// update diag(D) + rho z z^T solved by
+//   * deflation of negligible z_i and of close pairs (Givens rotation),
+//   * one thread per secular-equation root (two-pole rational iteration with
+//     a bisection bracket, in the coordinates of the nearer pole so d_i - lambda_j
+//     is formed without cancellation),
+//   * Gu-Eisenstat recomputation of z (Loewner formula) so the eigenvectors are
+//     orthogonal to working precision,
+//   * one GEMM per block for the new eigenvectors,
+// and finally the Householder back-transform.  Everything is parallel except
+// the (short) leaf QL chains and the per-block deflation scan -- unlike QL on the
+// full tridiagonal, whose ~m^2 dependent Givens rotations are FP64-latency bound
+// on B200 (1.2 ms at m = 64, 31 ms at m = 256).
+// Epilogue identical to eig.cu: descending order (ties: higher index first,
+// nystrom.py:151), drop rule s > max(drop_tol s_0, 0), W = V / sqrt(s).
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kLeaf = 8;
+constexpr int kDcMaxN = 256;
+constexpr int kDcThreads = 1024;
+constexpr int kMaxBlocks = kDcMaxN / kLeaf;
+constexpr double kEps = 2.220446049250313e-16;
+
+struct DcShared {
+  double d[kDcMaxN], e[kDcMaxN], beta[kDcMaxN], hv[kDcMaxN], hp[kDcMaxN];
+  double lam[kDcMaxN];    // eigenvalues aligned with the columns of Q
+  double ds[kDcMaxN];     // per block: sorted (sign-adjusted) D, deflation-modified
+  double zs[kDcMaxN];     // per block: sorted z (normalised), deflation-modified
+  double zh[kDcMaxN];     // per block: Gu-Eisenstat z over the kept entries
+  double rotc[kDcMaxN], rots[kDcMaxN];
+  int perm[kDcMaxN];      // per block: sorted index -> global column
+  int keep[kDcMaxN];      // per block: kept sorted indices (ascending), then deflated
+  int roti[kDcMaxN], rotj[kDcMaxN];
+  double rho[kMaxBlocks], sgn[kMaxBlocks];
+  int K[kMaxBlocks], nrot[kMaxBlocks];
+  int bs[kMaxBlocks], bmid[kMaxBlocks], be[kMaxBlocks];   // merge: start, boundary, end
+  double red[kDcThreads / 32];
+  int degenerate;
+};
+
+NYS_DEV double dc_block_sum(double x, DcShared& S) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if (lane == 0) S.red[w] = x;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += S.red[i];
+  return s;
+}
+
+// implicit QL on the leaf [s, s+len) of (d, e), eigenvectors into Q block
+NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
+  double* d = S.d + s;
+  double* e = S.e + s;   // e[i] couples i, i+1 inside the leaf; e[len-1] is unused
+  double ehold = len > 0 ? e[len - 1] : 0.0;
+  if (len > 0) e[len - 1] = 0.0;
+  for (int r = 0; r < len; ++r)
+    for (int c = 0; c < len; ++c) Q[(size_t)(s + r) * n + s + c] = (r == c) ? 1.0 : 0.0;
+  for (int l = 0; l < len; ++l) {
+    for (int iter = 0; iter < 60; ++iter) {
+      int mm = l;
+      for (; mm < len - 1; ++mm) {
+        const double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+        if (fabs(e[mm]) <= kEps * dd) break;
+      }
+      if (mm == l) break;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+      double sn = 1.0, cs = 1.0, p = 0.0;
+      int i = mm - 1;
+      bool early = false;
+      for (; i >= l; --i) {
+        const double f = sn * e[i], b = cs * e[i];
+        r = hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          early = true;
+          break;
+        }
+        sn = f / r;
+        cs = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * sn + 2.0 * cs * b;
+        p = sn * r;
+        d[i + 1] = g + p;
+        g = cs * r - b;
+        for (int k = 0; k < len; ++k) {   // columns i, i+1 of the leaf's Z
+          double* row = Q + (size_t)(s + k) * n + s;
+          const double zf = row[i + 1], zi = row[i];
+          row[i + 1] = sn * zi + cs * zf;
+          row[i] = cs * zi - sn * zf;
+        }
+      }
+      if (early) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  if (len > 0) e[len - 1] = ehold;
+  for (int c = 0; c < len; ++c) S.lam[s + c] = d[c];
+}
+
+// secular root j of diag(ds) + rho zz^T over the K kept entries of a block;
+// writes DL[i][j] = d_i - lambda_j (i < K) and returns lambda_j
+NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, double* DL,
+                            int n) {
+  const int* kp = S.keep + s;
+  auto dk = [&](int i) { return S.ds[s + kp[i]]; };
+  auto z2 = [&](int i) {
+    const double z = S.zs[s + kp[i]];
+    return z * z;
+  };
+  int org;
+  double lo, hi;
+  if (j < K - 1) {
+    const double mid = 0.5 * (dk(j) + dk(j + 1));
+    double f = 1.0 / rho;
+    for (int i = 0; i < K; ++i) f += z2(i) / (dk(i) - mid);
+    org = f >= 0.0 ? j : j + 1;
+    lo = dk(j) - dk(org);
+    hi = dk(j + 1) - dk(org);
+  } else {
+    org = K - 1;
+    double zz = 0.0;
+    for (int i = 0; i < K; ++i) zz += z2(i);
+    lo = 0.0;
+    hi = rho * zz;
+  }
+  const double dorg = dk(org);
+  double tau = 0.5 * (lo + hi);
+  for (int it = 0; it < 80; ++it) {
+    double f = 1.0 / rho, fabs_sum = 1.0 / rho, psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    for (int i = 0; i < K; ++i) {
+      const double dl = (dk(i) - dorg) - tau;
+      const double w = 1.0 / dl;
+      const double t = z2(i) * w;
+      f += t;
+      fabs_sum += fabs(t);
+      if (j == K - 1 || i <= j) {
+        psi += t;
+        dpsi += t * w;
+      } else {
+        phi += t;
+        dphi += t * w;
+      }
+    }
+    if (f > 0.0)
+      hi = tau;
+    else
+      lo = tau;
+    if (fabs(f) <= 8.0 * kEps * fabs_sum ||
+        (hi - lo) <= 2.0 * kEps * fmax(fmax(fabs(lo), fabs(hi)), 1e-300))
+      break;
+    // two-pole rational model c + s/(dj - x) + S/(dj1 - x) (fixed weight)
+    const double dj = (dk(j) - dorg) - tau;
+    double x;
+    bool ok = false;
+    if (j < K - 1) {
+      const double dj1 = (dk(j + 1) - dorg) - tau;
+      const double sw = dj * dj * dpsi, Sw = dj1 * dj1 * dphi;
+      const double c = 1.0 / rho + psi - dj * dpsi + phi - dj1 * dphi;
+      const double A = c, B = -(c * (dj + dj1) + sw + Sw), C = c * dj * dj1 + sw * dj1 + Sw * dj;
+      if (A != 0.0) {
+        const double disc = fmax(B * B - 4.0 * A * C, 0.0);
+        const double q = -0.5 * (B + copysign(sqrt(disc), B));
+        const double r1 = q / A, r2 = q != 0.0 ? C / q : r1;
+        if (r1 > lo - tau && r1 < hi - tau) {
+          x = r1;
+          ok = true;
+        } else if (r2 > lo - tau && r2 < hi - tau) {
+          x = r2;
+          ok = true;
+        }
+      } else if (B != 0.0) {
+        x = -C / B;
+        ok = x > lo - tau && x < hi - tau;
+      }
+    } else {
+      const double sw = dj * dj * dpsi;
+      const double c = 1.0 / rho + psi - dj * dpsi;
+      if (c != 0.0) {
+        x = dj + sw / c;
+        ok = x > lo - tau && x < hi - tau;
+      }
+    }
+    const double nt = ok ? tau + x : 0.5 * (lo + hi);
+    tau = (nt > lo && nt < hi) ? nt : 0.5 * (lo + hi);
+  }
+  for (int i = 0; i < K; ++i) DL[(size_t)(s + i) * n + s + j] = (dk(i) - dorg) - tau;
+  return dorg + tau;
+}
+
+__global__ void __launch_bounds__(kDcThreads, 1)
+    dc_eig_kernel(const double* __restrict__ lm, int n, double sigma2, double drop_tol,
+                  double* __restrict__ eigvals, double* __restrict__ eigvecs,
+                  double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
+                  double* __restrict__ gbuf, int use_smem) {
+  extern __shared__ __align__(16) double dyn[];
+  __shared__ DcShared S;
+  const int ld = n + 1;
+  double* base = use_smem ? dyn : gbuf;
+  double* A = base;                           // n x ld (Householder vectors below diagonal)
+  double* Q = A + (size_t)n * ld;             // n x n
+  double* Qn = Q + (size_t)n * n;             // n x n
+  double* DL = Qn + (size_t)n * n;            // n x n
+  const int tid = threadIdx.x, nt = blockDim.x;
+
+  if (tid == 0) S.degenerate = 0;
+  __syncthreads();
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, j = e % n;
+    const double d = lm[i] - lm[j];
+    A[(size_t)i * ld + j] = nys::rbf(d, sigma2);
+    if (i != j && fabs(d) <= 1e-12) S.degenerate = 1;
+  }
+  __syncthreads();
+  if (S.degenerate) {
+    if (tid == 0) {
+      *info = NYS_INFO_DEGENERATE;
+      *m_eff_out = 0;
+    }
+    return;
+  }
+
+  // ---------------- Householder tridiagonalisation (as eig.cu phase 1)
+  for (int k = 0; k + 2 < n; ++k) {
+    const int i0 = k + 1;
+    double tail = 0.0;
+    for (int i = i0 + tid; i < n; i += nt) {
+      const double x = A[(size_t)i * ld + k];
+      S.hv[i] = x;
+      if (i != i0) tail = fma(x, x, tail);
+    }
+    tail = dc_block_sum(tail, S);
+    if (tid == 0) {
+      const double x0 = S.hv[i0];
+      double beta = 0.0, alpha = x0;
+      if (tail > 0.0) {
+        const double nx = sqrt(fma(x0, x0, tail));
+        alpha = -copysign(nx, x0);
+        const double v0 = x0 - alpha;
+        beta = 2.0 / fma(v0, v0, tail);
+        S.hv[i0] = v0;
+        A[(size_t)i0 * ld + k] = v0;
+      }
+      S.e[k] = alpha;
+      S.beta[k] = beta;
+    }
+    __syncthreads();
+    const double beta = S.beta[k];
+    if (beta == 0.0) continue;
+    for (int i = i0 + tid; i < n; i += nt) {
+      const double* row = A + (size_t)i * ld;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int j = i0;
+      for (; j + 3 < n; j += 4) {
+        a0 = fma(row[j], S.hv[j], a0);
+        a1 = fma(row[j + 1], S.hv[j + 1], a1);
+        a2 = fma(row[j + 2], S.hv[j + 2], a2);
+        a3 = fma(row[j + 3], S.hv[j + 3], a3);
+      }
+      for (; j < n; ++j) a0 = fma(row[j], S.hv[j], a0);
+      S.hp[i] = beta * ((a0 + a1) + (a2 + a3));
+    }
+    __syncthreads();
+    double vp = 0.0;
+    for (int i = i0 + tid; i < n; i += nt) vp = fma(S.hv[i], S.hp[i], vp);
+    vp = dc_block_sum(vp, S);
+    const double Kc = 0.5 * beta * vp;
+    for (int i = i0 + tid; i < n; i += nt) S.hp[i] = S.hp[i] - Kc * S.hv[i];
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = i0 + warp; i < n; i += nw) {
+      double* row = A + (size_t)i * ld;
+      const double vi = S.hv[i], wi = S.hp[i];
+      for (int j = i0 + lane; j < n; j += 32) row[j] = row[j] - vi * S.hp[j] - wi * S.hv[j];
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += nt) S.d[i] = A[(size_t)i * ld + i];
+  if (tid == 0) {
+    if (n >= 2) S.e[n - 2] = A[(size_t)(n - 1) * ld + (n - 2)];
+    S.e[n - 1] = 0.0;
+  }
+  __syncthreads();
+
+  // ---------------- tears at every multiple of kLeaf, then leaves by QL
+  if (tid == 0)
+    for (int b = kLeaf; b < n; b += kLeaf) {
+      const double rho = S.e[b - 1];
+      S.d[b - 1] -= rho;
+      S.d[b] -= rho;
+    }
+  for (int e = tid; e < n * n; e += nt) Q[e] = 0.0;
+  __syncthreads();
+  const int nleaf = (n + kLeaf - 1) / kLeaf;
+  for (int t = tid; t < nleaf; t += nt) {
+    const int s = t * kLeaf, len = min(kLeaf, n - s);
+    leaf_ql(S, Q, n, s, len);
+  }
+  __syncthreads();
+
+  // ---------------- merge levels
+  for (int width = kLeaf; width < n; width *= 2) {
+    const int nmerge = (n + 2 * width - 1) / (2 * width);
+    // block geometry; a block without a right partner is carried unchanged
+    for (int b = tid; b < nmerge; b += nt) {
+      const int s = b * 2 * width;
+      S.bs[b] = s;
+      S.bmid[b] = min(s + width, n);
+      S.be[b] = min(s + 2 * width, n);
+      const double rho = S.bmid[b] < S.be[b] ? S.e[S.bmid[b] - 1] : 0.0;
+      S.sgn[b] = rho < 0.0 ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    // M1: rank-sort the (sign-adjusted) eigenvalues of both children, gather z
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
+      if (mid >= end) continue;
+      const double sg = S.sgn[b];
+      for (int c = tid; c < N; c += nt) {
+        const double lc = sg * S.lam[s + c];
+        int rank = 0;
+        for (int c2 = 0; c2 < N; ++c2) {
+          const double l2 = sg * S.lam[s + c2];
+          rank += (l2 < lc) || (l2 == lc && c2 < c);
+        }
+        S.perm[s + rank] = s + c;
+        S.ds[s + rank] = lc;
+        S.zs[s + rank] = (s + c < mid) ? Q[(size_t)(mid - 1) * n + s + c] : Q[(size_t)mid * n + s + c];
+      }
+    }
+    __syncthreads();
+    // M2: normalise, deflate (serial scan per block)
+    for (int b = tid; b < nmerge; b += nt) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
+      if (mid >= end) continue;
+      double zn2 = 0.0, dmax = 0.0;
+      for (int i = 0; i < N; ++i) {
+        zn2 += S.zs[s + i] * S.zs[s + i];
+        dmax = fmax(dmax, fabs(S.ds[s + i]));
+      }
+      const double rho = fabs(S.e[mid - 1]) * zn2;
+      const double inv = zn2 > 0.0 ? 1.0 / sqrt(zn2) : 0.0;
+      for (int i = 0; i < N; ++i) S.zs[s + i] *= inv;
+      S.rho[b] = rho;
+      const double tol = 8.0 * kEps * fmax(dmax, rho);
+      int K = 0, nd = 0, nrot = 0, prev = -1;
+      int* keep = S.keep + s;
+      // keep[] collects kept indices from the front and deflated ones from the back
+      if (rho <= tol) {
+        for (int i = 0; i < N; ++i) keep[N - 1 - i] = i;   // all deflated
+        nd = N;
+      } else {
+        for (int i = 0; i < N; ++i) {
+          if (fabs(rho * S.zs[s + i]) <= tol) {
+            keep[N - 1 - nd++] = i;
+            continue;
+          }
+          if (prev >= 0) {
+            const double zi = S.zs[s + i], zp = S.zs[s + prev];
+            const double r = hypot(zi, zp);
+            const double c = zi / r, sn = -zp / r;
+            const double t = S.ds[s + i] - S.ds[s + prev];
+            if (fabs(t * c * sn) <= tol) {
+              const double dp = S.ds[s + prev] * c * c + S.ds[s + i] * sn * sn;
+              const double di = S.ds[s + prev] * sn * sn + S.ds[s + i] * c * c;
+              S.ds[s + prev] = dp;
+              S.ds[s + i] = di;
+              S.zs[s + i] = r;
+              S.zs[s + prev] = 0.0;
+              S.roti[s + nrot] = prev;
+              S.rotj[s + nrot] = i;
+              S.rotc[s + nrot] = c;
+              S.rots[s + nrot] = sn;
+              ++nrot;
+              // prev becomes deflated: remove it from the kept list
+              --K;
+              keep[N - 1 - nd++] = prev;
+            }
+          }
+          keep[K++] = i;
+          prev = i;
+        }
+      }
+      S.K[b] = K;
+      S.nrot[b] = nrot;
+    }
+    __syncthreads();
+    // M3: secular roots, one thread per (block, root)
+    {
+      int total = 0;
+      for (int b = 0; b < nmerge; ++b) total += (S.bmid[b] < S.be[b]) ? S.K[b] : 0;
+      for (int w = tid; w < total; w += nt) {
+        int b = 0, j = w;
+        while (j >= ((S.bmid[b] < S.be[b]) ? S.K[b] : 0)) {
+          j -= (S.bmid[b] < S.be[b]) ? S.K[b] : 0;
+          ++b;
+        }
+        const int s = S.bs[b];
+        const double lj = secular_root(S, s, j, S.K[b], S.rho[b], DL, n);
+        S.zh[s + j] = lj;   // park lambda_j (zh is rebuilt in M4 from DL)
+      }
+    }
+    __syncthreads();
+    // M4: Gu-Eisenstat z over kept entries; lambda moves to lam after M6
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
+      if (mid >= end) continue;
+      const int K = S.K[b];
+      const double rho = S.rho[b];
+      for (int i = tid; i < K; i += nt) {
+        const double di = S.ds[s + S.keep[s + i]];
+        double v = -DL[(size_t)(s + i) * n + s + K - 1] / rho;
+        for (int jj = 0; jj < K - 1; ++jj) {
+          const double dj = jj < i ? S.ds[s + S.keep[s + jj]] : S.ds[s + S.keep[s + jj + 1]];
+          v *= (-DL[(size_t)(s + i) * n + s + jj]) / (dj - di);
+        }
+        S.hv[s + i] = copysign(sqrt(fmax(v, 0.0)), S.zs[s + S.keep[s + i]]);
+      }
+    }
+    __syncthreads();
+    // M5: U[i][j] = zhat_i / (d_i - lambda_j), then unit columns
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
+      if (mid >= end) continue;
+      const int K = S.K[b];
+      for (int e = tid; e < K * K; e += nt) {
+        const int i = e / K, j = e % K;
+        double* u = DL + (size_t)(s + i) * n + s + j;
+        *u = S.hv[s + i] / *u;
+      }
+    }
+    __syncthreads();
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
+      if (mid >= end) continue;
+      const int K = S.K[b];
+      for (int j = tid; j < K; j += nt) {
+        double nrm = 0.0;
+        for (int i = 0; i < K; ++i) {
+          const double u = DL[(size_t)(s + i) * n + s + j];
+          nrm = fma(u, u, nrm);
+        }
+        S.hp[s + j] = rsqrt(nrm);
+      }
+    }
+    __syncthreads();
+    // M6: deflation rotations on the columns of Q (order matters: serial over
+    // rotations, parallel over rows)
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
+      if (mid >= end) continue;
+      const int N = end - s;
+      for (int r = tid; r < N; r += nt) {
+        double* row = Q + (size_t)(s + r) * n;
+        for (int q = 0; q < S.nrot[b]; ++q) {
+          const int cp = S.perm[s + S.roti[s + q]], ci = S.perm[s + S.rotj[s + q]];
+          const double c = S.rotc[s + q], sn = S.rots[s + q];
+          const double gp = row[cp], gi = row[ci];
+          row[cp] = c * gp + sn * gi;
+          row[ci] = -sn * gp + c * gi;
+        }
+      }
+    }
+    __syncthreads();
+    // M7: new eigenvectors: kept columns Q[:, perm[keep]] U, deflated columns copied;
+    // carried blocks copied unchanged
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
+      if (mid >= end) {
+        for (int e = tid; e < N * N; e += nt) {
+          const int r = e / N, c = e % N;
+          Qn[(size_t)(s + r) * n + s + c] = Q[(size_t)(s + r) * n + s + c];
+        }
+        continue;
+      }
+      const int K = S.K[b];
+      for (int e = tid; e < N * N; e += nt) {
+        const int r = e / N, c = e % N;
+        const double* qr = Q + (size_t)(s + r) * n;
+        double acc;
+        if (c < K) {
+          acc = 0.0;
+          for (int i = 0; i < K; ++i)
+            acc = fma(qr[S.perm[s + S.keep[s + i]]], DL[(size_t)(s + i) * n + s + c], acc);
+          acc *= S.hp[s + c];
+        } else {
+          acc = qr[S.perm[s + S.keep[s + c]]];
+        }
+        Qn[(size_t)(s + r) * n + s + c] = acc;
+      }
+    }
+    __syncthreads();
+    for (int b = 0; b < nmerge; ++b) {
+      const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
+      if (mid >= end) continue;
+      const int K = S.K[b];
+      const double sg = S.sgn[b];
+      for (int c = tid; c < N; c += nt) {
+        const double l = c < K ? S.zh[s + c] : S.ds[s + S.keep[s + c]];
+        S.lam[s + c] = sg * l;
+      }
+    }
+    // swap Q <-> Qn (all threads hold the same pointers)
+    double* t = Q;
+    Q = Qn;
+    Qn = t;
+    __syncthreads();
+  }
+
+  // ---------------- back-transform Z = H_0 ... H_{n-3} Q (reflectors in A)
+  for (int k = n - 3; k >= 0; --k) {
+    const double beta = S.beta[k];
+    if (beta == 0.0) continue;
+    const int i0 = k + 1;
+    for (int c = tid; c < n; c += nt) {
+      double acc = 0.0;
+      for (int i = i0; i < n; ++i) acc = fma(A[(size_t)i * ld + k], Q[(size_t)i * n + c], acc);
+      S.hp[c] = beta * acc;
+    }
+    __syncthreads();
+    for (int e = tid; e < (n - i0) * n; e += nt) {
+      const int i = i0 + e / n, c = e % n;
+      Q[(size_t)i * n + c] -= A[(size_t)i * ld + k] * S.hp[c];
+    }
+    __syncthreads();
+  }
+
+  // ---------------- epilogue: descending order, drop rule, W
+  for (int i = tid; i < n; i += nt) {
+    const double di = S.lam[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = S.lam[j];
+      rank += (dj > di) || (dj == di && j > i);
+    }
+    S.perm[rank] = i;
+  }
+  __syncthreads();
+  const double s0 = S.lam[S.perm[0]];
+  const double cut = fmax(drop_tol * s0, 0.0);
+  for (int k = tid; k < n; k += nt) eigvals[k] = S.lam[S.perm[k]];
+  if (tid == 0) {
+    int me = 0;
+    while (me < n && S.lam[S.perm[me]] > cut) ++me;
+    *m_eff_out = me;
+    *info = NYS_INFO_OK;
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, k = e % n;
+    const int src = S.perm[k];
+    const double v = Q[(size_t)i * n + src];
+    eigvecs[e] = v;
+    const double sk = S.lam[src];
+    Wout[e] = (sk > cut) ? v / sqrt(sk) : 0.0;
+  }
+}
+
+}  // namespace
+
+namespace nys_host {
+size_t dc_buffer_bytes(int n) {
+  return ((size_t)n * (n + 1) + 3 * (size_t)n * n) * sizeof(double);
+}
+bool dc_fits(int n) { return n >= 1 && n <= kDcMaxN; }
+bool dc_uses_smem(int n) { return dc_buffer_bytes(n) <= 150 * 1024; }
+
+int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, double* eigvals,
+                  double* eigvecs, double* W, int* m_eff, int* info, void* ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  const size_t need = dc_buffer_bytes(n);
+  const int use_smem = dc_uses_smem(n);
+  size_t dyn = 0;
+  if (use_smem) {
+    dyn = need;
+    cudaError_t e = cudaFuncSetAttribute(dc_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn);
+    if (e != cudaSuccess) return record_cuda(e);
+  } else if (ws == nullptr || ws_bytes < need) {
+    return NYS_EWORKSPACE;
+  }
+  const int threads = n <= 64 ? 256 : kDcThreads;
+  dc_eig_kernel<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
+                                         static_cast<double*>(ws), use_smem);
+  count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+}  // namespace nys_host
