@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       S.sgn[b] = rho < 0.0 ? -1.0 : 1.0;
     }
     __syncthreads();
+    // the next Q is block diagonal: clear it so the off-diagonal child blocks
+    // that the GEMM of the next level reads are exact zeros
+    for (int e = tid; e < n * n; e += nt) Qn[e] = 0.0;
     // M1: rank-sort the (sign-adjusted) eigenvalues of both children, gather z
     for (int b = 0; b < nmerge; ++b) {
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
