@@ -17,6 +17,8 @@
 // Epilogue identical to eig.cu: descending order (ties: higher index first,
 // nystrom.py:151), drop rule s > max(drop_tol s_0, 0), W = V / sqrt(s).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     dc_eig_kernel(const double* __restrict__ lm, int n, double sigma2, double drop_tol,
                   double* __restrict__ eigvals, double* __restrict__ eigvecs,
                   double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
-                  double* __restrict__ gbuf, int use_smem) {
+                  double* __restrict__ gbuf, int use_smem, int debug) {
   extern __shared__ __align__(16) double dyn[];
   __shared__ DcShared S;
   const int ld = n + 1;
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
   double* Qn = Q + (size_t)n * n;             // n x n
   double* DL = Qn + (size_t)n * n;            // n x n
   const int tid = threadIdx.x, nt = blockDim.x;
+  long long tc0 = clock64(), tc1 = 0, tc2 = 0, tc3 = 0, tc4 = 0;
 
   if (tid == 0) S.degenerate = 0;
   __syncthreads();
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
   }
   __syncthreads();
 
+  tc1 = clock64();
   // ---------------- tears at every multiple of kLeaf, then leaves by QL
   if (tid == 0)
     for (int b = kLeaf; b < n; b += kLeaf) {
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
   }
   __syncthreads();
 
+  tc2 = clock64();
   // ---------------- merge levels
   for (int width = kLeaf; width < n; width *= 2) {
     const int nmerge = (n + 2 * width - 1) / (2 * width);
@@ -525,6 +530,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     __syncthreads();
   }
 
+  tc3 = clock64();
   // ---------------- back-transform Z = H_0 ... H_{n-3} Q (reflectors in A)
   for (int k = n - 3; k >= 0; --k) {
     const double beta = S.beta[k];
@@ -543,6 +549,8 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     __syncthreads();
   }
 
+  tc4 = clock64();
+  if (debug && tid == 0) printf("[nys dc] n=%d tridiag=%lld leaves=%lld merges=%lld backT=%lld\n", n, tc1 - tc0, tc2 - tc1, tc3 - tc2, tc4 - tc3);
   // ---------------- epilogue: descending order, drop rule, W
   for (int i = tid; i < n; i += nt) {
     const double di = S.lam[i];
@@ -598,7 +606,8 @@ int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, doubl
   }
   const int threads = n <= 64 ? 256 : kDcThreads;
   dc_eig_kernel<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
-                                         static_cast<double*>(ws), use_smem);
+                                         static_cast<double*>(ws), use_smem,
+                                         getenv("NYS_EIG_DEBUG") != nullptr);
   count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
