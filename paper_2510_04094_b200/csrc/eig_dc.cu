@@ -432,12 +432,15 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       const double rho = S.rho[b];
       for (int i = tid; i < K; i += nt) {
         const double di = S.ds[s + S.keep[s + i]];
-        double v = -DL[(size_t)(s + i) * n + s + K - 1] / rho;
+        // four interleaved partial products: the ratios are independent, only
+        // the running product is a dependency chain
+        double v[4] = {-DL[(size_t)(s + i) * n + s + K - 1] / rho, 1.0, 1.0, 1.0};
         for (int jj = 0; jj < K - 1; ++jj) {
           const double dj = jj < i ? S.ds[s + S.keep[s + jj]] : S.ds[s + S.keep[s + jj + 1]];
-          v *= (-DL[(size_t)(s + i) * n + s + jj]) / (dj - di);
+          v[jj & 3] *= (-DL[(size_t)(s + i) * n + s + jj]) / (dj - di);
         }
-        S.hv[s + i] = copysign(sqrt(fmax(v, 0.0)), S.zs[s + S.keep[s + i]]);
+        const double vv = (v[0] * v[1]) * (v[2] * v[3]);
+        S.hv[s + i] = copysign(sqrt(fmax(vv, 0.0)), S.zs[s + S.keep[s + i]]);
       }
     }
     __syncthreads();
@@ -497,19 +500,27 @@ __global__ void __launch_bounds__(kDcThreads, 1)
         continue;
       }
       const int K = S.K[b];
-      for (int e = tid; e < N * N; e += nt) {
-        const int r = e / N, c = e % N;
+      // kept columns: 4 outputs per thread (independent FMA chains share the
+      // Q-row loads); deflated columns: gathered copies
+      const int KQ = (K + 3) / 4;
+      for (int e = tid; e < N * KQ; e += nt) {
+        const int r = e / KQ, c0 = 4 * (e % KQ);
         const double* qr = Q + (size_t)(s + r) * n;
-        double acc;
-        if (c < K) {
-          acc = 0.0;
-          for (int i = 0; i < K; ++i)
-            acc = fma(qr[S.perm[s + S.keep[s + i]]], DL[(size_t)(s + i) * n + s + c], acc);
-          acc *= S.hp[s + c];
-        } else {
-          acc = qr[S.perm[s + S.keep[s + c]]];
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < K; ++i) {
+          const double q = qr[S.perm[s + S.keep[s + i]]];
+          const double* u = DL + (size_t)(s + i) * n + s + c0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (c0 + t < K) a[t] = fma(q, u[t], a[t]);
         }
-        Qn[(size_t)(s + r) * n + s + c] = acc;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (c0 + t < K) Qn[(size_t)(s + r) * n + s + c0 + t] = a[t] * S.hp[s + c0 + t];
+      }
+      for (int e = tid; e < N * (N - K); e += nt) {
+        const int r = e / (N - K), c = K + e % (N - K);
+        Qn[(size_t)(s + r) * n + s + c] = Q[(size_t)(s + r) * n + S.perm[s + S.keep[s + c]]];
       }
     }
     __syncthreads();
@@ -532,19 +543,37 @@ __global__ void __launch_bounds__(kDcThreads, 1)
 
   tc3 = clock64();
   // ---------------- back-transform Z = H_0 ... H_{n-3} Q (reflectors in A)
+  // tpc threads (adjacent lanes) share one column's dot product: FP64 FMA
+  // latency, not bandwidth, bounds a serial n-term chain on B200
+  const int tpc = (nt / n) >= 8 ? 8 : ((nt / n) >= 4 ? 4 : ((nt / n) >= 2 ? 2 : 1));
   for (int k = n - 3; k >= 0; --k) {
     const double beta = S.beta[k];
     if (beta == 0.0) continue;
     const int i0 = k + 1;
-    for (int c = tid; c < n; c += nt) {
-      double acc = 0.0;
-      for (int i = i0; i < n; ++i) acc = fma(A[(size_t)i * ld + k], Q[(size_t)i * n + c], acc);
-      S.hp[c] = beta * acc;
+    for (int i = i0 + tid; i < n; i += nt) S.hv[i] = A[(size_t)i * ld + k];
+    __syncthreads();
+    const int work = (n * tpc + 31) / 32 * 32;   // whole warps: the shuffles need all lanes
+    for (int t = tid; t < work; t += nt) {
+      const int c = t / tpc, sub = t % tpc;
+      double a0 = 0.0, a1 = 0.0;
+      if (c < n) {
+        int i = i0 + sub;
+        for (; i + tpc < n; i += 2 * tpc) {
+          a0 = fma(S.hv[i], Q[(size_t)i * n + c], a0);
+          a1 = fma(S.hv[i + tpc], Q[(size_t)(i + tpc) * n + c], a1);
+        }
+        if (i < n) a0 = fma(S.hv[i], Q[(size_t)i * n + c], a0);
+      }
+      double acc = a0 + a1;
+      for (int o = 1; o < tpc; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (sub == 0 && c < n) S.hp[c] = beta * acc;
     }
     __syncthreads();
-    for (int e = tid; e < (n - i0) * n; e += nt) {
-      const int i = i0 + e / n, c = e % n;
-      Q[(size_t)i * n + c] -= A[(size_t)i * ld + k] * S.hp[c];
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = i0 + warp; i < n; i += nw) {
+      const double vi = S.hv[i];
+      double* row = Q + (size_t)i * n;
+      for (int c = lane; c < n; c += 32) row[c] -= vi * S.hp[c];
     }
     __syncthreads();
   }
