@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
 
   tc2 = clock64();
   // ---------------- merge levels
+  long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tlast = clock64();
   for (int width = kLeaf; width < n; width *= 2) {
     const int nmerge = (n + 2 * width - 1) / (2 * width);
     // block geometry; a block without a right partner is carried unchanged
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     // the next Q is block diagonal: clear it so the off-diagonal child blocks
     // that the GEMM of the next level reads are exact zeros
     for (int e = tid; e < n * n; e += nt) Qn[e] = 0.0;
+    if (debug) { long long tn = clock64(); tm[0] += tn - tlast; tlast = tn; }
     // M1: rank-sort the (sign-adjusted) eigenvalues of both children, gather z
     for (int b = 0; b < nmerge; ++b) {
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       }
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[1] += tn - tlast; tlast = tn; }
     // M2: normalise, deflate (serial scan per block)
     for (int b = tid; b < nmerge; b += nt) {
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       S.nrot[b] = nrot;
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[2] += tn - tlast; tlast = tn; }
     // M3: secular roots, one thread per (block, root)
     {
       int total = 0;
@@ -424,6 +428,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       }
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[3] += tn - tlast; tlast = tn; }
     // M4: Gu-Eisenstat z over kept entries; lambda moves to lam after M6
     for (int b = 0; b < nmerge; ++b) {
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
@@ -444,6 +449,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       }
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[4] += tn - tlast; tlast = tn; }
     // M5: U[i][j] = zhat_i / (d_i - lambda_j), then unit columns
     for (int b = 0; b < nmerge; ++b) {
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
@@ -470,6 +476,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       }
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[5] += tn - tlast; tlast = tn; }
     // M6: deflation rotations on the columns of Q (order matters: serial over
     // rotations, parallel over rows)
     for (int b = 0; b < nmerge; ++b) {
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       }
     }
     __syncthreads();
+    if (debug) { long long tn = clock64(); tm[6] += tn - tlast; tlast = tn; }
     // M7: new eigenvectors: kept columns Q[:, perm[keep]] U, deflated columns copied;
     // carried blocks copied unchanged
     for (int b = 0; b < nmerge; ++b) {
@@ -534,6 +542,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
         S.lam[s + c] = sg * l;
       }
     }
+    if (debug) { long long tn = clock64(); tm[7] += tn - tlast; tlast = tn; }
     // swap Q <-> Qn (all threads hold the same pointers)
     double* t = Q;
     Q = Qn;
@@ -579,6 +588,9 @@ __global__ void __launch_bounds__(kDcThreads, 1)
   }
 
   tc4 = clock64();
+  if (debug && tid == 0)
+    printf("[nys dc] merge phases: pre %lld M1 %lld M2 %lld M3 %lld M4 %lld M5 %lld M6 %lld M7+ %lld\n",
+           tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], tm[7]);
   if (debug && tid == 0) printf("[nys dc] n=%d tridiag=%lld leaves=%lld merges=%lld backT=%lld\n", n, tc1 - tc0, tc2 - tc1, tc3 - tc2, tc4 - tc3);
   // ---------------- epilogue: descending order, drop rule, W
   for (int i = tid; i < n; i += nt) {
