@@ -117,8 +117,16 @@ NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
 
 // secular root j of diag(ds) + rho zz^T over the K kept entries of a block;
 // writes DL[i][j] = d_i - lambda_j (i < K) and returns lambda_j
+// G adjacent lanes (mask gm, lane index gl within the group) share one root:
+// every sum over the K poles is split G ways and butterfly-reduced, the model
+// step is computed redundantly (identical in all G lanes)
+NYS_DEV double gsum(double v, int G, unsigned gm) {
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(gm, v, o);
+  return v;
+}
+
 NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, double* DL,
-                            int n) {
+                            int n, int gl, int G, unsigned gm) {
   const int* kp = S.keep + s;
   auto dk = [&](int i) { return S.ds[s + kp[i]]; };
   auto z2 = [&](int i) {
@@ -129,23 +137,25 @@ NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, 
   double lo, hi;
   if (j < K - 1) {
     const double mid = 0.5 * (dk(j) + dk(j + 1));
-    double f = 1.0 / rho;
-    for (int i = 0; i < K; ++i) f += z2(i) / (dk(i) - mid);
+    double f = 0.0;
+    for (int i = gl; i < K; i += G) f += z2(i) / (dk(i) - mid);
+    f = 1.0 / rho + gsum(f, G, gm);
     org = f >= 0.0 ? j : j + 1;
     lo = dk(j) - dk(org);
     hi = dk(j + 1) - dk(org);
   } else {
     org = K - 1;
     double zz = 0.0;
-    for (int i = 0; i < K; ++i) zz += z2(i);
+    for (int i = gl; i < K; i += G) zz += z2(i);
+    zz = gsum(zz, G, gm);
     lo = 0.0;
     hi = rho * zz;
   }
   const double dorg = dk(org);
   double tau = 0.5 * (lo + hi);
   for (int it = 0; it < 80; ++it) {
-    double f = 1.0 / rho, fabs_sum = 1.0 / rho, psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
-    for (int i = 0; i < K; ++i) {
+    double f = 0.0, fabs_sum = 0.0, psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
+    for (int i = gl; i < K; i += G) {
       const double dl = (dk(i) - dorg) - tau;
       const double w = 1.0 / dl;
       const double t = z2(i) * w;
@@ -159,6 +169,12 @@ NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, 
         dphi += t * w;
       }
     }
+    f = 1.0 / rho + gsum(f, G, gm);
+    fabs_sum = 1.0 / rho + gsum(fabs_sum, G, gm);
+    psi = gsum(psi, G, gm);
+    dpsi = gsum(dpsi, G, gm);
+    phi = gsum(phi, G, gm);
+    dphi = gsum(dphi, G, gm);
     if (f > 0.0)
       hi = tau;
     else
@@ -201,7 +217,7 @@ NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, 
     const double nt = ok ? tau + x : 0.5 * (lo + hi);
     tau = (nt > lo && nt < hi) ? nt : 0.5 * (lo + hi);
   }
-  for (int i = 0; i < K; ++i) DL[(size_t)(s + i) * n + s + j] = (dk(i) - dorg) - tau;
+  for (int i = gl; i < K; i += G) DL[(size_t)(s + i) * n + s + j] = (dk(i) - dorg) - tau;
   return dorg + tau;
 }
 
@@ -416,15 +432,18 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     {
       int total = 0;
       for (int b = 0; b < nmerge; ++b) total += (S.bmid[b] < S.be[b]) ? S.K[b] : 0;
-      for (int w = tid; w < total; w += nt) {
+      constexpr int G = 4;
+      const int gl = tid % G;
+      const unsigned gm = 0xFu << ((tid & 31) & ~(G - 1));
+      for (int w = tid / G; w < total; w += nt / G) {
         int b = 0, j = w;
         while (j >= ((S.bmid[b] < S.be[b]) ? S.K[b] : 0)) {
           j -= (S.bmid[b] < S.be[b]) ? S.K[b] : 0;
           ++b;
         }
         const int s = S.bs[b];
-        const double lj = secular_root(S, s, j, S.K[b], S.rho[b], DL, n);
-        S.zh[s + j] = lj;   // park lambda_j (zh is rebuilt in M4 from DL)
+        const double lj = secular_root(S, s, j, S.K[b], S.rho[b], DL, n, gl, G, gm);
+        if (gl == 0) S.zh[s + j] = lj;   // park lambda_j (zh is rebuilt in M4 from DL)
       }
     }
     __syncthreads();
