@@ -40,6 +40,7 @@ struct DcShared {
   int perm[kDcMaxN];      // per block: sorted index -> global column
   int keep[kDcMaxN];      // per block: kept sorted indices (ascending), then deflated
   int roti[kDcMaxN], rotj[kDcMaxN];
+  int col[kDcMaxN];       // per block: Q column of kept / deflated entry c
   double rho[kMaxBlocks], sgn[kMaxBlocks];
   int K[kMaxBlocks], nrot[kMaxBlocks];
   int bs[kMaxBlocks], bmid[kMaxBlocks], be[kMaxBlocks];   // merge: start, boundary, end
@@ -454,17 +455,28 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       if (mid >= end) continue;
       const int K = S.K[b];
       const double rho = S.rho[b];
-      for (int i = tid; i < K; i += nt) {
+      // four lanes per entry, each a strided partial product (the ratios are
+      // independent; only the running products are dependency chains)
+      constexpr int G = 4;
+      const int gl = tid % G;
+      const unsigned gm = 0xFu << ((tid & 31) & ~(G - 1));
+      const int Kr = (K + G - 1) / G * G;   // whole groups
+      for (int w = tid / G; w < Kr; w += nt / G) {
+        const int i = w < K ? w : K - 1;
         const double di = S.ds[s + S.keep[s + i]];
-        // four interleaved partial products: the ratios are independent, only
-        // the running product is a dependency chain
-        double v[4] = {-DL[(size_t)(s + i) * n + s + K - 1] / rho, 1.0, 1.0, 1.0};
-        for (int jj = 0; jj < K - 1; ++jj) {
+        double v0 = gl == 0 ? -DL[(size_t)(s + i) * n + s + K - 1] / rho : 1.0, v1 = 1.0;
+        int t = 0;
+        for (int jj = gl; jj < K - 1; jj += G, ++t) {
           const double dj = jj < i ? S.ds[s + S.keep[s + jj]] : S.ds[s + S.keep[s + jj + 1]];
-          v[jj & 3] *= (-DL[(size_t)(s + i) * n + s + jj]) / (dj - di);
+          const double ratio = (-DL[(size_t)(s + i) * n + s + jj]) / (dj - di);
+          if (t & 1)
+            v1 *= ratio;
+          else
+            v0 *= ratio;
         }
-        const double vv = (v[0] * v[1]) * (v[2] * v[3]);
-        S.hv[s + i] = copysign(sqrt(fmax(vv, 0.0)), S.zs[s + S.keep[s + i]]);
+        double vv = v0 * v1;
+        for (int o = 1; o < G; o <<= 1) vv *= __shfl_xor_sync(gm, vv, o);
+        if (gl == 0 && w < K) S.hv[s + i] = copysign(sqrt(fmax(vv, 0.0)), S.zs[s + S.keep[s + i]]);
       }
     }
     __syncthreads();
@@ -502,6 +514,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b];
       if (mid >= end) continue;
       const int N = end - s;
+      for (int c = tid; c < N; c += nt) S.col[s + c] = S.perm[s + S.keep[s + c]];
       for (int r = tid; r < N; r += nt) {
         double* row = Q + (size_t)(s + r) * n;
         for (int q = 0; q < S.nrot[b]; ++q) {
@@ -534,8 +547,9 @@ __global__ void __launch_bounds__(kDcThreads, 1)
         const int r = e / KQ, c0 = 4 * (e % KQ);
         const double* qr = Q + (size_t)(s + r) * n;
         double a[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
         for (int i = 0; i < K; ++i) {
-          const double q = qr[S.perm[s + S.keep[s + i]]];
+          const double q = qr[S.col[s + i]];
           const double* u = DL + (size_t)(s + i) * n + s + c0;
 #pragma unroll
           for (int t = 0; t < 4; ++t)
