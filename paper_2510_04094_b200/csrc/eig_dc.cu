@@ -542,22 +542,24 @@ __global__ void __launch_bounds__(kDcThreads, 1)
       const int K = S.K[b];
       // kept columns: 4 outputs per thread (independent FMA chains share the
       // Q-row loads); deflated columns: gathered copies
-      const int KQ = (K + 3) / 4;
-      for (int e = tid; e < N * KQ; e += nt) {
-        const int r = e / KQ, c0 = 4 * (e % KQ);
-        const double* qr = Q + (size_t)(s + r) * n;
+      // adjacent lanes take adjacent output columns (conflict-free U reads); each
+      // thread owns 4 rows, whose Q entries are warp-broadcast loads
+      const int NQ = (N + 3) / 4;
+      for (int e = tid; e < NQ * K; e += nt) {
+        const int c = e % K, r0 = 4 * (e / K);
         double a[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll 4
         for (int i = 0; i < K; ++i) {
-          const double q = qr[S.col[s + i]];
-          const double* u = DL + (size_t)(s + i) * n + s + c0;
+          const double u = DL[(size_t)(s + i) * n + s + c];
+          const int qc = S.col[s + i];
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (c0 + t < K) a[t] = fma(q, u[t], a[t]);
+            if (r0 + t < N) a[t] = fma(Q[(size_t)(s + r0 + t) * n + qc], u, a[t]);
         }
+        const double h = S.hp[s + c];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          if (c0 + t < K) Qn[(size_t)(s + r) * n + s + c0 + t] = a[t] * S.hp[s + c0 + t];
+          if (r0 + t < N) Qn[(size_t)(s + r0 + t) * n + s + c] = a[t] * h;
       }
       for (int e = tid; e < N * (N - K); e += nt) {
         const int r = e / (N - K), c = K + e % (N - K);
