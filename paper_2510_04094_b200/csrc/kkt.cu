@@ -288,7 +288,8 @@ __global__ void __launch_bounds__(32)
 
 // ---------------------------------------------------------------------------
 // large sides: one CTA per system, LU in an L2-resident workspace slice
-constexpr int kKktThreads = 256;
+constexpr int kKktThreads = 1024;   // large sides only (config 4: n = 259, B = 1)
+constexpr int kCtaMaxN = 512;
 
 __global__ void __launch_bounds__(kKktThreads)
     kkt_cta_kernel(const double* __restrict__ gram, int m_eff, int ncond,
@@ -299,6 +300,7 @@ __global__ void __launch_bounds__(kKktThreads)
   __shared__ int piv_s;
   __shared__ int bad;
   __shared__ double red_v[kKktThreads / 32];
+  __shared__ double urow_s[kCtaMaxN], lcol_s[kCtaMaxN];
   __shared__ int red_i[kKktThreads / 32];
   extern __shared__ __align__(16) double vec[];   // ys | xs | perm  (3n)
 
@@ -362,20 +364,27 @@ __global__ void __launch_bounds__(kKktThreads)
     __syncthreads();
     if (bad) break;
     const int pr = piv_s;
-    if (pr != k)
-      for (int j = tid; j < n; j += nt) {
-        double t = LU[(size_t)k * n + j];
-        LU[(size_t)k * n + j] = LU[(size_t)pr * n + j];
-        LU[(size_t)pr * n + j] = t;
-      }
+    // swap rows k, pr and stage the pivot row in shared memory
+    for (int j = tid; j < n; j += nt) {
+      const double a = LU[(size_t)k * n + j], p = LU[(size_t)pr * n + j];
+      if (pr != k) LU[(size_t)pr * n + j] = a;
+      LU[(size_t)k * n + j] = p;
+      urow_s[j] = p;
+    }
     __syncthreads();
-    const double pivot = LU[(size_t)k * n + k];
-    for (int i = k + 1 + tid; i < n; i += nt) LU[(size_t)i * n + k] /= pivot;
+    const double inv = 1.0 / urow_s[k];
+    for (int i = k + 1 + tid; i < n; i += nt) {   // multipliers, staged too
+      const double l = LU[(size_t)i * n + k] * inv;
+      LU[(size_t)i * n + k] = l;
+      lcol_s[i] = l;
+    }
     __syncthreads();
-    const int w = n - k - 1;
-    for (int e = tid; e < w * w; e += nt) {
-      int i = k + 1 + e / w, j = k + 1 + e % w;
-      LU[(size_t)i * n + j] -= LU[(size_t)i * n + k] * LU[(size_t)k * n + j];
+    // trailing update: warp per row, lanes over columns (coalesced, one load +
+    // one store per element; l and u come from shared memory)
+    for (int i = k + 1 + wid; i < n; i += nt / 32) {
+      const double l = lcol_s[i];
+      double* row = LU + (size_t)i * n;
+      for (int j = k + 1 + lane; j < n; j += 32) row[j] -= l * urow_s[j];
     }
     __syncthreads();
   }
