@@ -146,3 +146,39 @@ def test_row_range_partials_sum_to_full_gram(name):
     parts = sum(L.gram_ext_device(fm, int(g["order"]), pts, coef, forc, lo, hi).cpu().numpy()
                 for lo, hi in D.row_ranges(g["pts"].size, 3))
     np.testing.assert_allclose(parts, full, rtol=0, atol=1e-11 * np.abs(full).max())
+
+
+@pytest.mark.parametrize("m", [80, 94, 134, 150, 256])
+def test_large_m_kspace_gram_matches_oracle(m):
+    """Large-m kernel (gram_large.cu) for every super-block shape: NB % 4 in
+    {3, 0, 1 (stub + corner), 3, 1} -- E = W_ext^T [G g r]^T [G g r] W_ext
+    with G built by the oracle's rbf_block (kernel.py:75-92)."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+
+    sigma2, p, n = 0.25, 2, 3001
+    rng = np.random.default_rng(m)
+    lm = np.linspace(0.0, 0.39 * (m - 1), m)
+    pts = np.sort(rng.uniform(lm[0], lm[-1], n))
+    coef = rng.normal(size=(p, n))
+    forcing = rng.normal(size=n)
+    fm = N.build_feature_map(RbfKernel(sigma2), lm)
+    assert fm.m_eff == m and fm.condition < L.KSPACE_MAX_COND
+    E = L.gram_ext_device(fm, p, torch.as_tensor(pts, device="cuda"),
+                          torch.as_tensor(coef, device="cuda"),
+                          torch.as_tensor(forcing, device="cuda")).cpu().numpy()
+    G = O.rbf_block(sigma2, p, lm, pts).T.copy()
+    for k in range(1, p + 1):
+        G -= coef[k - 1][:, None] * O.rbf_block(sigma2, p - k, lm, pts).T
+    X = np.column_stack([G, -coef[p - 1], forcing])
+    K = X.T @ X
+    Wd = fm.d_W[:, :m].cpu().numpy()
+    Wx = np.zeros((m + 2, m + 2))
+    Wx[:m, :m] = Wd
+    Wx[m, m] = Wx[m + 1, m + 1] = 1.0
+    Eo = Wx.T @ K @ Wx
+    assert np.allclose(E, E.T, rtol=0, atol=0)
+    np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
