@@ -9,121 +9,53 @@
 // to 2.6e-5 when m_eff < m, hence the host-side gate.  The n x m matrices
 // never exist outside a 32-row shared-memory tile.
 //
-// Layout.  The Pe = m + 2 columns form NB 8-wide blocks grouped in 4-block
-// super-blocks; the Gram's upper triangle is a set of super-tiles (a <= b),
-// each a 4 x 4 rectangle of 8x8 DMMA accumulators held by one warp (64
-// registers).  The 258-wide config-4 Gram (561 block pairs, 287 KB of FP64
-// accumulators) does not fit one SM's register file, so the super-tiles are
-// split over `ngroups` CTAs (one per SM, up to 18 warps each) that walk the
-// same row range; when the last super-block holds a single block (NB % 4 == 1,
-// config 4) the diagonal super-tile a and its stub (a, last) share one warp
-// (10 + 4 pairs in the 16 accumulator slots) and the corner (last, last) rides
-// along, so every DMMA issued is a block pair of the Gram.
+// Exact underflow skipping.  exp(-d^2/sigma2) is exactly 0.0 in IEEE double
+// once d^2/sigma2 > 745.14 (below 2^-1075); the kernel treats a landmark block
+// as dead for a set of rows when every (row, landmark) pair has
+// d^2/sigma2 > 747 (the margin absorbs the rounding of d, d^2 and the
+// quotient).  Dead entries are the exact zeros the reference computes, so
+// skipping their generation and their DMMAs leaves every sum bit-identical.
+// On config 4 (landmarks 0.39 apart, sigma 0.5) a 32-row tile sees ~11 of the
+// 33 column blocks, a CTA's row range ~12.
 //
-// Pipeline per CTA: 32-row tiles, double-buffered in shared memory in the
-// fragment-native layout X[ks][blk][lane] (conflict-free LDS.64).  Iteration t
-// issues the DMMAs of tile t and generates tile t+1 (exp + Hermite polynomial
-// per element) into the other buffer; the DMMA pipe and the generation
-// arithmetic overlap across warps, one __syncthreads per tile.  The per-row
-// polynomial coefficients are produced two tiles ahead.  Partials go to the
-// workspace and are reduced in fixed order (deterministic).
+// Work split.  One CTA per SM (18 warps), each owning a contiguous row range.
+// At start the CTA finds the blocks live anywhere in its range (its "window"),
+// compacts them, and tiles the compacted Gram triangle with 4 x 4 super-tiles
+// of 8x8 DMMA accumulators (64 registers per warp).  Few super-tiles (config
+// 4: 6) are replicated over the 18 warps, each replica taking every R-th
+// k-step; many (dense windows) run in several passes over the row range.
+// Per 32-row tile the fragment-native smem layout X[ks][c][lane] (c = compacted
+// live-block index, so every super-tile reads contiguous fragments) is double
+// buffered: iteration t issues the DMMAs of tile t and generates tile t+1
+// (half the warps of every SM sub-partition in the opposite order so the
+// exp arithmetic and the tensor pipe overlap); row coefficients are
+// produced two tiles ahead.  Each CTA writes its live
+// block pairs to a private dense slab (replicas added in fixed order) and one
+// reduce kernel sums the slabs in fixed order (deterministic).
 #include <cstdint>
-#include <algorithm>
-#include <cstring>
-#include <vector>
+#include <cstdio>
 
 #include "common.cuh"
 
 namespace {
 
 constexpr int kRT = 4;             // super-tile edge (blocks)
-constexpr int kMaxWarps = 18;      // warps per CTA (576 threads, 1 CTA / SM)
+constexpr int kWarps = 18;         // warps per CTA (576 threads, 1 CTA / SM)
 constexpr int kTileKs = 8;         // 4-row k-steps per row tile (32 rows)
-constexpr int kMaxTasks = 384;
 constexpr int kMaxSmem = 227 * 1024;
-
-// task word: a | b << 8 | mode << 16 | corner << 17   (mode 1 = diag a + stub (a, last))
-struct TaskTable {
-  int word[kMaxTasks];
-};
-
-NYS_DEV void task_decode(int w, int& a, int& b, int& stub, int& corner) {
-  a = w & 255;
-  b = (w >> 8) & 255;
-  stub = (w >> 16) & 1;
-  corner = (w >> 17) & 1;
-}
+constexpr double kDeadRatio = 747.0;   // d^2 / sigma2 beyond which exp() is exactly 0
 
 struct LargePlan {
-  int Pe, NB, NSB, NBpad, ntasks, ngroups, wpc, nrr, ntiles, tiles_per_cta, nbuf;
-  bool stub;
+  int Pe, NB, NBpad, ld, nrr, ntiles, tiles_per_cta, nbuf;
   size_t smem;
-  TaskTable tasks;
-
   static LargePlan make(int n_rows, int m) {
-    LargePlan L;
-    std::memset(&L, 0, sizeof(L));
+    LargePlan L{};
     L.Pe = m + 2;                                 // kernel-space extended width
     L.NB = (L.Pe + 7) / 8;
-    L.NSB = (L.NB + kRT - 1) / kRT;
-    L.NBpad = L.NSB * kRT;
-    L.stub = (L.NB % kRT == 1) && L.NSB >= 2;
-    // task list with DMMA weights
-    std::vector<std::pair<int, int>> t;   // (word, weight)
-    const int full = L.stub ? L.NSB - 1 : L.NSB;
-    for (int a = 0; a < full; ++a)
-      for (int b = a; b < L.NSB; ++b) {
-        if (L.stub && b == L.NSB - 1) continue;   // stub folded into the diagonal task
-        int w = a | (b << 8);
-        int weight = 0;
-        for (int i = 0; i < kRT; ++i)
-          for (int j = 0; j < kRT; ++j)
-            if (a * kRT + i < L.NB && b * kRT + j < L.NB && !(a == b && i > j)) ++weight;
-        if (L.stub && a == b) {
-          w |= 1 << 16;
-          weight += kRT;
-          if (a == L.NSB - 2) {
-            w |= 1 << 17;
-            weight += 1;
-          }
-        }
-        t.push_back({w, weight});
-      }
-    L.ntasks = (int)t.size();
-    L.ngroups = (L.ntasks + kMaxWarps - 1) / kMaxWarps;
-    L.wpc = (L.ntasks + L.ngroups - 1) / L.ngroups;
-    // deal tasks heaviest-first: round-robin over groups, then within a group
-    // over the 4 SM sub-partitions (warp w runs on SMSP w % 4) by least load
-    std::sort(t.begin(), t.end(), [](auto& x, auto& y) { return x.second > y.second; });
-    std::vector<std::vector<std::pair<int, int>>> grp(L.ngroups);
-    std::vector<int> gload(L.ngroups, 0);
-    for (auto& e : t) {
-      int best = -1;
-      for (int g = 0; g < L.ngroups; ++g)
-        if ((int)grp[g].size() < L.wpc && (best < 0 || gload[g] < gload[best])) best = g;
-      grp[best].push_back(e);
-      gload[best] += e.second;
-    }
-    for (int g = 0; g < L.ngroups; ++g) {
-      int cap[4], load[4] = {0, 0, 0, 0};
-      for (int s = 0; s < 4; ++s) cap[s] = (L.wpc - s + 3) / 4;
-      std::vector<int> slot_words[4];
-      for (auto& e : grp[g]) {
-        int best = -1;
-        for (int s = 0; s < 4; ++s)
-          if ((int)slot_words[s].size() < cap[s] && (best < 0 || load[s] < load[best])) best = s;
-        slot_words[best].push_back(e.first);
-        load[best] += e.second;
-      }
-      for (int w = 0; w < L.wpc; ++w) {
-        auto& v = slot_words[w % 4];
-        size_t k = (size_t)(w / 4);
-        L.tasks.word[g * L.wpc + w] = k < v.size() ? v[k] : -1;
-      }
-    }
+    L.NBpad = ((L.NB + kRT - 1) / kRT) * kRT;
+    L.ld = L.NB * 8;
     L.ntiles = (n_rows + 4 * kTileKs - 1) / (4 * kTileKs);
-    int nrr = nys::device_sm_count() / L.ngroups;
-    if (nrr < 1) nrr = 1;
+    int nrr = nys::device_sm_count();
     if (nrr > L.ntiles) nrr = L.ntiles > 0 ? L.ntiles : 1;
     L.nrr = nrr;
     L.tiles_per_cta = (L.ntiles + nrr - 1) / nrr;
@@ -133,18 +65,37 @@ struct LargePlan {
     L.smem = L.nbuf * xbuf + rowc;
     return L;
   }
-  bool fits() const {
-    return ntasks <= kMaxTasks && ngroups * wpc <= kMaxTasks && smem <= (size_t)kMaxSmem;
-  }
-  size_t part_doubles() const { return (size_t)nrr * ngroups * wpc * kRT * kRT * 64; }
+  bool fits() const { return NB <= 64 && smem <= (size_t)kMaxSmem; }
+  size_t slab_doubles() const { return (size_t)nrr * ld * ld; }
   size_t ws_bytes(int m_eff) const {
-    return (part_doubles() + (size_t)Pe * Pe + (size_t)Pe * (m_eff + 2)) * sizeof(double) + 256;
+    return (slab_doubles() + (size_t)Pe * Pe + (size_t)Pe * (m_eff + 2)) * sizeof(double) +
+           (size_t)nrr * sizeof(unsigned long long) + 512;
   }
 };
 
+// live-block test for rows spanning [tmin, tmax] (NaN rows: everything live)
+NYS_DEV unsigned long long live_blocks(const double* blo, const double* bhi, int NB,
+                                       unsigned long long special, double tmin, double tmax,
+                                       bool any_nan, double R2) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long mk = 0ull;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int blk = lane + 32 * h;
+    bool live = false;
+    if (blk < NB) {
+      const double dmin = fmax(blo[blk] - tmax, tmin - bhi[blk]);
+      live = any_nan || ((special >> blk) & 1ull) || !(dmin > 0.0 && dmin * dmin > R2);
+    }
+    mk |= (unsigned long long)__ballot_sync(0xffffffffu, live) << (32 * h);
+  }
+  return mk;
+}
+
 // per-row polynomial coefficients for one 32-row tile: t, q0..qP, g = -f_p, r
+// (one warp; rows past the end get an all-zero polynomial -> G = 0)
 template <int P>
-NYS_DEV void row_coeffs(const nys::Hermite& H, const double* __restrict__ pts,
+NYS_DEV void row_coeffs(const double (*hc)[nys::kMaxOrder + 1], const double* __restrict__ pts,
                         const double* __restrict__ coef, const double* __restrict__ forcing,
                         int n_c, int r0, int row_end, double* rowc) {
   const int lane = threadIdx.x & 31;
@@ -157,18 +108,19 @@ NYS_DEV void row_coeffs(const nys::Hermite& H, const double* __restrict__ pts,
   rc[0] = ok ? pts[i] : 0.0;
 #pragma unroll
   for (int j = 0; j <= P; ++j) {
-    double v = H.c[P][j];
+    double v = hc[P][j];
 #pragma unroll
-    for (int k = 1; k <= P; ++k) v = fma(-f[k - 1], H.c[P - k][j], v);
-    rc[1 + j] = ok ? v : 0.0;   // rows past the end: all-zero polynomial -> G = 0
+    for (int k = 1; k <= P; ++k) v = fma(-f[k - 1], hc[P - k][j], v);
+    rc[1 + j] = ok ? v : 0.0;
   }
   rc[6] = ok ? -f[P - 1] : 0.0;
   rc[7] = ok ? forcing[i] : 0.0;
 }
 
 // -(x / sigma2) for x >= 0, correctly rounded from the precomputed reciprocal:
-// q = x * inv, remainder by FMA, one correction (checked bit-exact against the
-// IEEE quotient by tools/div_check.cu) -- the kernel.py:78-79 division at 3 FP64 ops.
+// q = x * inv, remainder by FMA, one correction (bit-identical to the IEEE
+// quotient on 13 bandwidths x 2^32 samples, tools/div_check.cu) -- the
+// kernel.py:78-79 division at 3 FP64 ops.
 NYS_DEV double neg_div(double x, double sigma2, double inv) {
   double q = x * inv;
   double r = fma(-q, sigma2, x);
@@ -176,208 +128,290 @@ NYS_DEV double neg_div(double x, double sigma2, double inv) {
 }
 
 template <int P>
-NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int NB, int NBpad, double sigma2,
-                      double inv, uint64_t need, const double* rowc, double* X, int warp,
+NYS_DEV double g_entry(double l, const double* r, double sigma2, double inv) {
+  const double d = l - r[0];
+  double poly = r[1 + P];
+#pragma unroll
+  for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, r[1 + j]);
+  return poly * exp(neg_div(d * d, sigma2, inv));
+}
+
+// Generate the CTA's L live blocks of one 32-row tile into the compacted
+// fragment layout X[ks][c][lane] (c = compacted block index).  Work unit =
+// (block, k-step pair): two independent exp chains per lane.
+template <int P>
+NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int L, const int* lb, int NBpad,
+                      double sigma2, double inv, const double* rowc, double* X, int warp,
                       int nwarps) {
   const int lane = threadIdx.x & 31;
   const int rsub = lane & 3, csub = lane >> 2;
-  int blk = warp, ks = 0;
-  while (blk >= NB) { blk -= NB; ++ks; }
-  for (; ks < kTileKs;) {
-    if ((need >> blk) & 1ull) {
-      const int s = blk * 8 + csub;
-      const double* rc = rowc + (ks * 4 + rsub) * 8;
-      double v = 0.0;
-      if (s < m) {
-        const double d = __ldg(lm + s) - rc[0];
-        double poly = rc[1 + P];
-#pragma unroll
-        for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, rc[1 + j]);
-        v = poly * exp(neg_div(d * d, sigma2, inv));
-      } else if (s == m) {
-        v = rc[6];
-      } else if (s == m + 1) {
-        v = rc[7];
-      }
-      X[((size_t)ks * NBpad + blk) * 32 + lane] = v;
+  for (int u = warp; u < 4 * L; u += nwarps) {
+    const int c = u >> 2, ks = (u & 3) * 2;
+    const int s = lb[c] * 8 + csub;
+    double* Xo = X + ((size_t)ks * NBpad + c) * 32 + lane;
+    const double* r0 = rowc + (ks * 4 + rsub) * 8;   // rows ks*4 + rsub and +4
+    const double* r1 = r0 + 32;
+    double v0, v1;
+    if (s < m) {
+      const double l = __ldg(lm + s);
+      v0 = g_entry<P>(l, r0, sigma2, inv);
+      v1 = g_entry<P>(l, r1, sigma2, inv);
+    } else {
+      v0 = (s == m) ? r0[6] : (s == m + 1) ? r0[7] : 0.0;
+      v1 = (s == m) ? r1[6] : (s == m + 1) ? r1[7] : 0.0;
     }
-    blk += nwarps;
-    while (blk >= NB) { blk -= NB; ++ks; }
+    Xo[0] = v0;
+    Xo[(size_t)NBpad * 32] = v1;
   }
 }
 
+#ifndef NYS_LARGE_PROBE
+#define NYS_LARGE_PROBE 0   // probe builds: 1 = skip DMMA, 2 = skip generation, 3 = phase clocks
+#endif
+
 template <int P>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1)
+__global__ void __launch_bounds__(kWarps * 32, 1)
     large_kspace_kernel(const double* __restrict__ lm, int m, double sigma2,
                         const double* __restrict__ pts, const double* __restrict__ coef,
                         const double* __restrict__ forcing, int n_c, int row_begin, int row_end,
-                        int NB, int NBpad, int wpc, int nbuf, int tiles_per_cta,
-                        const __grid_constant__ TaskTable tasks, double* __restrict__ part) {
+                        int NB, int NBpad, int ld, int nbuf, int tiles_per_cta,
+                        double* __restrict__ slabs, unsigned long long* __restrict__ live_out) {
   extern __shared__ __align__(16) double sm[];
   const size_t xsz = (size_t)kTileKs * NBpad * 32;
   double* const X0 = sm;
   double* const X1 = sm + (nbuf - 1) * xsz;
-  double* rowc = sm + nbuf * xsz;   // [3][32][8]
+  double* const rowc = sm + nbuf * xsz;   // [3][32][8]
+  __shared__ double blo_s[64], bhi_s[64];
+  __shared__ double red_s[2][kWarps];
+  __shared__ int nan_s;
+  __shared__ unsigned long long live_s;
+  __shared__ int lb_s[64];
+  __shared__ double hc_s[nys::kMaxOrder + 1][nys::kMaxOrder + 1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  const int group = blockIdx.y;
-  const int word = warp < wpc ? tasks.word[group * wpc + warp] : -1;
-  int a = -1, b = -1, stub = 0, corner = 0;
-  if (word >= 0) task_decode(word, a, b, stub, corner);
-  const int last = NB - 1;
-
-  // blocks this CTA's warps read (NB <= 64)
-  __shared__ unsigned long long need_s;
-  if (threadIdx.x == 0) need_s = 0ull;
-  __syncthreads();
-  if (lane == 0 && a >= 0) {
-    unsigned long long mk = 0ull;
-    for (int i = 0; i < kRT; ++i) {
-      if (a * kRT + i < NB) mk |= 1ull << (a * kRT + i);
-      if (b * kRT + i < NB) mk |= 1ull << (b * kRT + i);
-    }
-    if (stub) mk |= 1ull << last;
-    atomicOr(&need_s, mk);
-  }
-  // DMMA predicate mask for the generic (non-stub) tasks
-  uint32_t valid = 0;
-  if (a >= 0 && !stub)
-    for (int i = 0; i < kRT; ++i)
-      for (int j = 0; j < kRT; ++j)
-        if (a * kRT + i < NB && b * kRT + j < NB && !(a == b && i > j)) valid |= 1u << (i * kRT + j);
-
-  nys::Hermite H;
-  H.init(sigma2, P);
-  const double inv = 1.0 / sigma2;
-
-  double acc[kRT][kRT][2];
-#pragma unroll
-  for (int i = 0; i < kRT; ++i)
-#pragma unroll
-    for (int j = 0; j < kRT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
   const int ntiles = (row_end - row_begin + 31) / 32;
   const int tile0 = blockIdx.x * tiles_per_cta;
   const int tile1 = min(ntiles, tile0 + tiles_per_cta);
-  const int cw = nwarps - 1;   // warp that prepares row coefficients
+  const double inv = 1.0 / sigma2;
+  const unsigned long long special = (1ull << (m / 8)) | (1ull << ((m + 1) / 8));
 
-  if (tile0 < tile1) {
-    if (warp == cw) {
-      row_coeffs<P>(H, pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, rowc);
-      if (tile0 + 1 < tile1)
-        row_coeffs<P>(H, pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end,
-                      rowc + 256);
-    }
-    __syncthreads();
-    gen_tile<P>(lm, m, NB, NBpad, sigma2, inv, need_s, rowc, X0, warp, nwarps);
-    __syncthreads();
+  // ---- Hermite coefficients (kernel.py:26-37) and landmark bounds per block
+  if (threadIdx.x == 0) {
+    nan_s = 0;
+    nys::Hermite H;
+    H.init(sigma2, P);
+    for (int a = 0; a <= nys::kMaxOrder; ++a)
+      for (int j = 0; j <= nys::kMaxOrder; ++j) hc_s[a][j] = H.c[a][j];
   }
-  const uint64_t need = need_s;
-  for (int tile = tile0; tile < tile1; ++tile) {
-    const int k = tile - tile0;
-    const double* X = (k & 1) ? X1 : X0;
-    if (a >= 0) {
-      const double* Xl = X + lane;
-      if (stub) {
-#pragma unroll 1
-        for (int ks = 0; ks < kTileKs; ++ks) {
-          const double* Xk = Xl + (size_t)ks * NBpad * 32;
-          double xa[kRT];
-#pragma unroll
-          for (int i = 0; i < kRT; ++i) xa[i] = Xk[(a * kRT + i) * 32];
-          const double xl = Xk[last * 32];
-#pragma unroll
-          for (int i = 0; i < kRT; ++i)
-#pragma unroll
-            for (int j = i; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xa[j]);
-          // stub (a-block i, last) in the lower slots (1,0) (2,0) (3,0) (2,1)
-          nys::dmma(acc[1][0][0], acc[1][0][1], xa[0], xl);
-          nys::dmma(acc[2][0][0], acc[2][0][1], xa[1], xl);
-          nys::dmma(acc[3][0][0], acc[3][0][1], xa[2], xl);
-          nys::dmma(acc[2][1][0], acc[2][1][1], xa[3], xl);
-          if (corner) nys::dmma(acc[3][1][0], acc[3][1][1], xl, xl);
-        }
-      } else {
-#pragma unroll 1
-        for (int ks = 0; ks < kTileKs; ++ks) {
-          const double* Xk = Xl + (size_t)ks * NBpad * 32;
-          double xa[kRT], xb[kRT];
-#pragma unroll
-          for (int i = 0; i < kRT; ++i) xa[i] = Xk[(a * kRT + i) * 32];
-#pragma unroll
-          for (int j = 0; j < kRT; ++j) xb[j] = Xk[(b * kRT + j) * 32];
-#pragma unroll
-          for (int i = 0; i < kRT; ++i)
-#pragma unroll
-            for (int j = 0; j < kRT; ++j)
-              if ((valid >> (i * kRT + j)) & 1u)
-                nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
-        }
+  if (warp == 1) {
+    for (int blk = lane; blk < NB; blk += 32) {
+      double lo = INFINITY, hi = -INFINITY;
+      for (int s = blk * 8; s < min(blk * 8 + 8, m); ++s) {
+        lo = fmin(lo, lm[s]);
+        hi = fmax(hi, lm[s]);
       }
+      blo_s[blk] = lo;
+      bhi_s[blk] = hi;
     }
-    if (nbuf == 1) __syncthreads();
-    if (tile + 1 < tile1)
-      gen_tile<P>(lm, m, NB, NBpad, sigma2, inv, need, rowc + ((k + 1) % 3) * 256,
-                  ((k + 1) & 1) ? X1 : X0, warp, nwarps);
-    if (warp == cw && tile + 2 < tile1)
-      row_coeffs<P>(H, pts, coef, forcing, n_c, row_begin + (tile + 2) * 32, row_end,
-                    rowc + ((k + 2) % 3) * 256);
-    __syncthreads();
   }
-  if (a >= 0) {
-    double* out = part + (((size_t)blockIdx.x * gridDim.y + group) * wpc + warp) *
-                             (kRT * kRT * 64) + lane * 2;
+  __syncthreads();
+  // ---- t-range of the CTA's rows -> its window of live blocks
+  {
+    double tmin = INFINITY, tmax = -INFINITY;
+    bool bad = false;
+    const int r_lo = row_begin + tile0 * 32, r_hi = min(row_end, row_begin + tile1 * 32);
+    for (int i = r_lo + threadIdx.x; i < r_hi; i += blockDim.x) {
+      const double t = pts[i];
+      tmin = fmin(tmin, t);
+      tmax = fmax(tmax, t);
+      bad |= t != t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) nan_s = 1;
+    if (lane == 0) {
+      red_s[0][warp] = tmin;
+      red_s[1][warp] = tmax;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double tmin = INFINITY, tmax = -INFINITY;
+    for (int w = 0; w < nwarps; ++w) {
+      tmin = fmin(tmin, red_s[0][w]);
+      tmax = fmax(tmax, red_s[1][w]);
+    }
+    const unsigned long long live =
+        live_blocks(blo_s, bhi_s, NB, special, tmin, tmax, nan_s != 0, kDeadRatio * sigma2);
+    for (int h = 0; h < 2; ++h) {   // compact the live blocks in ascending order
+      const int blk = lane + 32 * h;
+      if ((live >> blk) & 1ull) lb_s[__popcll(live & ((1ull << blk) - 1ull))] = blk;
+    }
+    if (lane == 0) {
+      live_s = live;
+      live_out[blockIdx.x] = live;
+    }
+  }
+  __syncthreads();
+  const int L = __popcll(live_s);
+  const int T = (L + kRT - 1) / kRT;
+  const int ntask = T * (T + 1) / 2;
+  int R = 1, npass = (ntask + nwarps - 1) / nwarps;
+  if (ntask <= nwarps) {
+    R = min(nwarps / ntask, kTileKs);
+    npass = 1;
+  }
+  const int cw = nwarps - 1;   // warp that prepares row coefficients
+  double* const slab = slabs + (size_t)blockIdx.x * ld * ld;
+
+  for (int pass = 0; pass < npass; ++pass) {
+    // ---- this warp's super-tile (p, q) of the compacted triangle, replica rep
+    int task = -1, rep = 0;
+    if (R > 1) {
+      if (warp < ntask * R) {
+        task = warp / R;
+        rep = warp % R;
+      }
+    } else {
+      task = pass * nwarps + warp;
+      if (task >= ntask) task = -1;
+    }
+    int p = 0, q = 0;
+    uint32_t valid = 0;
+    if (task >= 0) {
+      int idx = task;
+      while (idx >= T - p) {
+        idx -= T - p;
+        ++p;
+      }
+      q = p + idx;
+#pragma unroll
+      for (int i = 0; i < kRT; ++i)
+#pragma unroll
+        for (int j = 0; j < kRT; ++j)
+          if (p * kRT + i < L && q * kRT + j < L && !(p == q && i > j)) valid |= 1u << (i * kRT + j);
+    }
+
+    double acc[kRT][kRT][2];
 #pragma unroll
     for (int i = 0; i < kRT; ++i)
 #pragma unroll
-      for (int j = 0; j < kRT; ++j) {
-        out[(i * kRT + j) * 64] = acc[i][j][0];
-        out[(i * kRT + j) * 64 + 1] = acc[i][j][1];
+      for (int j = 0; j < kRT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    if (tile0 < tile1) {
+      if (warp == cw) {
+        row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, rowc);
+        if (tile0 + 1 < tile1)
+          row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end,
+                        rowc + 256);
       }
+      __syncthreads();
+      gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rowc, X0, warp, nwarps);
+      __syncthreads();
+    }
+    const bool full = valid == 0xFFFFu;
+    const int offa = p * kRT * 32 + lane, offb = q * kRT * 32 + lane;
+    for (int tile = tile0; tile < tile1; ++tile) {
+      const int k = tile - tile0;
+      const double* X = (k & 1) ? X1 : X0;
+      double* const Xn = ((k + 1) & 1) ? X1 : X0;
+      const double* const rcn = rowc + ((k + 1) % 3) * 256;
+      const bool gen_first = nbuf == 2 && ((warp >> 2) & 1);
+#if NYS_LARGE_PROBE == 3
+      long long TT[6];
+      TT[0] = clock64();
+#define NYS_T(i) TT[i] = clock64()
+#else
+#define NYS_T(i)
+#endif
+      if (NYS_LARGE_PROBE != 2 && gen_first && tile + 1 < tile1)
+        gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rcn, Xn, warp, nwarps);
+      NYS_T(1);
+      if (NYS_LARGE_PROBE != 1 && task >= 0) {
+#pragma unroll 1
+        for (int ks = rep; ks < kTileKs; ks += R) {
+          const double* Xk = X + (size_t)ks * NBpad * 32;
+          double xa[kRT], xb[kRT];
+#pragma unroll
+          for (int i = 0; i < kRT; ++i) xa[i] = Xk[offa + i * 32];
+#pragma unroll
+          for (int j = 0; j < kRT; ++j) xb[j] = Xk[offb + j * 32];
+          if (full) {
+#pragma unroll
+            for (int i = 0; i < kRT; ++i)
+#pragma unroll
+              for (int j = 0; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < kRT; ++i)
+#pragma unroll
+              for (int j = 0; j < kRT; ++j)
+                if ((valid >> (i * kRT + j)) & 1u)
+                  nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
+          }
+        }
+      }
+      NYS_T(2);
+      if (nbuf == 1) __syncthreads();
+      if (NYS_LARGE_PROBE != 2 && !gen_first && tile + 1 < tile1)
+        gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rcn, Xn, warp, nwarps);
+      NYS_T(3);
+      if (warp == cw && tile + 2 < tile1)
+        row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + (tile + 2) * 32, row_end,
+                      rowc + ((k + 2) % 3) * 256);
+      NYS_T(4);
+      __syncthreads();
+#if NYS_LARGE_PROBE == 3
+      NYS_T(5);
+      if (blockIdx.x == 5 && (k == 20 || k == 21) && lane == 0)
+        printf("k=%d w=%2d task=%d rep=%d/%d L=%d | gen1 %6lld dmma %6lld gen2 %6lld rc %6lld "
+               "bar %6lld\n",
+               k, warp, task, rep, R, L, TT[1] - TT[0], TT[2] - TT[1], TT[3] - TT[2],
+               TT[4] - TT[3], TT[5] - TT[4]);
+#endif
+    }
+    // ---- slab write: replicas of one super-tile are added in replica order
+    for (int r = 0; r < R; ++r) {
+      if (task >= 0 && rep == r) {
+#pragma unroll
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+          for (int j = 0; j < kRT; ++j)
+            if ((valid >> (i * kRT + j)) & 1u) {
+              const int I = lb_s[p * kRT + i], J = lb_s[q * kRT + j];
+              double* o = slab + (size_t)(I * 8 + (lane >> 2)) * ld + J * 8 + 2 * (lane & 3);
+              if (r == 0) {
+                o[0] = acc[i][j][0];
+                o[1] = acc[i][j][1];
+              } else {
+                o[0] += acc[i][j][0];
+                o[1] += acc[i][j][1];
+              }
+            }
+      }
+      __syncthreads();
+    }
   }
 }
 
-// sum partials over row ranges (fixed order) and scatter to dense K (Pe x Pe)
-__global__ void large_reduce_kernel(const double* __restrict__ part, int nrr, int nslots, int NB,
-                                    int Pe, const __grid_constant__ TaskTable tasks,
-                                    double* __restrict__ K) {
-  const int per = kRT * kRT * 64;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nslots * per;
-       e += gridDim.x * blockDim.x) {
-    const int slot = e / per, w = e % per;
-    const int word = tasks.word[slot];
-    if (word < 0) continue;
-    int a, b, stub, corner;
-    task_decode(word, a, b, stub, corner);
-    const int ij = w >> 6, lane = (w & 63) >> 1, jj = w & 1;
-    const int i = ij / kRT, j = ij % kRT;
-    int I, J;   // block row / column of this accumulator
-    if (stub && i > j) {
-      if (i == 3 && j == 1) {
-        if (!corner) continue;
-        I = J = NB - 1;
-      } else {
-        const int src = (i == 1) ? 0 : (i == 2 && j == 0) ? 1 : (i == 3) ? 2 : 3;
-        I = a * kRT + src;
-        J = NB - 1;
-        if (i == 3 && j == 2) continue;   // unused slot
-      }
-    } else {
-      if (a == b && i > j) continue;
-      I = a * kRT + i;
-      J = b * kRT + j;
-      if (I >= NB || J >= NB) continue;
-    }
-    double s = 0.0;
-    for (int rr = 0; rr < nrr; ++rr) s += part[((size_t)rr * nslots + slot) * per + w];
-    const int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + jj;
-    if (I == J && r > c) continue;   // inside a diagonal block write each pair once
-    if (r < Pe && c < Pe) {
-      K[(size_t)r * Pe + c] = s;
-      K[(size_t)c * Pe + r] = s;
-    }
-  }
+// K[r][c] = sum over CTAs (fixed order) of their slabs where both blocks are live
+__global__ void large_reduce_kernel(const double* __restrict__ slabs,
+                                    const unsigned long long* __restrict__ live, int nrr, int ld,
+                                    int Pe, double* __restrict__ K) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= Pe * Pe) return;
+  const int r = e / Pe, c = e % Pe;
+  if (c < r) return;
+  const unsigned long long need = (1ull << (r / 8)) | (1ull << (c / 8));
+  double s = 0.0;
+  for (int rr = 0; rr < nrr; ++rr)
+    if ((live[rr] & need) == need) s += slabs[((size_t)rr * ld + r) * ld + c];
+  K[(size_t)r * Pe + c] = s;
+  K[(size_t)c * Pe + r] = s;
 }
 
 // T = K W_ext  (Pe x Pw), then E = W_ext^T T (Pw x Pw);  W_ext = diag(W, 1, 1)
@@ -425,24 +459,24 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
                      int p, const double* pts, const double* coef, const double* forcing, int n_c,
                      int row_begin, int row_end, double* gram_ext, void* ws, size_t ws_bytes,
                      cudaStream_t st) {
-  static_assert(sizeof(TaskTable) <= 4000, "task table must fit the kernel parameter space");
   LargePlan L = LargePlan::make(row_end - row_begin, m);
-  if (L.NB > 64 || !L.fits()) return NYS_EUNSUPPORTED;
+  if (!L.fits()) return NYS_EUNSUPPORTED;
   if (ws == nullptr || ws_bytes < L.ws_bytes(m_eff)) return NYS_EWORKSPACE;
-  double* part = static_cast<double*>(ws);
-  double* K = part + L.part_doubles();
+  double* slabs = static_cast<double*>(ws);
+  double* K = slabs + L.slab_doubles();
   double* T = K + (size_t)L.Pe * L.Pe;
-  dim3 grid(L.nrr, L.ngroups);
-  const int nthreads = L.wpc * 32;
+  const int Pw = m_eff + 2;
+  auto* live = reinterpret_cast<unsigned long long*>(T + (size_t)L.Pe * Pw);
+  const int nthreads = kWarps * 32;
 #define NYS_LARGE(PP)                                                                              \
   do {                                                                                             \
     auto kern = large_kspace_kernel<PP>;                                                           \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                                          (int)L.smem);                                             \
     if (e != cudaSuccess) return record_cuda(e);                                                   \
-    kern<<<grid, nthreads, L.smem, st>>>(lm, m, sigma2, pts, coef, forcing, n_c, row_begin,        \
-                                         row_end, L.NB, L.NBpad, L.wpc, L.nbuf, L.tiles_per_cta,   \
-                                         L.tasks, part);                                           \
+    kern<<<L.nrr, nthreads, L.smem, st>>>(lm, m, sigma2, pts, coef, forcing, n_c, row_begin,       \
+                                          row_end, L.NB, L.NBpad, L.ld, L.nbuf, L.tiles_per_cta,   \
+                                          slabs, live);                                            \
     nys_host::count_launches(1);                                                                   \
   } while (0)
   switch (p) {
@@ -453,12 +487,9 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
   }
 #undef NYS_LARGE
   NYS_CHECK_LAUNCH();
-  const int nslots = L.ngroups * L.wpc;
-  int per = nslots * kRT * kRT * 64;
-  large_reduce_kernel<<<(per + 255) / 256, 256, 0, st>>>(part, L.nrr, nslots, L.NB, L.Pe, L.tasks,
-                                                         K);
+  large_reduce_kernel<<<(L.Pe * L.Pe + 255) / 256, 256, 0, st>>>(slabs, live, L.nrr, L.ld, L.Pe,
+                                                                 K);
   nys_host::count_launches(1);
-  const int Pw = m_eff + 2;
   proj_right_kernel<<<(L.Pe * Pw + 127) / 128, 128, 0, st>>>(K, L.Pe, W, ldw, m, m_eff, T);
   nys_host::count_launches(1);
   proj_left_kernel<<<(Pw * Pw + 127) / 128, 128, 0, st>>>(T, L.Pe, W, ldw, m, m_eff, gram_ext);
