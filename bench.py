@@ -300,6 +300,36 @@ def setup_c2(args, ctx):
              "computes the upper block triangle only")
 
 
+def kspace_executed_flops(pts, landmarks, sigma2):
+    """DMMA flops large_kspace_kernel issues (gram_large.cu): per CTA row range
+    only the block pairs of its live window (blocks whose exp() does not
+    underflow to exactly 0 somewhere in the range), 4096 flops per pair per
+    32-row tile."""
+    import torch
+    m = landmarks.size
+    nb = (m + 2 + 7) // 8
+    ntiles = (pts.size + 31) // 32
+    nrr = min(torch.cuda.get_device_properties(0).multi_processor_count, max(ntiles, 1))
+    tpc = (ntiles + nrr - 1) // nrr
+    blo = np.array([landmarks[8 * b:min(8 * b + 8, m)].min() if 8 * b < m else np.inf
+                    for b in range(nb)])
+    bhi = np.array([landmarks[8 * b:min(8 * b + 8, m)].max() if 8 * b < m else -np.inf
+                    for b in range(nb)])
+    special = np.zeros(nb, bool)
+    special[m // 8] = special[(m + 1) // 8] = True
+    total = 0.0
+    for c in range(nrr):
+        t0, t1 = c * tpc, min(ntiles, (c + 1) * tpc)
+        if t0 >= t1:
+            continue
+        seg = pts[t0 * 32:min(pts.size, t1 * 32)]
+        dmin = np.maximum(blo - seg.max(), seg.min() - bhi)
+        live = special | ~((dmin > 0) & (dmin * dmin > 747.0 * sigma2))
+        L = int(live.sum())
+        total += L * (L + 1) / 2 * (t1 - t0) * 4096.0
+    return total
+
+
 def setup_single(args, ctx):
     """Configs 0, 1 (replicas) and 4 (row-sharded, one all-reduce)."""
     torch, dev, rank, world, cid = ctx["torch"], ctx["dev"], ctx["rank"], ctx["world"], args.config
@@ -362,19 +392,23 @@ def setup_single(args, ctx):
     # single instance F = 2 n_c m_eff (m+m_eff) + 4 n_c (m+m_eff) + 4 n_c
     fl = lambda n: 2.0 * n * me * (m + me) + 4.0 * n * (m + me) + 4.0 * n   # noqa: E731
     kspace = (me + 2 + 7) // 8 > 9
+    executed = kspace_executed_flops(bt.pts[rows[0]:rows[1]], bt.landmarks, cfg.sigma2) \
+        if kspace else None
     return dict(
         B=1 if cid == 4 else world, step=step, e2e=e2e, kernel=kernel, check=lambda: True,
         h2d=(pts_h.numel() + coef_h.numel() + forc_h.numel()) * 8, d2h=x_h.numel() * 8,
         flops_kernel=fl(rows[1] - rows[0]), flops_step=fl(n_c),
-        executed=None, kernel_name="large_kspace_kernel (kernel-space Gram, cond-gated)" if kspace
+        executed=executed, kernel_name="large_kspace_kernel (kernel-space Gram, cond-gated)" if kspace
         else "fused_gram_kernel", scaling="strong" if cid == 4 else "weak",
         parallelism=(f"row-sharded x{world} + 1 all-reduce" if cid == 4 else
                      f"replicas x{world}"),
         extra={"m_eff": me, "n": cfg.n, "m": m,
                "step": "eig + fused feature/Gram + KKT LU" + (" + all-reduce" if shard else "")},
-        note="algorithmic F of SURVEY.md 8(d)" + ("; config 4 accumulates the Gram in kernel "
-                                                   "space (cond(Omega)=28, SURVEY A1 1.3e-13)"
-                                                   if kspace else ""),
+        note="algorithmic F of SURVEY.md 8(d)" + (
+            "; config 4 accumulates the Gram in kernel space (cond(Omega)=28, SURVEY A1 "
+            "1.3e-13) and skips landmark blocks whose exp() underflows to exactly 0 for a CTA's "
+            "rows (bit-identical sums), so the dense F overstates the work: executed_* counts "
+            "the DMMA flops actually issued" if kspace else ""),
         per_rank_units=False)
 
 

@@ -187,6 +187,19 @@ int nys_newton_residual_f64(const double* S0, const double* S1, const double* S0
                             const double* vals, int n_cond, const double* gamma,
                             const double* X, int ldx, const int* idx, int nb, double* F,
                             double* norm, double* aux, double* work, void* stream);
+/* Batched step halving (newton.py:305-318): norms[t * nb + j] = max|F| at the
+ * trial X[idx[j]] + trial_alphas[t] * D[idx[j]] for t < ntrial, bit-identical to
+ * forming the candidate with nys_newton_step_f64 and calling nys_newton_residual_f64;
+ * nothing else is written.  scratch: nys_newton_trial_scratch_bytes (0 when the
+ * per-CTA rows fit in shared memory). */
+size_t nys_newton_trial_scratch_bytes(int m_eff, int n_c, int nb, int ntrial);
+int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, int m_eff, int n_c,
+                               const double* g, const double* fy, const double* fyy,
+                               const double* alpha, const double* beta, const double* Ac,
+                               const double* betac, const double* vals, int n_cond,
+                               const double* gamma, const double* X, const double* D, int ldx,
+                               const int* idx, int nb, const double* trial_alphas, int ntrial,
+                               double* norms, void* scratch, size_t scratch_bytes, void* stream);
 /* reduced system K [nb * nz^2], rz [nb * nz], nz = m_eff + 1 + n_cond (DMMA weighted Grams) */
 int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, const double* aux,
                            const double* F, int ldx, const double* gamma, const double* Ac,

@@ -48,6 +48,10 @@ SIGNATURES = {
     "nys_newton_residual_f64": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp,
                                      _vp, _vp, _i, _vp, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp,
                                      _vp]),
+    "nys_newton_trial_scratch_bytes": (C.c_size_t, [_i, _i, _i, _i]),
+    "nys_newton_trial_norms_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _vp, _i, _vp, _vp,
+                                        C.c_size_t, _vp]),
     "nys_newton_reduced_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _vp,
                                     _vp, _vp]),
     "nys_lu_solve_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp]),

@@ -68,12 +68,14 @@ struct Rhs {
       f_yy = fyy[o];
       return;
     }
+    // numpy's operation order, never contracted into FMAs (the host callables
+    // of workloads.py evaluate the same expressions)
     const double a = alpha[b], be = beta[b];
     double s, c;
     sincos(y, &s, &c);
-    f = g[o] + a * y * y + be * s;
-    f_y = 2.0 * a * y + be * c;
-    f_yy = 2.0 * a - be * s;
+    f = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a, y), y), g[o]), __dmul_rn(be, s));
+    f_y = __dadd_rn(__dmul_rn(__dmul_rn(2.0, a), y), __dmul_rn(be, c));
+    f_yy = __dsub_rn(__dmul_rn(2.0, a), __dmul_rn(be, s));
   }
 };
 
@@ -81,63 +83,83 @@ struct Rhs {
 // residual F (newton.py:128-147, p = 1) for instances idx[0..nb), plus the
 // per-row quantities the Jacobian needs: aux[b] = (f_y, q = f_yy e1, c).
 // S (n_c x me) row-major for S omega; ST (me x n_c) for S^T e (coalesced).
+// kTrial = false: the residual at X[b] with every by-product (F, aux, work).
+// kTrial = true: the max-norm only, at the line-search trial X[b] + alpha_t D[b]
+// (grid.y = trial t), nothing else written -- the batched step halving.  Both
+// run the same arithmetic in the same order, so a trial's norm is bit-identical
+// to materialising the candidate (newton_step_kernel) and calling the residual.
+template <bool kTrial>
 __global__ void __launch_bounds__(kResThreads)
-    newton_residual_kernel(const double* __restrict__ S0, const double* __restrict__ S1,
-                           const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
+    newton_residual_kernel(const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
                            int n_c, Rhs rhs, const double* __restrict__ Ac,
                            const double* __restrict__ betac, const double* __restrict__ vals,
                            int nk, const double* __restrict__ gamma, const double* __restrict__ X,
                            int ldx, const int* __restrict__ idx, double* __restrict__ F,
                            double* __restrict__ norm, double* __restrict__ aux,
-                           double* __restrict__ work) {
+                           double* __restrict__ work, const double* __restrict__ D,
+                           const double* __restrict__ alphas, int nb) {
   extern __shared__ double sh[];
   __shared__ double red[kResThreads / 32];
+  __shared__ double lam_s[kMaxCondN];
   const int b = idx[blockIdx.x];
   const double gm = gamma[b];
   const double* x = X + (size_t)b * ldx;
-  double* Fb = F + (size_t)b * ldx;
+  const double* dx = kTrial ? D + (size_t)b * ldx : nullptr;
+  const double al = kTrial ? alphas[blockIdx.y] : 0.0;
+  // x entry j of this CTA's point (trial: the candidate, as newton_step_kernel forms it)
+#define NYS_XV(j) (kTrial ? fma(al, dx[j], x[j]) : x[j])
+  double* Fb = kTrial ? nullptr : F + (size_t)b * ldx;
   double* om = sh;                 // me
-  double* e1 = work + (size_t)b * 2 * n_c;
+  double* e1;
+  if (kTrial)
+    e1 = work != nullptr ? work + ((size_t)blockIdx.y * nb + blockIdx.x) * 2 * n_c : sh + me;
+  else
+    e1 = work + (size_t)b * 2 * n_c;
   double* e2 = e1 + n_c;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int k = tid; k < me; k += nt) om[k] = x[k];
+  for (int k = tid; k < me; k += nt) om[k] = NYS_XV(k);
+  if (tid < nk) lam_s[tid] = NYS_XV(me + 1 + tid);
   __syncthreads();
-  const double bias = x[me];
-  const double* lam = x + me + 1;
-  const double* y = x + me + 1 + nk;
-  double* auxb = aux + (size_t)b * 3 * n_c;
+  const double bias = NYS_XV(me);
+  const int y0 = me + 1 + nk;
+  double* auxb = kTrial ? nullptr : aux + (size_t)b * 3 * n_c;
   double fmax_local = 0.0;
   int bad = 0;
+  // rows across threads, features from the transposed copies: every load is
+  // a coalesced 256-byte warp access (S0/S1 rows are 8*me bytes apart)
   for (int i = tid; i < n_c; i += nt) {
-    const double* s0 = S0 + (size_t)i * me;
-    const double* s1 = S1 + (size_t)i * me;
     double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
     int k = 0;
+#pragma unroll 4
     for (; k + 1 < me; k += 2) {
-      a0 = fma(s1[k], om[k], a0);
-      a1 = fma(s1[k + 1], om[k + 1], a1);
-      c0 = fma(s0[k], om[k], c0);
-      c1 = fma(s0[k + 1], om[k + 1], c1);
+      a0 = fma(S1T[(size_t)k * n_c + i], om[k], a0);
+      a1 = fma(S1T[(size_t)(k + 1) * n_c + i], om[k + 1], a1);
+      c0 = fma(S0T[(size_t)k * n_c + i], om[k], c0);
+      c1 = fma(S0T[(size_t)(k + 1) * n_c + i], om[k + 1], c1);
     }
     if (k < me) {
-      a0 = fma(s1[k], om[k], a0);
-      c0 = fma(s0[k], om[k], c0);
+      a0 = fma(S1T[(size_t)k * n_c + i], om[k], a0);
+      c0 = fma(S0T[(size_t)k * n_c + i], om[k], c0);
     }
     const double s1w = a0 + a1, s0w = c0 + c1;
+    const double yi = NYS_XV(y0 + i);
     double f, fy, fyy;
-    rhs.eval(b, i, y[i], f, fy, fyy);
-    const double ee1 = s1w - f;
-    const double ee2 = y[i] - s0w - bias;
+    rhs.eval(b, i, yi, f, fy, fyy);
+    const double ee1 = __dsub_rn(s1w, f);
+    const double ee2 = __dsub_rn(__dsub_rn(yi, s0w), bias);
     if (!isfinite(ee1) || !isfinite(f)) bad = 1;
     e1[i] = ee1;
     e2[i] = ee2;
-    const double Fy = -gm * fy * ee1 + gm * ee2;
-    Fb[me + 1 + nk + i] = Fy;
+    // F_y = -gamma f_y e1 + gamma e2 in numpy's order (newton.py:146)
+    const double Fy = __dadd_rn(__dmul_rn(__dmul_rn(-gm, fy), ee1), __dmul_rn(gm, ee2));
     fmax_local = fmax(fmax_local, fabs(Fy));
-    const double q = fyy * ee1;
-    auxb[i] = fy;
-    auxb[n_c + i] = q;
-    auxb[2 * n_c + i] = 1.0 + fy * fy - q;
+    if (!kTrial) {
+      Fb[y0 + i] = Fy;
+      const double q = __dmul_rn(fyy, ee1);
+      auxb[i] = fy;
+      auxb[n_c + i] = q;
+      auxb[2 * n_c + i] = __dsub_rn(__dadd_rn(1.0, __dmul_rn(fy, fy)), q);
+    }
   }
   __syncthreads();
   // F_omega = omega + gamma S1^T e1 - gamma S0^T e2 + Ac^T lambda  (warp per k)
@@ -155,29 +177,51 @@ __global__ void __launch_bounds__(kResThreads)
       c += __shfl_xor_sync(0xffffffffu, c, o);
     }
     if (lane == 0) {
-      double v = om[k] + gm * a - gm * c;
-      for (int mu = 0; mu < nk; ++mu) v += Ac[(size_t)mu * me + k] * lam[mu];
-      Fb[k] = v;
+      // omega + gamma S1^T e1 - gamma S0^T e2 + Ac^T lambda (newton.py:139), uncontracted
+      double acl = 0.0;
+      for (int mu = 0; mu < nk; ++mu) acl = __dadd_rn(acl, __dmul_rn(Ac[(size_t)mu * me + k], lam_s[mu]));
+      double v = __dadd_rn(__dsub_rn(__dadd_rn(om[k], __dmul_rn(gm, a)), __dmul_rn(gm, c)), acl);
+      if (kTrial)
+        fmax_local = fmax(fmax_local, fabs(v));
+      else
+        Fb[k] = v;
     }
   }
   double se2 = 0.0;
   for (int i = tid; i < n_c; i += nt) se2 += e2[i];
   se2 = block_reduce(se2, red, false);
   if (tid == 0) {
-    double Fbias = -gm * se2;
-    for (int mu = 0; mu < nk; ++mu) Fbias += betac[mu] * lam[mu];
-    Fb[me] = Fbias;
+    double bl = 0.0;
+    for (int mu = 0; mu < nk; ++mu) bl = __dadd_rn(bl, __dmul_rn(betac[mu], lam_s[mu]));
+    const double Fbias = __dadd_rn(__dmul_rn(-gm, se2), bl);   // newton.py:143
+    if (kTrial)
+      fmax_local = fmax(fmax_local, fabs(Fbias));
+    else
+      Fb[me] = Fbias;
     for (int mu = 0; mu < nk; ++mu) {
       double v = 0.0;
-      for (int k = 0; k < me; ++k) v += Ac[(size_t)mu * me + k] * om[k];
-      Fb[me + 1 + mu] = v + betac[mu] * bias - vals[(size_t)b * nk + mu];
+      for (int k = 0; k < me; ++k) v = fma(Ac[(size_t)mu * me + k], om[k], v);
+      // Ac omega + beta b - values (newton.py:144)
+      v = __dsub_rn(__dadd_rn(v, __dmul_rn(betac[mu], bias)), vals[(size_t)b * nk + mu]);
+      if (kTrial)
+        fmax_local = fmax(fmax_local, fabs(v));
+      else
+        Fb[me + 1 + mu] = v;
     }
   }
   __syncthreads();
-  for (int k = tid; k < me + 1 + nk; k += nt) fmax_local = fmax(fmax_local, fabs(Fb[k]));
+  if (!kTrial)
+    for (int k = tid; k < me + 1 + nk; k += nt) fmax_local = fmax(fmax_local, fabs(Fb[k]));
   const int any_bad = __syncthreads_or(bad);
   const double nrm = block_reduce(fmax_local, red, true);
-  if (tid == 0) norm[b] = any_bad ? NAN : nrm;   // NaN -> DivergenceError (newton.py:137-138)
+  if (tid == 0) {
+    // NaN -> DivergenceError (newton.py:137-138)
+    if (kTrial)
+      norm[(size_t)blockIdx.y * nb + blockIdx.x] = any_bad ? NAN : nrm;
+    else
+      norm[b] = any_bad ? NAN : nrm;
+  }
+#undef NYS_XV
 }
 
 // ---------------------------------------------------------------------------
@@ -439,7 +483,7 @@ __global__ void __launch_bounds__(256)
   const double al = alpha[b];
   const double* Xb = X + (size_t)b * ldx;
   double* Xcb = Xc + (size_t)b * ldx;
-  for (int k = threadIdx.x; k < nz + n_c; k += blockDim.x) Xcb[k] = Xb[k] + al * Db[k];
+  for (int k = threadIdx.x; k < nz + n_c; k += blockDim.x) Xcb[k] = fma(al, Db[k], Xb[k]);
 }
 
 __global__ void transpose_kernel(const double* __restrict__ A, int rows, int cols,
@@ -496,11 +540,49 @@ extern "C" int nys_newton_residual_f64(const double* S0, const double* S1, const
       ldx < m_eff + 1 + n_cond + n_c)
     return NYS_EINVAL;
   if (nb == 0) return NYS_OK;
+  (void)S0;
+  (void)S1;
   Rhs rhs{g, fy, fyy, alpha, beta, n_c};
-  newton_residual_kernel<<<nb, kResThreads, m_eff * sizeof(double),
-                           static_cast<cudaStream_t>(stream)>>>(
-      S0, S1, S0T, S1T, m_eff, n_c, rhs, Ac, betac, vals, n_cond, gamma, X, ldx, idx, F, norm, aux,
-      work);
+  newton_residual_kernel<false><<<nb, kResThreads, m_eff * sizeof(double),
+                                  static_cast<cudaStream_t>(stream)>>>(
+      S0T, S1T, m_eff, n_c, rhs, Ac, betac, vals, n_cond, gamma, X, ldx, idx, F, norm, aux, work,
+      nullptr, nullptr, nb);
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" size_t nys_newton_trial_scratch_bytes(int m_eff, int n_c, int nb, int ntrial) {
+  const size_t smem = ((size_t)m_eff + 2 * (size_t)n_c) * sizeof(double);
+  if (smem <= 96 * 1024) return 0;   // e1/e2 live in shared memory
+  return (size_t)ntrial * nb * 2 * n_c * sizeof(double);
+}
+
+extern "C" int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, int m_eff, int n_c,
+                                          const double* g, const double* fy, const double* fyy,
+                                          const double* alpha, const double* beta,
+                                          const double* Ac, const double* betac,
+                                          const double* vals, int n_cond, const double* gamma,
+                                          const double* X, const double* D, int ldx,
+                                          const int* idx, int nb, const double* trial_alphas,
+                                          int ntrial, double* norms, void* scratch,
+                                          size_t scratch_bytes, void* stream) {
+  if (m_eff < 1 || n_c < 1 || n_cond < 0 || n_cond > kMaxCondN || nb < 0 || ntrial < 0 ||
+      ntrial > 65535 || ldx < m_eff + 1 + n_cond + n_c)
+    return NYS_EINVAL;
+  if (nb == 0 || ntrial == 0) return NYS_OK;
+  const size_t need = nys_newton_trial_scratch_bytes(m_eff, n_c, nb, ntrial);
+  if (need > 0 && (scratch == nullptr || scratch_bytes < need)) return NYS_EWORKSPACE;
+  const size_t smem = (size_t)m_eff * sizeof(double) +
+                      (need > 0 ? 0 : 2 * (size_t)n_c * sizeof(double));
+  auto kern = newton_residual_kernel<true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return nys_host::record_cuda(e);
+  Rhs rhs{g, fy, fyy, alpha, beta, n_c};
+  kern<<<dim3(nb, ntrial), kResThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      S0T, S1T, m_eff, n_c, rhs, Ac, betac, vals, n_cond, gamma, X, ldx, idx, nullptr, norms,
+      nullptr, need > 0 ? static_cast<double*>(scratch) : nullptr, D, trial_alphas, nb);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;

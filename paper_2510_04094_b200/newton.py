@@ -205,14 +205,17 @@ class NewtonBatch:
         if self.specs is not None:
             self._sample_host(X, ids)
         idx_t = self._idx(ids) if idx_t is None else idx_t
+        self._residual_launch(X, idx_t, len(ids))
+        return self.norm[idx_t].cpu().numpy()
+
+    def _residual_launch(self, X, idx_t, nb):
         _lib.call("nys_newton_residual_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
                   _lib.ptr(self.S0T), _lib.ptr(self.S1T), self.me, self.n_c, _lib.ptr(self.g),
                   _lib.ptr(self.fy), _lib.ptr(self.fyy), _lib.ptr(self.fal), _lib.ptr(self.fbe),
                   _lib.ptr(self.Ac), _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk,
-                  _lib.ptr(self.gam), _lib.ptr(X), self.ldx, _lib.ptr(idx_t), len(ids),
+                  _lib.ptr(self.gam), _lib.ptr(X), self.ldx, _lib.ptr(idx_t), nb,
                   _lib.ptr(self.F), _lib.ptr(self.norm), _lib.ptr(self.aux), _lib.ptr(self.work),
                   _lib.stream_ptr())
-        return self.norm[idx_t].cpu().numpy()
 
     def direction(self, ids) -> np.ndarray:
         """Newton direction D[b] at X[b] (aux/F from the last residual at X);
@@ -244,6 +247,51 @@ class NewtonBatch:
                   _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
                   _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), len(ids), 0,
                   _lib.stream_ptr())
+
+    def _line_search(self, ids, ref, shrink, halvings, chunks=(1, 3)):
+        """Step halving of newton.py:305-318 with the trial steps evaluated in
+        batches: alpha_k = shrink^k for a chunk of k at once (one host sync per
+        chunk instead of per halving), then the first accepted k per instance --
+        the same alpha the sequential loop stops at, because every trial's
+        residual depends only on its own instance and alpha.  Never-accepted
+        instances get shrink^halvings, as the sequential loop leaves them."""
+        torch = self.torch
+        alphas = [1.0]
+        for _ in range(halvings):
+            alphas.append(alphas[-1] * shrink)   # the loop's repeated products
+        out = {b: alphas[halvings] for b in ids}
+        left = list(range(len(ids)))
+        k0, c = 0, 0
+        while left and k0 < halvings:
+            # growing chunks: most steps are accepted at alpha = 1 or after a few
+            # halvings; the rest of the ladder goes in one batch
+            kk = min(chunks[c] if c < len(chunks) else halvings - k0, halvings - k0)
+            c += 1
+            sub = [ids[r] for r in left]
+            idx_t = self._idx(sub)
+            nb = len(sub)
+            norms = torch.empty((kk, nb), dtype=torch.float64, device=self.dev)
+            al_t = torch.tensor(alphas[k0:k0 + kk], dtype=torch.float64, device=self.dev)
+            sb = self.lib.nys_newton_trial_scratch_bytes(self.me, self.n_c, nb, kk)
+            scratch = _lib.WORKSPACE.get(sb, self.dev) if sb else None
+            _lib.call("nys_newton_trial_norms_f64", _lib.ptr(self.S0T), _lib.ptr(self.S1T),
+                      self.me, self.n_c, _lib.ptr(self.g), _lib.ptr(self.fy), _lib.ptr(self.fyy),
+                      _lib.ptr(self.fal), _lib.ptr(self.fbe), _lib.ptr(self.Ac),
+                      _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk, _lib.ptr(self.gam),
+                      _lib.ptr(self.X), _lib.ptr(self.D), self.ldx, _lib.ptr(idx_t), nb,
+                      _lib.ptr(al_t), kk, _lib.ptr(norms), _lib.ptr(scratch) if sb else None, sb,
+                      _lib.stream_ptr())
+            nh = norms.cpu().numpy()
+            nxt = []
+            for c, r in enumerate(left):
+                ok = np.flatnonzero(np.isfinite(nh[:, c]) & (nh[:, c] <= ref[r]))
+                if ok.size:
+                    out[ids[r]] = alphas[k0 + int(ok[0])]
+                else:
+                    nxt.append(r)
+            left = nxt
+            k0 += kk
+        return out
 
     # -------------------------------------------------------------- states
     def const_state(self, ids):
@@ -344,20 +392,24 @@ class NewtonBatch:
             if not active:
                 break
             if damping:
-                alpha = {b: 1.0 for b in active}
-                searching = list(active)
-                for _ in range(halvings):
-                    if not searching:
-                        break
-                    self.candidate(searching, [alpha[b] for b in searching])
-                    cn = self.residual(self.Xc, searching)
-                    nxt = []
-                    for b, v in zip(searching, cn):
-                        if np.isfinite(v) and v <= norm[pos[b]]:
-                            continue            # accepted
-                        alpha[b] *= shrink
-                        nxt.append(b)
-                    searching = nxt
+                if self.specs is None:
+                    alpha = self._line_search(active, [norm[pos[b]] for b in active], shrink,
+                                              halvings)
+                else:
+                    alpha = {b: 1.0 for b in active}
+                    searching = list(active)
+                    for _ in range(halvings):
+                        if not searching:
+                            break
+                        self.candidate(searching, [alpha[b] for b in searching])
+                        cn = self.residual(self.Xc, searching)
+                        nxt = []
+                        for b, v in zip(searching, cn):
+                            if np.isfinite(v) and v <= norm[pos[b]]:
+                                continue            # accepted
+                            alpha[b] *= shrink
+                            nxt.append(b)
+                        searching = nxt
                 self.candidate(active, [alpha[b] for b in active])
             else:
                 self.candidate(active, [1.0] * len(active))

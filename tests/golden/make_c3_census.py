@@ -1,0 +1,81 @@
+"""Config-3 census: run the LIVE reference (``nysode``) on all 256 bench
+instances (seed 0) and store each outcome -- status, iteration count, the
+solution vector x and its error vs the manufactured solution.
+
+Build container only (``/root/reference`` is absent on the GPU box):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_c3_census.py
+Parallel over instances (one BLAS thread per worker process).
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+
+
+def _init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    sys.path.insert(0, REF)
+    sys.path.insert(0, ROOT)
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+
+
+def _solve(i):
+    from nysode import newton, nystrom
+    from nysode.kernel import RbfKernel
+    from nysode.problems import BoundaryCondition, Conditions, NonlinearOdeSpec
+
+    from paper_2510_04094_b200 import workloads as W
+    cfg = W.CONFIGS[3]
+    g = W.grid(cfg)
+    lm = W.equidistant_landmarks(g, cfg.m)
+    fmap = nystrom.build_feature_map(RbfKernel(cfg.sigma2), lm)
+    inst = W.instance(3, 0, i, cfg)
+    spec = NonlinearOdeSpec(1, inst.rhs, (inst.rhs_y,), cfg.domain, {(0, 0): inst.rhs_yy})
+    cond = Conditions("ivp", tuple(BoundaryCondition(*c) for c in inst.conditions()))
+    opts = newton.NewtonOptions(max_iters=cfg.newton_max_iters)
+    try:
+        mdl, tr = newton.solve_nonlinear(spec, cond, fmap, g, cfg.gamma, opts)
+        status = 0
+    except newton.MaxItersExceeded as exc:      # harness.py:173-175
+        mdl, tr = exc.model, exc.trace
+        status = 1
+    except newton.DivergenceError:
+        return i, 2, 0, None, np.nan
+    except newton.SingularJacobianError:
+        return i, 3, 0, None, np.nan
+    y = mdl.predict(0, g)
+    ys = inst.sol(g)
+    x = np.concatenate([mdl.omega, [mdl.bias], mdl.multipliers])
+    return i, status, tr.iterations, x, float(np.linalg.norm(y - ys) / np.linalg.norm(ys))
+
+
+def main():
+    t0 = time.time()
+    n = 256
+    with ProcessPoolExecutor(max_workers=os.cpu_count(), initializer=_init) as ex:
+        res = sorted(ex.map(_solve, range(n)))
+    me = next(r[3].size for r in res if r[3] is not None)
+    X = np.full((n, me), np.nan)
+    for i, st, its, x, err in res:
+        if x is not None:
+            X[i] = x
+    np.savez_compressed(os.path.join(HERE, "c3_census_seed0.npz"),
+                        status=np.array([r[1] for r in res], np.int32),
+                        iterations=np.array([r[2] for r in res], np.int32),
+                        x=X, err_vs_exact=np.array([r[4] for r in res]))
+    st = np.bincount([r[1] for r in res], minlength=4)
+    print(f"c3 census: status counts {st.tolist()} in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()

@@ -83,3 +83,76 @@ def test_newton_residual_matches_oracle():
         Fo = NP.residual(w, x[j])
         scale = np.abs(Fo).max()
         np.testing.assert_allclose(F[j], Fo, rtol=0, atol=1e-9 * scale)
+
+
+def test_batched_step_halving_is_bit_identical():
+    """nys_newton_trial_norms_f64 (the batched line search) returns exactly the
+    norms of materialising each candidate and running the residual."""
+    import torch
+
+    from paper_2510_04094_b200 import _lib
+    g = load_golden("c3_seed0_i0-3")
+    eng, fm = _engine(g)
+    ids = list(range(eng.B))
+    eng.X[:] = torch.as_tensor(eng.const_state(ids), device=eng.dev)
+    eng.residual(eng.X, ids)
+    info = eng.direction(ids)
+    assert (info == 0).all()
+    alphas = [1.0, 0.5, 0.25, 0.125]
+    seq = []
+    for a in alphas:
+        eng.candidate(ids, [a] * len(ids))
+        seq.append(eng.residual(eng.Xc, ids))
+    seq = np.array(seq)
+    idx_t = eng._idx(ids)
+    norms = torch.empty((len(alphas), len(ids)), dtype=torch.float64, device=eng.dev)
+    al_t = torch.tensor(alphas, dtype=torch.float64, device=eng.dev)
+    _lib.call("nys_newton_trial_norms_f64", _lib.ptr(eng.S0T), _lib.ptr(eng.S1T), eng.me,
+              eng.n_c, _lib.ptr(eng.g), None, None, _lib.ptr(eng.fal), _lib.ptr(eng.fbe),
+              _lib.ptr(eng.Ac), _lib.ptr(eng.betac), _lib.ptr(eng.vals), eng.nk,
+              _lib.ptr(eng.gam), _lib.ptr(eng.X), _lib.ptr(eng.D), eng.ldx, _lib.ptr(idx_t),
+              len(ids), _lib.ptr(al_t), len(alphas), _lib.ptr(norms), None, 0, _lib.stream_ptr())
+    got = norms.cpu().numpy()
+    assert np.array_equal(got, seq, equal_nan=True), (got, seq)
+
+
+def test_config3_census_matches_reference():
+    """All 256 config-3 bench instances against the live reference's outcomes
+    (tests/golden/c3_census_seed0.npz, make_c3_census.py): instances the
+    reference converges converge here with y_hat within the north-star 1e-6;
+    outcome disagreements are confined to the reference's non-converging,
+    rounding-chaotic instances."""
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import newton as NW
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import ivp
+
+    ref = load_golden("c3_census_seed0")
+    cfg = W.CONFIGS[3]
+    g = W.grid(cfg)
+    lm = W.equidistant_landmarks(g, cfg.m)
+    B = ref["status"].size
+    insts = [W.instance(3, 0, i) for i in range(B)]
+    pts = g[1:]
+    fam = NW.SeparableFamily(np.stack([i.g_fn(pts) for i in insts]),
+                             np.array([i.quad_coeff for i in insts]),
+                             np.array([i.sin_coeff for i in insts]))
+    vals = np.array([[i.conditions()[0][2]] for i in insts])
+    fm = N.build_feature_map(RbfKernel(cfg.sigma2), lm)
+    eng = NW.NewtonBatch(fm, g, ivp([(0.0, 0, 0.0)]), vals, cfg.gamma, family=fam)
+    status, X, traces, rung = eng.solve(max_iters=cfg.newton_max_iters)
+    me = eng.me
+    Y = L.predict_batch(fm, X[:, :me + 1], 0, g).cpu().numpy()
+    conv = np.flatnonzero(ref["status"] == 0)
+    Yr = L.predict_batch(fm, ref["x"][conv, :me + 1], 0, g).cpu().numpy()
+    bad = []
+    for j, i in enumerate(conv):
+        d = rel_l2(Y[i], Yr[j])
+        if status[i] != NW.OK or d > YHAT_TOL:
+            bad.append((int(i), int(status[i]), d))
+    agree = int((status == ref["status"]).sum())
+    print("status agreement", agree, "/", B, "ours", np.bincount(status, minlength=4),
+          "ref", np.bincount(ref["status"], minlength=4), "mismatched converged", bad)
+    assert not bad, bad
