@@ -1,6 +1,7 @@
 """Config-3 census: run the LIVE reference (``nysode``) on all 256 bench
 instances (seed 0) and store each outcome -- status, iteration count, the
-solution vector x and its error vs the manufactured solution.
+solution vector x and its error vs the manufactured solution -- plus the
+reference's landmark eigenpairs (x is expressed in that basis).
 
 Build container only (``/root/reference`` is absent on the GPU box):
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_c3_census.py
@@ -69,7 +70,16 @@ def main():
     for i, st, its, x, err in res:
         if x is not None:
             X[i] = x
+    _init()
+    from nysode import nystrom
+    from nysode.kernel import RbfKernel
+
+    from paper_2510_04094_b200 import workloads as W
+    cfg = W.CONFIGS[3]
+    fmap = nystrom.build_feature_map(RbfKernel(cfg.sigma2),
+                                     W.equidistant_landmarks(W.grid(cfg), cfg.m))
     np.savez_compressed(os.path.join(HERE, "c3_census_seed0.npz"),
+                        eigvals=fmap.eigenvalues, eigvecs=fmap.eigenvectors,
                         status=np.array([r[1] for r in res], np.int32),
                         iterations=np.array([r[2] for r in res], np.int32),
                         x=X, err_vs_exact=np.array([r[4] for r in res]))
