@@ -281,6 +281,7 @@ def setup_c2(args, ctx):
                   _lib.ptr(forc_d), B, None, _lib.ptr(solver.ws), ws_bytes, _lib.stream_ptr())
 
     nb = (me + 2 + 7) // 8
+    nbd = nb - 1 if (me % 8 == 0 and nb >= 2) else nb   # gram_batch.cu ext mode: (g, r) by FMA
     return dict(
         B=B, step=step, e2e=e2e, kernel=kernel,
         check=lambda: int((info_h != 0).sum()) == 0,
@@ -290,14 +291,15 @@ def setup_c2(args, ctx):
         flops_kernel=B * (2.0 * n_c * me * me + 8.0 * n_c * me + 4.0 * n_c),
         flops_step=2.0 * (p + 1) * n_c * m * me + B * (2.0 * n_c * me * me + 8.0 * n_c * me
                                                         + 4.0 * n_c),
-        executed=B * (4 * ((n_c + 3) // 4)) * (nb * (nb + 1) // 2) * 64 * 2.0,
+        executed=B * (4 * ((n_c + 3) // 4)) * (nbd * (nbd + 1) // 2) * 64 * 2.0,
         kernel_name="batch_gram_kernel (+3 psi-pack launches)", scaling="weak",
         parallelism=f"instance-sharded x{ctx['world']}, no collective",
         extra={"m_eff": me, "global_batch": ctx["world"] * B,
                "l2": "samples 402 MB/GPU > 126 MB L2; no flush needed",
                "step": "eig + shared features + batched Gram + batched KKT"},
         note="algorithmic F (SURVEY.md 8d) counts the full m_eff^2 Gram; the kernel "
-             "computes the upper block triangle only")
+             "computes the upper block triangle only, and with m_eff % 8 == 0 accumulates the "
+             "(g, r) columns with FP64 FMAs instead of DMMA blocks (executed_* = DMMA flops)")
 
 
 def kspace_executed_flops(pts, landmarks, sigma2):

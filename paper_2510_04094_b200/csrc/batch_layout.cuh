@@ -15,6 +15,11 @@ int device_sm_count();              // cached cudaDevAttrMultiProcessorCount
 struct BatchLayout {
   int n_c, m_eff, p, B;
   int NB, NO, npair;
+  // ext: m_eff % 8 == 0, so the last 8-column block holds only the two extended
+  // columns (g, r); the kernel then accumulates D^T g, D^T r, g.g, g.r, r.r with
+  // FP64 FMAs instead of 9 mostly-empty DMMA blocks
+  bool ext;
+  int NBD;
   int nsplit, ks_per_split, nks_pad;
 
   static BatchLayout make(int n_c, int m_eff, int p, int B) {
@@ -26,6 +31,8 @@ struct BatchLayout {
     L.NB = (m_eff + 2 + 7) / 8;
     L.NO = p + 1;
     L.npair = L.NB * (L.NB + 1) / 2;
+    L.ext = (m_eff % 8 == 0) && L.NB >= 2;
+    L.NBD = L.ext ? L.NB - 1 : L.NB;
     const int nks = (n_c + 3) / 4;
     const int nchunks = (nks + kBatchChunkKs - 1) / kBatchChunkKs;
     // row splits: fill whole waves of one CTA per SM (the kernel is register
@@ -52,7 +59,14 @@ struct BatchLayout {
   }
   int rows_pad() const { return nks_pad * 4; }
   size_t psi_doubles() const { return (size_t)nks_pad * NO * NB * 32; }
-  size_t part_doubles() const { return (size_t)nsplit * B * npair * 64; }
+  // per-instance partial: upper block triangle of the DMMA blocks (MMA layout),
+  // then in ext mode [NBD][32 lanes][g, r] and [32 lanes][gg, gr, rr]
+  __host__ __device__ static size_t slot_doubles_for(bool ext, int NB, int NBD) {
+    return ext ? (size_t)NBD * (NBD + 1) / 2 * 64 + (size_t)NBD * 64 + 96
+               : (size_t)NB * (NB + 1) / 2 * 64;
+  }
+  size_t slot_doubles() const { return slot_doubles_for(ext, NB, NBD); }
+  size_t part_doubles() const { return (size_t)nsplit * B * slot_doubles(); }
   int Pe() const { return m_eff + 2; }
   size_t e_doubles() const { return (size_t)B * Pe() * Pe(); }
   size_t ws_bytes() const {

@@ -50,7 +50,9 @@ struct Role {
   }
 };
 
-template <int NB, int NO, int WARPS, int SPLIT, int Lo, int Hi>
+// NB = blocks in the packed Psi chunk; EXT: block NB-1 holds only (g, r) and
+// is accumulated with FMAs (DMMA over blocks 0..NB-2 only)
+template <int NB, int NO, int WARPS, int SPLIT, int Lo, int Hi, bool EXT>
 NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict__ coef,
                        const double* __restrict__ forcing, int n_c, int B, int b, int ks0,
                        int nchunks, int rcol, double* sm, uint64_t* bar,
@@ -59,14 +61,18 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
   constexpr int CH = nys::kBatchChunkKs;
   constexpr int kChunkDoubles = CH * NO * NB * 32;
   constexpr uint32_t kChunkBytes = kChunkDoubles * sizeof(double);
-  constexpr int NPAIR = Tri<NB>::kPairs;
-  using R = Role<NB, Lo, Hi>;
+  constexpr int NBD = EXT ? NB - 1 : NB;        // blocks that go through DMMA
+  constexpr int SLOT = EXT ? NBD * (NBD + 1) / 2 * 64 + NBD * 64 + 96 : NB * (NB + 1) / 2 * 64;
+  using R = Role<NBD, Lo, Hi>;
 
   const int lane = threadIdx.x & 31, tig = lane & 3, gid = lane >> 2;
   const bool active = b < B;
   double acc[R::kCount][2];
 #pragma unroll
   for (int q = 0; q < R::kCount; ++q) acc[q][0] = acc[q][1] = 0.0;
+  double accg[EXT ? NBD : 1], accr[EXT ? NBD : 1], accgg = 0.0, accgr = 0.0, accrr = 0.0;
+#pragma unroll
+  for (int F = 0; F < (EXT ? NBD : 1); ++F) accg[F] = accr[F] = 0.0;
 
   const double* cb = coef + (size_t)(active ? b : 0) * P * n_c;
   const double* rb = forcing + (size_t)(active ? b : 0) * n_c;
@@ -94,9 +100,9 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
 #pragma unroll
         for (int k = 0; k < P; ++k) f[k] = nys::shfl(fk[k], src);
         const double r = nys::shfl(rr, src);
-        double x[NB];
+        double x[NBD];
 #pragma unroll
-        for (int F = 0; F < NB; ++F) {
+        for (int F = 0; F < NBD; ++F) {
           if (!R::needs(F)) {
             x[F] = 0.0;
             continue;
@@ -106,18 +112,29 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
 #pragma unroll
           for (int k = 1; k <= P; ++k)
             v = fma(-f[k - 1], Q[((kk * NO + (P - k)) * NB + F) * 32], v);
-          x[F] = (F * 8 + gid == rcol) ? r : v;
+          x[F] = (!EXT && F * 8 + gid == rcol) ? r : v;
         }
 #pragma unroll
-        for (int I = 0; I < NB; ++I)
+        for (int I = 0; I < NBD; ++I)
 #pragma unroll
-          for (int J = I; J < NB; ++J)
+          for (int J = I; J < NBD; ++J)
             if (R::has(I, J)) {
-              constexpr int dummy = 0;
-              (void)dummy;
-              const int q = Tri<NB>::idx(I, J) - Lo;
+              const int q = Tri<NBD>::idx(I, J) - Lo;
               nys::dmma(acc[q][0], acc[q][1], x[I], x[J]);
             }
+        if constexpr (EXT) {
+          // extended columns of this lane's row: g = -f_p (what Psi_0's unit
+          // column makes of the combine), r = forcing
+          const double gq = -f[P - 1];
+#pragma unroll
+          for (int F = 0; F < NBD; ++F) {
+            accg[F] = fma(x[F], gq, accg[F]);
+            accr[F] = fma(x[F], r, accr[F]);
+          }
+          accgg = fma(gq, gq, accgg);
+          accgr = fma(gq, r, accgr);
+          accrr = fma(r, r, accrr);
+        }
       }
     }
     if (c + 1 < nchunks) {
@@ -133,16 +150,29 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
     }
   }
   if (active) {
-    double* out = part + (((size_t)blockIdx.y * B + b) * NPAIR + Lo) * 64 + lane * 2;
+    double* slot = part + ((size_t)blockIdx.y * B + b) * SLOT;
+    double* out = slot + (size_t)Lo * 64 + lane * 2;
 #pragma unroll
     for (int q = 0; q < R::kCount; ++q) {
       out[q * 64] = acc[q][0];
       out[q * 64 + 1] = acc[q][1];
     }
+    if constexpr (EXT) {
+      double* ex = slot + NBD * (NBD + 1) / 2 * 64;
+#pragma unroll
+      for (int F = 0; F < NBD; ++F) {
+        ex[(F * 32 + lane) * 2] = accg[F];
+        ex[(F * 32 + lane) * 2 + 1] = accr[F];
+      }
+      double* sc = ex + NBD * 64 + lane * 3;
+      sc[0] = accgg;
+      sc[1] = accgr;
+      sc[2] = accrr;
+    }
   }
 }
 
-template <int NB, int NO, int WARPS, int SPLIT>
+template <int NB, int NO, int WARPS, int SPLIT, bool EXT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     batch_gram_kernel(const double* __restrict__ psi, const double* __restrict__ coef,
                       const double* __restrict__ forcing, int n_c, int B, int ks_per_split,
@@ -150,7 +180,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   constexpr int CH = nys::kBatchChunkKs;
   constexpr int kChunkDoubles = CH * NO * NB * 32;
   constexpr uint32_t kChunkBytes = kChunkDoubles * sizeof(double);
-  constexpr int NPAIR = Tri<NB>::kPairs;
+  constexpr int NPAIR = Tri<EXT ? NB - 1 : NB>::kPairs;
   constexpr int H = (NPAIR + 1) / 2;
 
   extern __shared__ __align__(128) double sm[];   // [2][kChunkDoubles]
@@ -175,50 +205,79 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     }
   }
   if constexpr (SPLIT == 1) {
-    gram_body<NB, NO, WARPS, SPLIT, 0, NPAIR>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol,
-                                              sm, bar, part);
+    gram_body<NB, NO, WARPS, SPLIT, 0, NPAIR, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
+                                                   rcol, sm, bar, part);
   } else {
     if ((warp & 1) == 0)
-      gram_body<NB, NO, WARPS, SPLIT, 0, H>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol, sm,
-                                            bar, part);
+      gram_body<NB, NO, WARPS, SPLIT, 0, H, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
+                                                 rcol, sm, bar, part);
     else
-      gram_body<NB, NO, WARPS, SPLIT, H, NPAIR>(psi, coef, forcing, n_c, B, b, ks0, nchunks, rcol,
-                                                sm, bar, part);
+      gram_body<NB, NO, WARPS, SPLIT, H, NPAIR, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
+                                                     rcol, sm, bar, part);
   }
 }
 
-// partials -> dense E (Pe x Pe) per instance, summing splits in fixed order
+// partials -> dense E (Pe x Pe) per instance, summing splits (and, for the
+// FMA-accumulated extended columns, the lanes that share a column) in fixed order
 __global__ void batch_unpack_kernel(const double* __restrict__ part, int nsplit, int B, int NB,
-                                    int Pe, double* __restrict__ gram) {
+                                    int Pe, int ext, double* __restrict__ gram) {
   const int b = blockIdx.x;
-  const int npair = NB * (NB + 1) / 2;
+  const int NBD = ext ? NB - 1 : NB;
+  const int npair = NBD * (NBD + 1) / 2;
+  const size_t slot = nys::BatchLayout::slot_doubles_for(ext != 0, NB, NBD);
+  double* E = gram + (size_t)b * Pe * Pe;
   for (int e = threadIdx.x; e < npair * 64; e += blockDim.x) {
     const int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
     int I = 0, rem = q;
-    while (rem >= NB - I) {
-      rem -= NB - I;
+    while (rem >= NBD - I) {
+      rem -= NBD - I;
       ++I;
     }
     const int J = I + rem;
     double s = 0.0;
-    for (int sp = 0; sp < nsplit; ++sp) s += part[((size_t)sp * B + b) * npair * 64 + e];
+    for (int sp = 0; sp < nsplit; ++sp) s += part[((size_t)sp * B + b) * slot + e];
     const int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
     if (r < Pe && c < Pe) {
       if (I == J && r > c) continue;   // diagonal block: each pair once
-      gram[(size_t)b * Pe * Pe + (size_t)r * Pe + c] = s;
-      gram[(size_t)b * Pe * Pe + (size_t)c * Pe + r] = s;
+      E[(size_t)r * Pe + c] = s;
+      E[(size_t)c * Pe + r] = s;
     }
+  }
+  if (!ext) return;
+  const int me = Pe - 2;
+  const size_t xo = (size_t)npair * 64;
+  // D^T g (column me) and D^T r (column me + 1): row 8F + gid, lanes gid*4 + tig
+  for (int t = threadIdx.x; t < 2 * me; t += blockDim.x) {
+    const int row = t >> 1, which = t & 1, F = row >> 3, gid = row & 7;
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const double* ex = part + ((size_t)sp * B + b) * slot + xo;
+      for (int tig = 0; tig < 4; ++tig) s += ex[(F * 32 + gid * 4 + tig) * 2 + which];
+    }
+    E[(size_t)row * Pe + me + which] = s;
+    E[(size_t)(me + which) * Pe + row] = s;
+  }
+  if (threadIdx.x < 3) {
+    const int k = threadIdx.x;   // gg, gr, rr: rows are lanes 0..3 (gid 0)
+    double s = 0.0;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const double* sc = part + ((size_t)sp * B + b) * slot + xo + (size_t)NBD * 64;
+      for (int tig = 0; tig < 4; ++tig) s += sc[tig * 3 + k];
+    }
+    const int r = k == 2 ? me + 1 : me, c = k == 0 ? me : me + 1;
+    E[(size_t)r * Pe + c] = s;
+    E[(size_t)c * Pe + r] = s;
   }
 }
 
-template <int NB, int NO>
+template <int NB, int NO, bool EXT>
 int launch_gram(const double* psi, const double* coef, const double* forcing, int n_c, int B,
                 const BatchLayout& L, double* part, cudaStream_t st) {
   // SPLIT = 2 (two warps per instance, 128 registers each) measured slower on
   // B200 for NB = 9: 4.15 ms vs 3.33 ms (doubled combine + Psi reads, spills)
   constexpr int SPLIT = 1;
   constexpr int WARPS = nys::kBatchWarps * SPLIT;
-  auto kern = batch_gram_kernel<NB, NO, WARPS, SPLIT>;
+  auto kern = batch_gram_kernel<NB, NO, WARPS, SPLIT, EXT>;
   const size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return nys_host::record_cuda(e);
@@ -231,20 +290,25 @@ int launch_gram(const double* psi, const double* coef, const double* forcing, in
 }
 
 template <int NO>
-int dispatch_nb(int NB, const double* psi, const double* coef, const double* forcing, int n_c,
-                int B, const BatchLayout& L, double* part, cudaStream_t st) {
+int dispatch_nb(int NB, bool ext, const double* psi, const double* coef, const double* forcing,
+                int n_c, int B, const BatchLayout& L, double* part, cudaStream_t st) {
+#define NYS_NB(N)                                                                \
+  case N:                                                                        \
+    return ext ? launch_gram<N, NO, true>(psi, coef, forcing, n_c, B, L, part, st) \
+               : launch_gram<N, NO, false>(psi, coef, forcing, n_c, B, L, part, st);
   switch (NB) {
-    case 1: return launch_gram<1, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 2: return launch_gram<2, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 3: return launch_gram<3, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 4: return launch_gram<4, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 5: return launch_gram<5, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 6: return launch_gram<6, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 7: return launch_gram<7, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 8: return launch_gram<8, NO>(psi, coef, forcing, n_c, B, L, part, st);
-    case 9: return launch_gram<9, NO>(psi, coef, forcing, n_c, B, L, part, st);
+    case 1: return launch_gram<1, NO, false>(psi, coef, forcing, n_c, B, L, part, st);
+    NYS_NB(2)
+    NYS_NB(3)
+    NYS_NB(4)
+    NYS_NB(5)
+    NYS_NB(6)
+    NYS_NB(7)
+    NYS_NB(8)
+    NYS_NB(9)
     default: return NYS_EUNSUPPORTED;
   }
+#undef NYS_NB
 }
 
 }  // namespace
@@ -252,7 +316,8 @@ int dispatch_nb(int NB, const double* psi, const double* coef, const double* for
 namespace nys_host {
 int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, double* gram,
                         cudaStream_t st) {
-  batch_unpack_kernel<<<B, 256, 0, st>>>(part, nsplit, B, NB, Pe, gram);
+  const int ext = ((Pe - 2) % 8 == 0) && NB >= 2;   // BatchLayout::ext
+  batch_unpack_kernel<<<B, 256, 0, st>>>(part, nsplit, B, NB, Pe, ext, gram);
   count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
@@ -282,8 +347,8 @@ extern "C" int nys_batch_gram_f64(const double* landmarks, int m, const double* 
   int rc = nys_host::launch_psi_pack(landmarks, m, W, ldw, m_eff, sigma2, p, pts, n_c, L.NB,
                                      L.rows_pad(), psi, st);
   if (rc) return rc;
-  rc = (p == 1) ? dispatch_nb<2>(L.NB, psi, coef, forcing, n_c, B, L, part, st)
-                : dispatch_nb<3>(L.NB, psi, coef, forcing, n_c, B, L, part, st);
+  rc = (p == 1) ? dispatch_nb<2>(L.NB, L.ext, psi, coef, forcing, n_c, B, L, part, st)
+                : dispatch_nb<3>(L.NB, L.ext, psi, coef, forcing, n_c, B, L, part, st);
   if (rc) return rc;
   if (gram_ext != nullptr) return nys_host::launch_batch_unpack(part, L.nsplit, B, L.NB, m_eff + 2,
                                                                 gram_ext, st);
