@@ -30,6 +30,11 @@ constexpr int kDcThreads = 1024;
 constexpr int kMaxBlocks = kDcMaxN / kLeaf;
 constexpr double kEps = 2.220446049250313e-16;
 
+// leading dimension of A: ld = 4 (mod 16) doubles, so the matvec's 8 rows x 4
+// column-lanes per warp hit 16 distinct bank pairs twice (2 wavefronts, the
+// minimum for 256 bytes) instead of 4-way conflicts with ld = n + 1
+__host__ __device__ inline int dc_ld(int n) { return n + (((4 - n) % 16) + 16) % 16; }
+
 struct DcShared {
   double d[kDcMaxN], e[kDcMaxN], beta[kDcMaxN], hv[kDcMaxN], hp[kDcMaxN];
   double lam[kDcMaxN];    // eigenvalues aligned with the columns of Q
@@ -222,15 +227,20 @@ NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, 
   return dorg + tau;
 }
 
-__global__ void __launch_bounds__(kDcThreads, 1)
+// kSmem: the working matrices live in dynamic shared memory (n <= 64) -- a
+// compile-time address space, so the compiler emits LDS/STS; kT: columns per
+// lane in the rank-2 update (ceil(n / 32) bound)
+template <bool kSmem, int kT>
+__global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
     dc_eig_kernel(const double* __restrict__ lm, int n, double sigma2, double drop_tol,
                   double* __restrict__ eigvals, double* __restrict__ eigvecs,
                   double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
                   double* __restrict__ gbuf, int use_smem, int debug) {
   extern __shared__ __align__(16) double dyn[];
   __shared__ DcShared S;
-  const int ld = n + 1;
-  double* base = use_smem ? dyn : gbuf;
+  const int ld = dc_ld(n);
+  (void)use_smem;
+  double* base = kSmem ? dyn : gbuf;
   double* A = base;                           // n x ld (Householder vectors below diagonal)
   double* Q = A + (size_t)n * ld;             // n x n
   double* Qn = Q + (size_t)n * n;             // n x n
@@ -256,60 +266,115 @@ __global__ void __launch_bounds__(kDcThreads, 1)
   }
 
   // ---------------- Householder tridiagonalisation (as eig.cu phase 1)
-  for (int k = 0; k + 2 < n; ++k) {
-    const int i0 = k + 1;
-    double tail = 0.0;
-    for (int i = i0 + tid; i < n; i += nt) {
-      const double x = A[(size_t)i * ld + k];
-      S.hv[i] = x;
-      if (i != i0) tail = fma(x, x, tail);
-    }
-    tail = dc_block_sum(tail, S);
-    if (tid == 0) {
-      const double x0 = S.hv[i0];
-      double beta = 0.0, alpha = x0;
-      if (tail > 0.0) {
-        const double nx = sqrt(fma(x0, x0, tail));
-        alpha = -copysign(nx, x0);
-        const double v0 = x0 - alpha;
-        beta = 2.0 / fma(v0, v0, tail);
-        S.hv[i0] = v0;
-        A[(size_t)i0 * ld + k] = v0;
-      }
-      S.e[k] = alpha;
-      S.beta[k] = beta;
-    }
-    __syncthreads();
-    const double beta = S.beta[k];
-    if (beta == 0.0) continue;
-    for (int i = i0 + tid; i < n; i += nt) {
-      const double* row = A + (size_t)i * ld;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int j = i0;
-      for (; j + 3 < n; j += 4) {
-        a0 = fma(row[j], S.hv[j], a0);
-        a1 = fma(row[j + 1], S.hv[j + 1], a1);
-        a2 = fma(row[j + 2], S.hv[j + 2], a2);
-        a3 = fma(row[j + 3], S.hv[j + 3], a3);
-      }
-      for (; j < n; ++j) a0 = fma(row[j], S.hv[j], a0);
-      S.hp[i] = beta * ((a0 + a1) + (a2 + a3));
-    }
-    __syncthreads();
-    double vp = 0.0;
-    for (int i = i0 + tid; i < n; i += nt) vp = fma(S.hv[i], S.hp[i], vp);
-    vp = dc_block_sum(vp, S);
-    const double Kc = 0.5 * beta * vp;
-    for (int i = i0 + tid; i < n; i += nt) S.hp[i] = S.hp[i] - Kc * S.hv[i];
-    __syncthreads();
+  // Three barriers per reflector: warp 0 forms the reflector (norm by warp
+  // shuffles), the matvec splits every row over tpr lanes, and each warp
+  // recomputes v.p itself so the rank-2 update needs no extra barrier.
+  long long tq[4] = {0, 0, 0, 0};
+  const long long tsetup = clock64() - tc0;
+  {
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = i0 + warp; i < n; i += nw) {
-      double* row = A + (size_t)i * ld;
-      const double vi = S.hv[i], wi = S.hp[i];
-      for (int j = i0 + lane; j < n; j += 32) row[j] = row[j] - vi * S.hp[j] - wi * S.hv[j];
+    for (int k = 0; k + 2 < n; ++k) {
+      const int i0 = k + 1;
+      long long tt = clock64();
+      if (warp == 0) {
+        double tail = 0.0;
+        for (int i = i0 + 1 + lane; i < n; i += 32) {
+          const double x = A[(size_t)i * ld + k];
+          S.hv[i] = x;
+          tail = fma(x, x, tail);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) tail += __shfl_xor_sync(0xffffffffu, tail, o);
+        if (lane == 0) {
+          const double x0 = A[(size_t)i0 * ld + k];
+          double beta = 0.0, alpha = x0;
+          S.hv[i0] = x0;
+          if (tail > 0.0) {
+            const double nx = sqrt(fma(x0, x0, tail));
+            alpha = -copysign(nx, x0);
+            const double v0 = x0 - alpha;
+            beta = 2.0 / fma(v0, v0, tail);
+            S.hv[i0] = v0;
+            A[(size_t)i0 * ld + k] = v0;
+          }
+          S.e[k] = alpha;
+          S.beta[k] = beta;
+        }
+      }
+      __syncthreads();
+      if (debug) { long long t2 = clock64(); tq[0] += t2 - tt; tt = t2; }
+      const double beta = S.beta[k];
+      if (beta == 0.0) continue;
+      const int len = n - i0;
+      const int tpr = (nt >= 8 * len) ? 8 : (nt >= 4 * len) ? 4 : (nt >= 2 * len) ? 2 : 1;
+      const int rows_per_pass = nt / tpr;
+      const int npass = (len + rows_per_pass - 1) / rows_per_pass;
+      for (int ps = 0; ps < npass; ++ps) {   // whole passes: the shuffles need full warps
+        const int r = ps * rows_per_pass + tid / tpr, sub = tid % tpr;
+        const int i = i0 + r;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (r < len) {
+          const double* __restrict__ row = A + (size_t)i * ld;
+          const double* __restrict__ hv = S.hv;
+          int j = i0 + sub;
+          for (; j + 3 * tpr < n; j += 4 * tpr) {   // four independent loads per trip
+            a0 = fma(row[j], hv[j], a0);
+            a1 = fma(row[j + tpr], hv[j + tpr], a1);
+            a2 = fma(row[j + 2 * tpr], hv[j + 2 * tpr], a2);
+            a3 = fma(row[j + 3 * tpr], hv[j + 3 * tpr], a3);
+          }
+          for (; j < n; j += tpr) a0 = fma(row[j], hv[j], a0);
+        }
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int o = 1; o < tpr; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sub == 0 && r < len) S.hp[i] = beta * acc;
+      }
+      __syncthreads();
+      if (debug) { long long t2 = clock64(); tq[1] += t2 - tt; tt = t2; }
+      double vp = 0.0;
+      for (int i = i0 + lane; i < n; i += 32) vp = fma(S.hv[i], S.hp[i], vp);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) vp += __shfl_xor_sync(0xffffffffu, vp, o);
+      const double Kc = 0.5 * beta * vp;
+      // this lane's columns j = i0 + lane + 32 t: v_j and w_j in registers; rows
+      // in groups of kG whose loads are all issued before any store (the
+      // compiler cannot prove different rows do not alias)
+      double hvj[kT], wj[kT];
+#pragma unroll
+      for (int t = 0; t < kT; ++t) {
+        const int j = i0 + lane + 32 * t;
+        hvj[t] = j < n ? S.hv[j] : 0.0;
+        wj[t] = j < n ? S.hp[j] - Kc * S.hv[j] : 0.0;
+      }
+      constexpr int kG = kT <= 2 ? 4 : 1;
+      for (int ib = i0 + warp; ib < n; ib += nw * kG) {
+        double val[kG][kT];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int i = ib + g * nw;
+#pragma unroll
+          for (int t = 0; t < kT; ++t) {
+            const int j = i0 + lane + 32 * t;
+            val[g][t] = (i < n && j < n) ? A[(size_t)i * ld + j] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int i = ib + g * nw;
+          if (i >= n) break;
+          const double vi = S.hv[i], wi = S.hp[i] - Kc * vi;
+#pragma unroll
+          for (int t = 0; t < kT; ++t) {
+            const int j = i0 + lane + 32 * t;
+            if (j < n) A[(size_t)i * ld + j] = val[g][t] - vi * wj[t] - wi * hvj[t];
+          }
+        }
+      }
+      __syncthreads();
+      if (debug) { long long t2 = clock64(); tq[2] += t2 - tt; tt = t2; }
     }
-    __syncthreads();
   }
+  if (debug && tid == 0) printf("[nys dc] tridiag phases: setup %lld reflector %lld matvec %lld update %lld\n", tsetup, tq[0], tq[1], tq[2]);
   for (int i = tid; i < n; i += nt) S.d[i] = A[(size_t)i * ld + i];
   if (tid == 0) {
     if (n >= 2) S.e[n - 2] = A[(size_t)(n - 1) * ld + (n - 2)];
@@ -614,10 +679,33 @@ __global__ void __launch_bounds__(kDcThreads, 1)
     }
     __syncthreads();
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = i0 + warp; i < n; i += nw) {
-      const double vi = S.hv[i];
-      double* row = Q + (size_t)i * n;
-      for (int c = lane; c < n; c += 32) row[c] -= vi * S.hp[c];
+    // this lane's columns c = lane + 32 t; rows in groups of kG, loads first
+    double hpc[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) hpc[t] = lane + 32 * t < n ? S.hp[lane + 32 * t] : 0.0;
+    constexpr int kG = kT <= 2 ? 4 : 1;
+    for (int ib = i0 + warp; ib < n; ib += nw * kG) {
+      double val[kG][kT];
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const int i = ib + g * nw;
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int c = lane + 32 * t;
+          val[g][t] = (i < n && c < n) ? Q[(size_t)i * n + c] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < kG; ++g) {
+        const int i = ib + g * nw;
+        if (i >= n) break;
+        const double vi = S.hv[i];
+#pragma unroll
+        for (int t = 0; t < kT; ++t) {
+          const int c = lane + 32 * t;
+          if (c < n) Q[(size_t)i * n + c] = val[g][t] - vi * hpc[t];
+        }
+      }
     }
     __syncthreads();
   }
@@ -661,7 +749,7 @@ __global__ void __launch_bounds__(kDcThreads, 1)
 
 namespace nys_host {
 size_t dc_buffer_bytes(int n) {
-  return ((size_t)n * (n + 1) + 3 * (size_t)n * n) * sizeof(double);
+  return ((size_t)n * dc_ld(n) + 3 * (size_t)n * n) * sizeof(double);
 }
 bool dc_fits(int n) { return n >= 1 && n <= kDcMaxN; }
 bool dc_uses_smem(int n) { return dc_buffer_bytes(n) <= 150 * 1024; }
@@ -672,18 +760,26 @@ int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, doubl
   const size_t need = dc_buffer_bytes(n);
   const int use_smem = dc_uses_smem(n);
   size_t dyn = 0;
-  if (use_smem) {
-    dyn = need;
-    cudaError_t e = cudaFuncSetAttribute(dc_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)dyn);
-    if (e != cudaSuccess) return record_cuda(e);
-  } else if (ws == nullptr || ws_bytes < need) {
-    return NYS_EWORKSPACE;
-  }
+  if (!use_smem && (ws == nullptr || ws_bytes < need)) return NYS_EWORKSPACE;
   const int threads = n <= 64 ? 256 : kDcThreads;
-  dc_eig_kernel<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
-                                         static_cast<double*>(ws), use_smem,
-                                         getenv("NYS_EIG_DEBUG") != nullptr);
+  const int dbg = getenv("NYS_EIG_DEBUG") != nullptr;
+  auto launch = [&](auto kern) -> int {
+    if (use_smem) {
+      dyn = need;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)dyn);
+      if (e != cudaSuccess) return record_cuda(e);
+    }
+    kern<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
+                                  static_cast<double*>(ws), use_smem, dbg);
+    return NYS_OK;
+  };
+  int rc;
+  if (use_smem)
+    rc = n <= 64 ? launch(dc_eig_kernel<true, 2>) : launch(dc_eig_kernel<true, kDcMaxN / 32>);
+  else
+    rc = n <= 64 ? launch(dc_eig_kernel<false, 2>) : launch(dc_eig_kernel<false, kDcMaxN / 32>);
+  if (rc) return rc;
   count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
