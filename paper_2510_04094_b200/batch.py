@@ -176,7 +176,10 @@ class SharedGridPipeline:
 
     def prepare(self):
         """Eigendecomposition + solver state (the per-landmark-set work)."""
-        fm = self._build(self.kernel, self.landmarks, self.drop_tol, device=self.device)
+        from .nystrom import EigBuffers
+        if getattr(self, "_eigbuf", None) is None:
+            self._eigbuf = EigBuffers(self.landmarks, self.device)
+        fm = self._build(self.kernel, self.landmarks, self.drop_tol, buffers=self._eigbuf)
         if self.solver is None or self.solver.fmap.m_eff != fm.m_eff:
             self.solver = LinearBatchSolver(fm, self.grid, self.gamma, self.order, self.cond,
                                             self.max_batch)

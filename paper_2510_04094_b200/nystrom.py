@@ -126,26 +126,61 @@ class NystromFeatureMap:
         return self.feature_matrix(ell, [t])[0]
 
 
+class EigBuffers:
+    """Device buffers of one landmark set's eigendecomposition, reused across
+    repeated builds (SharedGridPipeline): the landmarks are copied once and the
+    m_eff read-back goes through pinned memory -- no per-step allocations or
+    pageable copies on the critical path.  A feature map built into these
+    buffers is overwritten by the next build."""
+
+    def __init__(self, landmarks, device=None):
+        lib, torch = _lib.require_device()
+        self.landmarks = np.asarray(landmarks, dtype=float).reshape(-1).copy()
+        self.device = torch.device(device or "cuda")
+        m = self.landmarks.size
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.d_lm = _lib.as_f64(self.landmarks, self.device)
+        self.s = torch.empty(m, **f64)
+        self.V = torch.empty((m, m), **f64)
+        self.W = torch.empty((m, m), **f64)
+        self.meta = torch.zeros(2, dtype=torch.int32, device=self.device)   # m_eff, info
+        self.meta_h = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self.wsb = lib.nys_landmark_eig_workspace_bytes(m)
+        self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.device) if self.wsb else None
+
+
 def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TOL,
-                      device=None) -> NystromFeatureMap:
+                      device=None, buffers: Optional[EigBuffers] = None) -> NystromFeatureMap:
     """Eigendecompose Omega_mm on the GPU and keep s > max(drop_tol s_0, 0)."""
     landmarks = np.asarray(landmarks, dtype=float).reshape(-1)
     if not 0 <= drop_tol < 1:
         raise ValueError(f"drop_tol must lie in [0, 1), got {drop_tol}")
     lib, torch = _lib.require_device()
-    device = torch.device(device or "cuda")
     m = landmarks.size
-    d_lm = _lib.as_f64(landmarks, device)
-    s = torch.empty(m, dtype=torch.float64, device=device)
-    V = torch.empty((m, m), dtype=torch.float64, device=device)
-    W = torch.empty((m, m), dtype=torch.float64, device=device)
-    meta = torch.zeros(2, dtype=torch.int32, device=device)   # m_eff, info
-    wsb = lib.nys_landmark_eig_workspace_bytes(m)
-    ws = _lib.WORKSPACE.get(wsb, device) if wsb else None
+    if buffers is not None:
+        if not np.array_equal(buffers.landmarks, landmarks):
+            raise ValueError("EigBuffers hold a different landmark set")
+        device = buffers.device
+        d_lm, s, V, W, meta, ws, wsb = (buffers.d_lm, buffers.s, buffers.V, buffers.W,
+                                        buffers.meta, buffers.ws, buffers.wsb)
+    else:
+        device = torch.device(device or "cuda")
+        d_lm = _lib.as_f64(landmarks, device)
+        s = torch.empty(m, dtype=torch.float64, device=device)
+        V = torch.empty((m, m), dtype=torch.float64, device=device)
+        W = torch.empty((m, m), dtype=torch.float64, device=device)
+        meta = torch.zeros(2, dtype=torch.int32, device=device)   # m_eff, info
+        wsb = lib.nys_landmark_eig_workspace_bytes(m)
+        ws = _lib.WORKSPACE.get(wsb, device) if wsb else None
     _lib.call("nys_landmark_eig_f64", _lib.ptr(d_lm), m, float(k.sigma2), float(drop_tol),
               _lib.ptr(s), _lib.ptr(V), _lib.ptr(W), _lib.ptr(meta), _lib.ptr(meta) + 4,
               _lib.ptr(ws), wsb, _lib.stream_ptr())
-    m_eff, info = (int(v) for v in meta.cpu())
+    if buffers is not None:
+        buffers.meta_h.copy_(meta, non_blocking=True)
+        torch.cuda.current_stream(device).synchronize()
+        m_eff, info = (int(v) for v in buffers.meta_h)
+    else:
+        m_eff, info = (int(v) for v in meta.cpu())
     sweeps, info = info >> 8, info & 0xFF      # bits 8+: Jacobi sweeps (diagnostic)
     if info == _lib.INFO_DEGENERATE:
         raise DegenerateLandmarksError("two landmarks coincide within 1e-12")
