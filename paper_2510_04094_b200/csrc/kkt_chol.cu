@@ -31,11 +31,13 @@ namespace {
 
 constexpr int kNeedsLu = 16;      // internal; kkt.cu's LU kernel clears it
 constexpr int kMaxNh = 96;
-constexpr int kNC = (kMaxNh + 31) / 32;
 
 NYS_DEV int pk(int i, int j) { return i * (i + 1) / 2 + j; }   // packed lower, j <= i
 
-template <int P>
+// kNC = ceil(nh / 32) column chunks per lane for whole rows; kNCU =
+// ceil((nh - 1) / 32) for the trailing update (columns k+1..nh-1), so the
+// config-2 side nh = 65 updates with two chunks instead of three
+template <int P, int kNC, int kNCU>
 __global__ void __launch_bounds__(32)
     kkt_chol_kernel(const double* __restrict__ gram, int m_eff, const double* __restrict__ Ac,
                     const double* __restrict__ beta, const double* __restrict__ values,
@@ -81,9 +83,9 @@ __global__ void __launch_bounds__(32)
       break;
     }
     const double inv = rsqrt(akk);   // 1 / L_kk
-    double colk[kNC];                 // L[j][k] for j = k+1+lane+32c, kept in registers
+    double colk[kNCU];                 // L[j][k] for j = k+1+lane+32c, kept in registers
 #pragma unroll
-    for (int c = 0; c < kNC; ++c) {
+    for (int c = 0; c < kNCU; ++c) {
       const int j = k + 1 + lane + 32 * c;
       colk[c] = j < nh ? L[pk(j, k)] * inv : 0.0;
     }
@@ -93,36 +95,39 @@ __global__ void __launch_bounds__(32)
       dinv[k] = inv;
     }
 #pragma unroll
-    for (int c = 0; c < kNC; ++c) {
+    for (int c = 0; c < kNCU; ++c) {
       const int j = k + 1 + lane + 32 * c;
       if (j < nh) L[pk(j, k)] = colk[c];
     }
     __syncwarp();
     // A[i][j] -= L[i][k] L[j][k], k < j <= i; column-owner lanes, 4 rows per batch
     int i = k + 1;
+    int rb = pk(i, 0);   // packed start of row i; row i + 1 starts i + 1 later
     for (; i + 3 < nh; i += 4) {
-      double li[4], a[4][kNC];
+      double li[4], a[4][kNCU];
+      const int rbr[4] = {rb, rb + i + 1, rb + 2 * i + 3, rb + 3 * i + 6};
 #pragma unroll
-      for (int r = 0; r < 4; ++r) li[r] = L[pk(i + r, k)];
+      for (int r = 0; r < 4; ++r) li[r] = L[rbr[r] + k];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < kNC; ++c) {
+        for (int c = 0; c < kNCU; ++c) {
           const int j = k + 1 + lane + 32 * c;
-          a[r][c] = j <= i + r ? L[pk(i + r, j)] : 0.0;
+          a[r][c] = j <= i + r ? L[rbr[r] + j] : 0.0;
         }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < kNC; ++c) {
+        for (int c = 0; c < kNCU; ++c) {
           const int j = k + 1 + lane + 32 * c;
-          if (j <= i + r) L[pk(i + r, j)] = a[r][c] - li[r] * colk[c];
+          if (j <= i + r) L[rbr[r] + j] = a[r][c] - li[r] * colk[c];
         }
+      rb += 4 * i + 10;   // start of row i + 4
     }
     for (; i < nh; ++i) {
       const double li = L[pk(i, k)];
 #pragma unroll
-      for (int c = 0; c < kNC; ++c) {
+      for (int c = 0; c < kNCU; ++c) {
         const int j = k + 1 + lane + 32 * c;
         if (j <= i) L[pk(i, j)] -= li * colk[c];
       }
@@ -319,13 +324,13 @@ __global__ void __launch_bounds__(32)
   if (lane == 0) info[b] = nonfinite ? kNeedsLu : NYS_INFO_OK;
 }
 
-template <int P>
-int launch_chol(const double* dense, int m_eff, const double* Ac, const double* beta,
+template <int P, int NC, int NCU>
+int launch_chol_nc(const double* dense, int m_eff, const double* Ac, const double* beta,
                 const double* values, double gamma, int B, double* x, int* info, cudaStream_t st) {
   const int nh = m_eff + 1;
   const size_t dyn =
       ((size_t)nh * (nh + 1) / 2 + nh + (size_t)nh * (P + 1) + nh + P) * sizeof(double);
-  auto kern = kkt_chol_kernel<P>;
+  auto kern = kkt_chol_kernel<P, NC, NCU>;
   if (dyn > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return nys_host::record_cuda(e);
@@ -334,6 +339,17 @@ int launch_chol(const double* dense, int m_eff, const double* Ac, const double* 
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
+}
+
+template <int P>
+int launch_chol(const double* dense, int m_eff, const double* Ac, const double* beta,
+                const double* values, double gamma, int B, double* x, int* info, cudaStream_t st) {
+  const int nh = m_eff + 1;
+  if (nh <= 32) return launch_chol_nc<P, 1, 1>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+  if (nh == 33) return launch_chol_nc<P, 2, 1>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+  if (nh <= 64) return launch_chol_nc<P, 2, 2>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+  if (nh == 65) return launch_chol_nc<P, 3, 2>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+  return launch_chol_nc<P, 3, 3>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
 }
 
 }  // namespace
