@@ -493,10 +493,10 @@ def main():
     lib = _lib.load()
     for _ in range(args.warmup):
         S["step"]()
-    n0 = lib.nys_launch_count()
+    n0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         ms = T.time(S["step"], args.steps)
-    launches = (lib.nys_launch_count() - n0) / args.steps
+    launches = (_lib.launch_count() - n0) / args.steps
     # whole-job solves per second: c2/c3 weak (B per rank), c0/c1 replicas, c4 one
     # solve across all ranks
     units = {2: world * S["B"], 3: world * S["B"], 0: world, 1: world, 4: 1}[cid]

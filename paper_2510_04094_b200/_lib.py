@@ -90,6 +90,21 @@ def load(path: str = LIB_PATH) -> C.CDLL:
     return lib
 
 
+_GRAPH_LAUNCHES = 0
+
+
+def note_graph_launches(n: int) -> None:
+    """Kernels replayed from a CUDA graph (the C-side counter only sees the
+    launches made while the graph was captured)."""
+    global _GRAPH_LAUNCHES
+    _GRAPH_LAUNCHES += int(n)
+
+
+def launch_count() -> int:
+    """nys_launch_count() plus kernels replayed from captured graphs."""
+    return int(load().nys_launch_count()) + _GRAPH_LAUNCHES
+
+
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
 

@@ -174,8 +174,8 @@ class SharedGridPipeline:
         self.device = device
         self.solver = None
 
-    def prepare(self):
-        """Eigendecomposition + solver state (the per-landmark-set work)."""
+    def _prepare_fmap(self):
+        """Eigendecomposition + solver object; True when the solver is new."""
         from .nystrom import EigBuffers
         if getattr(self, "_eigbuf", None) is None:
             self._eigbuf = EigBuffers(self.landmarks, self.device)
@@ -183,15 +183,60 @@ class SharedGridPipeline:
         if self.solver is None or self.solver.fmap.m_eff != fm.m_eff:
             self.solver = LinearBatchSolver(fm, self.grid, self.gamma, self.order, self.cond,
                                             self.max_batch)
-        else:   # same shapes: keep the workspace, refresh the condition rows on device
-            s = self.solver
-            s.fmap = fm
-            s.refresh_condition_rows()
-        return self.solver
+            self._graph = None
+            return self.solver, True
+        self.solver.fmap = fm
+        return self.solver, False
+
+    def prepare(self):
+        """Eigendecomposition + solver state (the per-landmark-set work)."""
+        solver, fresh = self._prepare_fmap()
+        if not fresh:   # same shapes: keep the workspace, refresh the condition rows on device
+            solver.refresh_condition_rows()
+        return solver
 
     def run_device(self, coef, forcing, values, out_x=None, out_info=None):
-        solver = self.prepare()
-        return solver.solve_device(coef, forcing, values, out_x, out_info)
+        """One step on device-resident samples.  After the eigendecomposition
+        (whose m_eff read-back is the step's one host sync) the condition-row
+        refresh, Psi pack, Gram and KKT launches are replayed from a CUDA graph
+        captured on the first call with the same buffers (NYS_GRAPHS=0 turns
+        this off).  Without out_x/out_info the results land in buffers owned by
+        the pipeline and are overwritten by the next call."""
+        import os
+
+        torch = _lib.require_device()[1]
+        solver, fresh = self._prepare_fmap()
+        B = int(coef.shape[0])
+        if out_x is None or out_info is None:
+            if getattr(self, "_outs", None) is None or self._outs[0].shape != (B, solver.side):
+                self._outs = (torch.empty((B, solver.side), dtype=torch.float64,
+                                          device=solver.fmap.device),
+                              torch.empty(B, dtype=torch.int32, device=solver.fmap.device))
+            out_x = self._outs[0] if out_x is None else out_x
+            out_info = self._outs[1] if out_info is None else out_info
+
+        def post():
+            solver.refresh_condition_rows()
+            solver.solve_device(coef, forcing, values, out_x, out_info)
+
+        if os.environ.get("NYS_GRAPHS", "1") == "0":
+            post()
+            return out_x, out_info
+        key = (id(solver), solver.fmap.m_eff, B, coef.data_ptr(), forcing.data_ptr(),
+               values.data_ptr(), out_x.data_ptr(), out_info.data_ptr())
+        if getattr(self, "_graph", None) is not None and self._gkey == key:
+            self._graph.replay()
+            _lib.note_graph_launches(self._gcount)
+            return out_x, out_info
+        post()   # eager: this call's result, and the kernels' one-time attribute setup
+        lib = _lib.load()
+        n0 = lib.nys_launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            post()
+        self._gcount = lib.nys_launch_count() - n0
+        self._graph, self._gkey = g, key
+        return out_x, out_info
 
     def run_host(self, coef_h, forcing_h, values_h, x_h, info_h, chunks: int = 4,
                  dev_bufs=None):
