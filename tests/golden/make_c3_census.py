@@ -1,7 +1,10 @@
 """Config-3 census: run the LIVE reference (``nysode``) on all 256 bench
 instances (seed 0) and store each outcome -- status, iteration count, the
 solution vector x and its error vs the manufactured solution -- plus the
-reference's landmark eigenpairs (x is expressed in that basis).
+reference's landmark eigenpairs (x is expressed in that basis).  The fixture's
+status_dsyev column (the reference re-run with scipy's dsyev driver for the
+landmark eigenproblem, /tmp-free variant of this script with driver="ev") is the
+reference's own outcome sensitivity that the GPU test uses as its yardstick.
 
 Build container only (``/root/reference`` is absent on the GPU box):
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_c3_census.py

@@ -167,5 +167,12 @@ def test_config3_census_matches_reference():
           "rungs", [int(rung[i]) for i in lost], "| same iteration count", same_its, "/",
           len(both), "| y_hat mismatches", bad)
     assert not bad, bad
-    # outcome flips only on trajectories that sit on a knife edge: a few per cent
-    assert len(lost) <= 0.04 * B, lost
+    # Outcome flips sit on knife-edge trajectories.  Yardstick: the reference
+    # against itself with only LAPACK's eigensolver driver swapped (dsyev for
+    # dsyevd, status_dsyev in the fixture) loses 6 of its converged instances
+    # and gains 9; allow three times that self-sensitivity.
+    self_lost = int(((ref["status"] == 0) & (ref["status_dsyev"] != 0)).sum())
+    self_agree = int((ref["status"] == ref["status_dsyev"]).sum())
+    print("reference self-sensitivity: agreement", self_agree, "lost", self_lost)
+    assert len(lost) <= 3 * self_lost, lost
+    assert B - agree <= 3 * (B - self_agree), (agree, self_agree)
