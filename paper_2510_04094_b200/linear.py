@@ -258,3 +258,113 @@ def check_kkt(model: PrimalModel, system: AssembledSystem) -> KktReport:
 
 def predict(model: PrimalModel, ell: int, points) -> np.ndarray:
     return model.predict(ell, points)
+
+
+class SingleSolvePipeline:
+    """One linear ODE per call on a fixed grid / landmark set (configs 0, 1, 4):
+    the reference's assemble + solve (linear.py:90-158) as a device pipeline.
+
+    Per call: the landmark eigendecomposition (its m_eff read-back is the one
+    host sync), then -- replayed from a CUDA graph captured on the first call
+    with the same buffers -- the condition rows A_c (feature rows at the
+    condition points, nys_feature_matrix_f64), the fused feature+Gram kernel and
+    the KKT LU + refinement.  Inputs are device tensors; x / info come back in
+    buffers owned by the pipeline (overwritten by the next call).
+    NYS_GRAPHS=0 runs everything eagerly.
+    """
+
+    def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
+                 drop_tol: float = 1e-16, device=None):
+        from .kernel import RbfKernel
+        from .nystrom import EigBuffers
+
+        lib, torch = _lib.require_device()
+        self.lib, self.torch = lib, torch
+        if gamma <= 0:
+            raise ValueError(f"gamma must be positive, got {gamma}")
+        self.kernel = RbfKernel(float(sigma2))
+        self.landmarks = np.asarray(landmarks, dtype=float).reshape(-1)
+        self.gamma, self.order, self.cond, self.drop_tol = float(gamma), int(order), cond, drop_tol
+        self.eig = EigBuffers(self.landmarks, device)
+        self.device = self.eig.device
+        self.nk = len(cond.entries)
+        self.cond_pts = _lib.as_f64([bc.point for bc in cond.entries], self.device)
+        self.beta = _lib.as_f64([1.0 if bc.order == 0 else 0.0 for bc in cond.entries],
+                                self.device)
+        self.vals = _lib.as_f64([bc.value for bc in cond.entries], self.device).reshape(1, -1)
+        self._shape = None
+        self._graph = None
+
+    def _buffers(self, me: int, n_c: int):
+        torch, lib = self.torch, self.lib
+        if self._shape == (me, n_c):
+            return
+        f64 = dict(dtype=torch.float64, device=self.device)
+        m = self.landmarks.size
+        self.Ac = torch.zeros((max(self.nk, 1), me), **f64)
+        self.E = torch.empty((me + 2, me + 2), **f64)
+        self.gws_b = lib.nys_fused_gram_workspace_bytes(n_c, m, me, self.order)
+        self.gws = torch.empty(self.gws_b, dtype=torch.uint8, device=self.device)
+        self.kws_b = lib.nys_kkt_workspace_bytes(me, self.nk, 1)
+        self.kws = (torch.empty(self.kws_b, dtype=torch.uint8, device=self.device)
+                    if self.kws_b else None)
+        self.x = torch.empty((1, me + 1 + self.nk), **f64)
+        self.info = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._shape = (me, n_c)
+        self._graph = None
+
+    def _post(self, fm, pts, coef, forcing):
+        me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
+        for mu, bc in enumerate(self.cond.entries):   # linear.py:56-63, on the device
+            _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), m,
+                      me, float(fm.kernel.sigma2), int(bc.order), _lib.ptr(self.cond_pts) + 8 * mu,
+                      1, _lib.ptr(self.Ac) + 8 * mu * me, me, st)
+        n_c = pts.numel()
+        _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), m, me,
+                  float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
+                  _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
+                  self.gws_b, st)
+        _lib.call("nys_kkt_solve_f64", _lib.ptr(self.E), me, self.nk, _lib.ptr(self.Ac),
+                  _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
+                  _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
+
+    def run_device(self, pts, coef, forcing):
+        """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info)."""
+        import os
+
+        from .nystrom import build_feature_map
+
+        fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
+        me = fm.m_eff
+        if (me + 2 + 7) // 8 > SMALL_NB_MAX and fm.condition > KSPACE_MAX_COND:
+            raise IllConditionedLargeMapError(
+                f"m_eff={me} with cond(Omega)={fm.condition:.2e} > {KSPACE_MAX_COND:.0e}")
+        n_c = int(pts.numel())
+        self._buffers(me, n_c)
+        if os.environ.get("NYS_GRAPHS", "1") == "0":
+            self._post(fm, pts, coef, forcing)
+            return self.x, self.info
+        key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c)
+        if self._graph is not None and self._gkey == key:
+            self._graph.replay()
+            _lib.note_graph_launches(self._gcount)
+            return self.x, self.info
+        self._post(fm, pts, coef, forcing)   # eager: this call's result + kernel attributes
+        n0 = self.lib.nys_launch_count()
+        g = self.torch.cuda.CUDAGraph()
+        with self.torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self._post(fm, pts, coef, forcing)
+        self._gcount = self.lib.nys_launch_count() - n0
+        self._graph, self._gkey = g, key
+        return self.x, self.info
+
+    def model(self):
+        """PrimalModel of the last call (raises the reference's errors from info)."""
+        raise_for_info(int(self.info[0]))
+        x = self.x[0].cpu().numpy()
+        me = self._shape[0]
+        fm = NystromFeatureMap(kernel=self.kernel, landmarks=self.landmarks, m_eff=me,
+                               device=self.device, d_landmarks=self.eig.d_lm, d_W=self.eig.W,
+                               d_eigvals=self.eig.s, d_eigvecs=self.eig.V)
+        return PrimalModel(omega=x[:me], bias=float(x[me]), multipliers=x[me + 1:],
+                           feature_map=fm)

@@ -145,6 +145,7 @@ class EigBuffers:
         self.W = torch.empty((m, m), **f64)
         self.meta = torch.zeros(2, dtype=torch.int32, device=self.device)   # m_eff, info
         self.meta_h = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self.s_h = torch.zeros(m, dtype=torch.float64).pin_memory()   # eigenvalues, same sync
         self.wsb = lib.nys_landmark_eig_workspace_bytes(m)
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.device) if self.wsb else None
 
@@ -177,6 +178,7 @@ def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TO
               _lib.ptr(ws), wsb, _lib.stream_ptr())
     if buffers is not None:
         buffers.meta_h.copy_(meta, non_blocking=True)
+        buffers.s_h.copy_(s, non_blocking=True)
         torch.cuda.current_stream(device).synchronize()
         m_eff, info = (int(v) for v in buffers.meta_h)
     else:
@@ -187,4 +189,6 @@ def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TO
     fm = NystromFeatureMap(kernel=k, landmarks=landmarks, m_eff=m_eff, device=device,
                            d_landmarks=d_lm, d_W=W, d_eigvals=s, d_eigvecs=V)
     fm._host["sweeps"] = sweeps
+    if buffers is not None:
+        fm._host["s"] = buffers.s_h[:m_eff].numpy().copy()
     return fm
