@@ -15,6 +15,7 @@
 // pivot), the trailing update keeps column k in registers and updates four
 // rows per batch of loads, and one forward sweep serves [C^T | r] together.
 #include <cmath>
+#include <cstdlib>
 
 #include "batch_layout.cuh"
 #include "common.cuh"
@@ -25,6 +26,9 @@ int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, d
 int launch_kkt(const double* gram, int m_eff, int ncond, const double* Ac, const double* beta,
                const double* values, double gamma, int B, double* x, int* info, double* M,
                double* rhs, void* ws, size_t ws_bytes, cudaStream_t st, bool only_flagged);
+int launch_kkt_blocked(const double* dense, int m_eff, int n_cond, const double* Ac,
+                       const double* beta, const double* values, double gamma, int B, double* x,
+                       int* info, cudaStream_t st);
 }  // namespace nys_host
 
 namespace {
@@ -367,6 +371,15 @@ extern "C" int nys_batch_kkt_solve_f64(const void* batch_workspace, int n_c, int
   int rc = nys_host::launch_batch_unpack(L.part(batch_workspace), L.nsplit, B, L.NB, L.Pe(), dense,
                                          st);
   if (rc) return rc;
+  // m_eff a multiple of 8 in [32, 64]: blocked DMMA Cholesky (kkt_block.cu)
+  rc = getenv("NYS_KKT_SCALAR") != nullptr
+           ? NYS_EUNSUPPORTED
+           : nys_host::launch_kkt_blocked(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x,
+                                          info, st);
+  if (rc == NYS_OK)
+    return nys_host::launch_kkt(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info,
+                                nullptr, nullptr, nullptr, 0, st, true);
+  if (rc != NYS_EUNSUPPORTED) return rc;
   switch (n_cond) {
     case 1: rc = launch_chol<1>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st); break;
     case 2: rc = launch_chol<2>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st); break;
