@@ -45,29 +45,30 @@ __global__ void __launch_bounds__(32)
   const double* vals = values + (size_t)b * P;
   double* L = dsm;                  // NBLK blocks x 64
   double* dinv = L + NBLK * 64;     // me
-  double* Y = dinv + me;            // me x R
-  double* xs = Y + me * R;          // me
+  double* Yb = dinv + me;           // me x 8: [block][row][column], columns >= R zero
+  double* xs = Yb + me * 8;         // me
   const double inv_gamma = 1.0 / gamma;
   auto at = [&](int i, int j) -> double& {   // element (i, j), j <= i
     return L[blk(i >> 3, j >> 3) * 64 + swz(i & 7, j & 7)];
   };
+  auto Y = [&](int i, int q) -> double& { return Yb[(i >> 3) * 64 + (i & 7) * 8 + q]; };
 
-  // ---- A = E[0:me, 0:me] + I / gamma into the lower blocks (pairs of columns)
-#pragma unroll 4
-  for (int q = 0; q < NBLK; ++q) {
-    int I = 0;
-    while (blk(I + 1, 0) <= q) ++I;
-    const int J = q - blk(I, 0);
-    const int r = fr, c = 2 * fc;
-    double2 v;
-    v.x = __ldg(E + (size_t)(8 * I + r) * Pe + 8 * J + c);
-    v.y = __ldg(E + (size_t)(8 * I + r) * Pe + 8 * J + c + 1);
-    if (I == J) {
-      if (r == c) v.x += inv_gamma;
-      if (r == c + 1) v.y += inv_gamma;
-    }
-    *reinterpret_cast<double2*>(L + q * 64 + swz(r, c)) = v;
-  }
+  // ---- A = E[0:me, 0:me] into the lower blocks: asynchronous global->shared
+  // copies (all of them in flight at once, no registers), then + I / gamma
+#pragma unroll
+  for (int I = 0; I < NBK; ++I)
+#pragma unroll
+    for (int J = 0; J <= I; ++J)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 2 * fc + h;
+        const double* src = E + (size_t)(8 * I + fr) * Pe + 8 * J + c;
+        const uint32_t dst = nys::smem_u32(L + blk(I, J) * 64 + swz(fr, c));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+      }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncwarp();
+  for (int i = lane; i < me; i += 32) at(i, i) += inv_gamma;
   __syncwarp();
 
   // ---- blocked right-looking Cholesky
@@ -134,48 +135,92 @@ __global__ void __launch_bounds__(32)
 
   // ---- Y = L^{-1} [D^T g | A_c^T | r1]
   for (int i = lane; i < me; i += 32) {
-    Y[i * R] = E[(size_t)i * Pe + me];
+    Y(i, 0) = E[(size_t)i * Pe + me];
 #pragma unroll
-    for (int mu = 0; mu < P; ++mu) Y[i * R + 1 + mu] = Ac[(size_t)mu * me + i];
-    Y[i * R + Q] = E[(size_t)i * Pe + me + 1];
+    for (int mu = 0; mu < P; ++mu) Y(i, 1 + mu) = Ac[(size_t)mu * me + i];
+    Y(i, Q) = E[(size_t)i * Pe + me + 1];
+#pragma unroll
+    for (int q = R; q < 8; ++q) Y(i, q) = 0.0;
   }
   __syncwarp();
-  auto forward = [&](int q0) {   // columns q0..R-1
-    for (int j = 0; j < me; ++j) {
-      double yj[R];
+  // Blocked triangular solves.  A lane holds the 8 x 8 block's MMA accumulator
+  // fragment (row fr, columns 2fc, 2fc+1); off-diagonal blocks arrive by DMMA,
+  // the diagonal block is solved row by row with shuffles.  Only the columns
+  // in `cols` (bit mask) are written back.
+  auto forward = [&](unsigned cols) {   // Y <- L^{-1} Y
+#pragma unroll 1
+    for (int I = 0; I < NBK; ++I) {
+      double2 cv = *reinterpret_cast<const double2*>(Yb + I * 64 + fr * 8 + 2 * fc);
+      for (int J = 0; J < I; ++J) {
 #pragma unroll
-      for (int q = 0; q < R; ++q) yj[q] = q >= q0 ? Y[j * R + q] * dinv[j] : 0.0;
-      __syncwarp();
-      if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-          if (q >= q0) Y[j * R + q] = yj[q];
-      for (int i = j + 1 + lane; i < me; i += 32) {
-        const double lij = at(i, j);
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-          if (q >= q0) Y[i * R + q] = fma(-lij, yj[q], Y[i * R + q]);
+        for (int kk = 0; kk < 2; ++kk) {
+          const double a = -L[blk(I, J) * 64 + swz(fr, 4 * kk + fc)];
+          const double bq = Yb[J * 64 + (4 * kk + fc) * 8 + fr];
+          nys::dmma(cv.x, cv.y, a, bq);
+        }
       }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        if (fr == c) {
+          const double d = dinv[8 * I + c];
+          cv.x *= d;
+          cv.y *= d;
+        }
+        const double yx = __shfl_sync(0xffffffffu, cv.x, c * 4 + fc);
+        const double yy = __shfl_sync(0xffffffffu, cv.y, c * 4 + fc);
+        if (fr > c) {
+          const double l = L[blk(I, I) * 64 + swz(fr, c)];
+          cv.x = fma(-l, yx, cv.x);
+          cv.y = fma(-l, yy, cv.y);
+        }
+      }
+      double* dst = Yb + I * 64 + fr * 8 + 2 * fc;
+      if ((cols >> (2 * fc)) & 1u) dst[0] = cv.x;
+      if ((cols >> (2 * fc + 1)) & 1u) dst[1] = cv.y;
       __syncwarp();
     }
   };
-  auto backward = [&]() {   // Y[:, Q] <- L^{-T} Y[:, Q]
-    for (int j = me - 1; j >= 0; --j) {
-      const double xj = Y[j * R + Q] * dinv[j];
-      __syncwarp();
-      if (lane == 0) Y[j * R + Q] = xj;
-      for (int i = lane; i < j; i += 32) Y[i * R + Q] = fma(-at(j, i), xj, Y[i * R + Q]);
+  auto backward = [&](unsigned cols) {   // Y <- L^{-T} Y
+#pragma unroll 1
+    for (int I = NBK - 1; I >= 0; --I) {
+      double2 cv = *reinterpret_cast<const double2*>(Yb + I * 64 + fr * 8 + 2 * fc);
+      for (int J = I + 1; J < NBK; ++J) {
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const double a = -L[blk(J, I) * 64 + swz(4 * kk + fc, fr)];   // (L_JI)^T
+          const double bq = Yb[J * 64 + (4 * kk + fc) * 8 + fr];
+          nys::dmma(cv.x, cv.y, a, bq);
+        }
+      }
+#pragma unroll
+      for (int c = 7; c >= 0; --c) {
+        if (fr == c) {
+          const double d = dinv[8 * I + c];
+          cv.x *= d;
+          cv.y *= d;
+        }
+        const double yx = __shfl_sync(0xffffffffu, cv.x, c * 4 + fc);
+        const double yy = __shfl_sync(0xffffffffu, cv.y, c * 4 + fc);
+        if (fr < c) {
+          const double l = L[blk(I, I) * 64 + swz(c, fr)];   // L[c][fr], c > fr
+          cv.x = fma(-l, yx, cv.x);
+          cv.y = fma(-l, yy, cv.y);
+        }
+      }
+      double* dst = Yb + I * 64 + fr * 8 + 2 * fc;
+      if ((cols >> (2 * fc)) & 1u) dst[0] = cv.x;
+      if ((cols >> (2 * fc + 1)) & 1u) dst[1] = cv.y;
       __syncwarp();
     }
   };
   auto warp_dot = [&](int qa, int qb) {
     double a = 0.0;
-    for (int i = lane; i < me; i += 32) a = fma(Y[i * R + qa], Y[i * R + qb], a);
+    for (int i = lane; i < me; i += 32) a = fma(Y(i, qa), Y(i, qb), a);
 #pragma unroll
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     return a;
   };
-  forward(0);
+  forward((1u << R) - 1u);
   // S = C' - Y_B^T Y_B (every lane holds the same copy), pivoted elimination
   double S[Q][Q];
 #pragma unroll
@@ -267,7 +312,7 @@ __global__ void __launch_bounds__(32)
         a = fma(E[(size_t)i * Pe + me], z[0], a);
 #pragma unroll
         for (int mu = 0; mu < P; ++mu) a = fma(Ac[(size_t)mu * me + i], z[1 + mu], a);
-        Y[i * R + Q] = E[(size_t)i * Pe + me + 1] - a;
+        Y(i, Q) = E[(size_t)i * Pe + me + 1] - a;
       }
       double gx = 0.0, cx[P];
 #pragma unroll
@@ -290,22 +335,22 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
       for (int mu = 0; mu < P; ++mu) rq[1 + mu] = vals[mu] - (cx[mu] + beta[mu] * z[0]);
       __syncwarp();
-      forward(Q);   // only the residual column; L^{-1} Bt is unchanged
+      forward(1u << Q);   // only the residual column; L^{-1} Bt is unchanged
     }
     double t[Q];
 #pragma unroll
     for (int a = 0; a < Q; ++a) t[a] = rq[a] - warp_dot(a, Q);
     solve_small(t);
     for (int i = lane; i < me; i += 32) {
-      double v = Y[i * R + Q];
+      double v = Y(i, Q);
 #pragma unroll
-      for (int a = 0; a < Q; ++a) v = fma(-Y[i * R + a], t[a], v);
-      Y[i * R + Q] = v;
+      for (int a = 0; a < Q; ++a) v = fma(-Y(i, a), t[a], v);
+      Y(i, Q) = v;
     }
     __syncwarp();
-    backward();
+    backward(1u << Q);
     for (int i = lane; i < me; i += 32) {
-      const double v = Y[i * R + Q];
+      const double v = Y(i, Q);
       xs[i] = pass == 0 ? v : xs[i] + v;
     }
 #pragma unroll
@@ -333,7 +378,7 @@ template <int P, int NBK>
 int launch_block(const double* dense, const double* Ac, const double* beta, const double* values,
                  double gamma, int B, double* x, int* info, cudaStream_t st) {
   constexpr int me = NBK * 8;
-  const size_t dyn = ((size_t)NBK * (NBK + 1) / 2 * 64 + me + (size_t)me * (P + 2) + me) *
+  const size_t dyn = ((size_t)NBK * (NBK + 1) / 2 * 64 + me + (size_t)me * 8 + me) *
                      sizeof(double);
   auto kern = kkt_block_kernel<P, NBK>;
   if (dyn > 48 * 1024) {
