@@ -29,6 +29,8 @@ namespace {
 
 using nys::BatchLayout;
 
+constexpr int kStages = 4;   // Psi chunks in flight (55 KB each at NB = 9, p = 2)
+
 template <int NB>
 struct Tri {
   static constexpr int kPairs = NB * (NB + 1) / 2;
@@ -55,7 +57,7 @@ struct Role {
 template <int NB, int NO, int WARPS, int SPLIT, int Lo, int Hi, bool EXT>
 NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict__ coef,
                        const double* __restrict__ forcing, int n_c, int B, int b, int ks0,
-                       int nchunks, int rcol, double* sm, uint64_t* bar,
+                       int nchunks, int rcol, double* sm, uint64_t* bar, int* cnt,
                        double* __restrict__ part) {
   constexpr int P = NO - 1;
   constexpr int CH = nys::kBatchChunkKs;
@@ -86,14 +88,15 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
   };
   load_rows(0, fk, rr);
 
+  constexpr int NS = kStages;
   for (int c = 0; c < nchunks; ++c) {
-    const int stage = c & 1;
-    const uint32_t phase = (c >> 1) & 1;
+    const int stage = c % NS;
+    const uint32_t phase = (c / NS) & 1;
     if (c + 1 < nchunks) load_rows(c + 1, fk_n, rr_n);
     nys::mbar_wait(&bar[stage], phase);
     const double* Q = sm + stage * kChunkDoubles + lane;
     if (active) {
-#pragma unroll 2
+#pragma unroll 1
       for (int kk = 0; kk < CH; ++kk) {
         const int src = kk * 4 + tig;
         double f[P];
@@ -142,11 +145,21 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
       for (int k = 0; k < P; ++k) fk[k] = fk_n[k];
       rr = rr_n;
     }
-    __syncthreads();   // every warp is done with this stage
-    if (threadIdx.x == 0 && c + 2 < nchunks) {
-      nys::mbar_expect_tx(&bar[stage], kChunkBytes);
-      nys::bulk_g2s(sm + stage * kChunkDoubles,
-                    psi + (size_t)(ks0 + (c + 2) * CH) * NO * NB * 32, kChunkBytes, &bar[stage]);
+    // release the stage without a CTA barrier: the last warp to finish it
+    // refills it with chunk c + NS (warps drift up to NS - 1 chunks apart)
+    __syncwarp();
+    if (lane == 0) {
+      const int done = atomicAdd(&cnt[stage], 1);
+      if (done == WARPS - 1) {
+        cnt[stage] = 0;
+        if (c + NS < nchunks) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          nys::mbar_expect_tx(&bar[stage], kChunkBytes);
+          nys::bulk_g2s(sm + stage * kChunkDoubles,
+                        psi + (size_t)(ks0 + (c + NS) * CH) * NO * NB * 32, kChunkBytes,
+                        &bar[stage]);
+        }
+      }
     }
   }
   if (active) {
@@ -183,8 +196,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   constexpr int NPAIR = Tri<EXT ? NB - 1 : NB>::kPairs;
   constexpr int H = (NPAIR + 1) / 2;
 
-  extern __shared__ __align__(128) double sm[];   // [2][kChunkDoubles]
-  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(128) double sm[];   // [kStages][kChunkDoubles]
+  __shared__ __align__(8) uint64_t bar[kStages];
+  __shared__ int cnt[kStages];
 
   const int warp = threadIdx.x >> 5;
   const int b = blockIdx.x * (WARPS / SPLIT) + warp / SPLIT;
@@ -192,13 +206,15 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   const int nchunks = ks_per_split / CH;
 
   if (threadIdx.x == 0) {
-    nys::mbar_init(&bar[0], 1);
-    nys::mbar_init(&bar[1], 1);
+    for (int s = 0; s < kStages; ++s) {
+      nys::mbar_init(&bar[s], 1);
+      cnt[s] = 0;
+    }
     nys::fence_mbar_init();
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2 && s < nchunks; ++s) {
+    for (int s = 0; s < kStages && s < nchunks; ++s) {
       nys::mbar_expect_tx(&bar[s], kChunkBytes);
       nys::bulk_g2s(sm + s * kChunkDoubles, psi + (size_t)(ks0 + s * CH) * NO * NB * 32,
                     kChunkBytes, &bar[s]);
@@ -206,14 +222,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
   }
   if constexpr (SPLIT == 1) {
     gram_body<NB, NO, WARPS, SPLIT, 0, NPAIR, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
-                                                   rcol, sm, bar, part);
+                                                   rcol, sm, bar, cnt, part);
   } else {
     if ((warp & 1) == 0)
       gram_body<NB, NO, WARPS, SPLIT, 0, H, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
-                                                 rcol, sm, bar, part);
+                                                 rcol, sm, bar, cnt, part);
     else
       gram_body<NB, NO, WARPS, SPLIT, H, NPAIR, EXT>(psi, coef, forcing, n_c, B, b, ks0, nchunks,
-                                                     rcol, sm, bar, part);
+                                                     rcol, sm, bar, cnt, part);
   }
 }
 
@@ -278,7 +294,7 @@ int launch_gram(const double* psi, const double* coef, const double* forcing, in
   constexpr int SPLIT = 1;
   constexpr int WARPS = nys::kBatchWarps * SPLIT;
   auto kern = batch_gram_kernel<NB, NO, WARPS, SPLIT, EXT>;
-  const size_t smem = 2 * (size_t)nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
+  const size_t smem = (size_t)kStages * nys::kBatchChunkKs * NO * NB * 32 * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return nys_host::record_cuda(e);
   dim3 grid((B + nys::kBatchWarps - 1) / nys::kBatchWarps, L.nsplit);
