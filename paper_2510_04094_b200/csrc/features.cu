@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(kFeatThreads)
                         int ldo, int mode, int n_blocks /*packed: NB*/, int n_orders,
                         int n_rows_pad) {
   extern __shared__ double kt[];   // [kTP][m]
+  if (mode == 1) ell = blockIdx.y;  // packed: one launch covers orders 0..n_orders-1
   nys::Hermite H;
   H.init(sigma2, ell);
   const int i0 = blockIdx.x * kTP;
@@ -40,9 +41,18 @@ __global__ void __launch_bounds__(kFeatThreads)
     int ii = e / ncols, k = e % ncols;
     int i = i0 + ii;
     double acc = 0.0;
-    if (k < m_eff) {
+    if (k < m_eff) {   // four independent partial sums (FP64 FMA latency)
       const double* kr = kt + ii * m;
-      for (int s = 0; s < m; ++s) acc += kr[s] * W[(size_t)s * ldw + k];
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int s = 0;
+      for (; s + 3 < m; s += 4) {
+        a0 = fma(kr[s], W[(size_t)s * ldw + k], a0);
+        a1 = fma(kr[s + 1], W[(size_t)(s + 1) * ldw + k], a1);
+        a2 = fma(kr[s + 2], W[(size_t)(s + 2) * ldw + k], a2);
+        a3 = fma(kr[s + 3], W[(size_t)(s + 3) * ldw + k], a3);
+      }
+      for (; s < m; ++s) a0 = fma(kr[s], W[(size_t)s * ldw + k], a0);
+      acc = (a0 + a1) + (a2 + a3);
     }
     if (mode == 0) {
       if (i < n_pts) out[(size_t)i * ldo + k] = acc;
@@ -153,13 +163,10 @@ int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return record_cuda(e);
   }
-  dim3 grid((n_rows_pad + kTP - 1) / kTP);
-  for (int ell = 0; ell <= p; ++ell) {
-    feature_tile_kernel<<<grid, kFeatThreads, sm, st>>>(lm, m, W, ldw, m_eff, sigma2, ell, pts,
-                                                        n_c, packed, 0, 1, n_blocks, p + 1,
-                                                        n_rows_pad);
-    nys_host::count_launches(1);
-  }
+  dim3 grid((n_rows_pad + kTP - 1) / kTP, p + 1);   // grid.y = order
+  feature_tile_kernel<<<grid, kFeatThreads, sm, st>>>(lm, m, W, ldw, m_eff, sigma2, 0, pts, n_c,
+                                                      packed, 0, 1, n_blocks, p + 1, n_rows_pad);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -18,7 +18,15 @@
 #include <cmath>
 
 #include "batch_layout.cuh"
+#include <cstdlib>
+
 #include "common.cuh"
+
+namespace nys_host {
+int launch_kkt_big(const double* E, int m_eff, int n_cond, const double* Ac, const double* beta,
+                   const double* values, double gamma, double* x, int* info, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
+}  // namespace nys_host
 
 namespace nys_host {
 int launch_batch_unpack(const double* part, int nsplit, int B, int NB, int Pe, double* gram,
@@ -296,7 +304,8 @@ __global__ void __launch_bounds__(kKktThreads)
                    const double* __restrict__ Ac, const double* __restrict__ beta,
                    const double* __restrict__ values, double gamma, int B,
                    double* __restrict__ xout, int* __restrict__ info, double* __restrict__ Mout,
-                   double* __restrict__ rhsout, double* __restrict__ gws) {
+                   double* __restrict__ rhsout, double* __restrict__ gws, int only_flagged) {
+  if (only_flagged && info[blockIdx.x] != 16 /* kNeedsLu */) return;
   __shared__ int piv_s;
   __shared__ int bad;
   __shared__ double red_v[kKktThreads / 32];
@@ -463,8 +472,18 @@ int launch_kkt(const double* gram, int m_eff, int ncond, const double* Ac, const
   }
   size_t need = (size_t)B * n * n * sizeof(double);
   if (ws == nullptr || ws_bytes < need) return NYS_EWORKSPACE;
+  if (B == 1 && M == nullptr && rhs == nullptr && !only_flagged &&
+      getenv("NYS_KKT_LU") == nullptr) {
+    // blocked Cholesky + Schur (kkt_big.cu); this LU re-solves it on breakdown
+    const int rc = launch_kkt_big(gram, m_eff, ncond, Ac, beta, values, gamma, x, info, ws,
+                                  ws_bytes, st);
+    if (rc == NYS_OK) return launch_kkt(gram, m_eff, ncond, Ac, beta, values, gamma, B, x, info,
+                                        M, rhs, ws, ws_bytes, st, true);
+    if (rc != NYS_EUNSUPPORTED) return rc;
+  }
   kkt_cta_kernel<<<B, kKktThreads, 3 * (size_t)n * sizeof(double), st>>>(
-      gram, m_eff, ncond, Ac, beta, values, gamma, B, x, info, M, rhs, static_cast<double*>(ws));
+      gram, m_eff, ncond, Ac, beta, values, gamma, B, x, info, M, rhs, static_cast<double*>(ws),
+      only_flagged ? 1 : 0);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
