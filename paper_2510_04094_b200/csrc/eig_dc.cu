@@ -227,6 +227,229 @@ NYS_DEV double secular_root(const DcShared& S, int s, int j, int K, double rho, 
   return dorg + tau;
 }
 
+// Blocked Householder tridiagonalisation (LAPACK dsytrd / dlatrd order) for the
+// global-memory path (n > 64).  Within a panel of kTNb columns the trailing
+// matrix is not touched: each column is corrected on the fly by the panel's
+// V W^T + W V^T, the matvec p = A v reads the panel-start matrix once (L2), and
+// the panel's rank-2 kTNb update of the trailing block runs as DMMA.8x8x4 GEMM
+// tiles at the end.  The unblocked loop re-read and re-wrote the whole trailing
+// matrix per reflector.  Same reflectors (alpha, beta, v) as the unblocked
+// form, stored the same way (v below the diagonal of A, beta, e, d in S).
+constexpr int kTNb = 32;
+NYS_DEV double dc_block_sum_all(double x, double* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if (lane == 0) red[w] = x;
+  __syncthreads();
+  double r = 0.0;
+  for (int i = 0; i < nw; ++i) r += red[i];
+  return r;
+}
+
+template <typename SharedT>
+NYS_DEV void tridiag_blocked(double* __restrict__ A, int ld, int n, SharedT& S, double* dynsm,
+                             int debug) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  constexpr int kLdv = kTNb + 1;      // padded rows: column reads across rows hit
+  double* V = dynsm;                  // distinct banks (stride 32 would serialise)
+  double* Wm = V + (size_t)n * kLdv;  // n x kLdv
+  double* t1 = Wm + (size_t)n * kLdv; // kTNb
+  double* t2 = t1 + kTNb;             // kTNb
+  double* pacc = t2 + kTNb;           // (nt / 256) x 256 matvec partials
+  long long tp = 0, tu = 0, ts[6] = {0, 0, 0, 0, 0, 0};
+  for (int k0 = 0; k0 + 2 < n; k0 += kTNb) {
+    const int nb = min(kTNb, n - 2 - k0);
+    for (int e = tid; e < n * kLdv; e += nt) {
+      V[e] = 0.0;
+      Wm[e] = 0.0;
+    }
+    __syncthreads();
+    long long ta = clock64();
+    for (int jj = 0; jj < nb; ++jj) {
+      const int j = k0 + jj;
+      long long c0k = clock64();
+      // (1) corrected column j, rows i >= j
+      for (int i = j + tid; i < n; i += nt) {
+        double c = A[(size_t)i * ld + j];
+        const double* Vi = V + (size_t)i * kLdv;
+        const double* Wi = Wm + (size_t)i * kLdv;
+        const double* Vj = V + (size_t)j * kLdv;
+        const double* Wj = Wm + (size_t)j * kLdv;
+        for (int q = 0; q < jj; ++q) c = c - Vi[q] * Wj[q] - Wi[q] * Vj[q];
+        S.hv[i] = c;
+      }
+      __syncthreads();
+      long long c1k = clock64();
+      ts[0] += c1k - c0k;
+      // (2) reflector of x = c[j+1:]
+      double tail = 0.0;
+      for (int i = j + 2 + tid; i < n; i += nt) tail = fma(S.hv[i], S.hv[i], tail);
+      tail = dc_block_sum_all(tail, S.red);
+      if (tid == 0) {
+        S.d[j] = S.hv[j];
+        const double x0 = S.hv[j + 1];
+        double beta = 0.0, alpha = x0;
+        if (tail > 0.0) {
+          const double nx = sqrt(fma(x0, x0, tail));
+          alpha = -copysign(nx, x0);
+          const double v0 = x0 - alpha;
+          beta = 2.0 / fma(v0, v0, tail);
+          S.hv[j + 1] = v0;
+        }
+        S.e[j] = alpha;
+        S.beta[j] = beta;
+      }
+      __syncthreads();
+      long long c2k = clock64();
+      ts[1] += c2k - c1k;
+      const double beta = S.beta[j];
+      if (beta == 0.0) continue;   // identity reflector: V, W columns stay zero
+      for (int i = j + 1 + tid; i < n; i += nt) {
+        const double v = S.hv[i];
+        A[(size_t)i * ld + j] = v;   // Householder vector for the back-transform
+        V[(size_t)i * kLdv + jj] = v;
+      }
+      // (3) p = A v over rows i > j (panel-start matrix).  A is symmetric, so
+      // p_i = sum_c A[c][i] v_c: a warp reads 32 consecutive doubles of row c
+      // (one 256-byte line) and each thread owns one p_i; the c range is split
+      // over nt / 256 groups whose partial sums meet in shared memory.
+      {
+        const int ng = nt >> 8, g = tid >> 8, ii = tid & 255;
+        const int i = j + 1 + ii;
+        const int len = n - j - 1;
+        const int chunk = (len + ng - 1) / ng;
+        const int cb = j + 1 + g * chunk, ce = min(n, cb + chunk);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (i < n) {
+          int c = cb;
+          for (; c + 7 < ce; c += 8) {   // eight L2 loads in flight per thread
+            double x[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) x[t] = A[(size_t)(c + t) * ld + i];
+            a0 = fma(x[0], S.hv[c], a0);
+            a1 = fma(x[1], S.hv[c + 1], a1);
+            a2 = fma(x[2], S.hv[c + 2], a2);
+            a3 = fma(x[3], S.hv[c + 3], a3);
+            a0 = fma(x[4], S.hv[c + 4], a0);
+            a1 = fma(x[5], S.hv[c + 5], a1);
+            a2 = fma(x[6], S.hv[c + 6], a2);
+            a3 = fma(x[7], S.hv[c + 7], a3);
+          }
+          for (; c < ce; ++c) a0 = fma(A[(size_t)c * ld + i], S.hv[c], a0);
+        }
+        pacc[g * 256 + ii] = (a0 + a1) + (a2 + a3);
+        __syncthreads();
+        if (g == 0 && i < n) {
+          double s2 = 0.0;
+          for (int q = 0; q < ng; ++q) s2 += pacc[q * 256 + ii];
+          S.hp[i] = s2;
+        }
+      }
+      long long c3k = clock64();
+      ts[2] += c3k - c2k;
+      // (4) t1 = W^T v, t2 = V^T v (warp q for column q < jj)
+      for (int q = warp; q < jj; q += nw) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int i = j + 1 + lane; i < n; i += 32) {
+          const double v = S.hv[i];
+          a1 = fma(Wm[(size_t)i * kLdv + q], v, a1);
+          a2 = fma(V[(size_t)i * kLdv + q], v, a2);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+          a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+        }
+        if (lane == 0) {
+          t1[q] = a1;
+          t2[q] = a2;
+        }
+      }
+      __syncthreads();
+      long long c4k = clock64();
+      ts[3] += c4k - c3k;
+      // (5) p <- beta (A v - V t1 - W t2);  w = p - (beta/2)(v.p) v
+      double vp = 0.0;
+      for (int i = j + 1 + tid; i < n; i += nt) {
+        double pi = S.hp[i];
+        const double* Vi = V + (size_t)i * kLdv;
+        const double* Wi = Wm + (size_t)i * kLdv;
+        for (int q = 0; q < jj; ++q) pi = pi - Vi[q] * t1[q] - Wi[q] * t2[q];
+        pi *= beta;
+        S.hp[i] = pi;
+        vp = fma(S.hv[i], pi, vp);
+      }
+      vp = dc_block_sum_all(vp, S.red);
+      const double Kc = 0.5 * beta * vp;
+      for (int i = j + 1 + tid; i < n; i += nt)
+        Wm[(size_t)i * kLdv + jj] = S.hp[i] - Kc * S.hv[i];
+      __syncthreads();
+      ts[4] += clock64() - c4k;
+    }
+    long long tb = clock64();
+    tp += tb - ta;
+    // trailing update A[r][c] -= (V W^T + W V^T)[r][c], r, c >= k0 + nb
+    {
+      const int t0 = k0 + nb, nn = n - t0;
+      const int fr = lane >> 2, fc = lane & 3;
+      const int trows = (nn + 15) / 16, tcols = (nn + 31) / 32;
+      for (int tt = warp; tt < trows * tcols; tt += nw) {
+        const int r0 = t0 + (tt / tcols) * 16, c0 = t0 + (tt % tcols) * 32;
+        double acc[2][4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            const int r = r0 + 8 * i + fr;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c0 + 8 * jb + 2 * fc + h;
+              acc[i][jb][h] = (r < n && c < n) ? A[(size_t)r * ld + c] : 0.0;
+            }
+          }
+        for (int k4 = 0; k4 < 2 * kTNb; k4 += 4) {
+          const int kq = k4 + fc;   // 0..2kTNb: [V | W] against [W | V]
+          double a[2], bq[4];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int r = r0 + 8 * i + fr;
+            a[i] = r < n ? -(kq < kTNb ? V[(size_t)r * kLdv + kq] : Wm[(size_t)r * kLdv + kq - kTNb])
+                         : 0.0;
+          }
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            const int c = c0 + 8 * jb + fr;
+            bq[jb] = c < n ? (kq < kTNb ? Wm[(size_t)c * kLdv + kq] : V[(size_t)c * kLdv + kq - kTNb])
+                           : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int jb = 0; jb < 4; ++jb) nys::dmma(acc[i][jb][0], acc[i][jb][1], a[i], bq[jb]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            const int r = r0 + 8 * i + fr;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c0 + 8 * jb + 2 * fc + h;
+              if (r < n && c < n) A[(size_t)r * ld + c] = acc[i][jb][h];
+            }
+          }
+      }
+    }
+    __syncthreads();
+    tu += clock64() - tb;
+  }
+  if (debug && tid == 0)
+    printf("[nys dc] blocked tridiag: panels %lld (col %lld refl %lld matvec %lld t12 %lld w %lld) trailing %lld\n",
+           tp, ts[0], ts[1], ts[2], ts[3], ts[4], tu);
+}
+
 // kSmem: the working matrices live in dynamic shared memory (n <= 64) -- a
 // compile-time address space, so the compiler emits LDS/STS; kT: columns per
 // lane in the rank-2 update (ceil(n / 32) bound)
@@ -271,7 +494,9 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   // recomputes v.p itself so the rank-2 update needs no extra barrier.
   long long tq[4] = {0, 0, 0, 0};
   const long long tsetup = clock64() - tc0;
-  {
+  if constexpr (!kSmem) {
+    tridiag_blocked(A, ld, n, S, dyn, debug);
+  } else {
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     for (int k = 0; k + 2 < n; ++k) {
       const int i0 = k + 1;
@@ -375,7 +600,11 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
     }
   }
   if (debug && tid == 0) printf("[nys dc] tridiag phases: setup %lld reflector %lld matvec %lld update %lld\n", tsetup, tq[0], tq[1], tq[2]);
-  for (int i = tid; i < n; i += nt) S.d[i] = A[(size_t)i * ld + i];
+  if constexpr (kSmem) {
+    for (int i = tid; i < n; i += nt) S.d[i] = A[(size_t)i * ld + i];
+  } else {   // tridiag_blocked set d[0..n-3] from the corrected panel columns
+    for (int i = max(n - 2, 0) + tid; i < n; i += nt) S.d[i] = A[(size_t)i * ld + i];
+  }
   if (tid == 0) {
     if (n >= 2) S.e[n - 2] = A[(size_t)(n - 1) * ld + (n - 2)];
     S.e[n - 1] = 0.0;
@@ -605,6 +834,50 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
         continue;
       }
       const int K = S.K[b];
+      if (N >= 64 && K >= 16) {
+        // kept columns by DMMA.8x8x4: warp tiles of 16 rows x 32 columns
+        // (2 x 4 accumulator blocks), A = Q[:, col[k]] gathered, B = U
+        const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+        const int fr = lane >> 2, fc = lane & 3;
+        const int trows = (N + 15) / 16, tcols = (K + 31) / 32;
+        for (int tt = warp; tt < trows * tcols; tt += nw) {
+          const int r0 = (tt / tcols) * 16, c0 = (tt % tcols) * 32;
+          double acc[2][4][2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+          for (int k0 = 0; k0 < K; k0 += 4) {
+            const int k = k0 + fc;
+            const bool kok = k < K;
+            const int qc = kok ? S.col[s + k] : 0;
+            double a[2], bb[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int r = r0 + 8 * i + fr;
+              a[i] = (kok && r < N) ? Q[(size_t)(s + r) * n + qc] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int c = c0 + 8 * j + fr;
+              bb[j] = (kok && c < K) ? DL[(size_t)(s + k) * n + s + c] : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int r = r0 + 8 * i + fr, c = c0 + 8 * j + 2 * fc + h;
+                if (r < N && c < K) Qn[(size_t)(s + r) * n + s + c] = acc[i][j][h] * S.hp[s + c];
+              }
+        }
+      } else {
       // kept columns: 4 outputs per thread (independent FMA chains share the
       // Q-row loads); deflated columns: gathered copies
       // adjacent lanes take adjacent output columns (conflict-free U reads); each
@@ -625,6 +898,7 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           if (r0 + t < N) Qn[(size_t)(s + r0 + t) * n + s + c] = a[t] * h;
+      }
       }
       for (int e = tid; e < N * (N - K); e += nt) {
         const int r = e / (N - K), c = K + e % (N - K);
@@ -651,6 +925,18 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   }
 
   tc3 = clock64();
+  if (!kSmem) {
+    // large n: the back-transform and the epilogue run as separate kernels
+    // (dc_backtransform_kernel: one warp per column of Q in registers, all SMs)
+    double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;   // lam | beta | qsel
+    for (int i = tid; i < n; i += nt) {
+      tail[i] = S.lam[i];
+      tail[n + i] = S.beta[i];
+    }
+    if (tid == 0) reinterpret_cast<int*>(tail + 2 * n)[0] = (Q == base + (size_t)n * ld) ? 0 : 1;
+    if (debug && tid == 0) printf("[nys dc] n=%d tridiag=%lld leaves=%lld merges=%lld (backT split)\n", n, tc1 - tc0, tc2 - tc1, tc3 - tc2);
+    return;
+  }
   // ---------------- back-transform Z = H_0 ... H_{n-3} Q (reflectors in A)
   // tpc threads (adjacent lanes) share one column's dot product: FP64 FMA
   // latency, not bandwidth, bounds a serial n-term chain on B200
@@ -745,11 +1031,114 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   }
 }
 
+// Back-transform for large n: Z = H_0 H_1 ... H_{n-3} Q, one warp per column of
+// Q held in registers (kRows rows per lane), reflectors applied in reverse order
+// straight from the Householder vectors in A (the next one prefetched).  No
+// block-level synchronisation: every column is independent.
+template <int kRows>
+__global__ void __launch_bounds__(256)
+    dc_backtransform_kernel(const double* __restrict__ gbuf, int n) {
+  const int ld = dc_ld(n);
+  const double* A = gbuf;
+  const double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;
+  const double* beta = tail + n;
+  const int qsel = reinterpret_cast<const int*>(tail + 2 * n)[0];
+  double* Q = const_cast<double*>(gbuf) + (size_t)n * ld + (qsel ? (size_t)n * n : 0);
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  double z[kRows];
+#pragma unroll
+  for (int t = 0; t < kRows; ++t) {
+    const int i = lane + 32 * t;
+    z[t] = i < n ? Q[(size_t)i * n + c] : 0.0;
+  }
+  double vn[kRows];
+  auto loadv = [&](int k, double* v) {
+#pragma unroll
+    for (int t = 0; t < kRows; ++t) {
+      const int i = lane + 32 * t;
+      v[t] = (i > k && i < n) ? A[(size_t)i * ld + k] : 0.0;
+    }
+  };
+  if (n >= 3) loadv(n - 3, vn);
+  for (int k = n - 3; k >= 0; --k) {
+    double v[kRows];
+#pragma unroll
+    for (int t = 0; t < kRows; ++t) v[t] = vn[t];
+    if (k > 0) loadv(k - 1, vn);
+    const double bk = beta[k];
+    if (bk == 0.0) continue;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int t = 0; t < kRows; t += 2) {
+      a0 = fma(v[t], z[t], a0);
+      if (t + 1 < kRows) a1 = fma(v[t + 1], z[t + 1], a1);
+    }
+    double d = a0 + a1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const double w = bk * d;
+#pragma unroll
+    for (int t = 0; t < kRows; ++t) z[t] = fma(-v[t], w, z[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < kRows; ++t) {
+    const int i = lane + 32 * t;
+    if (i < n) Q[(size_t)i * n + c] = z[t];
+  }
+}
+
+// descending order (ties: higher index first, nystrom.py:151), drop rule, W
+__global__ void __launch_bounds__(1024)
+    dc_epilogue_kernel(const double* __restrict__ gbuf, int n, double drop_tol,
+                       double* __restrict__ eigvals, double* __restrict__ eigvecs,
+                       double* __restrict__ Wout, int* __restrict__ m_eff_out,
+                       int* __restrict__ info) {
+  __shared__ int perm[kDcMaxN];
+  __shared__ double lam[kDcMaxN];
+  const int ld = dc_ld(n);
+  const double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;
+  const int qsel = reinterpret_cast<const int*>(tail + 2 * n)[0];
+  const double* Q = gbuf + (size_t)n * ld + (qsel ? (size_t)n * n : 0);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < n; i += nt) lam[i] = tail[i];
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) {
+    const double di = lam[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = lam[j];
+      rank += (dj > di) || (dj == di && j > i);
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  const double s0 = lam[perm[0]];
+  const double cut = fmax(drop_tol * s0, 0.0);
+  for (int k = tid; k < n; k += nt) eigvals[k] = lam[perm[k]];
+  if (tid == 0) {
+    int me = 0;
+    while (me < n && lam[perm[me]] > cut) ++me;
+    *m_eff_out = me;
+    *info = NYS_INFO_OK;
+  }
+  for (int e = tid; e < n * n; e += nt) {
+    const int i = e / n, k = e % n;
+    const int src = perm[k];
+    const double v = Q[(size_t)i * n + src];
+    eigvecs[e] = v;
+    const double sk = lam[src];
+    Wout[e] = (sk > cut) ? v / sqrt(sk) : 0.0;
+  }
+}
+
 }  // namespace
 
 namespace nys_host {
 size_t dc_buffer_bytes(int n) {
-  return ((size_t)n * dc_ld(n) + 3 * (size_t)n * n) * sizeof(double);
+  // A (n x ld) | Q | Qn | DL (n x n each) | lam, beta (n each) | qsel
+  return ((size_t)n * dc_ld(n) + 3 * (size_t)n * n + 2 * (size_t)n + 2) * sizeof(double);
 }
 bool dc_fits(int n) { return n >= 1 && n <= kDcMaxN; }
 bool dc_uses_smem(int n) { return dc_buffer_bytes(n) <= 150 * 1024; }
@@ -764,12 +1153,12 @@ int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, doubl
   const int threads = n <= 64 ? 256 : kDcThreads;
   const int dbg = getenv("NYS_EIG_DEBUG") != nullptr;
   auto launch = [&](auto kern) -> int {
-    if (use_smem) {
-      dyn = need;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)dyn);
-      if (e != cudaSuccess) return record_cuda(e);
-    }
+    // smem path: the matrices; global path: the panel's V and W (tridiag_blocked)
+    dyn = use_smem ? need
+                   : (2 * (size_t)n * (kTNb + 1) + 2 * kTNb + 4 * 256) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn);
+    if (e != cudaSuccess) return record_cuda(e);
     kern<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
                                   static_cast<double*>(ws), use_smem, dbg);
     return NYS_OK;
@@ -782,6 +1171,18 @@ int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, doubl
   if (rc) return rc;
   count_launches(1);
   NYS_CHECK_LAUNCH();
+  if (!use_smem) {
+    double* g = static_cast<double*>(ws);
+    const int warps = 8;
+    const int grid = (n + warps - 1) / warps;
+    if (n <= 128)
+      dc_backtransform_kernel<4><<<grid, 32 * warps, 0, st>>>(g, n);
+    else
+      dc_backtransform_kernel<kDcMaxN / 32><<<grid, 32 * warps, 0, st>>>(g, n);
+    dc_epilogue_kernel<<<1, 1024, 0, st>>>(g, n, drop_tol, eigvals, eigvecs, W, m_eff, info);
+    count_launches(2);
+    NYS_CHECK_LAUNCH();
+  }
   return NYS_OK;
 }
 }  // namespace nys_host
