@@ -205,6 +205,14 @@ int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, const doubl
                            const double* F, int ldx, const double* gamma, const double* Ac,
                            const double* betac, int n_cond, const int* idx, int nb, double* K,
                            double* rz, void* stream);
+/* Same, with the row range of every instance split over several CTAs (about two
+ * per SM) whose partial sums are added in fixed order: workspace of
+ * nys_newton_reduced_workspace_bytes(m_eff, n_c, nb) bytes (0 = one CTA per instance). */
+size_t nys_newton_reduced_workspace_bytes(int m_eff, int n_c, int nb);
+int nys_newton_reduced_ws_f64(const double* packed, int m_eff, int n_c, const double* aux,
+                              const double* F, int ldx, const double* gamma, const double* Ac,
+                              const double* betac, int n_cond, const int* idx, int nb, double* K,
+                              double* rz, void* workspace, size_t workspace_bytes, void* stream);
 /* batched dense LU (partial pivoting) solve, one system of side n <= 96 per slot */
 int nys_lu_solve_f64(double* M, double* rhs, int n, int nb, double* out, int* info, void* stream);
 /* D[b] = (dz, dy) (compute_delta = 1) and Xc[b] = X[b] + alpha[b] * D[b] */

@@ -54,6 +54,9 @@ SIGNATURES = {
                                         C.c_size_t, _vp]),
     "nys_newton_reduced_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _vp,
                                     _vp, _vp]),
+    "nys_newton_reduced_workspace_bytes": (_sz, [_i, _i, _i]),
+    "nys_newton_reduced_ws_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i,
+                                       _vp, _vp, _vp, _sz, _vp]),
     "nys_lu_solve_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _i, _vp, _i, _i, _vp]),

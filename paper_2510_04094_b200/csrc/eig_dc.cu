@@ -53,17 +53,6 @@ struct DcShared {
   int degenerate;
 };
 
-NYS_DEV double dc_block_sum(double x, DcShared& S) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  __syncthreads();
-  if (lane == 0) S.red[w] = x;
-  __syncthreads();
-  double s = 0.0;
-  for (int i = 0; i < nw; ++i) s += S.red[i];
-  return s;
-}
 
 // implicit QL on the leaf [s, s+len) of (d, e), eigenvectors into Q block
 NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {

@@ -234,13 +234,61 @@ struct Tri {
 
 constexpr int kRedWarps = 4;
 
+// Reduced (omega, b, lambda) system from the summed partials red[e] (e over the
+// NPAIR*64 Gram entries in MMA layout, then NB*8 rhs entries).
+template <int NB>
+NYS_DEV void build_reduced(const double* red, int stride, int nparts, int me, int nk,
+                           const double* __restrict__ F, int ldx, double gm,
+                           const double* __restrict__ Ac, const double* __restrict__ betac, int b,
+                           double* Kb, double* rb) {
+  constexpr int NPAIR = Tri<NB>::kPairs;
+  const int nz = me + 1 + nk, nh = me + 1;
+  const double* Fb = F + (size_t)b * ldx;
+  for (int e = threadIdx.x; e < NPAIR * 64; e += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nparts; ++w) s += red[(size_t)w * stride + e];
+    const int t = e >> 6, l = (e & 63) >> 1, j2 = e & 1;
+    int I = 0, rem = t;
+    while (rem >= NB - I) {
+      rem -= NB - I;
+      ++I;
+    }
+    const int J = I + rem;
+    const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + j2;
+    if (r < nh && c < nh && !(I == J && r > c)) {
+      const double v = gm * s + ((r == c && r < me) ? 1.0 : 0.0);
+      Kb[(size_t)r * nz + c] = v;
+      Kb[(size_t)c * nz + r] = v;
+    }
+  }
+  for (int e = threadIdx.x; e < NB * 8; e += blockDim.x) {
+    if (e >= nh) continue;
+    double s = 0.0;
+    for (int w = 0; w < nparts; ++w) s += red[(size_t)w * stride + NPAIR * 64 + e];
+    rb[e] = -Fb[e] - s;   // rhs_(omega,b) = -F - sum wh F_y / c
+  }
+  for (int e = threadIdx.x; e < nk * nh; e += blockDim.x) {
+    const int mu = e / nh, j = e % nh;
+    const double v = j < me ? Ac[(size_t)mu * me + j] : betac[mu];
+    Kb[(size_t)(nh + mu) * nz + j] = v;
+    Kb[(size_t)j * nz + nh + mu] = v;
+  }
+  for (int e = threadIdx.x; e < nk * nk; e += blockDim.x)
+    Kb[(size_t)(nh + e / nk) * nz + nh + e % nk] = 0.0;
+  for (int mu = threadIdx.x; mu < nk; mu += blockDim.x) rb[nh + mu] = -Fb[nh + mu];
+}
+
+// grid (instances, nsplit): CTA (j, s) accumulates k-steps [s kps, (s+1) kps)
+// of instance idx[j]; with part == nullptr (nsplit = 1) it builds K directly,
+// otherwise it stores its partial sums for newton_reduce_finalize_kernel.
 template <int NB>
 __global__ void __launch_bounds__(kRedWarps * 32)
     newton_reduce_kernel(const double* __restrict__ psi, int nks, int me, int n_c,
                          const double* __restrict__ aux, const double* __restrict__ F, int ldx,
                          const double* __restrict__ gamma, const double* __restrict__ Ac,
                          const double* __restrict__ betac, int nk, const int* __restrict__ idx,
-                         double* __restrict__ K, double* __restrict__ rz) {
+                         double* __restrict__ K, double* __restrict__ rz, int kps,
+                         double* __restrict__ part) {
   constexpr int NPAIR = Tri<NB>::kPairs;
   extern __shared__ double red[];   // [kRedWarps][NPAIR*64 + NB*8]
   const int b = idx[blockIdx.x];
@@ -254,7 +302,8 @@ __global__ void __launch_bounds__(kRedWarps * 32)
 #pragma unroll
   for (int F_ = 0; F_ < NB; ++F_) racc[F_] = 0.0;
 
-  for (int ks = warp; ks < nks; ks += kRedWarps) {
+  const int ks_lo = blockIdx.y * kps, ks_hi = min(nks, ks_lo + kps);
+  for (int ks = ks_lo + warp; ks < ks_hi; ks += kRedWarps) {
     const int row = ks * 4 + tig;
     const bool ok = row < n_c;
     const double fy = ok ? auxb[row] : 0.0;
@@ -302,43 +351,36 @@ __global__ void __launch_bounds__(kRedWarps * 32)
 #pragma unroll
     for (int F_ = 0; F_ < NB; ++F_) mine[NPAIR * 64 + F_ * 8 + gid] = racc[F_];
   __syncthreads();
-  const int nz = me + 1 + nk, nh = me + 1;
-  const double gm = gamma[b];
-  double* Kb = K + (size_t)blockIdx.x * nz * nz;
-  double* rb = rz + (size_t)blockIdx.x * nz;
-  const double* Fb = F + (size_t)b * ldx;
-  for (int e = threadIdx.x; e < NPAIR * 64; e += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < kRedWarps; ++w) s += red[(size_t)w * stride + e];
-    const int t = e >> 6, l = (e & 63) >> 1, j2 = e & 1;
-    int I = 0, rem = t;
-    while (rem >= NB - I) {
-      rem -= NB - I;
-      ++I;
+  if (part != nullptr) {   // this split's partial, warps summed in fixed order
+    double* out = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * stride;
+    for (int e = threadIdx.x; e < stride; e += blockDim.x) {
+      double s2 = 0.0;
+      for (int w = 0; w < kRedWarps; ++w) s2 += red[(size_t)w * stride + e];
+      out[e] = s2;
     }
-    const int J = I + rem;
-    const int r = I * 8 + (l >> 2), c = J * 8 + 2 * (l & 3) + j2;
-    if (r < nh && c < nh && !(I == J && r > c)) {
-      const double v = gm * s + ((r == c && r < me) ? 1.0 : 0.0);
-      Kb[(size_t)r * nz + c] = v;
-      Kb[(size_t)c * nz + r] = v;
-    }
+    return;
   }
-  for (int e = threadIdx.x; e < NB * 8; e += blockDim.x) {
-    if (e >= nh) continue;
-    double s = 0.0;
-    for (int w = 0; w < kRedWarps; ++w) s += red[(size_t)w * stride + NPAIR * 64 + e];
-    rb[e] = -Fb[e] - s;   // rhs_(omega,b) = -F - sum wh F_y / c
-  }
-  for (int e = threadIdx.x; e < nk * nh; e += blockDim.x) {
-    const int mu = e / nh, j = e % nh;
-    const double v = j < me ? Ac[(size_t)mu * me + j] : betac[mu];
-    Kb[(size_t)(nh + mu) * nz + j] = v;
-    Kb[(size_t)j * nz + nh + mu] = v;
-  }
-  for (int e = threadIdx.x; e < nk * nk; e += blockDim.x)
-    Kb[(size_t)(nh + e / nk) * nz + nh + e % nk] = 0.0;
-  for (int mu = threadIdx.x; mu < nk; mu += blockDim.x) rb[nh + mu] = -Fb[nh + mu];
+  const int nz = me + 1 + nk;
+  build_reduced<NB>(red, stride, kRedWarps, me, nk, F, ldx, gamma[b], Ac, betac, b,
+                    K + (size_t)blockIdx.x * nz * nz, rz + (size_t)blockIdx.x * nz);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256)
+    newton_reduce_finalize_kernel(const double* __restrict__ part, int nsplit, int nb, int me,
+                                  const double* __restrict__ F, int ldx,
+                                  const double* __restrict__ gamma, const double* __restrict__ Ac,
+                                  const double* __restrict__ betac, int nk,
+                                  const int* __restrict__ idx, double* __restrict__ K,
+                                  double* __restrict__ rz) {
+  constexpr int NPAIR = Tri<NB>::kPairs;
+  const int stride = NPAIR * 64 + NB * 8;
+  const int b = idx[blockIdx.x];
+  const int nz = me + 1 + nk;
+  // partials of this instance sit nb * stride apart (one per split)
+  build_reduced<NB>(part + (size_t)blockIdx.x * stride, nb * stride, nsplit, me, nk, F, ldx,
+                    gamma[b], Ac, betac, b, K + (size_t)blockIdx.x * nz * nz,
+                    rz + (size_t)blockIdx.x * nz);
 }
 
 // ---------------------------------------------------------------------------
@@ -588,15 +630,38 @@ extern "C" int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, 
   return NYS_OK;
 }
 
-extern "C" int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, const double* aux,
-                                      const double* F, int ldx, const double* gamma,
-                                      const double* Ac, const double* betac, int n_cond,
-                                      const int* idx, int nb, double* K, double* rz,
-                                      void* stream) {
+static int newton_reduce_splits(int nb, int nks) {
+  // enough CTAs for about two per SM, at least 16 k-steps per split
+  int ns = (2 * nys::device_sm_count() + nb - 1) / (nb > 0 ? nb : 1);
+  ns = ns < 1 ? 1 : (ns > 16 ? 16 : ns);
+  while (ns > 1 && nks / ns < 16) --ns;
+  return ns;
+}
+
+extern "C" size_t nys_newton_reduced_workspace_bytes(int m_eff, int n_c, int nb) {
+  const int NB = (m_eff + 2 + 7) / 8;
+  const int nks = (n_c + 3) / 4;
+  const int ns = newton_reduce_splits(nb, nks);
+  if (ns <= 1) return 0;
+  return (size_t)ns * nb * (NB * (NB + 1) / 2 * 64 + NB * 8) * sizeof(double);
+}
+
+extern "C" int nys_newton_reduced_ws_f64(const double* packed, int m_eff, int n_c,
+                                         const double* aux, const double* F, int ldx,
+                                         const double* gamma, const double* Ac,
+                                         const double* betac, int n_cond, const int* idx, int nb,
+                                         double* K, double* rz, void* workspace,
+                                         size_t workspace_bytes, void* stream) {
   if (m_eff < 1 || n_c < 1 || n_cond < 0 || nb < 0) return NYS_EINVAL;
   if (nb == 0) return NYS_OK;
   const int NB = (m_eff + 2 + 7) / 8;
   const int nks = (n_c + 3) / 4;
+  int ns = newton_reduce_splits(nb, nks);
+  if (ns > 1 && (workspace == nullptr ||
+                 workspace_bytes < nys_newton_reduced_workspace_bytes(m_eff, n_c, nb)))
+    ns = 1;   // no (or too small a) workspace: one CTA per instance
+  const int kps = (nks + ns - 1) / ns;
+  double* part = ns > 1 ? static_cast<double*>(workspace) : nullptr;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define NYS_RED(nbv)                                                                             \
   case nbv: {                                                                                    \
@@ -608,8 +673,14 @@ extern "C" int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, 
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
       if (e != cudaSuccess) return nys_host::record_cuda(e);                                     \
     }                                                                                            \
-    kern<<<nb, kRedWarps * 32, smem, st>>>(packed, nks, m_eff, n_c, aux, F, ldx, gamma, Ac, betac, \
-                                           n_cond, idx, K, rz);                                  \
+    kern<<<dim3(nb, ns), kRedWarps * 32, smem, st>>>(packed, nks, m_eff, n_c, aux, F, ldx, gamma, \
+                                                     Ac, betac, n_cond, idx, K, rz, kps, part);  \
+    nys_host::count_launches(1);                                                                 \
+    if (ns > 1) {                                                                                \
+      newton_reduce_finalize_kernel<nbv><<<nb, 256, 0, st>>>(part, ns, nb, m_eff, F, ldx, gamma,  \
+                                                            Ac, betac, n_cond, idx, K, rz);      \
+      nys_host::count_launches(1);                                                               \
+    }                                                                                            \
     break;                                                                                       \
   }
   switch (NB) {
@@ -625,9 +696,17 @@ extern "C" int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, 
     default: return NYS_EUNSUPPORTED;
   }
 #undef NYS_RED
-  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
+}
+
+extern "C" int nys_newton_reduced_f64(const double* packed, int m_eff, int n_c, const double* aux,
+                                      const double* F, int ldx, const double* gamma,
+                                      const double* Ac, const double* betac, int n_cond,
+                                      const int* idx, int nb, double* K, double* rz,
+                                      void* stream) {
+  return nys_newton_reduced_ws_f64(packed, m_eff, n_c, aux, F, ldx, gamma, Ac, betac, n_cond, idx,
+                                   nb, K, rz, nullptr, 0, stream);
 }
 
 extern "C" int nys_lu_solve_f64(double* M, double* rhs, int n, int nb, double* out, int* info,

@@ -222,10 +222,12 @@ class NewtonBatch:
         returns LU info per id."""
         idx_t = self._idx(ids)
         nb, st = len(ids), _lib.stream_ptr()
-        _lib.call("nys_newton_reduced_f64", _lib.ptr(self.packed), self.me, self.n_c,
+        wsb = self.lib.nys_newton_reduced_workspace_bytes(self.me, self.n_c, nb)
+        ws = _lib.WORKSPACE.get(wsb, self.dev) if wsb else None
+        _lib.call("nys_newton_reduced_ws_f64", _lib.ptr(self.packed), self.me, self.n_c,
                   _lib.ptr(self.aux), _lib.ptr(self.F), self.ldx, _lib.ptr(self.gam),
                   _lib.ptr(self.Ac), _lib.ptr(self.betac), self.nk, _lib.ptr(idx_t), nb,
-                  _lib.ptr(self.K), _lib.ptr(self.rz), st)
+                  _lib.ptr(self.K), _lib.ptr(self.rz), _lib.ptr(ws), wsb, st)
         _lib.call("nys_lu_solve_f64", _lib.ptr(self.K), _lib.ptr(self.rz), self.nz, nb,
                   _lib.ptr(self.dz), _lib.ptr(self.info), st)
         _lib.call("nys_newton_step_f64", _lib.ptr(self.S0), _lib.ptr(self.S1), self.me, self.n_c,
