@@ -190,8 +190,8 @@ int nys_newton_residual_f64(const double* S0, const double* S1, const double* S0
 /* Batched step halving (newton.py:305-318): norms[t * nb + j] = max|F| at the
  * trial X[idx[j]] + trial_alphas[t] * D[idx[j]] for t < ntrial, bit-identical to
  * forming the candidate with nys_newton_step_f64 and calling nys_newton_residual_f64;
- * nothing else is written.  scratch: nys_newton_trial_scratch_bytes (0 when the
- * per-CTA rows fit in shared memory). */
+ * nothing else is written.  scratch: nys_newton_trial_scratch_bytes (row-range
+ * partial sums of every instance and trial). */
 size_t nys_newton_trial_scratch_bytes(int m_eff, int n_c, int nb, int ntrial);
 int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, int m_eff, int n_c,
                                const double* g, const double* fy, const double* fyy,

@@ -88,19 +88,30 @@ struct Rhs {
 // (grid.y = trial t), nothing else written -- the batched step halving.  Both
 // run the same arithmetic in the same order, so a trial's norm is bit-identical
 // to materialising the candidate (newton_step_kernel) and calling the residual.
+// The residual in two kernels.  newton_residual_kernel: grid (slots, splits) --
+// a CTA takes one row range of one instance (kTrial: of one trial point
+// X[b] + alpha_t D[b]), forms e1, e2 and F_y there (non-trial: F_y and aux are
+// written), and stores its partial S1^T e1, S0^T e2, sum e2, max|F_y| and a
+// non-finite flag.  newton_residual_finalize_kernel adds the row ranges in
+// fixed order and forms F_omega, F_b, F_lambda and the max-norm.  Splitting
+// the rows puts several CTAs on every instance: one CTA per instance was
+// bound by the latency of streaming S^T from L2 (ncu: long-scoreboard stalls).
+// The trial form evaluates line-search points with the same arithmetic, so a
+// trial's norm is bit-identical to materialising the candidate
+// (newton_step_kernel) and calling the non-trial residual.
+constexpr int kResSplit = 4;
+NYS_DEV int res_rows_per_split(int n_c) { return ((n_c + kResSplit - 1) / kResSplit + 31) / 32 * 32; }
+
 template <bool kTrial>
 __global__ void __launch_bounds__(kResThreads)
     newton_residual_kernel(const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
-                           int n_c, Rhs rhs, const double* __restrict__ Ac,
-                           const double* __restrict__ betac, const double* __restrict__ vals,
-                           int nk, const double* __restrict__ gamma, const double* __restrict__ X,
-                           int ldx, const int* __restrict__ idx, double* __restrict__ F,
-                           double* __restrict__ norm, double* __restrict__ aux,
-                           double* __restrict__ work, const double* __restrict__ D,
-                           const double* __restrict__ alphas, int nb) {
+                           int n_c, Rhs rhs, const double* __restrict__ gamma,
+                           const double* __restrict__ X, int ldx, const int* __restrict__ idx,
+                           double* __restrict__ F, double* __restrict__ aux,
+                           const double* __restrict__ D, const double* __restrict__ alphas, int nb,
+                           int nk, double* __restrict__ part) {
   extern __shared__ double sh[];
   __shared__ double red[kResThreads / 32];
-  __shared__ double lam_s[kMaxCondN];
   const int b = idx[blockIdx.x];
   const double gm = gamma[b];
   const double* x = X + (size_t)b * ldx;
@@ -108,17 +119,15 @@ __global__ void __launch_bounds__(kResThreads)
   const double al = kTrial ? alphas[blockIdx.y] : 0.0;
   // x entry j of this CTA's point (trial: the candidate, as newton_step_kernel forms it)
 #define NYS_XV(j) (kTrial ? fma(al, dx[j], x[j]) : x[j])
+  const int split = blockIdx.z;
+  const int rpc = res_rows_per_split(n_c);
+  const int r0 = split * rpc, r1 = min(n_c, r0 + rpc);
   double* Fb = kTrial ? nullptr : F + (size_t)b * ldx;
   double* om = sh;                 // me
-  double* e1;
-  if (kTrial)
-    e1 = work != nullptr ? work + ((size_t)blockIdx.y * nb + blockIdx.x) * 2 * n_c : sh + me;
-  else
-    e1 = work + (size_t)b * 2 * n_c;
-  double* e2 = e1 + n_c;
+  double* e1 = sh + me;            // rpc (this CTA's rows)
+  double* e2 = e1 + rpc;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int k = tid; k < me; k += nt) om[k] = NYS_XV(k);
-  if (tid < nk) lam_s[tid] = NYS_XV(me + 1 + tid);
   __syncthreads();
   const double bias = NYS_XV(me);
   const int y0 = me + 1 + nk;
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(kResThreads)
   int bad = 0;
   // rows across threads, features from the transposed copies: every load is
   // a coalesced 256-byte warp access (S0/S1 rows are 8*me bytes apart)
-  for (int i = tid; i < n_c; i += nt) {
+  for (int i = r0 + tid; i < r1; i += nt) {
     double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
     int k = 0;
 #pragma unroll 4
@@ -148,8 +157,8 @@ __global__ void __launch_bounds__(kResThreads)
     const double ee1 = __dsub_rn(s1w, f);
     const double ee2 = __dsub_rn(__dsub_rn(yi, s0w), bias);
     if (!isfinite(ee1) || !isfinite(f)) bad = 1;
-    e1[i] = ee1;
-    e2[i] = ee2;
+    e1[i - r0] = ee1;
+    e2[i - r0] = ee2;
     // F_y = -gamma f_y e1 + gamma e2 in numpy's order (newton.py:146)
     const double Fy = __dadd_rn(__dmul_rn(__dmul_rn(-gm, fy), ee1), __dmul_rn(gm, ee2));
     fmax_local = fmax(fmax_local, fabs(Fy));
@@ -162,14 +171,17 @@ __global__ void __launch_bounds__(kResThreads)
     }
   }
   __syncthreads();
-  // F_omega = omega + gamma S1^T e1 - gamma S0^T e2 + Ac^T lambda  (warp per k)
+  const size_t slot = kTrial ? (size_t)blockIdx.y * nb + blockIdx.x : (size_t)blockIdx.x;
+  const int pstride = 2 * me + 3;
+  double* out = part + (slot * kResSplit + split) * pstride;
+  // partial S1^T e1 and S0^T e2 over this row range (warp per k)
   for (int k = warp; k < me; k += nw) {
-    const double* r1 = S1T + (size_t)k * n_c;
-    const double* r0 = S0T + (size_t)k * n_c;
+    const double* rr1 = S1T + (size_t)k * n_c;
+    const double* rr0 = S0T + (size_t)k * n_c;
     double a = 0.0, c = 0.0;
-    for (int i = lane; i < n_c; i += 32) {
-      a = fma(r1[i], e1[i], a);
-      c = fma(r0[i], e2[i], c);
+    for (int i = r0 + lane; i < r1; i += 32) {
+      a = fma(rr1[i], e1[i - r0], a);
+      c = fma(rr0[i], e2[i - r0], c);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -177,49 +189,98 @@ __global__ void __launch_bounds__(kResThreads)
       c += __shfl_xor_sync(0xffffffffu, c, o);
     }
     if (lane == 0) {
-      // omega + gamma S1^T e1 - gamma S0^T e2 + Ac^T lambda (newton.py:139), uncontracted
-      double acl = 0.0;
-      for (int mu = 0; mu < nk; ++mu) acl = __dadd_rn(acl, __dmul_rn(Ac[(size_t)mu * me + k], lam_s[mu]));
-      double v = __dadd_rn(__dsub_rn(__dadd_rn(om[k], __dmul_rn(gm, a)), __dmul_rn(gm, c)), acl);
-      if (kTrial)
-        fmax_local = fmax(fmax_local, fabs(v));
-      else
-        Fb[k] = v;
+      out[k] = a;
+      out[me + k] = c;
     }
   }
   double se2 = 0.0;
-  for (int i = tid; i < n_c; i += nt) se2 += e2[i];
+  for (int i = r0 + tid; i < r1; i += nt) se2 += e2[i - r0];
   se2 = block_reduce(se2, red, false);
+  const int any_bad = __syncthreads_or(bad);
+  const double fmx = block_reduce(fmax_local, red, true);
   if (tid == 0) {
+    out[2 * me] = se2;
+    out[2 * me + 1] = fmx;
+    out[2 * me + 2] = any_bad ? 1.0 : 0.0;
+  }
+#undef NYS_XV
+}
+
+template <bool kTrial>
+__global__ void __launch_bounds__(64)
+    newton_residual_finalize_kernel(int me, const double* __restrict__ Ac,
+                                    const double* __restrict__ betac,
+                                    const double* __restrict__ vals, int nk,
+                                    const double* __restrict__ gamma,
+                                    const double* __restrict__ X, int ldx,
+                                    const int* __restrict__ idx, double* __restrict__ F,
+                                    double* __restrict__ norm, const double* __restrict__ D,
+                                    const double* __restrict__ alphas, int nb,
+                                    const double* __restrict__ part) {
+  __shared__ double red[2];
+  __shared__ double lam_s[kMaxCondN];
+  const int b = idx[blockIdx.x];
+  const double gm = gamma[b];
+  const double* x = X + (size_t)b * ldx;
+  const double* dx = kTrial ? D + (size_t)b * ldx : nullptr;
+  const double al = kTrial ? alphas[blockIdx.y] : 0.0;
+#define NYS_XV(j) (kTrial ? fma(al, dx[j], x[j]) : x[j])
+  const size_t slot = kTrial ? (size_t)blockIdx.y * nb + blockIdx.x : (size_t)blockIdx.x;
+  const int pstride = 2 * me + 3;
+  const double* pp = part + slot * kResSplit * pstride;
+  double* Fb = kTrial ? nullptr : F + (size_t)b * ldx;
+  const int tid = threadIdx.x;
+  if (tid < nk) lam_s[tid] = NYS_XV(me + 1 + tid);
+  __syncthreads();
+  double fmax_local = 0.0;
+  int bad = 0;
+  for (int s2 = 0; s2 < kResSplit; ++s2) bad |= pp[s2 * pstride + 2 * me + 2] != 0.0;
+  for (int k = tid; k < me; k += blockDim.x) {
+    double a = 0.0, c = 0.0;
+    for (int s2 = 0; s2 < kResSplit; ++s2) {   // fixed order over row ranges
+      a += pp[s2 * pstride + k];
+      c += pp[s2 * pstride + me + k];
+    }
+    // omega + gamma S1^T e1 - gamma S0^T e2 + Ac^T lambda (newton.py:139), uncontracted
+    double acl = 0.0;
+    for (int mu = 0; mu < nk; ++mu) acl = __dadd_rn(acl, __dmul_rn(Ac[(size_t)mu * me + k], lam_s[mu]));
+    const double v = __dadd_rn(__dsub_rn(__dadd_rn(NYS_XV(k), __dmul_rn(gm, a)), __dmul_rn(gm, c)), acl);
+    if (!kTrial) Fb[k] = v;
+    fmax_local = fmax(fmax_local, fabs(v));
+  }
+  if (tid == 0) {
+    double se2 = 0.0, fy = 0.0;
+    for (int s2 = 0; s2 < kResSplit; ++s2) {
+      se2 += pp[s2 * pstride + 2 * me];
+      fy = fmax(fy, pp[s2 * pstride + 2 * me + 1]);
+    }
+    fmax_local = fmax(fmax_local, fy);
     double bl = 0.0;
     for (int mu = 0; mu < nk; ++mu) bl = __dadd_rn(bl, __dmul_rn(betac[mu], lam_s[mu]));
     const double Fbias = __dadd_rn(__dmul_rn(-gm, se2), bl);   // newton.py:143
-    if (kTrial)
-      fmax_local = fmax(fmax_local, fabs(Fbias));
-    else
-      Fb[me] = Fbias;
+    if (!kTrial) Fb[me] = Fbias;
+    fmax_local = fmax(fmax_local, fabs(Fbias));
+    const double bias = NYS_XV(me);
     for (int mu = 0; mu < nk; ++mu) {
       double v = 0.0;
-      for (int k = 0; k < me; ++k) v = fma(Ac[(size_t)mu * me + k], om[k], v);
+      for (int k = 0; k < me; ++k) v = fma(Ac[(size_t)mu * me + k], NYS_XV(k), v);
       // Ac omega + beta b - values (newton.py:144)
       v = __dsub_rn(__dadd_rn(v, __dmul_rn(betac[mu], bias)), vals[(size_t)b * nk + mu]);
-      if (kTrial)
-        fmax_local = fmax(fmax_local, fabs(v));
-      else
-        Fb[me + 1 + mu] = v;
+      if (!kTrial) Fb[me + 1 + mu] = v;
+      fmax_local = fmax(fmax_local, fabs(v));
     }
   }
+  // max over the block (two warps)
+  for (int o = 16; o; o >>= 1) fmax_local = fmax(fmax_local, __shfl_xor_sync(0xffffffffu, fmax_local, o));
+  if ((tid & 31) == 0) red[tid >> 5] = fmax_local;
   __syncthreads();
-  if (!kTrial)
-    for (int k = tid; k < me + 1 + nk; k += nt) fmax_local = fmax(fmax_local, fabs(Fb[k]));
-  const int any_bad = __syncthreads_or(bad);
-  const double nrm = block_reduce(fmax_local, red, true);
   if (tid == 0) {
-    // NaN -> DivergenceError (newton.py:137-138)
+    double nrm = fmax(red[0], blockDim.x > 32 ? red[1] : 0.0);
+    const double outv = bad ? NAN : nrm;   // NaN -> DivergenceError (newton.py:137-138)
     if (kTrial)
-      norm[(size_t)blockIdx.y * nb + blockIdx.x] = any_bad ? NAN : nrm;
+      norm[slot] = outv;
     else
-      norm[b] = any_bad ? NAN : nrm;
+      norm[b] = outv;
   }
 #undef NYS_XV
 }
@@ -585,19 +646,29 @@ extern "C" int nys_newton_residual_f64(const double* S0, const double* S1, const
   (void)S0;
   (void)S1;
   Rhs rhs{g, fy, fyy, alpha, beta, n_c};
-  newton_residual_kernel<false><<<nb, kResThreads, m_eff * sizeof(double),
-                                  static_cast<cudaStream_t>(stream)>>>(
-      S0T, S1T, m_eff, n_c, rhs, Ac, betac, vals, n_cond, gamma, X, ldx, idx, F, norm, aux, work,
-      nullptr, nullptr, nb);
-  nys_host::count_launches(1);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // `work` (2 n_c doubles per instance) holds the row-range partials
+  if ((size_t)kResSplit * (2 * m_eff + 3) > 2 * (size_t)n_c) return NYS_EUNSUPPORTED;
+  const int rpc = ((n_c + kResSplit - 1) / kResSplit + 31) / 32 * 32;
+  const size_t smem = ((size_t)m_eff + 2 * (size_t)rpc) * sizeof(double);
+  auto kern = newton_residual_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return nys_host::record_cuda(e);
+  kern<<<dim3(nb, 1, kResSplit), kResThreads, smem, st>>>(S0T, S1T, m_eff, n_c, rhs, gamma, X,
+                                                          ldx, idx, F, aux, nullptr, nullptr, nb,
+                                                          n_cond, work);
+  newton_residual_finalize_kernel<false><<<nb, 64, 0, st>>>(m_eff, Ac, betac, vals, n_cond, gamma,
+                                                            X, ldx, idx, F, norm, nullptr,
+                                                            nullptr, nb, work);
+  nys_host::count_launches(2);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
 
 extern "C" size_t nys_newton_trial_scratch_bytes(int m_eff, int n_c, int nb, int ntrial) {
-  const size_t smem = ((size_t)m_eff + 2 * (size_t)n_c) * sizeof(double);
-  if (smem <= 96 * 1024) return 0;   // e1/e2 live in shared memory
-  return (size_t)ntrial * nb * 2 * n_c * sizeof(double);
+  (void)n_c;   // partial sums of every (instance, trial, row range)
+  return (size_t)ntrial * nb * kResSplit * (2 * (size_t)m_eff + 3) * sizeof(double);
 }
 
 extern "C" int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, int m_eff, int n_c,
@@ -614,17 +685,23 @@ extern "C" int nys_newton_trial_norms_f64(const double* S0T, const double* S1T, 
     return NYS_EINVAL;
   if (nb == 0 || ntrial == 0) return NYS_OK;
   const size_t need = nys_newton_trial_scratch_bytes(m_eff, n_c, nb, ntrial);
-  if (need > 0 && (scratch == nullptr || scratch_bytes < need)) return NYS_EWORKSPACE;
-  const size_t smem = (size_t)m_eff * sizeof(double) +
-                      (need > 0 ? 0 : 2 * (size_t)n_c * sizeof(double));
+  if (scratch == nullptr || scratch_bytes < need) return NYS_EWORKSPACE;
+  const int rpc = ((n_c + kResSplit - 1) / kResSplit + 31) / 32 * 32;
+  const size_t smem = ((size_t)m_eff + 2 * (size_t)rpc) * sizeof(double);
   auto kern = newton_residual_kernel<true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return nys_host::record_cuda(e);
   Rhs rhs{g, fy, fyy, alpha, beta, n_c};
-  kern<<<dim3(nb, ntrial), kResThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      S0T, S1T, m_eff, n_c, rhs, Ac, betac, vals, n_cond, gamma, X, ldx, idx, nullptr, norms,
-      nullptr, need > 0 ? static_cast<double*>(scratch) : nullptr, D, trial_alphas, nb);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(scratch);
+  kern<<<dim3(nb, ntrial, kResSplit), kResThreads, smem, st>>>(S0T, S1T, m_eff, n_c, rhs, gamma,
+                                                               X, ldx, idx, nullptr, nullptr, D,
+                                                               trial_alphas, nb, n_cond, part);
+  newton_residual_finalize_kernel<true><<<dim3(nb, ntrial), 64, 0, st>>>(
+      m_eff, Ac, betac, vals, n_cond, gamma, X, ldx, idx, nullptr, norms, D, trial_alphas, nb,
+      part);
+  nys_host::count_launches(2);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;

@@ -186,7 +186,17 @@ class NewtonBatch:
 
     # -------------------------------------------------------------- kernels
     def _idx(self, ids):
-        return self.torch.as_tensor(np.asarray(ids, dtype=np.int32), device=self.dev)
+        """Device index tensor for an id list; the active sets of consecutive
+        iterations repeat, so they are cached (one small H2D copy per new set)."""
+        key = tuple(ids)
+        cache = self.__dict__.setdefault("_idx_cache", {})
+        t = cache.get(key)
+        if t is None:
+            if len(cache) > 256:
+                cache.clear()
+            t = self.torch.as_tensor(np.asarray(ids, dtype=np.int32), device=self.dev)
+            cache[key] = t
+        return t
 
     def _sample_host(self, X, ids):
         """Sampled mode: evaluate the spec callables at the current y (host)."""
@@ -234,11 +244,11 @@ class NewtonBatch:
                   self.nk, _lib.ptr(self.aux), _lib.ptr(self.F), _lib.ptr(self.dz),
                   _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
                   _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), nb, 1, st)
-        info = self.info[:nb].cpu().numpy().copy()
-        D = self.D[idx_t]
-        bad = ~self.torch.isfinite(D).all(dim=1).cpu().numpy()
-        info[bad] = _lib.INFO_NONFINITE
-        return info
+        # LU info and the finiteness of D in one read-back
+        bad = ~self.torch.isfinite(self.D[idx_t]).all(dim=1)
+        both = self.torch.where(bad, self.torch.full_like(self.info[:nb], _lib.INFO_NONFINITE),
+                                self.info[:nb])
+        return both.cpu().numpy()
 
     def candidate(self, ids, alphas):
         """Xc[b] = X[b] + alpha_b D[b]."""

@@ -107,11 +107,14 @@ def test_batched_step_halving_is_bit_identical():
     idx_t = eng._idx(ids)
     norms = torch.empty((len(alphas), len(ids)), dtype=torch.float64, device=eng.dev)
     al_t = torch.tensor(alphas, dtype=torch.float64, device=eng.dev)
+    sb = eng.lib.nys_newton_trial_scratch_bytes(eng.me, eng.n_c, len(ids), len(alphas))
+    scratch = torch.empty(max(sb, 8), dtype=torch.uint8, device=eng.dev)
     _lib.call("nys_newton_trial_norms_f64", _lib.ptr(eng.S0T), _lib.ptr(eng.S1T), eng.me,
               eng.n_c, _lib.ptr(eng.g), None, None, _lib.ptr(eng.fal), _lib.ptr(eng.fbe),
               _lib.ptr(eng.Ac), _lib.ptr(eng.betac), _lib.ptr(eng.vals), eng.nk,
               _lib.ptr(eng.gam), _lib.ptr(eng.X), _lib.ptr(eng.D), eng.ldx, _lib.ptr(idx_t),
-              len(ids), _lib.ptr(al_t), len(alphas), _lib.ptr(norms), None, 0, _lib.stream_ptr())
+              len(ids), _lib.ptr(al_t), len(alphas), _lib.ptr(norms), _lib.ptr(scratch), sb,
+              _lib.stream_ptr())
     got = norms.cpu().numpy()
     assert np.array_equal(got, seq, equal_nan=True), (got, seq)
 
