@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kFeatThreads)
   for (int e = threadIdx.x; e < kTP * ncols; e += blockDim.x) {
     int ii = e / ncols, k = e % ncols;
     int i = i0 + ii;
+    if (mode == 0 && i >= n_pts) continue;   // partial tile (condition rows: one point)
     double acc = 0.0;
     if (k < m_eff) {   // four independent partial sums (FP64 FMA latency)
       const double* kr = kt + ii * m;
