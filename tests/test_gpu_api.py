@@ -1,0 +1,152 @@
+"""GPU tests of the device pipelines and the reference's error behaviour
+(golden fixtures only; the GPU box has no /root/reference)."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from gpu_util import conditions, fmap_from_golden, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _predict(fm, x, grid):
+    from paper_2510_04094_b200 import linear as L
+    return L.predict_batch(fm, x, 0, grid).cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0"])
+def test_single_pipeline_matches_reference_and_replays(name):
+    """SingleSolvePipeline (eig + graph-replayed condition rows / Gram / KKT):
+    y_hat within 1e-6 of the reference, and the replayed call reproduces the
+    first (eager) call bit for bit."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden(name)
+    cond = conditions(g, 0)
+    pipe = L.SingleSolvePipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                 float(g["gamma"]), int(g["order"]), cond)
+    pts = torch.as_tensor(g["pts"], device="cuda")
+    coef = torch.as_tensor(g["coef"][0], device="cuda")
+    forc = torch.as_tensor(g["forcing"][0], device="cuda")
+    x1 = pipe.run_device(pts, coef, forc)[0].clone()
+    x2 = pipe.run_device(pts, coef, forc)[0].clone()   # captured graph now exists
+    x3 = pipe.run_device(pts, coef, forc)[0].clone()   # replay
+    assert torch.equal(x1, x2) and torch.equal(x2, x3)
+    mdl = pipe.model()
+    y = mdl.predict(0, g["grid"])
+    assert rel_l2(y, g["yhat"][0]) <= 1e-6
+
+
+def test_shared_pipeline_graph_equals_eager():
+    import torch
+
+    from paper_2510_04094_b200 import batch as BT
+    g = load_golden("c2_seed0_i0-7")
+    cond = conditions(g, 0)
+    coef = torch.as_tensor(g["coef"], device="cuda")
+    forc = torch.as_tensor(g["forcing"], device="cuda")
+    vals = torch.as_tensor(g["cond_values"], device="cuda")
+    pipe = BT.SharedGridPipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                 float(g["gamma"]), 2, cond, 8)
+    xs = [pipe.run_device(coef, forc, vals)[0].clone() for _ in range(3)]
+    os.environ["NYS_GRAPHS"] = "0"
+    try:
+        xe = pipe.run_device(coef, forc, vals)[0].clone()
+    finally:
+        del os.environ["NYS_GRAPHS"]
+    assert all(torch.equal(xs[0], x) for x in xs[1:] + [xe])
+    fm = pipe.solver.fmap
+    Y = _predict(fm, xs[0], g["grid"])
+    for b in range(8):
+        assert rel_l2(Y[b], g["yhat"][b]) <= 1e-6
+
+
+def test_blocked_kkt_matches_scalar_cholesky():
+    """kkt_block.cu (DMMA-blocked omega Cholesky + Schur) against the scalar
+    whole-H Cholesky on the same Grams: the same solutions to 1e-9 in y_hat."""
+    import torch
+
+    from paper_2510_04094_b200 import batch as BT
+    g = load_golden("c2_seed0_i0-7")
+    fm = fmap_from_golden(g)
+    solver = BT.LinearBatchSolver(fm, g["grid"], float(g["gamma"]), 2, conditions(g, 0), 8)
+    xb, ib = solver.solve(g["coef"], g["forcing"], g["cond_values"])
+    xb = xb.clone()
+    os.environ["NYS_KKT_SCALAR"] = "1"
+    try:
+        xs, is_ = solver.solve(g["coef"], g["forcing"], g["cond_values"])
+    finally:
+        del os.environ["NYS_KKT_SCALAR"]
+    assert (ib.cpu().numpy() == 0).all() and (is_.cpu().numpy() == 0).all()
+    Yb = _predict(fm, xb, g["grid"])
+    Ys = _predict(fm, xs, g["grid"])
+    for b in range(8):
+        assert rel_l2(Yb[b], Ys[b]) <= 1e-9
+
+
+def test_large_kkt_cholesky_matches_lu():
+    """kkt_big.cu (c4-shaped side 259) against the reference's LU (kkt.cu)."""
+    from gpu_util import solve_golden_instance
+
+    g = load_golden("c4_n16384")
+    fm = fmap_from_golden(g)
+    _, m_chol = solve_golden_instance(g, fm, 0)
+    os.environ["NYS_KKT_LU"] = "1"
+    try:
+        _, m_lu = solve_golden_instance(g, fm, 0)
+    finally:
+        del os.environ["NYS_KKT_LU"]
+    y1 = m_chol.predict(0, g["grid"])
+    y2 = m_lu.predict(0, g["grid"])
+    assert rel_l2(y1, y2) <= 1e-10
+    assert rel_l2(y1, g["yhat"][0]) <= 1e-6
+
+
+def test_singular_system_raises():
+    """Two identical conditions make M singular: linear.solve raises
+    SingularSystemError like linear.py:148-151 (and so does the batch path)."""
+    from gpu_util import ArraySpec
+
+    from paper_2510_04094_b200 import batch as BT
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200.problems import BoundaryCondition, Conditions
+    g = load_golden("c0_seed0")
+    fm = fmap_from_golden(g)
+    bc = BoundaryCondition(float(g["cond_points"][0]), int(g["cond_orders"][0]),
+                           float(g["cond_values"][0][0]))
+    cond = Conditions("ivp", (bc, bc))
+    spec = ArraySpec(int(g["order"]), g["coef"][0], g["forcing"][0], g["pts"])
+    sy = L.assemble(spec, cond, fm, g["grid"], float(g["gamma"]))
+    with pytest.raises(L.SingularSystemError):
+        L.solve(sy, fm)
+    solver = BT.LinearBatchSolver(fm, g["grid"], float(g["gamma"]), int(g["order"]), cond, 2)
+    vals = np.array([[bc.value, bc.value]] * 2)
+    _, info = solver.solve(np.stack([g["coef"][0]] * 2), np.stack([g["forcing"][0]] * 2), vals)
+    info = info.cpu().numpy()
+    assert (info != 0).all()
+    with pytest.raises(L.SingularSystemError):
+        L.raise_for_info(int(info[0]))
+
+
+def test_degenerate_landmarks_and_bad_arguments_raise():
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+    with pytest.raises(N.DegenerateLandmarksError):
+        N.build_feature_map(RbfKernel(0.01), np.array([0.0, 0.5, 0.5, 1.0]))
+    with pytest.raises(ValueError):
+        N.build_feature_map(RbfKernel(0.01), np.linspace(0, 1, 5), drop_tol=1.5)
+    g = load_golden("c0_seed0")
+    fm = fmap_from_golden(g)
+    from gpu_util import ArraySpec
+    spec = ArraySpec(int(g["order"]), g["coef"][0], g["forcing"][0], g["pts"])
+    with pytest.raises(ValueError):
+        L.assemble(spec, conditions(g, 0), fm, g["grid"], 0.0)
+    bad = g["forcing"][0].copy()
+    bad[3] = np.nan
+    spec_bad = ArraySpec(int(g["order"]), g["coef"][0], bad, g["pts"])
+    with pytest.raises(FloatingPointError):
+        L.assemble(spec_bad, conditions(g, 0), fm, g["grid"], float(g["gamma"]))
