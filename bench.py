@@ -296,7 +296,10 @@ def setup_c2(args, ctx):
         parallelism=f"instance-sharded x{ctx['world']}, no collective",
         extra={"m_eff": me, "global_batch": ctx["world"] * B,
                "l2": "samples 402 MB/GPU > 126 MB L2; no flush needed",
-               "step": "eig + shared features + batched Gram + batched KKT"},
+               "step": "eig + shared features + batched Gram + batched KKT; every step runs "
+                       "its own landmark eigendecomposition, on a side stream with two "
+                       "alternating buffer sets, so step k+1's (one-SM) eigensolver overlaps "
+                       "step k's Gram"},
         note="algorithmic F (SURVEY.md 8d) counts the full m_eff^2 Gram; the kernel "
              "computes the upper block triangle only, and with m_eff % 8 == 0 accumulates the "
              "(g, r) columns with FP64 FMAs instead of DMMA blocks (executed_* = DMMA flops)")

@@ -174,16 +174,24 @@ class SharedGridPipeline:
         self.device = device
         self.solver = None
 
-    def _prepare_fmap(self):
+    def _prepare_fmap(self, eigbuf=None, stream=None):
         """Eigendecomposition + solver object; True when the solver is new."""
         from .nystrom import EigBuffers
-        if getattr(self, "_eigbuf", None) is None:
-            self._eigbuf = EigBuffers(self.landmarks, self.device)
-        fm = self._build(self.kernel, self.landmarks, self.drop_tol, buffers=self._eigbuf)
+        if eigbuf is None:
+            if getattr(self, "_eigbuf", None) is None:
+                self._eigbuf = EigBuffers(self.landmarks, self.device)
+            eigbuf = self._eigbuf
+        if stream is None:
+            fm = self._build(self.kernel, self.landmarks, self.drop_tol, buffers=eigbuf)
+        else:
+            torch = _lib.require_device()[1]
+            with torch.cuda.stream(stream):
+                fm = self._build(self.kernel, self.landmarks, self.drop_tol, buffers=eigbuf)
+            torch.cuda.current_stream().wait_stream(stream)
         if self.solver is None or self.solver.fmap.m_eff != fm.m_eff:
             self.solver = LinearBatchSolver(fm, self.grid, self.gamma, self.order, self.cond,
                                             self.max_batch)
-            self._graph = None
+            self._graphs = None
             return self.solver, True
         self.solver.fmap = fm
         return self.solver, False
@@ -200,12 +208,35 @@ class SharedGridPipeline:
         (whose m_eff read-back is the step's one host sync) the condition-row
         refresh, Psi pack, Gram and KKT launches are replayed from a CUDA graph
         captured on the first call with the same buffers (NYS_GRAPHS=0 turns
-        this off).  Without out_x/out_info the results land in buffers owned by
-        the pipeline and are overwritten by the next call."""
+        this off).  The eigendecomposition itself runs on a side stream with two
+        alternating buffer sets, so consecutive calls overlap it with the
+        previous call's Gram (NYS_EIG_OVERLAP=0 turns this off).  Without
+        out_x/out_info the results land in buffers owned by the pipeline and are
+        overwritten by the next call."""
         import os
 
+        from .nystrom import EigBuffers
+
         torch = _lib.require_device()[1]
-        solver, fresh = self._prepare_fmap()
+        graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
+        if graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0":
+            # Two eigen-buffer sets used alternately, the eigendecomposition on its
+            # own stream: this call's (one-SM) eigensolver runs while the previous
+            # call's Gram is still executing.  A set is overwritten only after the
+            # main-stream work of the call that last read it (event).
+            if getattr(self, "_eigbufs", None) is None:
+                self._eigbufs = [EigBuffers(self.landmarks, self.device) for _ in range(2)]
+                self._eig_done = [None, None]
+                self._eig_stream = torch.cuda.Stream(device=self._eigbufs[0].device)
+                self._parity = 0
+            k = self._parity
+            self._parity ^= 1
+            if self._eig_done[k] is not None:
+                self._eig_stream.wait_event(self._eig_done[k])
+            solver, fresh = self._prepare_fmap(self._eigbufs[k], self._eig_stream)
+        else:
+            k = None
+            solver, fresh = self._prepare_fmap()
         B = int(coef.shape[0])
         if out_x is None or out_info is None:
             if getattr(self, "_outs", None) is None or self._outs[0].shape != (B, solver.side):
@@ -219,23 +250,29 @@ class SharedGridPipeline:
             solver.refresh_condition_rows()
             solver.solve_device(coef, forcing, values, out_x, out_info)
 
-        if os.environ.get("NYS_GRAPHS", "1") == "0":
+        if not graphs:
             post()
             return out_x, out_info
-        key = (id(solver), solver.fmap.m_eff, B, coef.data_ptr(), forcing.data_ptr(),
-               values.data_ptr(), out_x.data_ptr(), out_info.data_ptr())
-        if getattr(self, "_graph", None) is not None and self._gkey == key:
-            self._graph.replay()
-            _lib.note_graph_launches(self._gcount)
-            return out_x, out_info
-        post()   # eager: this call's result, and the kernels' one-time attribute setup
-        lib = _lib.load()
-        n0 = lib.nys_launch_count()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            post()
-        self._gcount = lib.nys_launch_count() - n0
-        self._graph, self._gkey = g, key
+        key = (id(solver), solver.fmap.m_eff, solver.fmap.d_W.data_ptr(), B, coef.data_ptr(),
+               forcing.data_ptr(), values.data_ptr(), out_x.data_ptr(), out_info.data_ptr())
+        if fresh or getattr(self, "_graphs", None) is None:
+            self._graphs = {}
+        hit = self._graphs.get(key)
+        if hit is not None:
+            hit[0].replay()
+            _lib.note_graph_launches(hit[1])
+        else:
+            post()   # eager: this call's result, and the kernels' one-time attribute setup
+            lib = _lib.load()
+            n0 = lib.nys_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                post()
+            self._graphs[key] = (g, lib.nys_launch_count() - n0)
+        if k is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream())
+            self._eig_done[k] = ev
         return out_x, out_info
 
     def run_host(self, coef_h, forcing_h, values_h, x_h, info_h, chunks: int = 4,
