@@ -213,6 +213,30 @@ int nys_newton_reduced_ws_f64(const double* packed, int m_eff, int n_c, const do
                               const double* F, int ldx, const double* gamma, const double* Ac,
                               const double* betac, int n_cond, const int* idx, int nb, double* K,
                               double* rz, void* workspace, size_t workspace_bytes, void* stream);
+/* ---- second-order nonlinear ODEs y'' = f(t, y, y') (newton2.cu) ------------------
+ * samples [6][B][n_c]: f, f_y, f_y', f_yy, f_yy', f_y'y' at (t, y, S1 omega) of
+ * instance b (host-evaluated reference callables).  aux [B][6][n_c]; workspace of
+ * nys_newton2_workspace_bytes(m_eff, n_c, nb) bytes for both calls.  The packed
+ * Psi_0..Psi_2 come from nys_newton2_pack_f64. */
+size_t nys_newton2_workspace_bytes(int m_eff, int n_c, int nb);
+size_t nys_newton2_pack_doubles(int m_eff, int n_c);
+int nys_newton2_pack_f64(const double* landmarks, int m, const double* W, int ldw, int m_eff,
+                         double sigma2, const double* pts, int n_c, double* packed, void* stream);
+int nys_newton2_residual_f64(const double* S0T, const double* S1T, const double* S2T, int m_eff,
+                             int n_c, const double* samples, int B, const double* Ac,
+                             const double* betac, const double* vals, int n_cond,
+                             const double* gamma, const double* X, int ldx, const int* idx,
+                             int nb, double* F, double* norm, double* aux, void* workspace,
+                             size_t workspace_bytes, void* stream);
+int nys_newton2_reduced_f64(const double* packed, int m_eff, int n_c, const double* aux,
+                            const double* F, int ldx, const double* gamma, const double* Ac,
+                            const double* betac, int n_cond, const int* idx, int nb, double* K,
+                            double* rz, void* workspace, size_t workspace_bytes, void* stream);
+int nys_newton2_step_f64(const double* S0T, const double* S1T, const double* S2T, int m_eff,
+                         int n_c, int n_cond, const double* aux, const double* F,
+                         const double* dz, const double* gamma, const double* X, double* D,
+                         double* Xc, const double* alpha, int ldx, const int* idx, int nb,
+                         void* stream);
 /* batched dense LU (partial pivoting) solve, one system of side n <= 96 per slot */
 int nys_lu_solve_f64(double* M, double* rhs, int n, int nb, double* out, int* info, void* stream);
 /* D[b] = (dz, dy) (compute_delta = 1) and Xc[b] = X[b] + alpha[b] * D[b] */

@@ -58,6 +58,15 @@ SIGNATURES = {
     "nys_newton_reduced_ws_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i,
                                        _vp, _vp, _vp, _sz, _vp]),
     "nys_lu_solve_f64": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp]),
+    "nys_newton2_workspace_bytes": (_sz, [_i, _i, _i]),
+    "nys_newton2_pack_doubles": (_sz, [_i, _i]),
+    "nys_newton2_pack_f64": (_i, [_vp, _i, _vp, _i, _i, _d, _vp, _i, _vp, _vp]),
+    "nys_newton2_residual_f64": (_i, [_vp, _vp, _vp, _i, _i, _vp, _i, _vp, _vp, _vp, _i, _vp,
+                                      _vp, _i, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "nys_newton2_reduced_f64": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _i,
+                                     _vp, _vp, _vp, _sz, _vp]),
+    "nys_newton2_step_f64": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _i, _vp, _i, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _i, _vp, _i, _i, _vp]),
 }

@@ -626,6 +626,20 @@ extern "C" int nys_newton_pack_f64(const double* landmarks, int m, const double*
                                    packed, static_cast<cudaStream_t>(stream));
 }
 
+extern "C" int nys_newton2_pack_f64(const double* landmarks, int m, const double* W, int ldw,
+                                    int m_eff, double sigma2, const double* pts, int n_c,
+                                    double* packed, void* stream) {
+  const int NB = (m_eff + 2 + 7) / 8;
+  const int nks = (n_c + 3) / 4;
+  return nys_host::launch_psi_pack(landmarks, m, W, ldw, m_eff, sigma2, 2, pts, n_c, NB, nks * 4,
+                                   packed, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" size_t nys_newton2_pack_doubles(int m_eff, int n_c) {
+  const int NB = (m_eff + 2 + 7) / 8;
+  return (size_t)((n_c + 3) / 4) * 3 * NB * 32;
+}
+
 extern "C" size_t nys_newton_pack_doubles(int m_eff, int n_c) {
   const int NB = (m_eff + 2 + 7) / 8;
   return (size_t)((n_c + 3) / 4) * 2 * NB * 32;

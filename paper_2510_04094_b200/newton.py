@@ -22,8 +22,9 @@ Two ways to give the nonlinearity f(t, y):
 * a reference ``NonlinearOdeSpec`` (callables) -- evaluated on the host at the
   current y every residual call (the generic drop-in path; slower).
 
-Only first-order problems (p = 1) run on the device; higher orders are
-SURVEY.md §8f next-row 2 and raise ``NotImplementedError``.
+First- and second-order problems run on the device (p = 2: newton2.cu, the
+SURVEY.md §8f next-row 2 families P14 / P15, with host-sampled callables);
+higher orders raise ``NotImplementedError``.
 """
 from __future__ import annotations
 
@@ -133,6 +134,10 @@ class NewtonBatch:
         if (family is None) == (specs is None):
             raise ValueError("give exactly one of family / specs")
         self.family, self.specs = family, specs
+        orders = {1} if specs is None else {int(sp.order) for sp in specs}
+        if len(orders) != 1 or not orders <= {1, 2}:
+            raise NotImplementedError("device Newton: one common order p in {1, 2} per batch")
+        self.p = orders.pop()
         f64 = dict(dtype=torch.float64, device=dev)
         self.pts = _lib.as_f64(self.pts_host, dev)
         st = _lib.stream_ptr()
@@ -143,10 +148,16 @@ class NewtonBatch:
         self.S1T = torch.empty((self.me, self.n_c), **f64)
         _lib.call("nys_transpose_f64", _lib.ptr(self.S0), self.n_c, self.me, _lib.ptr(self.S0T), st)
         _lib.call("nys_transpose_f64", _lib.ptr(self.S1), self.n_c, self.me, _lib.ptr(self.S1T), st)
-        self.packed = torch.zeros(lib.nys_newton_pack_doubles(self.me, self.n_c), **f64)
-        _lib.call("nys_newton_pack_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
+        pack = "nys_newton_pack" if self.p == 1 else "nys_newton2_pack"
+        self.packed = torch.zeros(getattr(lib, pack + "_doubles")(self.me, self.n_c), **f64)
+        _lib.call(pack + "_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
                   fmap.m, self.me, float(fmap.kernel.sigma2), _lib.ptr(self.pts), self.n_c,
                   _lib.ptr(self.packed), st)
+        if self.p == 2:   # Psi_2 rows (transposed) for e1 = S2 omega - f and the step
+            S2 = fmap.feature_matrix_device(2, self.pts).contiguous()
+            self.S2T = torch.empty((self.me, self.n_c), **f64)
+            _lib.call("nys_transpose_f64", _lib.ptr(S2), self.n_c, self.me, _lib.ptr(self.S2T),
+                      st)
         Ac, beta, _ = condition_rows(cond, fmap)
         self.Ac = _lib.as_f64(Ac.reshape(self.nk, self.me), dev)
         self.betac = _lib.as_f64(beta, dev)
@@ -157,7 +168,7 @@ class NewtonBatch:
         self.F = torch.zeros((B, ldx), **f64)
         self.D = torch.zeros((B, ldx), **f64)
         self.norm = torch.zeros(B, **f64)
-        self.aux = torch.zeros((B, 3, self.n_c), **f64)
+        self.aux = torch.zeros((B, 3 if self.p == 1 else 6, self.n_c), **f64)
         self.work = torch.zeros((B, 2, self.n_c), **f64)
         self.gam = torch.full((B,), self.gamma_target, **f64)
         self.alpha = torch.ones(B, **f64)
@@ -175,13 +186,14 @@ class NewtonBatch:
             self.fy = torch.zeros((B, self.n_c), **f64)
             self.fyy = torch.zeros((B, self.n_c), **f64)
             self.fal = self.fbe = None
+            need = [(0, 0)] if self.p == 1 else [(0, 0), (0, 1), (1, 1)]
             for sp in specs:
-                if sp.order != 1:
-                    raise NotImplementedError("device Newton supports first-order ODEs (p = 1)")
                 tab = sp.rhs_second_partials
-                if tab is None or ((0, 0) not in tab):
+                if tab is None or any(k not in tab and k[::-1] not in tab for k in need):
                     raise PartialsMissingError(
                         "rhs_second_partials required for analytic Jacobian")
+            if self.p == 2:   # f, f_y, f_y', f_yy, f_yy', f_y'y' at (t, y, y')
+                self.samples = torch.zeros((6, B, self.n_c), **f64)
         self.launches = 0
 
     # -------------------------------------------------------------- kernels
@@ -199,7 +211,10 @@ class NewtonBatch:
         return t
 
     def _sample_host(self, X, ids):
-        """Sampled mode: evaluate the spec callables at the current y (host)."""
+        """Sampled mode: evaluate the spec callables at the current y (host);
+        p = 2 also at y' = S1 omega (newton.py:120-125: derivatives from the model)."""
+        if self.p == 2:
+            return self._sample_host2(X, ids)
         Y = X[:, self.nz:].cpu().numpy()
         t = self.pts_host
         for b in ids:
@@ -210,6 +225,25 @@ class NewtonBatch:
             self.fyy[b] = _lib.as_f64(np.asarray(sp.rhs_second_partials[(0, 0)](t, y),
                                                  dtype=float), self.dev)
 
+    def _sample_host2(self, X, ids):
+        idx_t = self._idx(ids)
+        Y = X[idx_t, self.nz:].cpu().numpy()
+        YP = predict_batch(self.fmap, X[idx_t, :self.me + 1], 1, self.pts).cpu().numpy()
+        t = self.pts_host
+        host = np.empty((6, len(ids), self.n_c))
+        for r, b in enumerate(ids):
+            sp = self.specs[b]
+            a = (t, Y[r], YP[r])
+            tab = sp.rhs_second_partials
+            sec = lambda j, k: tab[(j, k)] if (j, k) in tab else tab[(k, j)]  # noqa: E731
+            host[0, r] = np.asarray(sp.rhs(*a), dtype=float)
+            host[1, r] = np.asarray(sp.rhs_partials[0](*a), dtype=float)
+            host[2, r] = np.asarray(sp.rhs_partials[1](*a), dtype=float)
+            host[3, r] = np.asarray(sec(0, 0)(*a), dtype=float)
+            host[4, r] = np.asarray(sec(0, 1)(*a), dtype=float)
+            host[5, r] = np.asarray(sec(1, 1)(*a), dtype=float)
+        self.samples[:, idx_t] = self.torch.as_tensor(host, device=self.dev)
+
     def residual(self, X, ids, idx_t=None) -> np.ndarray:
         """F(X[b]) for b in ids; returns max|F| per id (NaN = non-finite rhs)."""
         if self.specs is not None:
@@ -218,7 +252,20 @@ class NewtonBatch:
         self._residual_launch(X, idx_t, len(ids))
         return self.norm[idx_t].cpu().numpy()
 
+    def _ws2(self, nb):
+        wsb = self.lib.nys_newton2_workspace_bytes(self.me, self.n_c, nb)
+        return _lib.WORKSPACE.get(wsb, self.dev), wsb
+
     def _residual_launch(self, X, idx_t, nb):
+        if self.p == 2:
+            ws, wsb = self._ws2(nb)
+            _lib.call("nys_newton2_residual_f64", _lib.ptr(self.S0T), _lib.ptr(self.S1T),
+                      _lib.ptr(self.S2T), self.me, self.n_c, _lib.ptr(self.samples), self.B,
+                      _lib.ptr(self.Ac), _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk,
+                      _lib.ptr(self.gam), _lib.ptr(X), self.ldx, _lib.ptr(idx_t), nb,
+                      _lib.ptr(self.F), _lib.ptr(self.norm), _lib.ptr(self.aux), _lib.ptr(ws), wsb,
+                      _lib.stream_ptr())
+            return
         _lib.call("nys_newton_residual_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
                   _lib.ptr(self.S0T), _lib.ptr(self.S1T), self.me, self.n_c, _lib.ptr(self.g),
                   _lib.ptr(self.fy), _lib.ptr(self.fyy), _lib.ptr(self.fal), _lib.ptr(self.fbe),
@@ -232,6 +279,8 @@ class NewtonBatch:
         returns LU info per id."""
         idx_t = self._idx(ids)
         nb, st = len(ids), _lib.stream_ptr()
+        if self.p == 2:
+            return self._direction2(idx_t, nb, st)
         wsb = self.lib.nys_newton_reduced_workspace_bytes(self.me, self.n_c, nb)
         ws = _lib.WORKSPACE.get(wsb, self.dev) if wsb else None
         _lib.call("nys_newton_reduced_ws_f64", _lib.ptr(self.packed), self.me, self.n_c,
@@ -245,6 +294,24 @@ class NewtonBatch:
                   _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
                   _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), nb, 1, st)
         # LU info and the finiteness of D in one read-back
+        bad = ~self.torch.isfinite(self.D[idx_t]).all(dim=1)
+        both = self.torch.where(bad, self.torch.full_like(self.info[:nb], _lib.INFO_NONFINITE),
+                                self.info[:nb])
+        return both.cpu().numpy()
+
+    def _direction2(self, idx_t, nb, st):
+        ws, wsb = self._ws2(nb)
+        _lib.call("nys_newton2_reduced_f64", _lib.ptr(self.packed), self.me, self.n_c,
+                  _lib.ptr(self.aux), _lib.ptr(self.F), self.ldx, _lib.ptr(self.gam),
+                  _lib.ptr(self.Ac), _lib.ptr(self.betac), self.nk, _lib.ptr(idx_t), nb,
+                  _lib.ptr(self.K), _lib.ptr(self.rz), _lib.ptr(ws), wsb, st)
+        _lib.call("nys_lu_solve_f64", _lib.ptr(self.K), _lib.ptr(self.rz), self.nz, nb,
+                  _lib.ptr(self.dz), _lib.ptr(self.info), st)
+        _lib.call("nys_newton2_step_f64", _lib.ptr(self.S0T), _lib.ptr(self.S1T),
+                  _lib.ptr(self.S2T), self.me, self.n_c, self.nk, _lib.ptr(self.aux),
+                  _lib.ptr(self.F), _lib.ptr(self.dz), _lib.ptr(self.gam), _lib.ptr(self.X),
+                  _lib.ptr(self.D), _lib.ptr(self.Xc), _lib.ptr(self.alpha), self.ldx,
+                  _lib.ptr(idx_t), nb, st)
         bad = ~self.torch.isfinite(self.D[idx_t]).all(dim=1)
         both = self.torch.where(bad, self.torch.full_like(self.info[:nb], _lib.INFO_NONFINITE),
                                 self.info[:nb])
@@ -336,10 +403,19 @@ class NewtonBatch:
         x0 = self.const_state(ids)
         b0 = x0[:, self.me]
         t = self.pts_host
-        coef = np.empty((len(ids), 1, self.n_c))
+        p = self.p
+        coef = np.empty((len(ids), p, self.n_c))
         forcing = np.empty((len(ids), self.n_c))
         for r, b in enumerate(ids):
             yb = np.full_like(t, b0[r])
+            if p == 2:   # args (t, b0, 0); f_k = df/dy^(p-k) (newton.py:256-266)
+                sp = self.specs[b]
+                a = (t, yb, np.zeros_like(t))
+                for k in (1, 2):
+                    coef[r, k - 1] = np.asarray(sp.rhs_partials[p - k](*a), dtype=float)
+                forcing[r] = (np.asarray(sp.rhs(*a), dtype=float)
+                              - np.asarray(sp.rhs_partials[0](*a), dtype=float) * b0[r])
+                continue
             if self.family is not None:
                 a, be = self.family.alpha[b], self.family.beta[b]
                 f0 = self.family.g[b] + a * yb * yb + be * np.sin(yb)
@@ -350,7 +426,7 @@ class NewtonBatch:
                 fy = np.asarray(sp.rhs_partials[0](t, yb), dtype=float)
             coef[r, 0] = fy
             forcing[r] = f0 - fy * b0[r]
-        solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, 1, self.cond, len(ids))
+        solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, p, self.cond, len(ids))
         xl, info = solver.solve(coef, forcing, self.values[ids])
         xl = xl.cpu().numpy()
         info = info.cpu().numpy()
@@ -528,9 +604,9 @@ def _raise_for(status, msg, model, trace):
 
 def solve_nonlinear(spec, cond, fmap: NystromFeatureMap, grid, gamma: float,
                     opts: NewtonOptions = NewtonOptions(), x0: Optional[NewtonState] = None):
-    """newton.solve_nonlinear (newton.py:376-412) for one first-order spec."""
-    if spec.order != 1:
-        raise NotImplementedError("device Newton supports first-order ODEs (p = 1)")
+    """newton.solve_nonlinear (newton.py:376-412) for one first- or second-order spec."""
+    if spec.order not in (1, 2):
+        raise NotImplementedError("device Newton supports orders p = 1 and p = 2")
     if opts.jacobian != "analytic":
         raise NotImplementedError("finite-difference Jacobians are not on the device path")
     values = np.array([[bc.value for bc in cond.entries]])

@@ -211,6 +211,79 @@ class NonlinearInstance:
         return 1.0 if self.kind == "sin" else 0.0
 
 
+@dataclass(frozen=True)
+class NonlinearInstance2:
+    """Second-order IVP y'' = f(t, y, y') -- the SURVEY.md §8f next-row-2 shape
+    (the catalog's P14/P15 are second-order nonlinear BVPs), manufactured like
+    config 3:
+
+    kind "drag": f = -k (y')^2 + g(t),      g = y*'' + k (y*')^2
+    kind "pend": f = -sin(y) - k y' + g(t), g = y*'' + sin(y*) + k y*'
+    Even instances are "drag", odd ones "pend"; conditions y(t0), y'(t0).
+    """
+
+    seed: int
+    index: int
+    kind: str
+    k: float
+    domain: tuple[float, float]
+    sol: SinusoidSum
+
+    def g_fn(self, t):
+        t = np.asarray(t, dtype=float)
+        ys, d1, d2 = self.sol(t), self.sol.deriv(t, 1), self.sol.deriv(t, 2)
+        if self.kind == "drag":
+            return d2 + self.k * d1 * d1
+        return d2 + np.sin(ys) + self.k * d1
+
+    def rhs(self, t, y, yp):
+        y, yp = np.asarray(y, dtype=float), np.asarray(yp, dtype=float)
+        if self.kind == "drag":
+            return -self.k * yp * yp + self.g_fn(t)
+        return -np.sin(y) - self.k * yp + self.g_fn(t)
+
+    def rhs_y(self, t, y, yp):
+        y = np.asarray(y, dtype=float)
+        return np.zeros_like(y) if self.kind == "drag" else -np.cos(y)
+
+    def rhs_yp(self, t, y, yp):
+        yp = np.asarray(yp, dtype=float)
+        return -2.0 * self.k * yp if self.kind == "drag" else np.full_like(yp, -self.k)
+
+    def rhs_yy(self, t, y, yp):
+        y = np.asarray(y, dtype=float)
+        return np.zeros_like(y) if self.kind == "drag" else np.sin(y)
+
+    def rhs_yyp(self, t, y, yp):
+        return np.zeros_like(np.asarray(y, dtype=float))
+
+    def rhs_ypyp(self, t, y, yp):
+        y = np.asarray(y, dtype=float)
+        return np.full_like(y, -2.0 * self.k) if self.kind == "drag" else np.zeros_like(y)
+
+    def second_partials(self) -> dict:
+        return {(0, 0): self.rhs_yy, (0, 1): self.rhs_yyp, (1, 1): self.rhs_ypyp}
+
+    def conditions(self) -> list[tuple[float, int, float]]:
+        t0 = np.array([float(self.domain[0])])
+        return [(float(t0[0]), 0, float(self.sol(t0)[0])),
+                (float(t0[0]), 1, float(self.sol.deriv(t0, 1)[0]))]
+
+
+# second-order nonlinear workload (tests): n, m, sigma, gamma of the c3 scale
+NONLINEAR2 = dict(n=400, m=40, domain=(0.0, 1.0), terms=3, gamma=1e8, sigma=0.2,
+                  newton_max_iters=30)
+
+
+def nonlinear2_instance(seed: int = 0, index: int = 0) -> NonlinearInstance2:
+    # draw order: A[K], w[K], phi[K], k  (rng seeded by [5, seed, index])
+    rng = np.random.default_rng([5, seed, index])
+    sol = _draw_solution(rng, NONLINEAR2["terms"])
+    k = float(rng.uniform(0.2, 1.0))
+    kind = "drag" if index % 2 == 0 else "pend"
+    return NonlinearInstance2(seed, index, kind, k, NONLINEAR2["domain"], sol)
+
+
 def _draw_solution(rng: np.random.Generator, terms: int) -> SinusoidSum:
     amp = rng.uniform(0.5, 1.5, size=terms)
     freq = rng.uniform(1.0, 10.0, size=terms)

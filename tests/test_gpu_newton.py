@@ -179,3 +179,78 @@ def test_config3_census_matches_reference():
     print("reference self-sensitivity: agreement", self_agree, "lost", self_lost)
     assert len(lost) <= 3 * self_lost, lost
     assert B - agree <= 3 * (B - self_agree), (agree, self_agree)
+
+
+# ---------------------------------------------------------------- p = 2
+def _engine2(g):
+    from paper_2510_04094_b200 import newton as NW
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import Conditions, BoundaryCondition, NonlinearOdeSpec
+
+    fm = N.build_feature_map(RbfKernel(float(g["sigma2"])), g["landmarks"])
+    insts = [W.nonlinear2_instance(0, int(i)) for i in g["indices"]]
+    specs = [NonlinearOdeSpec(2, it.rhs, (it.rhs_y, it.rhs_yp), it.domain, it.second_partials())
+             for it in insts]
+    cond = Conditions("ivp", tuple(BoundaryCondition(*c) for c in insts[0].conditions()))
+    vals = np.array([[c[2] for c in it.conditions()] for it in insts])
+    eng = NW.NewtonBatch(fm, g["grid"], cond, vals, float(g["gamma"]), specs=specs)
+    return eng, fm, insts
+
+
+def test_newton2_residual_and_direction_match_oracle():
+    """p = 2 (newton2.cu): the device residual equals the oracle's, and the
+    Schur-reduced Newton direction solves the oracle's dense analytic system
+    J d = -F (newton.py:160-211) to a backward error of 1e-12."""
+    from oracle import newton_port as NP
+    g = load_golden("n2_seed0_i0-5")
+    eng, fm, insts = _engine2(g)
+    rng = np.random.default_rng(1)
+    x = np.zeros((eng.B, eng.ldx))
+    x[:, :eng.me] = rng.normal(scale=0.05, size=(eng.B, eng.me))
+    x[:, eng.me] = 0.7
+    x[:, eng.nz:] = 0.7 + 0.05 * rng.normal(size=(eng.B, eng.n_c))
+    eng.X[:] = eng.torch.as_tensor(x, device=eng.dev)
+    ids = list(range(eng.B))
+    eng.residual(eng.X, ids)
+    info = eng.direction(ids)
+    assert (info == 0).all()
+    F = eng.F.cpu().numpy()
+    Dd = eng.D.cpu().numpy()
+    Wd = fm.d_W[:, :fm.m_eff].cpu().numpy()
+    S0 = fm.feature_matrix(0, eng.pts_host)
+    for j, it in enumerate(insts):
+        spec = NP.NlSpec(2, it.rhs, (it.rhs_y, it.rhs_yp), it.second_partials())
+        w = NP.Work(spec, it.conditions(), g["grid"], float(g["gamma"]), float(g["sigma2"]),
+                    g["landmarks"], Wd)
+        Fo = NP.residual(w, x[j])
+        np.testing.assert_allclose(F[j], Fo, rtol=0, atol=1e-9 * np.abs(Fo).max())
+        J = NP.jacobian(w, x[j])
+        d = Dd[j]
+        # backward error of the device direction in the oracle's dense system
+        # (J reaches cond ~1e16 at gamma = 1e8, so forward differences say little)
+        berr = np.abs(J @ d + Fo).max() / (np.abs(J).sum(axis=1).max() * np.abs(d).max()
+                                           + np.abs(Fo).max())
+        assert berr <= 1e-12, (j, berr)
+        do = np.linalg.solve(J, -Fo)
+        me = eng.me
+        yo = S0 @ do[:me] + do[me]
+        yd = S0 @ d[:me] + d[me]
+        assert rel_l2(yd, yo) <= 1e-3, (j, rel_l2(yd, yo))
+
+
+def test_newton2_ladder_matches_reference():
+    """solve_nonlinear with p = 2 specs against the live reference's outcomes
+    (tests/golden/make_newton2.py): same status, y_hat within 1e-6."""
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import newton as NW
+    g = load_golden("n2_seed0_i0-5")
+    eng, fm, insts = _engine2(g)
+    status, X, traces, rung = eng.solve(max_iters=30)
+    Y = L.predict_batch(fm, X[:, :eng.me + 1], 0, g["grid"]).cpu().numpy()
+    for j in range(len(insts)):
+        ours = "converged" if status[j] == NW.OK else f"status{status[j]}"
+        assert ours == str(g["status"][j]), (j, ours, traces[j][-3:])
+        assert rel_l2(Y[j], g["yhat"][j]) <= YHAT_TOL, (j, rel_l2(Y[j], g["yhat"][j]))
+        print(j, "its", len(traces[j]) - 1, "ref", int(g["iterations"][j]), "rung", rung[j])
