@@ -71,3 +71,21 @@ def test_two_landmark_eigenvalues():
     s, _ = O.eig_landmarks(1.0, [0.0, 1.0])
     c = np.exp(-1.0)
     np.testing.assert_allclose(s, [1 + c, 1 - c], rtol=1e-12)
+
+
+def test_oracle_newton2_reproduces_reference():
+    """Second-order Newton (p = 2): the oracle port against the live reference's
+    golden (tests/golden/make_newton2.py) -- pins the oracle for newton2.cu."""
+    g = load_golden("n2_seed0_i0-5")
+    s, v = O.eig_landmarks(float(g["sigma2"]), g["landmarks"])
+    Wb = O.scaled_basis(s, v)
+    for j, idx in enumerate(g["indices"][:2]):
+        inst = W.nonlinear2_instance(0, int(idx))
+        spec = NP.NlSpec(2, inst.rhs, (inst.rhs_y, inst.rhs_yp), inst.second_partials())
+        x, tr = NP.solve_nonlinear(spec, inst.conditions(), g["grid"], float(g["gamma"]),
+                                   float(g["sigma2"]), g["landmarks"], Wb,
+                                   max_iters=W.NONLINEAR2["newton_max_iters"])
+        me = Wb.shape[1]
+        y = O.predict(float(g["sigma2"]), g["landmarks"], Wb, x[:me], x[me], 0, g["grid"])
+        assert O.rel_l2(y, g["yhat"][j]) <= 1e-9
+        np.testing.assert_allclose(tr.norms, g[f"norms_{j}"], rtol=1e-6)
