@@ -406,7 +406,17 @@ class NewtonBatch:
         p = self.p
         coef = np.empty((len(ids), p, self.n_c))
         forcing = np.empty((len(ids), self.n_c))
-        for r, b in enumerate(ids):
+        if self.family is not None:   # vectorised over the instances (family mode)
+            # y = b0 is constant along t, so the y-dependent terms are one scalar
+            # per instance (the same numbers the elementwise form produces)
+            fam = self.family
+            ida = np.asarray(ids)
+            a, be = fam.alpha[ida], fam.beta[ida]
+            f0 = fam.g[ida] + (a * b0 * b0 + be * np.sin(b0))[:, None]
+            fy = 2.0 * a * b0 + be * np.cos(b0)
+            coef[:, 0] = fy[:, None]
+            forcing[:] = f0 - (fy * b0)[:, None]
+        for r, b in enumerate(ids if self.family is None else ()):
             yb = np.full_like(t, b0[r])
             if p == 2:   # args (t, b0, 0); f_k = df/dy^(p-k) (newton.py:256-266)
                 sp = self.specs[b]
@@ -416,17 +426,16 @@ class NewtonBatch:
                 forcing[r] = (np.asarray(sp.rhs(*a), dtype=float)
                               - np.asarray(sp.rhs_partials[0](*a), dtype=float) * b0[r])
                 continue
-            if self.family is not None:
-                a, be = self.family.alpha[b], self.family.beta[b]
-                f0 = self.family.g[b] + a * yb * yb + be * np.sin(yb)
-                fy = 2.0 * a * yb + be * np.cos(yb)
-            else:
-                sp = self.specs[b]
-                f0 = np.asarray(sp.rhs(t, yb), dtype=float)
-                fy = np.asarray(sp.rhs_partials[0](t, yb), dtype=float)
+            sp = self.specs[b]
+            f0 = np.asarray(sp.rhs(t, yb), dtype=float)
+            fy = np.asarray(sp.rhs_partials[0](t, yb), dtype=float)
             coef[r, 0] = fy
             forcing[r] = f0 - fy * b0[r]
-        solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, p, self.cond, len(ids))
+        solver = self.__dict__.get("_lin_solver")
+        if solver is None:   # one batched linear solver (max batch B) for every rung
+            solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, p, self.cond,
+                                       self.B)
+            self._lin_solver = solver
         xl, info = solver.solve(coef, forcing, self.values[ids])
         xl = xl.cpu().numpy()
         info = info.cpu().numpy()
