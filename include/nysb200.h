@@ -246,6 +246,20 @@ int nys_newton_step_f64(const double* S0, const double* S1, int m_eff, int n_c, 
                         const double* alpha, int ldx, const int* idx, int nb, int compute_delta,
                         void* stream);
 
+/* ---- ridge leverage scores -------------------------
+ * Replaces the exact branch of nystrom.ridge_leverage_scores (nystrom.py:58-70,
+ * n <= _LEVERAGE_EXACT_LIMIT = 4000): scores[i] = diag(Omega (Omega + n*ridge*I)^-1)_i,
+ * Omega = kernel_matrix(RBF(sigma2), 0, grid, grid), clipped below at 1e-300
+ * (nystrom.py:81).  Computed as 1 - n*ridge*diag(A^-1) from a tiled DMMA Cholesky
+ * A = L L^T fused with X = L^-1.  info[0] = NYS_INFO_SINGULAR when A is not
+ * numerically positive definite (the reference's dgesv would still return; the
+ * host mirror raises np.linalg.LinAlgError).  The sketch branch for n > 4000
+ * (nystrom.py:71-80) is not served by this entry. */
+#define NYS_LEVERAGE_MAX_N 8192
+size_t nys_leverage_workspace_bytes(int n);
+int nys_leverage_scores_f64(const double* grid, int n, double sigma2, double ridge, double* scores,
+                            int* info, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,36 @@ def equidistant(grid: np.ndarray, m: int) -> np.ndarray:
     return grid[np.round(np.arange(m) * (n - 1) / (m - 1)).astype(int)]
 
 
+LEVERAGE_EXACT_LIMIT = 4000  # nystrom.py:25
+
+
+def leverage_scores(sigma2: float, grid, ridge: float) -> np.ndarray:
+    """Exact ridge leverage scores (nystrom.py:58-70, n <= 4000 branch).
+
+    diag of solve(Omega + n ridge I, Omega), clipped below at 1e-300 (:81).
+    """
+    grid = np.asarray(grid, dtype=float)
+    n = grid.size
+    if n > LEVERAGE_EXACT_LIMIT:
+        raise OracleError("sketch branch (nystrom.py:71-80) not restated")
+    omega = rbf_block(sigma2, 0, grid, grid)
+    res = np.linalg.solve(omega + n * ridge * np.eye(n), omega)
+    return np.clip(np.diagonal(res).copy(), 1e-300, None)
+
+
+def leverage_landmarks(scores: np.ndarray, seed: int, m: int) -> np.ndarray:
+    """Landmark indices drawn from the scores (nystrom.py:95-103)."""
+    rng = np.random.default_rng(seed)
+    p = scores / scores.sum()
+    return np.sort(rng.choice(scores.size, size=m, replace=False, p=p))
+
+
+def leverage_default_sigma2(grid) -> float:
+    """Neutral score kernel: length scale span / 10 (nystrom.py:97-100)."""
+    span = float(grid[-1] - grid[0])
+    return max(span / 10.0, 1e-6) ** 2
+
+
 def eig_landmarks(sigma2: float, landmarks, drop_tol: float = DROP_TOL):
     """Kept eigenpairs of Omega_mm, descending (nystrom.py:136-160).
 

@@ -67,6 +67,8 @@ SIGNATURES = {
                                      _vp, _vp, _vp, _sz, _vp]),
     "nys_newton2_step_f64": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _i, _vp, _i, _vp]),
+    "nys_leverage_workspace_bytes": (_sz, [_i]),
+    "nys_leverage_scores_f64": (_i, [_vp, _i, _d, _d, _vp, _vp, _vp, _sz, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _i, _vp, _i, _i, _vp]),
 }

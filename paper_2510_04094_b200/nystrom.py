@@ -2,9 +2,10 @@
 
 Mirror of ``pkg/src/nysode/nystrom.py`` (same names, arguments, errors):
 
-* :func:`select_landmarks` -- host index logic, identical to nystrom.py:84-106
-  for ``Equidistant`` and ``Random``; ``LeverageScore`` is SURVEY.md §8f
-  "next" row 3 and raises ``NotImplementedError``.
+* :func:`select_landmarks` -- host index logic, identical to nystrom.py:84-106;
+  for ``LeverageScore`` the scores come from the device
+  (:func:`ridge_leverage_scores`, C-ABI ``nys_leverage_scores_f64``) and the
+  draw uses the reference's own numpy Generator stream on the host.
 * :func:`build_feature_map` -- device Jacobi eigendecomposition of Omega_mm
   (C-ABI ``nys_landmark_eig_f64``), replacing nystrom.py:136-160.
 * :class:`NystromFeatureMap` -- holds the device copies (landmarks, W);
@@ -22,6 +23,7 @@ from . import _lib
 from .kernel import RbfKernel, check_order
 
 DEFAULT_DROP_TOL = 1e-16     # nystrom.py:21
+_LEVERAGE_EXACT_LIMIT = 4000  # nystrom.py:25
 
 
 class DegenerateLandmarksError(ValueError):
@@ -62,10 +64,47 @@ def select_landmarks(strategy, grid, m: int) -> np.ndarray:
         rng = np.random.default_rng(strategy.seed)
         idx = np.sort(rng.choice(n, size=m, replace=False))
     elif name == "LeverageScore":
-        raise NotImplementedError("leverage-score sampling is SURVEY.md §8f next-row 3")
+        # nystrom.py:95-103: default score kernel is an RBF of length span / 10
+        rng = np.random.default_rng(strategy.seed)
+        score_kernel = strategy.kernel
+        if score_kernel is None:
+            span = float(grid[-1] - grid[0])
+            score_kernel = RbfKernel(sigma2=max(span / 10.0, 1e-6) ** 2)
+        scores = ridge_leverage_scores(score_kernel, grid, strategy.ridge)
+        p = scores / scores.sum()
+        idx = np.sort(rng.choice(n, size=m, replace=False, p=p))
     else:
         raise TypeError(f"unknown sampling strategy {strategy!r}")
     return grid[idx]
+
+
+def ridge_leverage_scores(k: RbfKernel, grid, ridge: float, device=None) -> np.ndarray:
+    """diag(Omega (Omega + n ridge I)^-1) over the grid (nystrom.py:58-81).
+
+    The exact branch (n <= 4000) runs on the device as 1 - n ridge diag(A^-1)
+    from one tiled DMMA Cholesky + inverse sweep (csrc/leverage.cu).  The
+    reference's uniform-sketch branch for larger grids (nystrom.py:71-80) needs
+    a 2000 x 2000 eigendecomposition and is not served yet: it raises
+    ``NotImplementedError`` rather than falling back to the host.
+    """
+    grid = np.asarray(grid, dtype=float).reshape(-1)
+    n = grid.size
+    if n > _LEVERAGE_EXACT_LIMIT:
+        raise NotImplementedError(
+            f"leverage scores for n={n} > {_LEVERAGE_EXACT_LIMIT} use the reference's "
+            "sketch branch (nystrom.py:71-80), not built for the device yet")
+    lib, torch = _lib.require_device()
+    device = torch.device(device or "cuda")
+    d_grid = _lib.as_f64(grid, device)
+    scores = torch.empty(n, dtype=torch.float64, device=device)
+    info = torch.zeros(1, dtype=torch.int32, device=device)
+    wsb = lib.nys_leverage_workspace_bytes(n)
+    ws = _lib.WORKSPACE.get(wsb, device)
+    _lib.call("nys_leverage_scores_f64", _lib.ptr(d_grid), n, float(k.sigma2), float(ridge),
+              _lib.ptr(scores), _lib.ptr(info), _lib.ptr(ws), wsb, _lib.stream_ptr())
+    if int(info.item()) != _lib.INFO_OK:
+        raise np.linalg.LinAlgError("Omega + n*ridge*I is not numerically positive definite")
+    return scores.cpu().numpy()
 
 
 @dataclass(eq=False)

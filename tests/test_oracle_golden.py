@@ -89,3 +89,25 @@ def test_oracle_newton2_reproduces_reference():
         y = O.predict(float(g["sigma2"]), g["landmarks"], Wb, x[:me], x[me], 0, g["grid"])
         assert O.rel_l2(y, g["yhat"][j]) <= 1e-9
         np.testing.assert_allclose(tr.norms, g[f"norms_{j}"], rtol=1e-6)
+
+
+def _lev_cases():
+    g = load_golden("leverage")
+    return g, [str(c) for c in g["cases"]]
+
+
+def test_oracle_leverage_reproduces_reference():
+    """Exact leverage scores and the seeded draw (nystrom.py:58-103)."""
+    g, cases = _lev_cases()
+    for c in cases:
+        grid = g[f"{c}_grid"]
+        if grid.size > 1000:          # the 4000-point solve is checked on the GPU side
+            continue
+        s2 = float(g[f"{c}_sigma2"])
+        if not bool(g[f"{c}_explicit_kernel"]):
+            assert s2 == O.leverage_default_sigma2(grid)
+        sc = O.leverage_scores(s2, grid, float(g[f"{c}_ridge"]))
+        np.testing.assert_allclose(sc, g[f"{c}_scores"], rtol=1e-12, atol=0)
+        for sd in g[f"{c}_seeds"]:
+            idx = O.leverage_landmarks(sc, int(sd), int(g[f"{c}_m"]))
+            np.testing.assert_array_equal(grid[idx], g[f"{c}_lm{int(sd)}"])
