@@ -260,6 +260,33 @@ size_t nys_leverage_workspace_bytes(int n);
 int nys_leverage_scores_f64(const double* grid, int n, double sigma2, double ridge, double* scores,
                             int* info, void* ws, size_t ws_bytes, void* stream);
 
+/* Sketch branch of ridge_leverage_scores (nystrom.py:71-80, n > 4000), in two
+ * calls so the host can size the second from the rank of the first:
+ *   nys_pchol_rbf_f64: pivoted Cholesky W ~ G G^T of the c x c sketch kernel
+ *     matrix W = K(x, x) (x = grid[idx] from the host, nystrom.py:72-74), stopped
+ *     when the largest remaining diagonal is <= tol or after cap columns;
+ *     G is cap x c (row k = column k of the factor); out[0] = rank r,
+ *     out[1] = 1 if it converged before cap.
+ *   nys_leverage_sketch_f64: eigh of G^T G (r <= 256) with the reference's
+ *     keep rule vals > 1e-12 vals.max() (:75-76), A = C V_k / sqrt(vals_k)
+ *     (:77), scores = diag(A (A^T A + n ridge I)^-1 A^T) (:78-79) clipped at
+ *     1e-300; info[0] = NYS_INFO_SINGULAR if the r x r system is not SPD. */
+int nys_pchol_rbf_f64(const double* x, int c, double sigma2, double tol, int cap, double* G,
+                      int* out, void* stream);
+size_t nys_leverage_sketch_workspace_bytes(int n, int c, int r);
+int nys_leverage_sketch_f64(const double* grid, int n, const double* x, int c, double sigma2,
+                            double ridge, const double* G, int r, double* scores, int* info,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Dense symmetric eigendecomposition of an explicit n x n matrix (n <= 256,
+ * divide and conquer as nys_landmark_eig_f64): eigenvalues descending,
+ * eigvecs[i*n + k] = V[i][k], W[:, k] = V[:, k] / sqrt(s_k) for the kept
+ * s_k > drop_tol * s_0, m_eff = number kept. */
+size_t nys_sym_eig_workspace_bytes(int n);
+int nys_sym_eig_f64(const double* A, int n, double drop_tol, double* eigvals, double* eigvecs,
+                    double* W, int* m_eff, int* info, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
 #ifdef __cplusplus
 }
 #endif

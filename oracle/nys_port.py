@@ -70,17 +70,27 @@ LEVERAGE_EXACT_LIMIT = 4000  # nystrom.py:25
 
 
 def leverage_scores(sigma2: float, grid, ridge: float) -> np.ndarray:
-    """Exact ridge leverage scores (nystrom.py:58-70, n <= 4000 branch).
+    """Ridge leverage scores (nystrom.py:58-81).
 
-    diag of solve(Omega + n ridge I, Omega), clipped below at 1e-300 (:81).
+    n <= 4000: diag of solve(Omega + n ridge I, Omega); otherwise the uniform
+    column sketch of :71-80.  Clipped below at 1e-300 (:81).
     """
     grid = np.asarray(grid, dtype=float)
     n = grid.size
-    if n > LEVERAGE_EXACT_LIMIT:
-        raise OracleError("sketch branch (nystrom.py:71-80) not restated")
-    omega = rbf_block(sigma2, 0, grid, grid)
-    res = np.linalg.solve(omega + n * ridge * np.eye(n), omega)
-    return np.clip(np.diagonal(res).copy(), 1e-300, None)
+    if n <= LEVERAGE_EXACT_LIMIT:
+        omega = rbf_block(sigma2, 0, grid, grid)
+        res = np.linalg.solve(omega + n * ridge * np.eye(n), omega)
+        return np.clip(np.diagonal(res).copy(), 1e-300, None)
+    # uniform column sketch (nystrom.py:71-80)
+    c = LEVERAGE_EXACT_LIMIT // 2
+    idx = np.linspace(0, n - 1, c).round().astype(int)
+    C = rbf_block(sigma2, 0, grid, grid[idx])
+    W = C[idx, :]
+    vals, vecs = np.linalg.eigh((W + W.T) / 2.0)
+    keep = vals > vals.max() * 1e-12
+    A = C @ (vecs[:, keep] / np.sqrt(vals[keep]))
+    inner = np.linalg.solve(A.T @ A + n * ridge * np.eye(A.shape[1]), A.T)
+    return np.clip(np.einsum("ij,ji->i", A, inner), 1e-300, None)
 
 
 def leverage_landmarks(scores: np.ndarray, seed: int, m: int) -> np.ndarray:

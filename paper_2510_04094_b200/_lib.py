@@ -69,6 +69,11 @@ SIGNATURES = {
                                   _vp, _i, _vp, _i, _vp]),
     "nys_leverage_workspace_bytes": (_sz, [_i]),
     "nys_leverage_scores_f64": (_i, [_vp, _i, _d, _d, _vp, _vp, _vp, _sz, _vp]),
+    "nys_pchol_rbf_f64": (_i, [_vp, _i, _d, _d, _i, _vp, _vp, _vp]),
+    "nys_leverage_sketch_workspace_bytes": (_sz, [_i, _i, _i]),
+    "nys_leverage_sketch_f64": (_i, [_vp, _i, _vp, _i, _d, _d, _vp, _i, _vp, _vp, _vp, _sz, _vp]),
+    "nys_sym_eig_workspace_bytes": (_sz, [_i]),
+    "nys_sym_eig_f64": (_i, [_vp, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _i, _vp, _i, _i, _vp]),
 }

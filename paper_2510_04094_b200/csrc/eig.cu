@@ -26,9 +26,9 @@ namespace nys_host {
 size_t dc_buffer_bytes(int n);
 bool dc_fits(int n);
 bool dc_uses_smem(int n);
-int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, double* eigvals,
-                  double* eigvecs, double* W, int* m_eff, int* info, void* ws, size_t ws_bytes,
-                  cudaStream_t st);
+int launch_dc_eig(const double* lm, const double* Ain, int n, double sigma2, double drop_tol,
+                  double* eigvals, double* eigvecs, double* W, int* m_eff, int* info, void* ws,
+                  size_t ws_bytes, cudaStream_t st);
 bool jacobi_small_fits(int m);
 int launch_jacobi_small(const double* lm, int m, double sigma2, double drop_tol, double* eigvals,
                         double* eigvecs, double* W, int* m_eff, int* info, cudaStream_t st);
@@ -346,7 +346,7 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
     return nys_host::launch_jacobi_small(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W,
                                          m_eff, info, static_cast<cudaStream_t>(stream));
   if (!force_ql && !force_jac && nys_host::dc_fits(m))
-    return nys_host::launch_dc_eig(landmarks, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff,
+    return nys_host::launch_dc_eig(landmarks, nullptr, m, sigma2, drop_tol, eigvals, eigvecs, W, m_eff,
                                    info, workspace, workspace_bytes,
                                    static_cast<cudaStream_t>(stream));
   const size_t need = eig_storage_bytes(m);
@@ -370,4 +370,18 @@ extern "C" int nys_landmark_eig_f64(const double* landmarks, int m, double sigma
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
+}
+
+extern "C" size_t nys_sym_eig_workspace_bytes(int n) {
+  if (!nys_host::dc_fits(n)) return 0;
+  return nys_host::dc_uses_smem(n) ? 0 : nys_host::dc_buffer_bytes(n);
+}
+
+extern "C" int nys_sym_eig_f64(const double* A, int n, double drop_tol, double* eigvals,
+                               double* eigvecs, double* W, int* m_eff, int* info, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (A == nullptr || !(drop_tol >= 0.0 && drop_tol < 1.0)) return NYS_EINVAL;
+  if (!nys_host::dc_fits(n)) return NYS_EUNSUPPORTED;
+  return nys_host::launch_dc_eig(nullptr, A, n, 1.0, drop_tol, eigvals, eigvecs, W, m_eff, info,
+                                 workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }

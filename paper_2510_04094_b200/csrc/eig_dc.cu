@@ -444,7 +444,8 @@ NYS_DEV void tridiag_blocked(double* __restrict__ A, int ld, int n, SharedT& S, 
 // lane in the rank-2 update (ceil(n / 32) bound)
 template <bool kSmem, int kT>
 __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
-    dc_eig_kernel(const double* __restrict__ lm, int n, double sigma2, double drop_tol,
+    dc_eig_kernel(const double* __restrict__ lm, const double* __restrict__ Ain, int n,
+                  double sigma2, double drop_tol,
                   double* __restrict__ eigvals, double* __restrict__ eigvecs,
                   double* __restrict__ Wout, int* __restrict__ m_eff_out, int* __restrict__ info,
                   double* __restrict__ gbuf, int use_smem, int debug) {
@@ -464,6 +465,10 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   __syncthreads();
   for (int e = tid; e < n * n; e += nt) {
     const int i = e / n, j = e % n;
+    if (Ain != nullptr) {          // explicit symmetric input (nys_sym_eig_f64)
+      A[(size_t)i * ld + j] = Ain[e];
+      continue;
+    }
     const double d = lm[i] - lm[j];
     A[(size_t)i * ld + j] = nys::rbf(d, sigma2);
     if (i != j && fabs(d) <= 1e-12) S.degenerate = 1;
@@ -1132,9 +1137,9 @@ size_t dc_buffer_bytes(int n) {
 bool dc_fits(int n) { return n >= 1 && n <= kDcMaxN; }
 bool dc_uses_smem(int n) { return dc_buffer_bytes(n) <= 150 * 1024; }
 
-int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, double* eigvals,
-                  double* eigvecs, double* W, int* m_eff, int* info, void* ws, size_t ws_bytes,
-                  cudaStream_t st) {
+int launch_dc_eig(const double* lm, const double* Ain, int n, double sigma2, double drop_tol,
+                  double* eigvals, double* eigvecs, double* W, int* m_eff, int* info, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
   const size_t need = dc_buffer_bytes(n);
   const int use_smem = dc_uses_smem(n);
   size_t dyn = 0;
@@ -1148,7 +1153,7 @@ int launch_dc_eig(const double* lm, int n, double sigma2, double drop_tol, doubl
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)dyn);
     if (e != cudaSuccess) return record_cuda(e);
-    kern<<<1, threads, dyn, st>>>(lm, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
+    kern<<<1, threads, dyn, st>>>(lm, Ain, n, sigma2, drop_tol, eigvals, eigvecs, W, m_eff, info,
                                   static_cast<double*>(ws), use_smem, dbg);
     return NYS_OK;
   };

@@ -418,6 +418,37 @@ __global__ void lev_finalize_kernel(const double* __restrict__ part, int n, int 
   scores[col] = s > 1e-300 ? s : 1e-300;
 }
 
+// Right-looking tile sweep over the assembled lower tiles At (B = I): leaves
+// X = L^-1 in Bt.  Returns the number of launches.
+int tile_sweep(double* At, double* Bt, int nt, int* info, cudaStream_t st) {
+  static bool attr_done = false;
+  const int pair_smem = 2 * kTT * (int)sizeof(double);
+  if (!attr_done) {
+    cudaFuncSetAttribute(lev_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
+    cudaFuncSetAttribute(lev_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
+    cudaFuncSetAttribute(lev_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
+    attr_done = true;
+  }
+  int launches = 0;
+  // diagonal tile 0 alone; tile k+1 is factored inside the update of step k
+  lev_diag_kernel<<<1, kThreads, pair_smem, st>>>(At, Bt, 0, info);
+  ++launches;
+  for (int k = 0; k < nt; ++k) {
+    const int m = nt - k - 1;
+    const int npanel = m + k;
+    if (npanel > 0) {
+      lev_panel_kernel<<<npanel, kThreads, pair_smem, st>>>(At, Bt, k, nt);
+      ++launches;
+    }
+    const int nupd = m * (m + 1) / 2 + m * (k + 1);
+    if (nupd > 0) {
+      lev_update_kernel<<<nupd, kThreads, pair_smem, st>>>(At, Bt, k, nt, info);
+      ++launches;
+    }
+  }
+  return launches;
+}
+
 struct LevLayout {
   int nt;
   size_t ntl;
@@ -432,6 +463,293 @@ struct LevLayout {
   }
 };
 
+
+// ---- sketch branch (nystrom.py:71-80, n > 4000) -------------------------------
+// The reference eigendecomposes the c x c sketch W = K(x, x) (x = grid[idx],
+// c = 2000) and keeps vals > 1e-12 vals.max().  The kept spectrum is the
+// numerical range of W, so W is compressed first by a pivoted Cholesky
+// W ~ G G^T (stopped when the largest remaining diagonal falls below 1e-15,
+// far under the 1e-12 relative cut), and the small r x r problem G^T G = U M U^T
+// (same nonzero spectrum, eigenvectors v = G u / sqrt(mu)) goes to the
+// divide-and-conquer eigensolver.  With T = G U_k M_k^-1:
+//   A = C T (n x k, C = K(grid, x)),   scores_i = a_i^T (A^T A + n ridge I)^-1 a_i
+// the latter from the same tile Cholesky + inverse sweep: ||L^-1 a_i||^2.
+constexpr int kPcThreads = 1024;
+
+__global__ void __launch_bounds__(kPcThreads)
+    lev_pchol_kernel(const double* __restrict__ x, int c, double sigma2, double tol, int cap,
+                     double* __restrict__ G, int* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];
+  double* d = sm;          // remaining diagonal
+  double* xs = sm + c;     // sketch points
+  __shared__ double rv[32];
+  __shared__ int ri[32];
+  __shared__ int s_p;
+  __shared__ double s_dp;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < c; i += kPcThreads) {
+    d[i] = 1.0;            // rbf(0) = exp(-0) = 1
+    xs[i] = x[i];
+  }
+  __syncthreads();
+  int k = 0;
+  bool converged = false;
+  for (; k < cap; ++k) {
+    // argmax of the remaining diagonal, first index on ties
+    double bv = -1.0;
+    int bi = 0;
+    for (int i = tid; i < c; i += kPcThreads)
+      if (d[i] > bv) {
+        bv = d[i];
+        bi = i;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      rv[w] = bv;
+      ri[w] = bi;
+    }
+    __syncthreads();
+    if (w == 0) {
+      bv = rv[lane];
+      bi = ri[lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        s_p = bi;
+        s_dp = bv;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    const double dp = s_dp;
+    if (!(dp > tol)) {
+      converged = true;
+      break;
+    }
+    const double inv = 1.0 / sqrt(dp);
+    const double xp = xs[p];
+    double* gk = G + (size_t)k * c;
+    for (int i = tid; i < c; i += kPcThreads) {
+      double g0 = rbf(xs[i] - xp, sigma2), g1 = 0.0;
+      int kk = 0;
+      for (; kk + 1 < k; kk += 2) {
+        g0 = fma(-G[(size_t)kk * c + i], G[(size_t)kk * c + p], g0);
+        g1 = fma(-G[(size_t)(kk + 1) * c + i], G[(size_t)(kk + 1) * c + p], g1);
+      }
+      if (kk < k) g0 = fma(-G[(size_t)kk * c + i], G[(size_t)kk * c + p], g0);
+      const double g = (g0 + g1) * inv;
+      gk[i] = g;
+      d[i] = (i == p) ? 0.0 : d[i] - g * g;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    out[0] = k;
+    out[1] = converged ? 1 : 0;
+  }
+}
+
+// H = G^T G (r x r), one warp per lower entry, mirrored
+__global__ void lev_gtg_kernel(const double* __restrict__ G, int c, int r, double* __restrict__ H) {
+  const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pair >= r * (r + 1) / 2) return;
+  int a = (int)((sqrt(8.0 * pair + 1.0) - 1.0) * 0.5);
+  while (a * (a + 1) / 2 > pair) --a;
+  while ((a + 1) * (a + 2) / 2 <= pair) ++a;
+  const int b = pair - a * (a + 1) / 2;
+  const double* ga = G + (size_t)a * c;
+  const double* gb = G + (size_t)b * c;
+  double s = 0.0;
+  for (int i = lane; i < c; i += 32) s = fma(ga[i], gb[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    H[(size_t)a * r + b] = s;
+    H[(size_t)b * r + a] = s;
+  }
+}
+
+// T[j][l] = (sum_a G[a][j] U[a][l]) / mu[l] for l < k_eff   (T: c x r, row-major)
+__global__ void lev_sketch_T_kernel(const double* __restrict__ G, int c, int r,
+                                    const double* __restrict__ U, const double* __restrict__ mu,
+                                    const int* __restrict__ meta, double* __restrict__ T) {
+  const int l = blockIdx.y;
+  if (l >= meta[0]) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= c) return;
+  double s = 0.0;
+  for (int a = 0; a < r; ++a) s = fma(G[(size_t)a * c + j], U[(size_t)a * r + l], s);
+  T[(size_t)j * r + l] = s / mu[l];
+}
+
+// A[l][i] = sum_j rbf(grid_i - x_j) T[j][l]   (A: r x n, l < k_eff)
+// block: 64 rows i x 32 columns l, j streamed through shared memory in chunks
+__global__ void __launch_bounds__(256)
+    lev_sketch_A_kernel(const double* __restrict__ grid, int n, const double* __restrict__ x,
+                        int c, double sigma2, const double* __restrict__ T, int r,
+                        const int* __restrict__ meta, double* __restrict__ A) {
+  constexpr int kI = 64, kL = 32, kJ = 48;
+  __shared__ double Cs[kJ][kI + 1];
+  __shared__ double Ts[kJ][kL];
+  const int keff = meta[0];
+  const int i0 = blockIdx.x * kI, l0 = blockIdx.y * kL;
+  if (l0 >= keff) return;
+  const int t = threadIdx.x;
+  const int ii = t & 63, lg = t >> 6;      // row, group of 8 columns
+  const double gi = (i0 + ii < n) ? grid[i0 + ii] : 0.0;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  for (int j0 = 0; j0 < c; j0 += kJ) {
+    __syncthreads();
+    for (int e = t; e < kJ * kI; e += 256) {
+      const int jj = e / kI, iq = e % kI;
+      const int j = j0 + jj;
+      const double g = (i0 + iq < n) ? grid[i0 + iq] : 0.0;
+      Cs[jj][iq] = (j < c) ? rbf(g - x[j], sigma2) : 0.0;
+    }
+    for (int e = t; e < kJ * kL; e += 256) {
+      const int jj = e / kL, lq = e % kL;
+      const int j = j0 + jj, l = l0 + lq;
+      Ts[jj][lq] = (j < c && l < keff) ? T[(size_t)j * r + l] : 0.0;
+    }
+    __syncthreads();
+    (void)gi;
+#pragma unroll 4
+    for (int jj = 0; jj < kJ; ++jj) {
+      const double cv = Cs[jj][ii];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fma(cv, Ts[jj][lg * 8 + q], acc[q]);
+    }
+  }
+  if (i0 + ii < n) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int l = l0 + lg * 8 + q;
+      if (l < keff) A[(size_t)l * n + i0 + ii] = acc[q];
+    }
+  }
+}
+
+// lower tiles of M = A^T A + cI on the k_eff block, identity padding; B = I
+__global__ void lev_sketch_M_kernel(const double* __restrict__ A, int n, double cdiag,
+                                    const int* __restrict__ meta, double* __restrict__ At,
+                                    double* __restrict__ Bt) {
+  const int keff = meta[0];
+  const int ti = blockIdx.y, tj = blockIdx.z;
+  if (tj > ti) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // blockIdx.x covers the 4096 entries of the tile, 8 per block (one per warp)
+  const int e = blockIdx.x * 8 + w;
+  const int rr = e >> 6, cc = e & 63;
+  const int a = ti * kT + rr, b = tj * kT + cc;
+  double v;
+  if (a < keff && b < keff) {
+    const double* pa = A + (size_t)a * n;
+    const double* pb = A + (size_t)b * n;
+    double s0 = 0.0, s1 = 0.0;
+    int i = lane;
+    for (; i + 32 < n; i += 64) {
+      s0 = fma(pa[i], pb[i], s0);
+      s1 = fma(pa[i + 32], pb[i + 32], s1);
+    }
+    if (i < n) s0 = fma(pa[i], pb[i], s0);
+    double s = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    v = (a == b) ? s + cdiag : s;
+  } else {
+    v = (a == b) ? 1.0 : 0.0;
+  }
+  if (lane == 0) {
+    At[tile_off(ti, tj) + sw(rr, cc)] = v;
+    Bt[tile_off(ti, tj) + sw(rr, cc)] = (a == b) ? 1.0 : 0.0;
+  }
+}
+
+// scores_i = sum_{l < k} (sum_{j <= l} X[l][j] A[j][i])^2, clipped at 1e-300.
+// Block: 64 rows i x 4 interleaved l-sets; A rows staged in shared memory.
+__global__ void __launch_bounds__(256)
+    lev_sketch_scores_kernel(const double* __restrict__ A, int n, const double* __restrict__ Bt,
+                             const int* __restrict__ meta, double* __restrict__ scores) {
+  extern __shared__ __align__(16) double As[];     // [keff][64]
+  __shared__ double red[4][64];
+  const int keff = meta[0];
+  const int i0 = blockIdx.x * 64;
+  const int t = threadIdx.x, ii = t & 63, ls = t >> 6;
+  for (int e = t; e < keff * 64; e += 256) {
+    const int j = e >> 6, q = e & 63;
+    As[e] = (i0 + q < n) ? A[(size_t)j * n + i0 + q] : 0.0;
+  }
+  __syncthreads();
+  double s = 0.0;
+  for (int l = ls; l < keff; l += 4) {
+    const double* xl = Bt + tile_off(l / kT, 0);
+    double y0 = 0.0, y1 = 0.0;
+    int j = 0;
+    for (; j + 1 <= l; j += 2) {
+      y0 = fma(Bt[tile_off(l / kT, j / kT) + sw(l % kT, j % kT)], As[j * 64 + ii], y0);
+      y1 = fma(Bt[tile_off(l / kT, (j + 1) / kT) + sw(l % kT, (j + 1) % kT)],
+               As[(j + 1) * 64 + ii], y1);
+    }
+    if (j <= l) y0 = fma(Bt[tile_off(l / kT, j / kT) + sw(l % kT, j % kT)], As[j * 64 + ii], y0);
+    (void)xl;
+    const double y = y0 + y1;
+    s = fma(y, y, s);
+  }
+  red[ls][ii] = s;
+  __syncthreads();
+  if (ls == 0 && i0 + ii < n) {
+    const double v = ((red[0][ii] + red[1][ii]) + red[2][ii]) + red[3][ii];
+    scores[i0 + ii] = v > 1e-300 ? v : 1e-300;
+  }
+}
+
+struct SketchLayout {
+  int r, ntk;
+  size_t ntl;
+  size_t off_H, off_mu, off_U, off_W, off_meta, off_eig, off_T, off_A, off_At, off_Bt, total;
+  static SketchLayout make(int n, int c, int r) {
+    SketchLayout L{};
+    L.r = r;
+    L.ntk = (r + kT - 1) / kT;
+    L.ntl = (size_t)L.ntk * (L.ntk + 1) / 2;
+    size_t o = 0;
+    auto take = [&](size_t doubles) {
+      size_t at = o;
+      o += (doubles + 15) / 16 * 16;
+      return at;
+    };
+    L.off_H = take((size_t)r * r);
+    L.off_mu = take(r);
+    L.off_U = take((size_t)r * r);
+    L.off_W = take((size_t)r * r);
+    L.off_meta = take(2);
+    L.off_eig = take(nys_sym_eig_workspace_bytes(r) / sizeof(double) + 1);
+    L.off_T = take((size_t)c * r);
+    L.off_A = take((size_t)r * n);
+    L.off_At = take(L.ntl * kTT);
+    L.off_Bt = take(L.ntl * kTT);
+    L.total = o * sizeof(double) + 256;
+    return L;
+  }
+};
 }  // namespace
 
 extern "C" size_t nys_leverage_workspace_bytes(int n) {
@@ -453,38 +771,85 @@ extern "C" int nys_leverage_scores_f64(const double* grid, int n, double sigma2,
   // n * ridge * np.eye(n) (nystrom.py:66): float(n) * ridge
   const double c = (double)n * ridge;
   const int nt = L.nt;
-  static bool attr_done = false;
-  const int pair_smem = 2 * kTT * (int)sizeof(double);
-  if (!attr_done) {
-    cudaFuncSetAttribute(lev_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
-    cudaFuncSetAttribute(lev_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
-    cudaFuncSetAttribute(lev_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
-    attr_done = true;
-  }
   int launches = 0;
   lev_assemble_kernel<<<dim3(nt, nt), 256, 0, st>>>(grid, n, sigma2, c, At, Bt, info);
   ++launches;
   NYS_CHECK_LAUNCH();
-  // diagonal tile 0 alone; tile k+1 is factored inside the update of step k
-  lev_diag_kernel<<<1, kThreads, pair_smem, st>>>(At, Bt, 0, info);
-  ++launches;
-  for (int k = 0; k < nt; ++k) {
-    const int m = nt - k - 1;
-    const int npanel = m + k;
-    if (npanel > 0) {
-      lev_panel_kernel<<<npanel, kThreads, pair_smem, st>>>(At, Bt, k, nt);
-      ++launches;
-    }
-    const int nupd = m * (m + 1) / 2 + m * (k + 1);
-    if (nupd > 0) {
-      lev_update_kernel<<<nupd, kThreads, pair_smem, st>>>(At, Bt, k, nt, info);
-      ++launches;
-    }
-  }
+  launches += tile_sweep(At, Bt, nt, info, st);
   NYS_CHECK_LAUNCH();
   lev_colnorm_kernel<<<dim3(nt, nt), 256, 0, st>>>(Bt, nt, part);
   lev_finalize_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, n, nt, c, scores);
   launches += 2;
+  nys_host::count_launches(launches);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" int nys_pchol_rbf_f64(const double* x, int c, double sigma2, double tol, int cap,
+                                 double* G, int* out, void* stream) {
+  if (c < 1 || c > 8192 || cap < 1 || !(sigma2 > 0.0) || !(tol >= 0.0)) return NYS_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int smem = 2 * c * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(lev_pchol_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return nys_host::record_cuda(e);
+  lev_pchol_kernel<<<1, kPcThreads, smem, st>>>(x, c, sigma2, tol, cap, G, out);
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" size_t nys_leverage_sketch_workspace_bytes(int n, int c, int r) {
+  if (n < 1 || c < 1 || r < 1) return 0;
+  return SketchLayout::make(n, c, r).total;
+}
+
+extern "C" int nys_leverage_sketch_f64(const double* grid, int n, const double* x, int c,
+                                       double sigma2, double ridge, const double* G, int r,
+                                       double* scores, int* info, void* ws, size_t ws_bytes,
+                                       void* stream) {
+  if (n < 1 || c < 1 || r < 1 || !(sigma2 > 0.0) || !(ridge >= 0.0)) return NYS_EINVAL;
+  if (r > 256) return NYS_EUNSUPPORTED;
+  const SketchLayout L = SketchLayout::make(n, c, r);
+  if (ws == nullptr || ws_bytes < L.total) return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* base = reinterpret_cast<double*>((reinterpret_cast<size_t>(ws) + 127) & ~(size_t)127);
+  double* H = base + L.off_H;
+  double* mu = base + L.off_mu;
+  double* U = base + L.off_U;
+  double* Wd = base + L.off_W;
+  int* meta = reinterpret_cast<int*>(base + L.off_meta);   // k_eff, eig info
+  double* T = base + L.off_T;
+  double* A = base + L.off_A;
+  double* At = base + L.off_At;
+  double* Bt = base + L.off_Bt;
+  int launches = 0;
+  const int npairs = r * (r + 1) / 2;
+  lev_gtg_kernel<<<(npairs + 7) / 8, 256, 0, st>>>(G, c, r, H);
+  ++launches;
+  NYS_CHECK_LAUNCH();
+  // keep = vals > vals.max() * 1e-12 (nystrom.py:76): the eigensolver's drop rule
+  int rc = nys_sym_eig_f64(H, r, 1e-12, mu, U, Wd, meta, meta + 1, base + L.off_eig,
+                           nys_sym_eig_workspace_bytes(r), stream);
+  if (rc != NYS_OK) return rc;
+  lev_sketch_T_kernel<<<dim3((c + 127) / 128, r), 128, 0, st>>>(G, c, r, U, mu, meta, T);
+  lev_sketch_A_kernel<<<dim3((n + 63) / 64, (r + 31) / 32), 256, 0, st>>>(grid, n, x, c, sigma2, T,
+                                                                          r, meta, A);
+  // n * ridge * np.eye(A.shape[1]) (nystrom.py:78)
+  lev_sketch_M_kernel<<<dim3(kTT / 8, L.ntk, L.ntk), 256, 0, st>>>(A, n, (double)n * ridge, meta,
+                                                                   At, Bt);
+  launches += 3;
+  NYS_CHECK_LAUNCH();
+  cudaMemsetAsync(info, 0, sizeof(int), st);
+  launches += tile_sweep(At, Bt, L.ntk, info, st);
+  const int smem = r * 64 * (int)sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(lev_sketch_scores_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+  }
+  lev_sketch_scores_kernel<<<(n + 63) / 64, 256, smem, st>>>(A, n, Bt, meta, scores);
+  ++launches;
   nys_host::count_launches(launches);
   NYS_CHECK_LAUNCH();
   return NYS_OK;

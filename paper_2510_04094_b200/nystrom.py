@@ -78,32 +78,57 @@ def select_landmarks(strategy, grid, m: int) -> np.ndarray:
     return grid[idx]
 
 
+_SKETCH_PCHOL_TOL = 1e-15    # stop of the sketch compression (diag of W is 1)
+_SKETCH_MAX_RANK = 256       # r x r eigensolver limit (divide and conquer)
+
+
 def ridge_leverage_scores(k: RbfKernel, grid, ridge: float, device=None) -> np.ndarray:
     """diag(Omega (Omega + n ridge I)^-1) over the grid (nystrom.py:58-81).
 
-    The exact branch (n <= 4000) runs on the device as 1 - n ridge diag(A^-1)
-    from one tiled DMMA Cholesky + inverse sweep (csrc/leverage.cu).  The
-    reference's uniform-sketch branch for larger grids (nystrom.py:71-80) needs
-    a 2000 x 2000 eigendecomposition and is not served yet: it raises
-    ``NotImplementedError`` rather than falling back to the host.
+    Exact branch (n <= 4000): 1 - n ridge diag(A^-1) from one tiled DMMA
+    Cholesky + inverse sweep on the device (``nys_leverage_scores_f64``).
+    Sketch branch (n > 4000, nystrom.py:71-80): the same column sketch
+    (c = 2000 points idx = linspace(0, n-1, c).round(), chosen on the host as
+    the reference does); the sketch matrix is compressed on the device by a
+    pivoted Cholesky and its kept spectrum (vals > 1e-12 vals.max()) taken from
+    the small G^T G eigenproblem (``nys_pchol_rbf_f64`` +
+    ``nys_leverage_sketch_f64``).  A sketch whose numerical rank exceeds 256
+    raises ``NotImplementedError`` instead of falling back to the host.
     """
     grid = np.asarray(grid, dtype=float).reshape(-1)
     n = grid.size
-    if n > _LEVERAGE_EXACT_LIMIT:
-        raise NotImplementedError(
-            f"leverage scores for n={n} > {_LEVERAGE_EXACT_LIMIT} use the reference's "
-            "sketch branch (nystrom.py:71-80), not built for the device yet")
     lib, torch = _lib.require_device()
     device = torch.device(device or "cuda")
     d_grid = _lib.as_f64(grid, device)
     scores = torch.empty(n, dtype=torch.float64, device=device)
     info = torch.zeros(1, dtype=torch.int32, device=device)
-    wsb = lib.nys_leverage_workspace_bytes(n)
-    ws = _lib.WORKSPACE.get(wsb, device)
-    _lib.call("nys_leverage_scores_f64", _lib.ptr(d_grid), n, float(k.sigma2), float(ridge),
-              _lib.ptr(scores), _lib.ptr(info), _lib.ptr(ws), wsb, _lib.stream_ptr())
+    st = _lib.stream_ptr()
+    if n <= _LEVERAGE_EXACT_LIMIT:
+        wsb = lib.nys_leverage_workspace_bytes(n)
+        ws = _lib.WORKSPACE.get(wsb, device)
+        _lib.call("nys_leverage_scores_f64", _lib.ptr(d_grid), n, float(k.sigma2), float(ridge),
+                  _lib.ptr(scores), _lib.ptr(info), _lib.ptr(ws), wsb, st)
+    else:
+        c = _LEVERAGE_EXACT_LIMIT // 2
+        idx = np.linspace(0, n - 1, c).round().astype(int)      # nystrom.py:72
+        d_x = _lib.as_f64(grid[idx], device)
+        cap = _SKETCH_MAX_RANK
+        G = torch.empty(cap * c, dtype=torch.float64, device=device)
+        out = torch.zeros(2, dtype=torch.int32, device=device)
+        _lib.call("nys_pchol_rbf_f64", _lib.ptr(d_x), c, float(k.sigma2), _SKETCH_PCHOL_TOL,
+                  cap, _lib.ptr(G), _lib.ptr(out), st)
+        r, converged = (int(v) for v in out.cpu())
+        if not converged:
+            raise NotImplementedError(
+                f"sketch kernel matrix has numerical rank > {cap}; the device eigensolver "
+                "for the sketch branch stops there")
+        wsb = lib.nys_leverage_sketch_workspace_bytes(n, c, r)
+        ws = _lib.WORKSPACE.get(wsb, device)
+        _lib.call("nys_leverage_sketch_f64", _lib.ptr(d_grid), n, _lib.ptr(d_x), c,
+                  float(k.sigma2), float(ridge), _lib.ptr(G), r, _lib.ptr(scores),
+                  _lib.ptr(info), _lib.ptr(ws), wsb, st)
     if int(info.item()) != _lib.INFO_OK:
-        raise np.linalg.LinAlgError("Omega + n*ridge*I is not numerically positive definite")
+        raise np.linalg.LinAlgError("leverage system is not numerically positive definite")
     return scores.cpu().numpy()
 
 

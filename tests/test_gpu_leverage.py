@@ -66,6 +66,40 @@ def test_leverage_ragged_sizes_match_solve(n):
     np.testing.assert_allclose(sc, np.clip(ref, 1e-300, None), rtol=1e-9, atol=0)
 
 
-def test_leverage_sketch_branch_not_served():
+def _unused_sketch_not_served():
     with pytest.raises(NotImplementedError):
         N.ridge_leverage_scores(RbfKernel(0.01), np.linspace(0, 1, 4001), 1e-6)
+
+
+SKETCH = ["s4001", "s6000", "s10000", "s8192r"]
+
+
+@pytest.mark.parametrize("case", SKETCH)
+def test_leverage_sketch_branch_matches_reference(case):
+    """n > 4000: device pivoted-Cholesky compression + small eigensolver against
+    the reference's dsyevd sketch.  Yardstick: the reference moves by
+    ``|dsyev - dsyevd|`` (stored) when only its LAPACK driver changes; the device
+    must stay within 1e-8 relative (a few hundred times that yardstick) and draw
+    the same landmarks."""
+    g = load_golden("leverage_sketch")
+    grid = np.linspace(float(g[f"{case}_lo"]), float(g[f"{case}_hi"]), int(g[f"{case}_n"]))
+    k = RbfKernel(float(g[f"{case}_sigma2"]))
+    sc = N.ridge_leverage_scores(k, grid, float(g[f"{case}_ridge"]))
+    ref = g[f"{case}_scores"]
+    self_sens = float(np.max(np.abs(g[f"{case}_scores_dsyev"] / ref - 1)))
+    err = float(np.max(np.abs(sc / ref - 1)))
+    assert self_sens < 1e-9
+    assert err < 1e-8, (err, self_sens)
+    kern = k if bool(g[f"{case}_explicit_kernel"]) else None
+    for sd in g[f"{case}_seeds"]:
+        st = N.LeverageScore(seed=int(sd), ridge=float(g[f"{case}_ridge"]), kernel=kern)
+        lm = N.select_landmarks(st, grid, int(g[f"{case}_m"]))
+        np.testing.assert_array_equal(lm, g[f"{case}_lm{int(sd)}"])
+
+
+def test_leverage_sketch_rank_beyond_eigensolver_fails_loudly():
+    """A sketch kernel much narrower than the grid spacing has numerical rank
+    far above 256: the device path raises instead of falling back."""
+    grid = np.linspace(0.0, 1.0, 5000)
+    with pytest.raises(NotImplementedError):
+        N.ridge_leverage_scores(RbfKernel(1e-7), grid, 1e-6)

@@ -111,3 +111,14 @@ def test_oracle_leverage_reproduces_reference():
         for sd in g[f"{c}_seeds"]:
             idx = O.leverage_landmarks(sc, int(sd), int(g[f"{c}_m"]))
             np.testing.assert_array_equal(grid[idx], g[f"{c}_lm{int(sd)}"])
+
+
+def test_oracle_leverage_sketch_reproduces_reference():
+    """Sketch branch (nystrom.py:71-80) on the smallest golden grid."""
+    g = load_golden("leverage_sketch")
+    c = "s4001"
+    grid = np.linspace(float(g[f"{c}_lo"]), float(g[f"{c}_hi"]), int(g[f"{c}_n"]))
+    sc = O.leverage_scores(float(g[f"{c}_sigma2"]), grid, float(g[f"{c}_ridge"]))
+    np.testing.assert_allclose(sc, g[f"{c}_scores"], rtol=1e-12, atol=0)
+    idx = O.leverage_landmarks(sc, 0, int(g[f"{c}_m"]))
+    np.testing.assert_array_equal(grid[idx], g[f"{c}_lm0"])

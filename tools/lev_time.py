@@ -43,3 +43,21 @@ for n in [int(a) for a in sys.argv[1:]] or [1000, 4000]:
     err = float(np.max(np.abs(sc.cpu().numpy() / ref - 1))) if ref is not None else -1
     print(f"n={n} device {ms:.3f} ms  ({flops / ms / 1e9:.2f} TF/s on 2n^3/3)  cpu {tc*1e3:.1f} ms"
           f"  maxrel {err:.2e} info {int(info.item())}")
+
+# sketch branch timing (n > 4000) through the Python mirror (includes the rank read-back)
+for n in [6000, 10000, 100000]:
+    grid = np.linspace(0.0, 1.0, n)
+    k = RbfKernel(0.01)
+    for _ in range(2):
+        N.ridge_leverage_scores(k, grid, 1e-6)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        N.ridge_leverage_scores(k, grid, 1e-6)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    from oracle import nys_port as O
+    ref = O.leverage_scores(0.01, grid, 1e-6) if n <= 10000 else None
+    tc = time.perf_counter() - t0
+    print(f"sketch n={n}: device+host {dt*1e3:.2f} ms   cpu {tc*1e3:.1f} ms")
