@@ -278,6 +278,25 @@ int nys_leverage_sketch_f64(const double* grid, int n, const double* x, int c, d
                             double ridge, const double* G, int r, double* scores, int* info,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* Large landmark sets (m > 512; the m = n full-feature comparator,
+ * baselines.py:170-194): after nys_pchol_rbf_f64 on the landmarks (Omega ~ G G^T,
+ * rank r <= 256), the kept eigenpairs of G G^T from the r x r problem G^T G:
+ * eigvals [r] descending, eigvecs / W [m x ldv] (columns >= m_eff zero),
+ * drop rule s > max(drop_tol s_0, 0) as nystrom.py:150-154. */
+size_t nys_landmark_eig_compressed_workspace_bytes(int r);
+int nys_landmark_eig_compressed_f64(const double* G, int m, int r, double drop_tol,
+                                    double* eigvals, double* eigvecs, double* W, int ldv,
+                                    int* m_eff, int* info, void* ws, size_t ws_bytes,
+                                    void* stream);
+
+/* Extended Gram E = [D g r]^T [D g r] from explicit feature matrices
+ * psi[(ell * n + i) * m_eff + k] = Psi_ell(pts_i)[k], ell = 0..p (the large-m
+ * path of linear.assemble, linear.py:103-133). */
+size_t nys_explicit_gram_workspace_bytes(int n, int m_eff);
+int nys_explicit_gram_f64(const double* psi, int n, int m_eff, int p, const double* coef,
+                          const double* forcing, double* gram_ext, void* ws, size_t ws_bytes,
+                          void* stream);
+
 /* Dense symmetric eigendecomposition of an explicit n x n matrix (n <= 256,
  * divide and conquer as nys_landmark_eig_f64): eigenvalues descending,
  * eigvecs[i*n + k] = V[i][k], W[:, k] = V[:, k] / sqrt(s_k) for the kept

@@ -60,7 +60,7 @@ class LinearBatchSolver:
         st = _lib.stream_ptr()
         for mu, bc in enumerate(self.cond.entries):
             _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W),
-                      fm.m, fm.m_eff, float(fm.kernel.sigma2), int(bc.order),
+                      fm.ldw, fm.m_eff, float(fm.kernel.sigma2), int(bc.order),
                       _lib.ptr(self.cond_pts) + 8 * mu, 1, _lib.ptr(self.Ac) + 8 * mu * fm.m_eff,
                       fm.m_eff, st)
 
@@ -78,7 +78,7 @@ class LinearBatchSolver:
         info = out_info if out_info is not None else torch.empty(B, dtype=torch.int32,
                                                                  device=fm.device)
         st = _lib.stream_ptr()
-        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.ldw,
                   fm.m_eff, float(fm.kernel.sigma2), self.order, _lib.ptr(self.pts), self.n_c,
                   _lib.ptr(coef), _lib.ptr(forcing), B, None, _lib.ptr(self.ws), ws_bytes, st)
         _lib.call("nys_batch_kkt_solve_f64", _lib.ptr(self.ws), self.n_c, fm.m_eff, self.order,
@@ -93,7 +93,7 @@ class LinearBatchSolver:
         B = int(coef.shape[0])
         ws_bytes = self.lib.nys_batch_gram_workspace_bytes(self.n_c, fm.m_eff, self.order, B)
         E = torch.empty((B, fm.m_eff + 2, fm.m_eff + 2), dtype=torch.float64, device=fm.device)
-        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+        _lib.call("nys_batch_gram_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.ldw,
                   fm.m_eff, float(fm.kernel.sigma2), self.order, _lib.ptr(self.pts), self.n_c,
                   _lib.ptr(coef), _lib.ptr(forcing), B, _lib.ptr(E), _lib.ptr(self.ws), ws_bytes,
                   _lib.stream_ptr())

@@ -152,6 +152,165 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Large landmark sets (m = n full-feature maps): the kTP x m kernel tile no
+// longer fits shared memory, so the landmarks stream through it in chunks of
+// kMC while the Psi tile (kTP x ncols) accumulates in shared memory.  Same
+// outputs as feature_tile_kernel (mode 0 dense, mode 1 packed) and
+// predict_kernel (mode 2).
+constexpr int kMC = 1024;
+__global__ void __launch_bounds__(kFeatThreads)
+    feature_chunked_kernel(const double* __restrict__ lm, int m, const double* __restrict__ W,
+                           int ldw, int m_eff, double sigma2, int ell,
+                           const double* __restrict__ pts, int n_pts, double* __restrict__ out,
+                           int ldo, int mode, int n_blocks, int n_orders, int n_rows_pad,
+                           const double* __restrict__ x, int ldx, int B) {
+  extern __shared__ double sm[];
+  if (mode == 1) ell = blockIdx.y;
+  const int ncols = mode == 1 ? n_blocks * 8 : m_eff;
+  double* kt = sm;                   // [kTP][kMC]
+  double* psi = sm + kTP * kMC;      // [kTP][ncols]
+  nys::Hermite H;
+  H.init(sigma2, ell);
+  const int i0 = blockIdx.x * kTP;
+  for (int e = threadIdx.x; e < kTP * ncols; e += blockDim.x) psi[e] = 0.0;
+  for (int c0 = 0; c0 < m; c0 += kMC) {
+    const int mc = min(kMC, m - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTP * mc; e += blockDim.x) {
+      const int ii = e / mc, s = e % mc, i = i0 + ii;
+      double v = 0.0;
+      if (i < n_pts) {
+        const double d = lm[c0 + s] - pts[i];
+        v = H.poly(ell, d) * nys::rbf(d, sigma2);
+      }
+      kt[ii * kMC + s] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTP * ncols; e += blockDim.x) {
+      const int ii = e / ncols, k = e % ncols;
+      if (k >= m_eff) continue;
+      const double* kr = kt + ii * kMC;
+      const double* wk = W + (size_t)c0 * ldw + k;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int s = 0;
+      for (; s + 3 < mc; s += 4) {
+        a0 = fma(kr[s], wk[(size_t)s * ldw], a0);
+        a1 = fma(kr[s + 1], wk[(size_t)(s + 1) * ldw], a1);
+        a2 = fma(kr[s + 2], wk[(size_t)(s + 2) * ldw], a2);
+        a3 = fma(kr[s + 3], wk[(size_t)(s + 3) * ldw], a3);
+      }
+      for (; s < mc; ++s) a0 = fma(kr[s], wk[(size_t)s * ldw], a0);
+      psi[e] += (a0 + a1) + (a2 + a3);
+    }
+  }
+  __syncthreads();
+  if (mode == 0) {
+    for (int e = threadIdx.x; e < kTP * m_eff; e += blockDim.x) {
+      const int ii = e / m_eff, k = e % m_eff, i = i0 + ii;
+      if (i < n_pts) out[(size_t)i * ldo + k] = psi[e];
+    }
+  } else if (mode == 1) {
+    for (int e = threadIdx.x; e < kTP * ncols; e += blockDim.x) {
+      const int ii = e / ncols, k = e % ncols, i = i0 + ii;
+      double acc = psi[e];
+      if (k == m_eff && ell == 0 && i < n_pts) acc = 1.0;
+      if (i >= n_pts) acc = 0.0;
+      if (i < n_rows_pad) {
+        const int ks = i >> 2, t = i & 3, F = k >> 3, g = k & 7;
+        out[(((size_t)ks * n_orders + ell) * n_blocks + F) * 32 + g * 4 + t] = acc;
+      }
+    }
+  } else {
+    const int b0 = blockIdx.y * blockDim.x;
+    for (int b = b0 + threadIdx.x; b < min(B, b0 + (int)blockDim.x); b += blockDim.x) {
+      const double* xb = x + (size_t)b * ldx;
+      const double bias = ell == 0 ? xb[m_eff] : 0.0;
+      for (int ii = 0; ii < kTP; ++ii) {
+        const int i = i0 + ii;
+        if (i >= n_pts) break;
+        double acc = 0.0;
+        for (int k = 0; k < m_eff; ++k) acc += psi[ii * m_eff + k] * xb[k];
+        out[(size_t)b * ldo + i] = acc + bias;
+      }
+    }
+  }
+}
+
+// kernel tile budget of the single-pass kernels above
+constexpr size_t kTileSmemMax = 200 * 1024;
+
+size_t chunked_smem(int ncols) { return ((size_t)kTP * kMC + (size_t)kTP * ncols) * sizeof(double); }
+
+int launch_chunked(dim3 grid, const double* lm, int m, const double* W, int ldw, int m_eff,
+                   double sigma2, int ell, const double* pts, int n_pts, double* out, int ldo,
+                   int mode, int n_blocks, int n_orders, int n_rows_pad, const double* x, int ldx,
+                   int B, cudaStream_t st) {
+  const size_t sm = chunked_smem(mode == 1 ? n_blocks * 8 : m_eff);
+  cudaError_t e = cudaFuncSetAttribute(feature_chunked_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return nys_host::record_cuda(e);
+  feature_chunked_kernel<<<grid, kFeatThreads, sm, st>>>(lm, m, W, ldw, m_eff, sigma2, ell, pts,
+                                                         n_pts, out, ldo, mode, n_blocks, n_orders,
+                                                         n_rows_pad, x, ldx, B);
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+// Extended Gram from explicit feature matrices (large landmark sets, where
+// the fused kernels cannot hold the landmark tile): D_ext = [D g r] with
+// D = Psi_p - sum_k f_k Psi_{p-k} in the reference's order (linear.py:103-112:
+// each f_k Psi_{p-k} product rounded, then subtracted), g = -f_p, r = forcing;
+// then E = D_ext^T D_ext, one warp per lower entry.
+__global__ void explicit_dext_kernel(const double* __restrict__ psi, int n, int me, int p,
+                                     const double* __restrict__ coef,
+                                     const double* __restrict__ forcing, double* __restrict__ dext) {
+  const int i = blockIdx.x;
+  const int ld = me + 2;
+  for (int k = threadIdx.x; k < ld; k += blockDim.x) {
+    double v;
+    if (k < me) {
+      v = psi[((size_t)p * n + i) * me + k];
+      for (int j = 1; j <= p; ++j) {
+        const double t = __dmul_rn(coef[(size_t)(j - 1) * n + i], psi[((size_t)(p - j) * n + i) * me + k]);
+        v = __dsub_rn(v, t);
+      }
+    } else if (k == me) {
+      v = -coef[(size_t)(p - 1) * n + i];
+    } else {
+      v = forcing[i];
+    }
+    dext[(size_t)k * n + i] = v;     // column-major: coalesced pair dots
+  }
+}
+
+__global__ void explicit_gram_kernel(const double* __restrict__ dext, int n, int ld,
+                                     double* __restrict__ E) {
+  const int pair = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (pair >= ld * (ld + 1) / 2) return;
+  int a = (int)((sqrt(8.0 * pair + 1.0) - 1.0) * 0.5);
+  while (a * (a + 1) / 2 > pair) --a;
+  while ((a + 1) * (a + 2) / 2 <= pair) ++a;
+  const int b = pair - a * (a + 1) / 2;
+  const double* pa = dext + (size_t)a * n;
+  const double* pb = dext + (size_t)b * n;
+  double s0 = 0.0, s1 = 0.0;
+  int i = lane;
+  for (; i + 32 < n; i += 64) {
+    s0 = fma(pa[i], pb[i], s0);
+    s1 = fma(pa[i + 32], pb[i + 32], s1);
+  }
+  if (i < n) s0 = fma(pa[i], pb[i], s0);
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    E[(size_t)a * ld + b] = s;
+    E[(size_t)b * ld + a] = s;
+  }
+}
+
 }  // namespace
 
 namespace nys_host {
@@ -159,6 +318,10 @@ int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff
                     int p, const double* pts, int n_c, int n_blocks, int n_rows_pad,
                     double* packed, cudaStream_t st) {
   size_t sm = (size_t)kTP * m * sizeof(double);
+  if (sm > kTileSmemMax)
+    return launch_chunked(dim3((n_rows_pad + kTP - 1) / kTP, p + 1), lm, m, W, ldw, m_eff, sigma2,
+                          0, pts, n_c, packed, 0, 1, n_blocks, p + 1, n_rows_pad, nullptr, 0, 0,
+                          st);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(feature_tile_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -181,6 +344,10 @@ extern "C" int nys_feature_matrix_f64(const double* landmarks, int m, const doub
     return NYS_EINVAL;
   if (n_pts == 0 || m_eff == 0) return NYS_OK;
   size_t sm = (size_t)kTP * m * sizeof(double);
+  if (sm > kTileSmemMax)
+    return launch_chunked(dim3((n_pts + kTP - 1) / kTP), landmarks, m, W, ldw, m_eff, sigma2, ell,
+                          pts, n_pts, out, ldo, 0, 0, 0, 0, nullptr, 0, 0,
+                          static_cast<cudaStream_t>(stream));
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(feature_tile_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -203,6 +370,10 @@ extern "C" int nys_predict_f64(const double* landmarks, int m, const double* W, 
     return NYS_EINVAL;
   if (n_pts == 0 || B == 0) return NYS_OK;
   size_t sm = (size_t)kTP * (m + m_eff) * sizeof(double);
+  if (sm > kTileSmemMax)
+    return launch_chunked(dim3((n_pts + kTP - 1) / kTP, (B + kFeatThreads - 1) / kFeatThreads),
+                          landmarks, m, W, ldw, m_eff, sigma2, ell, pts, n_pts, out, ldo, 2, 0, 0,
+                          0, x, ldx, B, static_cast<cudaStream_t>(stream));
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(predict_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -229,6 +400,27 @@ extern "C" int nys_ode_residual_f64(const double* landmarks, int m, const double
   ode_residual_kernel<<<(n_c + rows_per_block - 1) / rows_per_block, 256, m * sizeof(double), st>>>(
       landmarks, m, W, ldw, m_eff, sigma2, p, pts, coef, forcing, n_c, x, e);
   nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" size_t nys_explicit_gram_workspace_bytes(int n, int m_eff) {
+  return ((size_t)n * (m_eff + 2)) * sizeof(double) + 256;
+}
+
+extern "C" int nys_explicit_gram_f64(const double* psi, int n, int m_eff, int p,
+                                     const double* coef, const double* forcing, double* gram_ext,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || m_eff < 1 || p < 1 || p > nys::kMaxOrder) return NYS_EINVAL;
+  if (ws == nullptr || ws_bytes < nys_explicit_gram_workspace_bytes(n, m_eff))
+    return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* dext = static_cast<double*>(ws);
+  const int ld = m_eff + 2;
+  if (n > 0) explicit_dext_kernel<<<n, 128, 0, st>>>(psi, n, m_eff, p, coef, forcing, dext);
+  const int npairs = ld * (ld + 1) / 2;
+  explicit_gram_kernel<<<(npairs + 7) / 8, 256, 0, st>>>(dext, n, ld, gram_ext);
+  nys_host::count_launches(n > 0 ? 2 : 1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

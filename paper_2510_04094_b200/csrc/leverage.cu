@@ -721,6 +721,35 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
+// Large landmark sets (m > 512, e.g. the m = n full-feature comparator,
+// baselines.py:170-194): Omega = K(L, L) compressed by the pivoted Cholesky
+// above, Omega ~ G G^T, and the eigenpairs of G G^T taken from G^T G = U M U^T:
+// V[:, k] = G u_k / sqrt(mu_k), W[:, k] = V[:, k] / sqrt(mu_k) = G u_k / mu_k.
+__global__ void lev_vw_kernel(const double* __restrict__ G, int m, int r,
+                              const double* __restrict__ U, const double* __restrict__ mu,
+                              const int* __restrict__ m_eff, int ldv, double* __restrict__ V,
+                              double* __restrict__ W) {
+  const int k = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double v = 0.0, w = 0.0;
+  if (k < *m_eff) {
+    double s0 = 0.0, s1 = 0.0;
+    int a = 0;
+    for (; a + 1 < r; a += 2) {
+      s0 = fma(G[(size_t)a * m + i], U[(size_t)a * r + k], s0);
+      s1 = fma(G[(size_t)(a + 1) * m + i], U[(size_t)(a + 1) * r + k], s1);
+    }
+    if (a < r) s0 = fma(G[(size_t)a * m + i], U[(size_t)a * r + k], s0);
+    const double s = s0 + s1;
+    v = s / sqrt(mu[k]);
+    w = s / mu[k];
+  }
+  V[(size_t)i * ldv + k] = v;
+  W[(size_t)i * ldv + k] = w;
+}
+
 struct SketchLayout {
   int r, ntk;
   size_t ntl;
@@ -851,6 +880,40 @@ extern "C" int nys_leverage_sketch_f64(const double* grid, int n, const double* 
   lev_sketch_scores_kernel<<<(n + 63) / 64, 256, smem, st>>>(A, n, Bt, meta, scores);
   ++launches;
   nys_host::count_launches(launches);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" size_t nys_landmark_eig_compressed_workspace_bytes(int r) {
+  if (r < 1) return 0;
+  return (2 * (size_t)r * r + 16) * sizeof(double) + nys_sym_eig_workspace_bytes(r) + 256;
+}
+
+extern "C" int nys_landmark_eig_compressed_f64(const double* G, int m, int r, double drop_tol,
+                                               double* eigvals, double* eigvecs, double* W,
+                                               int ldv, int* m_eff, int* info, void* ws,
+                                               size_t ws_bytes, void* stream) {
+  if (m < 1 || r < 1 || ldv < r || !(drop_tol >= 0.0 && drop_tol < 1.0)) return NYS_EINVAL;
+  if (r > 256) return NYS_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < nys_landmark_eig_compressed_workspace_bytes(r))
+    return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* base = reinterpret_cast<double*>((reinterpret_cast<size_t>(ws) + 127) & ~(size_t)127);
+  double* H = base;
+  double* U = H + (size_t)r * r;
+  double* eig_ws = U + (size_t)r * r + 16;
+  const int npairs = r * (r + 1) / 2;
+  lev_gtg_kernel<<<(npairs + 7) / 8, 256, 0, st>>>(G, m, r, H);
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  // eigenvalues (descending) and the drop rule s > max(drop_tol s_0, 0) of
+  // nystrom.py:150-154; the r x r W of the small problem goes to H's storage
+  int rc = nys_sym_eig_f64(H, r, drop_tol, eigvals, U, H, m_eff, info, eig_ws,
+                           nys_sym_eig_workspace_bytes(r), stream);
+  if (rc != NYS_OK) return rc;
+  lev_vw_kernel<<<dim3((m + 127) / 128, ldv), 128, 0, st>>>(G, m, r, U, eigvals, m_eff, ldv,
+                                                           eigvecs, W);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -67,7 +67,7 @@ def predict_batch(fmap: NystromFeatureMap, x, ell: int, points):
     x = _lib.as_f64(x, fmap.device)
     B, ldx = x.shape
     out = torch.empty((B, pts.numel()), dtype=torch.float64, device=fmap.device)
-    _lib.call("nys_predict_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W), fmap.m,
+    _lib.call("nys_predict_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W), fmap.ldw,
               fmap.m_eff, float(fmap.kernel.sigma2), int(ell), _lib.ptr(pts), pts.numel(),
               _lib.ptr(x), ldx, B, _lib.ptr(out), pts.numel(), _lib.stream_ptr())
     return out
@@ -100,6 +100,8 @@ def gram_ext_device(fmap: NystromFeatureMap, order: int, pts, coef, forcing,
     n_c = pts.numel()
     row_end = n_c if row_end is None else row_end
     me = fmap.m_eff
+    if "compressed" in fmap._host:
+        return _gram_ext_explicit(fmap, order, pts, coef, forcing, row_begin, row_end)
     if (me + 2 + 7) // 8 > SMALL_NB_MAX and fmap.condition > KSPACE_MAX_COND:
         raise IllConditionedLargeMapError(
             f"m_eff={me} with cond(Omega)={fmap.condition:.2e} > {KSPACE_MAX_COND:.0e}")
@@ -107,9 +109,33 @@ def gram_ext_device(fmap: NystromFeatureMap, order: int, pts, coef, forcing,
     wsb = lib.nys_fused_gram_workspace_bytes(row_end - row_begin, fmap.m, me, order)
     ws = _lib.WORKSPACE.get(wsb, dev)
     _lib.call("nys_fused_gram_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
-              fmap.m, me, float(fmap.kernel.sigma2), int(order), _lib.ptr(pts), _lib.ptr(coef),
+              fmap.ldw, me, float(fmap.kernel.sigma2), int(order), _lib.ptr(pts), _lib.ptr(coef),
               _lib.ptr(forcing), n_c, int(row_begin), int(row_end), _lib.ptr(E), _lib.ptr(ws),
               wsb, _lib.stream_ptr())
+    return E
+
+
+def _gram_ext_explicit(fmap, order, pts, coef, forcing, row_begin, row_end):
+    """Large landmark sets: Psi_0..Psi_p as explicit device matrices (the
+    reference's own per-order feature matrices, linear.py:103-112), then
+    E = [D g r]^T [D g r] (nys_explicit_gram_f64)."""
+    lib, torch = _lib.require_device()
+    dev = fmap.device
+    me = fmap.m_eff
+    n = row_end - row_begin
+    psi = torch.empty((order + 1, max(n, 1), me), dtype=torch.float64, device=dev)
+    st = _lib.stream_ptr()
+    for ell in range(order + 1):
+        _lib.call("nys_feature_matrix_f64", _lib.ptr(fmap.d_landmarks), fmap.m,
+                  _lib.ptr(fmap.d_W), fmap.ldw, me, float(fmap.kernel.sigma2), ell,
+                  _lib.ptr(pts) + 8 * row_begin, n, _lib.ptr(psi[ell]), me, st)
+    c = coef[:, row_begin:row_end].contiguous()
+    f = forcing[row_begin:row_end].contiguous()
+    E = torch.empty((me + 2, me + 2), dtype=torch.float64, device=dev)
+    wsb = lib.nys_explicit_gram_workspace_bytes(n, me)
+    ws = _lib.WORKSPACE.get(wsb, dev)
+    _lib.call("nys_explicit_gram_f64", _lib.ptr(psi), n, me, int(order), _lib.ptr(c), _lib.ptr(f),
+              _lib.ptr(E), _lib.ptr(ws), wsb, st)
     return E
 
 
@@ -249,7 +275,7 @@ def check_kkt(model: PrimalModel, system: AssembledSystem) -> KktReport:
     r = _lib.as_f64(system.r, dev)
     xd = _lib.as_f64(x, dev)
     e = torch.empty(pts.numel(), dtype=torch.float64, device=dev)
-    _lib.call("nys_ode_residual_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.m,
+    _lib.call("nys_ode_residual_f64", _lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.ldw,
               fm.m_eff, float(fm.kernel.sigma2), system.order, _lib.ptr(pts), _lib.ptr(coef),
               _lib.ptr(r), pts.numel(), _lib.ptr(xd), _lib.ptr(e), _lib.stream_ptr())
     return KktReport(linear_residual=lin, rhs_scale=float(np.max(np.abs(rhs))),
@@ -316,11 +342,11 @@ class SingleSolvePipeline:
     def _post(self, fm, pts, coef, forcing):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
         for mu, bc in enumerate(self.cond.entries):   # linear.py:56-63, on the device
-            _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), m,
+            _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw,
                       me, float(fm.kernel.sigma2), int(bc.order), _lib.ptr(self.cond_pts) + 8 * mu,
                       1, _lib.ptr(self.Ac) + 8 * mu * me, me, st)
         n_c = pts.numel()
-        _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), m, me,
+        _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw, me,
                   float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
                   _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
                   self.gws_b, st)

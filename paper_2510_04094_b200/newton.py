@@ -151,7 +151,7 @@ class NewtonBatch:
         pack = "nys_newton_pack" if self.p == 1 else "nys_newton2_pack"
         self.packed = torch.zeros(getattr(lib, pack + "_doubles")(self.me, self.n_c), **f64)
         _lib.call(pack + "_f64", _lib.ptr(fmap.d_landmarks), fmap.m, _lib.ptr(fmap.d_W),
-                  fmap.m, self.me, float(fmap.kernel.sigma2), _lib.ptr(self.pts), self.n_c,
+                  fmap.ldw, self.me, float(fmap.kernel.sigma2), _lib.ptr(self.pts), self.n_c,
                   _lib.ptr(self.packed), st)
         if self.p == 2:   # Psi_2 rows (transposed) for e1 = S2 omega - f and the step
             S2 = fmap.feature_matrix_device(2, self.pts).contiguous()

@@ -79,6 +79,9 @@ def select_landmarks(strategy, grid, m: int) -> np.ndarray:
 
 
 _SKETCH_PCHOL_TOL = 1e-15    # stop of the sketch compression (diag of W is 1)
+DENSE_EIG_MAX_M = 512        # nys_landmark_eig_f64 (D&C <= 256, QL <= 512)
+_LARGE_PCHOL_TOL = 1e-15     # compression stop for large landmark sets
+_LARGE_MAX_RANK = 256
 _SKETCH_MAX_RANK = 256       # r x r eigensolver limit (divide and conquer)
 
 
@@ -151,6 +154,12 @@ class NystromFeatureMap:
         return int(self.landmarks.size)
 
     @property
+    def ldw(self) -> int:
+        """Row stride of d_W (m for the dense eigensolvers, the rank cap for
+        the compressed large-m path)."""
+        return int(self.d_W.shape[1])
+
+    @property
     def eigenvalues(self) -> np.ndarray:
         if "s" not in self._host:
             self._host["s"] = self.d_eigvals[: self.m_eff].cpu().numpy()
@@ -176,7 +185,7 @@ class NystromFeatureMap:
                           self.device).reshape(-1)
         out = torch.empty((pts.numel(), self.m_eff), dtype=torch.float64, device=self.device)
         _lib.call("nys_feature_matrix_f64", _lib.ptr(self.d_landmarks), self.m, _lib.ptr(self.d_W),
-                  self.m, self.m_eff, float(self.kernel.sigma2), int(ell), _lib.ptr(pts),
+                  self.ldw, self.m_eff, float(self.kernel.sigma2), int(ell), _lib.ptr(pts),
                   pts.numel(), _lib.ptr(out), self.m_eff, _lib.stream_ptr())
         return out
 
@@ -222,6 +231,8 @@ def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TO
         raise ValueError(f"drop_tol must lie in [0, 1), got {drop_tol}")
     lib, torch = _lib.require_device()
     m = landmarks.size
+    if m > DENSE_EIG_MAX_M:
+        return _build_compressed(k, landmarks, drop_tol, device)
     if buffers is not None:
         if not np.array_equal(buffers.landmarks, landmarks):
             raise ValueError("EigBuffers hold a different landmark set")
@@ -255,4 +266,48 @@ def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TO
     fm._host["sweeps"] = sweeps
     if buffers is not None:
         fm._host["s"] = buffers.s_h[:m_eff].numpy().copy()
+    return fm
+
+
+def _build_compressed(k: RbfKernel, landmarks: np.ndarray, drop_tol: float, device=None):
+    """Feature map of a large landmark set (m > 512, e.g. the m = n comparator
+    of baselines.py:170-194).
+
+    Omega = K(L, L) is compressed on the device by a pivoted Cholesky
+    (Omega ~ G G^T, stopped when the largest remaining diagonal is below 1e-15),
+    and the eigenpairs of G G^T come from the r x r problem G^T G with the
+    reference's drop rule s > max(drop_tol s_0, 0) (nystrom.py:150-154).  The
+    kept spectrum is the numerical range of Omega; eigenpairs at the rounding
+    floor (s ~ 1e-16 s_0) are noise in the reference's dense dsyevd as well.
+    """
+    if landmarks.size >= 2 and np.min(np.diff(np.sort(landmarks))) <= 1e-12:
+        raise DegenerateLandmarksError("two landmarks coincide within 1e-12")   # nystrom.py:145
+    lib, torch = _lib.require_device()
+    device = torch.device(device or "cuda")
+    m = landmarks.size
+    d_lm = _lib.as_f64(landmarks, device)
+    cap = _LARGE_MAX_RANK
+    G = torch.empty(cap * m, dtype=torch.float64, device=device)
+    out = torch.zeros(2, dtype=torch.int32, device=device)
+    st = _lib.stream_ptr()
+    _lib.call("nys_pchol_rbf_f64", _lib.ptr(d_lm), m, float(k.sigma2), _LARGE_PCHOL_TOL, cap,
+              _lib.ptr(G), _lib.ptr(out), st)
+    r, converged = (int(v) for v in out.cpu())
+    if not converged:
+        raise NotImplementedError(
+            f"landmark kernel matrix (m={m}) has numerical rank > {cap}: beyond the device "
+            "eigensolver of the compressed path")
+    s = torch.empty(r, dtype=torch.float64, device=device)
+    V = torch.zeros((m, r), dtype=torch.float64, device=device)
+    W = torch.zeros((m, r), dtype=torch.float64, device=device)
+    meta = torch.zeros(2, dtype=torch.int32, device=device)
+    wsb = lib.nys_landmark_eig_compressed_workspace_bytes(r)
+    ws = _lib.WORKSPACE.get(wsb, device)
+    _lib.call("nys_landmark_eig_compressed_f64", _lib.ptr(G), m, r, float(drop_tol), _lib.ptr(s),
+              _lib.ptr(V), _lib.ptr(W), r, _lib.ptr(meta), _lib.ptr(meta) + 4, _lib.ptr(ws), wsb,
+              st)
+    m_eff = int(meta[0].item())
+    fm = NystromFeatureMap(kernel=k, landmarks=landmarks, m_eff=m_eff, device=device,
+                           d_landmarks=d_lm, d_W=W, d_eigvals=s, d_eigvecs=V)
+    fm._host["compressed"] = r
     return fm
