@@ -80,7 +80,7 @@ def select_landmarks(strategy, grid, m: int) -> np.ndarray:
 
 _SKETCH_PCHOL_TOL = 1e-15    # stop of the sketch compression (diag of W is 1)
 DENSE_EIG_MAX_M = 512        # nys_landmark_eig_f64 (D&C <= 256, QL <= 512)
-_LARGE_PCHOL_TOL = 1e-15     # compression stop for large landmark sets
+_LARGE_PCHOL_TOL = 1e-16     # compression stop for large landmark sets (diag of Omega is 1)
 _LARGE_MAX_RANK = 256
 _SKETCH_MAX_RANK = 256       # r x r eigensolver limit (divide and conquer)
 
@@ -274,7 +274,7 @@ def _build_compressed(k: RbfKernel, landmarks: np.ndarray, drop_tol: float, devi
     of baselines.py:170-194).
 
     Omega = K(L, L) is compressed on the device by a pivoted Cholesky
-    (Omega ~ G G^T, stopped when the largest remaining diagonal is below 1e-15),
+    (Omega ~ G G^T, stopped when the largest remaining diagonal is below 1e-16),
     and the eigenpairs of G G^T come from the r x r problem G^T G with the
     reference's drop rule s > max(drop_tol s_0, 0) (nystrom.py:150-154).  The
     kept spectrum is the numerical range of Omega; eigenpairs at the rounding

@@ -63,3 +63,48 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def main_newton(indices=(0, 1)):
+    """Full-feature Newton (the nonlinear branch of baselines.py:186-191) on
+    config-3 instances, whose callables live in this package's workloads."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from nysode import newton
+    from nysode.kernel import RbfKernel
+    from nysode.problems import BoundaryCondition, Conditions, NonlinearOdeSpec
+    from paper_2510_04094_b200 import workloads as W
+    cfg = W.CONFIGS[3]
+    g = W.grid(cfg)
+    out = dict(grid=g, sigma2=cfg.sigma2, gamma=cfg.gamma, max_iters=cfg.newton_max_iters,
+               indices=np.array(indices))
+    orig = np.linalg.eigh
+    for i in indices:
+        inst = W.instance(3, 0, i, cfg)
+        spec = NonlinearOdeSpec(1, inst.rhs, (inst.rhs_y,), cfg.domain, {(0, 0): inst.rhs_yy})
+        cond = Conditions("ivp", tuple(BoundaryCondition(*c) for c in inst.conditions()))
+        res = []
+        for drv in ("evd", "ev"):
+            if drv == "ev":
+                nystrom.np.linalg.eigh = lambda A: sl.eigh(A, driver="ev")
+            try:
+                fm = nystrom.build_feature_map(RbfKernel(cfg.sigma2), g)
+                try:
+                    mdl, tr = newton.solve_nonlinear(spec, cond, fm, g, cfg.gamma,
+                                                     newton.NewtonOptions(max_iters=cfg.newton_max_iters))
+                    st = "converged"
+                except newton.MaxItersExceeded as exc:
+                    mdl, tr, st = exc.model, exc.trace, "max_iters"
+            finally:
+                nystrom.np.linalg.eigh = orig
+            res.append((mdl.predict(0, g), st, fm.m_eff, tr.iterations))
+        out[f"i{i}_yhat"], out[f"i{i}_status"], out[f"i{i}_m_eff"], out[f"i{i}_its"] = res[0]
+        out[f"i{i}_yhat_dsyev"] = res[1][0]
+        out[f"i{i}_status_dsyev"] = res[1][1]
+        out[f"i{i}_ystar"] = inst.sol(g)
+        ss = np.linalg.norm(res[1][0] - res[0][0]) / np.linalg.norm(res[0][0])
+        print(f"c3[{i}] full-feature: {res[0][1]} its={res[0][3]} m_eff={res[0][2]} self-sens {ss:.2e}")
+    np.savez_compressed(os.path.join(HERE, "full_feature_newton.npz"), **out)
+
+
+if __name__ == "__main__" and os.environ.get("NYS_FF_NEWTON"):
+    main_newton()

@@ -63,3 +63,36 @@ def test_full_feature_memory_guard():
     g = load_golden("full_feature")
     with pytest.raises(BL.MemoryGuardError):
         BL.full_feature_baseline(_problem(g, "p1"), 1e7, 10.0, BL.FULL_FEATURE_MAX_N + 1)
+
+
+@pytest.mark.parametrize("i", [0, 1])
+def test_full_feature_newton_matches_reference(i):
+    """The nonlinear branch (baselines.py:186-191): config-3 instances with every
+    grid point a landmark.  Instance 0's Newton path is rounding-chaotic in the
+    reference itself (dsyev vs dsyevd moves y_hat by ~5e-3); the device must
+    converge and land within 20x the yardstick (or 1e-6) and match the
+    reference's error vs the manufactured solution."""
+    from paper_2510_04094_b200 import newton as NW
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import NonlinearOdeSpec
+
+    g = load_golden("full_feature_newton")
+    cfg = W.CONFIGS[3]
+    grid = g["grid"]
+    assert np.array_equal(grid, W.grid(cfg))
+    inst = W.instance(3, 0, i, cfg)
+    spec = NonlinearOdeSpec(1, inst.rhs, (inst.rhs_y,), cfg.domain, {(0, 0): inst.rhs_yy})
+    cond = Conditions("ivp", tuple(BoundaryCondition(*c) for c in inst.conditions()))
+    fm = N.build_feature_map(RbfKernel(float(g["sigma2"])), grid)
+    assert "compressed" in fm._host
+    model, trace = NW.solve_nonlinear(spec, cond, fm, grid, float(g["gamma"]),
+                                      NW.NewtonOptions(max_iters=int(g["max_iters"])))
+    y = model.predict(0, grid)
+    ref = g[f"i{i}_yhat"]
+    yard = _rel(g[f"i{i}_yhat_dsyev"], ref)
+    assert _rel(y, ref) <= max(20 * yard, 1e-6), (_rel(y, ref), yard)
+    ys = g[f"i{i}_ystar"]
+    e_dev, e_ref = _rel(y, ys), _rel(ref, ys)
+    assert e_dev <= 2 * e_ref + 1e-9, (e_dev, e_ref)
