@@ -278,6 +278,21 @@ int nys_leverage_sketch_f64(const double* grid, int n, const double* x, int c, d
                             double ridge, const double* G, int r, double* scores, int* info,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* Kernel-space Gram split in two (config 4, m_eff + 2 > 72): the first part
+ * needs no eigenvectors, so it can run concurrently with nys_landmark_eig_f64
+ * (max_ctas < #SMs leaves SMs for it); the second projects with W.
+ *   K [(m+2)^2]: kernel-space extended Gram [G g r]^T [G g r], G the
+ *                order-combined kernel rows (same sums as nys_fused_gram_f64)
+ *   gram_ext [(m_eff+2)^2] = W_ext^T K W_ext */
+size_t nys_kspace_gram_workspace_bytes(int n_c, int m, int max_ctas);
+int nys_kspace_gram_f64(const double* landmarks, int m, double sigma2, int p, const double* pts,
+                        const double* coef, const double* forcing, int n_c, int row_begin,
+                        int row_end, int max_ctas, double* K, void* ws, size_t ws_bytes,
+                        void* stream);
+size_t nys_kspace_project_workspace_bytes(int m, int m_eff);
+int nys_kspace_project_f64(const double* K, int m, const double* W, int ldw, int m_eff,
+                           double* gram_ext, void* ws, size_t ws_bytes, void* stream);
+
 /* Large landmark sets (m > 512; the m = n full-feature comparator,
  * baselines.py:170-194): after nys_pchol_rbf_f64 on the landmarks (Omega ~ G G^T,
  * rank r <= 256), the kept eigenpairs of G G^T from the r x r problem G^T G:

@@ -77,6 +77,11 @@ SIGNATURES = {
     "nys_landmark_eig_compressed_f64": (_i, [_vp, _i, _i, _d, _vp, _vp, _vp, _i, _vp, _vp, _vp,
                                              _sz, _vp]),
     "nys_explicit_gram_workspace_bytes": (_sz, [_i, _i]),
+    "nys_kspace_gram_workspace_bytes": (_sz, [_i, _i, _i]),
+    "nys_kspace_gram_f64": (_i, [_vp, _i, _d, _i, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _sz,
+                                 _vp]),
+    "nys_kspace_project_workspace_bytes": (_sz, [_i, _i]),
+    "nys_kspace_project_f64": (_i, [_vp, _i, _vp, _i, _i, _vp, _vp, _sz, _vp]),
     "nys_explicit_gram_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_sym_eig_f64": (_i, [_vp, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

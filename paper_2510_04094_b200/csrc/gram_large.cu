@@ -48,7 +48,7 @@ constexpr double kDeadRatio = 747.0;   // d^2 / sigma2 beyond which exp() is exa
 struct LargePlan {
   int Pe, NB, NBpad, ld, nrr, ntiles, tiles_per_cta, nbuf;
   size_t smem;
-  static LargePlan make(int n_rows, int m) {
+  static LargePlan make(int n_rows, int m, int max_ctas = 0) {
     LargePlan L{};
     L.Pe = m + 2;                                 // kernel-space extended width
     L.NB = (L.Pe + 7) / 8;
@@ -56,6 +56,7 @@ struct LargePlan {
     L.ld = L.NB * 8;
     L.ntiles = (n_rows + 4 * kTileKs - 1) / (4 * kTileKs);
     int nrr = nys::device_sm_count();
+    if (max_ctas > 0 && nrr > max_ctas) nrr = max_ctas;   // leave SMs to a concurrent kernel
     if (nrr > L.ntiles) nrr = L.ntiles > 0 ? L.ntiles : 1;
     L.nrr = nrr;
     L.tiles_per_cta = (L.ntiles + nrr - 1) / nrr;
@@ -499,3 +500,68 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
 }
 
 }  // namespace nys_host
+
+// ---- split entry points: the kernel-space Gram needs no eigenvectors, so it can
+// run concurrently with the landmark eigendecomposition (config 4); the
+// projection E = W_ext^T K W_ext follows once W exists.
+extern "C" size_t nys_kspace_gram_workspace_bytes(int n_c, int m, int max_ctas) {
+  const LargePlan L = LargePlan::make(n_c, m, max_ctas);
+  return L.slab_doubles() * sizeof(double) + (size_t)L.nrr * sizeof(unsigned long long) + 512;
+}
+
+extern "C" int nys_kspace_gram_f64(const double* landmarks, int m, double sigma2, int p,
+                                   const double* pts, const double* coef, const double* forcing,
+                                   int n_c, int row_begin, int row_end, int max_ctas, double* K,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  if (m < 1 || p < 1 || p > nys::kMaxOrder || n_c < 0 || row_begin < 0 || row_end > n_c ||
+      row_begin > row_end || !(sigma2 > 0.0))
+    return NYS_EINVAL;
+  const LargePlan L = LargePlan::make(row_end - row_begin, m, max_ctas);
+  if (!L.fits()) return NYS_EUNSUPPORTED;
+  if (ws == nullptr || ws_bytes < nys_kspace_gram_workspace_bytes(row_end - row_begin, m, max_ctas))
+    return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* slabs = static_cast<double*>(ws);
+  auto* live = reinterpret_cast<unsigned long long*>(slabs + L.slab_doubles());
+  const int nthreads = kWarps * 32;
+#define NYS_LARGE(PP)                                                                              \
+  do {                                                                                             \
+    auto kern = large_kspace_kernel<PP>;                                                           \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                                         (int)L.smem);                                             \
+    if (e != cudaSuccess) return nys_host::record_cuda(e);                                         \
+    kern<<<L.nrr, nthreads, L.smem, st>>>(landmarks, m, sigma2, pts, coef, forcing, n_c,           \
+                                          row_begin, row_end, L.NB, L.NBpad, L.ld, L.nbuf,         \
+                                          L.tiles_per_cta, slabs, live);                           \
+  } while (0)
+  switch (p) {
+    case 1: NYS_LARGE(1); break;
+    case 2: NYS_LARGE(2); break;
+    case 3: NYS_LARGE(3); break;
+    default: NYS_LARGE(4); break;
+  }
+#undef NYS_LARGE
+  NYS_CHECK_LAUNCH();
+  large_reduce_kernel<<<(L.Pe * L.Pe + 255) / 256, 256, 0, st>>>(slabs, live, L.nrr, L.ld, L.Pe, K);
+  nys_host::count_launches(2);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+extern "C" size_t nys_kspace_project_workspace_bytes(int m, int m_eff) {
+  return (size_t)(m + 2) * (m_eff + 2) * sizeof(double) + 256;
+}
+
+extern "C" int nys_kspace_project_f64(const double* K, int m, const double* W, int ldw, int m_eff,
+                                      double* gram_ext, void* ws, size_t ws_bytes, void* stream) {
+  if (m < 1 || m_eff < 1 || m_eff > m || ldw < m_eff) return NYS_EINVAL;
+  if (ws == nullptr || ws_bytes < nys_kspace_project_workspace_bytes(m, m_eff)) return NYS_EWORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int Pe = m + 2, Pw = m_eff + 2;
+  double* T = static_cast<double*>(ws);
+  proj_right_kernel<<<(Pe * Pw + 127) / 128, 128, 0, st>>>(K, Pe, W, ldw, m, m_eff, T);
+  proj_left_kernel<<<(Pw * Pw + 127) / 128, 128, 0, st>>>(T, Pe, W, ldw, m, m_eff, gram_ext);
+  nys_host::count_launches(2);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}

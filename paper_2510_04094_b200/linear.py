@@ -18,6 +18,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 from typing import Any, Optional
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -320,6 +322,36 @@ class SingleSolvePipeline:
         self.vals = _lib.as_f64([bc.value for bc in cond.entries], self.device).reshape(1, -1)
         self._shape = None
         self._graph = None
+        # kernel-space Gram (m_eff + 2 > 72) needs no eigenvectors: when the
+        # landmark count allows that path it is launched speculatively on a side
+        # stream with one SM left free, concurrent with the eigendecomposition
+        m = self.landmarks.size
+        self._kspace = ((m + 2 + 7) // 8 > SMALL_NB_MAX and (m + 2 + 7) // 8 <= 64
+                        and os.environ.get("NYS_KSPACE_OVERLAP", "1") != "0")
+        if self._kspace:
+            self._side = torch.cuda.Stream(device=self.device)
+            self._kev = torch.cuda.Event()
+            self._kctas = torch.cuda.get_device_properties(self.device).multi_processor_count - 1
+            self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
+            self._kn_c = None
+
+    def _kspace_launch(self, pts, coef, forcing):
+        torch, lib = self.torch, self.lib
+        n_c = int(pts.numel())
+        m = self.landmarks.size
+        if self._kn_c != n_c:
+            self.kgws_b = lib.nys_kspace_gram_workspace_bytes(n_c, m, self._kctas)
+            self.kgws = torch.empty(self.kgws_b, dtype=torch.uint8, device=self.device)
+            self.kpws_b = lib.nys_kspace_project_workspace_bytes(m, m)
+            self.kpws = torch.empty(self.kpws_b, dtype=torch.uint8, device=self.device)
+            self._kn_c = n_c
+        cur = torch.cuda.current_stream(self.device)
+        self._side.wait_stream(cur)
+        _lib.call("nys_kspace_gram_f64", _lib.ptr(self.eig.d_lm), m, float(self.kernel.sigma2),
+                  self.order, _lib.ptr(pts), _lib.ptr(coef), _lib.ptr(forcing), n_c, 0, n_c,
+                  self._kctas, _lib.ptr(self.K), _lib.ptr(self.kgws), self.kgws_b,
+                  self._side.cuda_stream)
+        self._kev.record(self._side)
 
     def _buffers(self, me: int, n_c: int):
         torch, lib = self.torch, self.lib
@@ -339,17 +371,21 @@ class SingleSolvePipeline:
         self._shape = (me, n_c)
         self._graph = None
 
-    def _post(self, fm, pts, coef, forcing):
+    def _post(self, fm, pts, coef, forcing, use_k=False):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
         for mu, bc in enumerate(self.cond.entries):   # linear.py:56-63, on the device
             _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw,
                       me, float(fm.kernel.sigma2), int(bc.order), _lib.ptr(self.cond_pts) + 8 * mu,
                       1, _lib.ptr(self.Ac) + 8 * mu * me, me, st)
         n_c = pts.numel()
-        _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw, me,
-                  float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
-                  _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
-                  self.gws_b, st)
+        if use_k:
+            _lib.call("nys_kspace_project_f64", _lib.ptr(self.K), m, _lib.ptr(fm.d_W), fm.ldw, me,
+                      _lib.ptr(self.E), _lib.ptr(self.kpws), self.kpws_b, st)
+        else:
+            _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw, me,
+                      float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
+                      _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
+                      self.gws_b, st)
         _lib.call("nys_kkt_solve_f64", _lib.ptr(self.E), me, self.nk, _lib.ptr(self.Ac),
                   _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
                   _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
@@ -360,26 +396,32 @@ class SingleSolvePipeline:
 
         from .nystrom import build_feature_map
 
+        if self._kspace:
+            self._kspace_launch(pts, coef, forcing)
         fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
         me = fm.m_eff
-        if (me + 2 + 7) // 8 > SMALL_NB_MAX and fm.condition > KSPACE_MAX_COND:
+        big = (me + 2 + 7) // 8 > SMALL_NB_MAX
+        if self._kspace:   # inputs and K are shared with the side stream
+            self.torch.cuda.current_stream(self.device).wait_event(self._kev)
+        if big and fm.condition > KSPACE_MAX_COND:
             raise IllConditionedLargeMapError(
                 f"m_eff={me} with cond(Omega)={fm.condition:.2e} > {KSPACE_MAX_COND:.0e}")
+        use_k = self._kspace and big
         n_c = int(pts.numel())
         self._buffers(me, n_c)
         if os.environ.get("NYS_GRAPHS", "1") == "0":
-            self._post(fm, pts, coef, forcing)
+            self._post(fm, pts, coef, forcing, use_k)
             return self.x, self.info
-        key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c)
+        key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c, use_k)
         if self._graph is not None and self._gkey == key:
             self._graph.replay()
             _lib.note_graph_launches(self._gcount)
             return self.x, self.info
-        self._post(fm, pts, coef, forcing)   # eager: this call's result + kernel attributes
+        self._post(fm, pts, coef, forcing, use_k)   # eager: this call's result + attributes
         n0 = self.lib.nys_launch_count()
         g = self.torch.cuda.CUDAGraph()
         with self.torch.cuda.graph(g, capture_error_mode="thread_local"):
-            self._post(fm, pts, coef, forcing)
+            self._post(fm, pts, coef, forcing, use_k)
         self._gcount = self.lib.nys_launch_count() - n0
         self._graph, self._gkey = g, key
         return self.x, self.info

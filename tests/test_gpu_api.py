@@ -16,7 +16,7 @@ def _predict(fm, x, grid):
     return L.predict_batch(fm, x, 0, grid).cpu().numpy()
 
 
-@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0"])
+@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0", "c4_n16384"])
 def test_single_pipeline_matches_reference_and_replays(name):
     """SingleSolvePipeline (eig + graph-replayed condition rows / Gram / KKT):
     y_hat within 1e-6 of the reference, and the replayed call reproduces the
@@ -38,6 +38,22 @@ def test_single_pipeline_matches_reference_and_replays(name):
     mdl = pipe.model()
     y = mdl.predict(0, g["grid"])
     assert rel_l2(y, g["yhat"][0]) <= 1e-6
+    if name.startswith("c4"):
+        # m = 256: the kernel-space Gram ran on the side stream, concurrent with
+        # the eigendecomposition; the serial path gives the same model
+        assert pipe._kspace
+        import os
+        os.environ["NYS_KSPACE_OVERLAP"] = "0"
+        try:
+            serial = L.SingleSolvePipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                           float(g["gamma"]), int(g["order"]), cond)
+        finally:
+            del os.environ["NYS_KSPACE_OVERLAP"]
+        assert not serial._kspace
+        xs = serial.run_device(pts, coef, forc)[0]
+        ys = serial.model().predict(0, g["grid"])
+        assert rel_l2(y, ys) <= 1e-12
+        assert float(torch.max(torch.abs(xs - x1))) <= 1e-9 * float(torch.max(torch.abs(xs)))
 
 
 def test_shared_pipeline_graph_equals_eager():
