@@ -297,7 +297,11 @@ class SingleSolvePipeline:
     with the same buffers -- the condition rows A_c (feature rows at the
     condition points, nys_feature_matrix_f64), the fused feature+Gram kernel and
     the KKT LU + refinement.  Inputs are device tensors; x / info come back in
-    buffers owned by the pipeline (overwritten by the next call).
+    buffers owned by the pipeline (overwritten by the next call).  The
+    eigendecomposition runs on its own stream with two alternating buffer sets,
+    so a call's eigensolver overlaps the previous call's Gram and KKT
+    (NYS_EIG_OVERLAP=0 turns this off); with m_eff + 2 > 72 the kernel-space
+    Gram also runs concurrently with it on a second side stream.
     NYS_GRAPHS=0 runs everything eagerly.
     """
 
@@ -322,6 +326,10 @@ class SingleSolvePipeline:
         self.vals = _lib.as_f64([bc.value for bc in cond.entries], self.device).reshape(1, -1)
         self._shape = None
         self._graph = None
+        self._eigbufs = None
+        self._pending = []
+        self._me_known = None
+        self._cond_known = None
         # kernel-space Gram (m_eff + 2 > 72) needs no eigenvectors: when the
         # landmark count allows that path it is launched speculatively on a side
         # stream with one SM left free, concurrent with the eigendecomposition
@@ -334,6 +342,23 @@ class SingleSolvePipeline:
             self._kctas = torch.cuda.get_device_properties(self.device).multi_processor_count - 1
             self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
             self._kn_c = None
+
+    def _verify_pending(self, keep: int = 0):
+        """Check steady-state eigendecompositions (m_eff, info) once their
+        events have completed, leaving the newest ``keep`` unchecked (so the
+        host never waits for the eigensolver that is still running)."""
+        while len(self._pending) > keep:
+            self._check(*self._pending.pop(0))
+
+    def _check(self, ev, buf, me):
+        ev.synchronize()
+        m_eff, info = (int(v) for v in buf.meta_h)
+        if (info & 0xFF) == _lib.INFO_DEGENERATE:
+            from .nystrom import DegenerateLandmarksError
+            raise DegenerateLandmarksError("two landmarks coincide within 1e-12")
+        if m_eff != me:
+            raise RuntimeError(f"landmark eigendecomposition changed m_eff {me} -> {m_eff} "
+                               "between calls on the same landmarks")
 
     def _kspace_launch(self, pts, coef, forcing):
         torch, lib = self.torch, self.lib
@@ -394,40 +419,89 @@ class SingleSolvePipeline:
         """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info)."""
         import os
 
-        from .nystrom import build_feature_map
+        from .nystrom import build_feature_map, launch_eig_async
 
+        torch = self.torch
+        graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
         if self._kspace:
             self._kspace_launch(pts, coef, forcing)
-        fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
+        par = None
+        if graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0":
+            # the eigendecomposition (one SM) runs on its own stream with two
+            # alternating buffer sets, so this call's eigensolver overlaps the
+            # previous call's Gram/KKT (a set is rewritten only after the
+            # main-stream work that last read it: event)
+            if self._eigbufs is None:
+                from .nystrom import EigBuffers
+                self._eigbufs = [self.eig, EigBuffers(self.landmarks, self.device)]
+                self._eig_done = [None, None]
+                self._eig_stream = torch.cuda.Stream(device=self.device)
+                self._parity = 0
+            par = self._parity
+            self._parity ^= 1
+            if self._eig_done[par] is not None:
+                self._eig_stream.wait_event(self._eig_done[par])
+            self._verify_pending(keep=1)
+            buf = self._eigbufs[par]
+            if self._me_known is None:
+                # first call: synchronous build (m_eff, degenerate check, cond gate)
+                with torch.cuda.stream(self._eig_stream):
+                    fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol,
+                                           buffers=buf)
+                self._me_known = fm.m_eff
+                self._cond_known = fm.condition
+            else:
+                # steady state: the same landmarks give the same m_eff (deterministic
+                # kernels), so the host does not wait for the eigensolver; this
+                # call's m_eff / info are checked at the start of the next call
+                ev = launch_eig_async(self.kernel, buf, self.drop_tol, self._eig_stream)
+                self._pending.append((ev, buf, self._me_known))
+                fm = NystromFeatureMap(kernel=self.kernel, landmarks=self.landmarks,
+                                       m_eff=self._me_known, device=self.device,
+                                       d_landmarks=buf.d_lm, d_W=buf.W, d_eigvals=buf.s,
+                                       d_eigvecs=buf.V)
+            torch.cuda.current_stream(self.device).wait_stream(self._eig_stream)
+            self.eig = buf
+        else:
+            fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
         me = fm.m_eff
         big = (me + 2 + 7) // 8 > SMALL_NB_MAX
         if self._kspace:   # inputs and K are shared with the side stream
             self.torch.cuda.current_stream(self.device).wait_event(self._kev)
-        if big and fm.condition > KSPACE_MAX_COND:
+        cond_omega = self._cond_known if par is not None else fm.condition
+        if big and cond_omega > KSPACE_MAX_COND:
             raise IllConditionedLargeMapError(
                 f"m_eff={me} with cond(Omega)={fm.condition:.2e} > {KSPACE_MAX_COND:.0e}")
         use_k = self._kspace and big
         n_c = int(pts.numel())
         self._buffers(me, n_c)
-        if os.environ.get("NYS_GRAPHS", "1") == "0":
+        if not graphs:
             self._post(fm, pts, coef, forcing, use_k)
             return self.x, self.info
-        key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c, use_k)
-        if self._graph is not None and self._gkey == key:
-            self._graph.replay()
-            _lib.note_graph_launches(self._gcount)
-            return self.x, self.info
-        self._post(fm, pts, coef, forcing, use_k)   # eager: this call's result + attributes
-        n0 = self.lib.nys_launch_count()
-        g = self.torch.cuda.CUDAGraph()
-        with self.torch.cuda.graph(g, capture_error_mode="thread_local"):
-            self._post(fm, pts, coef, forcing, use_k)
-        self._gcount = self.lib.nys_launch_count() - n0
-        self._graph, self._gkey = g, key
+        key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c, use_k,
+               fm.d_W.data_ptr())
+        if self._graph is None:
+            self._graph = {}
+        hit = self._graph.get(key)
+        if hit is not None:
+            hit[0].replay()
+            _lib.note_graph_launches(hit[1])
+        else:
+            self._post(fm, pts, coef, forcing, use_k)   # eager: this call's result + attributes
+            n0 = self.lib.nys_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._post(fm, pts, coef, forcing, use_k)
+            self._graph[key] = (g, self.lib.nys_launch_count() - n0)
+        if par is not None:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(self.device))
+            self._eig_done[par] = ev
         return self.x, self.info
 
     def model(self):
         """PrimalModel of the last call (raises the reference's errors from info)."""
+        self._verify_pending()
         raise_for_info(int(self.info[0]))
         x = self.x[0].cpu().numpy()
         me = self._shape[0]

@@ -223,6 +223,24 @@ class EigBuffers:
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.device) if self.wsb else None
 
 
+def launch_eig_async(k: RbfKernel, buffers: EigBuffers, drop_tol: float, stream):
+    """Enqueue the eigendecomposition into ``buffers`` on ``stream`` without
+    waiting for it: m_eff / info land in ``buffers.meta_h`` (pinned) when the
+    returned event completes.  For pipelines that already know m_eff from an
+    earlier build of the same landmarks and verify it one call later."""
+    lib, torch = _lib.require_device()
+    m = buffers.landmarks.size
+    with torch.cuda.stream(stream):
+        _lib.call("nys_landmark_eig_f64", _lib.ptr(buffers.d_lm), m, float(k.sigma2),
+                  float(drop_tol), _lib.ptr(buffers.s), _lib.ptr(buffers.V), _lib.ptr(buffers.W),
+                  _lib.ptr(buffers.meta), _lib.ptr(buffers.meta) + 4, _lib.ptr(buffers.ws),
+                  buffers.wsb, stream.cuda_stream)
+        buffers.meta_h.copy_(buffers.meta, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+    return ev
+
+
 def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TOL,
                       device=None, buffers: Optional[EigBuffers] = None) -> NystromFeatureMap:
     """Eigendecompose Omega_mm on the GPU and keep s > max(drop_tol s_0, 0)."""
