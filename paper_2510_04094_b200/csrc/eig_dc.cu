@@ -54,14 +54,21 @@ struct DcShared {
 };
 
 
-// implicit QL on the leaf [s, s+len) of (d, e), eigenvectors into Q block
-NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
+// implicit QL on the leaf [s, s+len) of (d, e), eigenvectors into Q block.
+// One warp per leaf: every lane runs the (short) scalar recurrence redundantly
+// -- identical values, so the shared d/e writes agree -- and lane k < len
+// applies each Givens rotation to row k of the leaf's Z, so no rotation waits
+// for a serial len-long row loop.  The arithmetic is the serial version's, op
+// for op (results unchanged bit for bit).
+NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len, int lane) {
   double* d = S.d + s;
   double* e = S.e + s;   // e[i] couples i, i+1 inside the leaf; e[len-1] is unused
-  double ehold = len > 0 ? e[len - 1] : 0.0;
+  const double ehold = len > 0 ? e[len - 1] : 0.0;
+  __syncwarp();
   if (len > 0) e[len - 1] = 0.0;
-  for (int r = 0; r < len; ++r)
-    for (int c = 0; c < len; ++c) Q[(size_t)(s + r) * n + s + c] = (r == c) ? 1.0 : 0.0;
+  double* row = lane < len ? Q + (size_t)(s + lane) * n + s : nullptr;
+  if (row)
+    for (int c = 0; c < len; ++c) row[c] = (lane == c) ? 1.0 : 0.0;
   for (int l = 0; l < len; ++l) {
     for (int iter = 0; iter < 60; ++iter) {
       int mm = l;
@@ -74,9 +81,8 @@ NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
       double r = hypot(g, 1.0);
       g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
       double sn = 1.0, cs = 1.0, p = 0.0;
-      int i = mm - 1;
       bool early = false;
-      for (; i >= l; --i) {
+      for (int i = mm - 1; i >= l; --i) {
         const double f = sn * e[i], b = cs * e[i];
         r = hypot(f, g);
         e[i + 1] = r;
@@ -93,8 +99,7 @@ NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
         p = sn * r;
         d[i + 1] = g + p;
         g = cs * r - b;
-        for (int k = 0; k < len; ++k) {   // columns i, i+1 of the leaf's Z
-          double* row = Q + (size_t)(s + k) * n + s;
+        if (row) {   // columns i, i+1 of the leaf's Z, this lane's row
           const double zf = row[i + 1], zi = row[i];
           row[i + 1] = sn * zi + cs * zf;
           row[i] = cs * zi - sn * zf;
@@ -106,8 +111,9 @@ NYS_DEV void leaf_ql(DcShared& S, double* Q, int n, int s, int len) {
       e[mm] = 0.0;
     }
   }
+  __syncwarp();
   if (len > 0) e[len - 1] = ehold;
-  for (int c = 0; c < len; ++c) S.lam[s + c] = d[c];
+  if (lane < len) S.lam[s + lane] = d[lane];
 }
 
 // secular root j of diag(ds) + rho zz^T over the K kept entries of a block;
@@ -616,9 +622,9 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   for (int e = tid; e < n * n; e += nt) Q[e] = 0.0;
   __syncthreads();
   const int nleaf = (n + kLeaf - 1) / kLeaf;
-  for (int t = tid; t < nleaf; t += nt) {
+  for (int t = tid >> 5; t < nleaf; t += nt >> 5) {   // one warp per leaf
     const int s = t * kLeaf, len = min(kLeaf, n - s);
-    leaf_ql(S, Q, n, s, len);
+    leaf_ql(S, Q, n, s, len, tid & 31);
   }
   __syncthreads();
 
