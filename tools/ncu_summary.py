@@ -38,9 +38,9 @@ uh = dict(zip(h, units))
 rd *= scale.get(uh.get("dram__bytes_read.sum", "byte"), 1)
 wr *= scale.get(uh.get("dram__bytes_write.sum", "byte"), 1)
 t_ms = f("gpu__time_duration.sum")
-if uh.get("gpu__time_duration.sum") == "usecond":
+if uh.get("gpu__time_duration.sum") in ("usecond", "us"):
     t_ms /= 1e3
-elif uh.get("gpu__time_duration.sum") == "nsecond":
+elif uh.get("gpu__time_duration.sum") in ("nsecond", "ns"):
     t_ms /= 1e6
 stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace(
     "_per_issue_active.ratio", ""): f(k) for k in h
