@@ -18,18 +18,20 @@
 // On config 4 (landmarks 0.39 apart, sigma 0.5) a 32-row tile sees ~11 of the
 // 33 column blocks, a CTA's row range ~12.
 //
-// Work split.  One CTA per SM (18 warps), each owning a contiguous row range.
+// Work split.  One CTA per SM (12 warps), each owning a contiguous row range.
 // At start the CTA finds the blocks live anywhere in its range (its "window"),
 // compacts them, and tiles the compacted Gram triangle with 4 x 4 super-tiles
 // of 8x8 DMMA accumulators (64 registers per warp).  Few super-tiles (config
-// 4: 6) are replicated over the 18 warps, each replica taking every R-th
+// 4: 6) are replicated over the 12 warps, each replica taking every R-th
 // k-step; many (dense windows) run in several passes over the row range.
 // Per 32-row tile the fragment-native smem layout X[ks][c][lane] (c = compacted
 // live-block index, so every super-tile reads contiguous fragments) is double
 // buffered: iteration t issues the DMMAs of tile t and generates tile t+1
 // (half the warps of every SM sub-partition in the opposite order so the
 // exp arithmetic and the tensor pipe overlap); row coefficients are
-// produced two tiles ahead.  Each CTA writes its live
+// produced two tiles ahead (raw row data loaded three ahead).  Diagonal
+// super-tiles that are complete run an unpredicated i <= j DMMA pattern (a
+// predicated mma.sync costs a WARPSYNC + NOP in SASS).  Each CTA writes its live
 // block pairs to a private dense slab (replicas added in fixed order) and one
 // reduce kernel sums the slabs in fixed order (deterministic).
 #include <cstdint>
@@ -40,7 +42,10 @@
 namespace {
 
 constexpr int kRT = 4;             // super-tile edge (blocks)
-constexpr int kWarps = 18;         // warps per CTA (576 threads, 1 CTA / SM)
+#ifndef NYS_LARGE_WARPS
+#define NYS_LARGE_WARPS 12
+#endif
+constexpr int kWarps = NYS_LARGE_WARPS;   // warps per CTA (1 CTA / SM; 12: 3 per SMSP, 168 registers)
 constexpr int kTileKs = 8;         // 4-row k-steps per row tile (32 rows)
 constexpr int kMaxSmem = 227 * 1024;
 constexpr double kDeadRatio = 747.0;   // d^2 / sigma2 beyond which exp() is exactly 0
@@ -94,28 +99,40 @@ NYS_DEV unsigned long long live_blocks(const double* blo, const double* bhi, int
 }
 
 // per-row polynomial coefficients for one 32-row tile: t, q0..qP, g = -f_p, r
-// (one warp; rows past the end get an all-zero polynomial -> G = 0)
+// (one warp; rows past the end get an all-zero polynomial -> G = 0).  The raw
+// row data are loaded a tile ahead (RowRaw in registers) so the global-load
+// latency overlaps a whole tile of DMMA work.
 template <int P>
-NYS_DEV void row_coeffs(const double (*hc)[nys::kMaxOrder + 1], const double* __restrict__ pts,
-                        const double* __restrict__ coef, const double* __restrict__ forcing,
-                        int n_c, int r0, int row_end, double* rowc) {
-  const int lane = threadIdx.x & 31;
-  const int i = r0 + lane;
-  const bool ok = i < row_end;
-  double f[P];
+struct RowRaw {
+  double t, f[P], r;
+  bool ok;
+};
+
+template <int P>
+NYS_DEV void row_load(const double* __restrict__ pts, const double* __restrict__ coef,
+                      const double* __restrict__ forcing, int n_c, int r0, int row_end,
+                      RowRaw<P>& w) {
+  const int i = r0 + (threadIdx.x & 31);
+  w.ok = i < row_end;
 #pragma unroll
-  for (int k = 0; k < P; ++k) f[k] = ok ? coef[(size_t)k * n_c + i] : 0.0;
-  double* rc = rowc + lane * 8;
-  rc[0] = ok ? pts[i] : 0.0;
+  for (int k = 0; k < P; ++k) w.f[k] = w.ok ? coef[(size_t)k * n_c + i] : 0.0;
+  w.t = w.ok ? pts[i] : 0.0;
+  w.r = w.ok ? forcing[i] : 0.0;
+}
+
+template <int P>
+NYS_DEV void row_store(const double (*hc)[nys::kMaxOrder + 1], const RowRaw<P>& w, double* rowc) {
+  double* rc = rowc + (threadIdx.x & 31) * 8;
+  rc[0] = w.t;
 #pragma unroll
   for (int j = 0; j <= P; ++j) {
     double v = hc[P][j];
 #pragma unroll
-    for (int k = 1; k <= P; ++k) v = fma(-f[k - 1], hc[P - k][j], v);
-    rc[1 + j] = ok ? v : 0.0;
+    for (int k = 1; k <= P; ++k) v = fma(-w.f[k - 1], hc[P - k][j], v);
+    rc[1 + j] = w.ok ? v : 0.0;
   }
-  rc[6] = ok ? -f[P - 1] : 0.0;
-  rc[7] = ok ? forcing[i] : 0.0;
+  rc[6] = w.ok ? -w.f[P - 1] : 0.0;
+  rc[7] = w.r;
 }
 
 // -(x / sigma2) for x >= 0, correctly rounded from the precomputed reciprocal:
@@ -143,7 +160,7 @@ NYS_DEV double g_entry(double l, const double* r, double sigma2, double inv) {
 template <int P>
 NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int L, const int* lb, int NBpad,
                       double sigma2, double inv, const double* rowc, double* X, int warp,
-                      int nwarps) {
+                      int nwarps) {   // (all warps share the 4 L units)
   const int lane = threadIdx.x & 31;
   const int rsub = lane & 3, csub = lane >> 2;
   for (int u = warp; u < 4 * L; u += nwarps) {
@@ -166,8 +183,31 @@ NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int L, const int* lb
   }
 }
 
+// Uniform grids (t_i = t_0 + i h to 8 ulp, checked per CTA at start): the
+// generating warp of a compacted block keeps, per lane (row residue rsub,
+// landmark 8 lb[c] + csub), an anchor at row A and forms the rows A + jH
+// (H = 4h, j < 32) as
+//     e_j = e_A rho_A^j Q^{j(j-1)/2},
+//     e_A = exp(-d_A^2 / sigma2),  rho_A = exp((2 H d_A - H^2) / sigma2),
+//     Q = exp(-2 H^2 / sigma2)
+// (e(t + H) = e(t) rho(t), rho(t + H) = rho(t) Q).  rho_A^{8u} is carried from
+// tile to tile, rho_A^i (i <= 8) comes from a depth-3 product tree and
+// Q^{j(j-1)/2} from a per-CTA table, so the eight entries of a lane are
+// independent (no serial DMUL chain: the FP64 datapath is shared with the
+// DMMAs of the other warps, which makes a dependent chain slow).  Two exp()
+// per lane every kAnchorTiles tiles, computed one tile early.  Error: <= ~20
+// roundings per entry (~2e-15 relative) plus the anchor's ideal-vs-actual grid
+// position (<= 8 ulp(t): <= 2|d| dt / sigma2 relative, < 1e-12 wherever an
+// entry exceeds 1e-17).  The Hermite factor P(d) uses the exact d of every row.
+// Stores are lane-contiguous (X[ks][c][lane]).
+constexpr int kAnchorTiles = 4;
+constexpr int kGenMax = 2;      // blocks one warp generates (register state)
+
 #ifndef NYS_LARGE_PROBE
 #define NYS_LARGE_PROBE 0   // probe builds: 1 = skip DMMA, 2 = skip generation, 3 = phase clocks
+#endif
+#ifndef NYS_LARGE_REC
+#define NYS_LARGE_REC 1     // 0: exp() per entry on uniform grids too (A/B builds)
 #endif
 
 template <int P>
@@ -183,8 +223,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   double* const X1 = sm + (nbuf - 1) * xsz;
   double* const rowc = sm + nbuf * xsz;   // [3][32][8]
   __shared__ double blo_s[64], bhi_s[64];
-  __shared__ double red_s[2][kWarps];
+  __shared__ double red_s[3][kWarps];
   __shared__ int nan_s;
+  __shared__ double hstep_s, hstep_ta_s;
   __shared__ unsigned long long live_s;
   __shared__ int lb_s[64];
   __shared__ double hc_s[nys::kMaxOrder + 1][nys::kMaxOrder + 1];
@@ -219,33 +260,47 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   __syncthreads();
   // ---- t-range of the CTA's rows -> its window of live blocks
   {
-    double tmin = INFINITY, tmax = -INFINITY;
+    double tmin = INFINITY, tmax = -INFINITY, dev = 0.0;
     bool bad = false;
     const int r_lo = row_begin + tile0 * 32, r_hi = min(row_end, row_begin + tile1 * 32);
+    // uniform-grid test against the chord of the range (NaN fails it)
+    const double ta = r_hi > r_lo ? pts[r_lo] : 0.0, tb = r_hi > r_lo ? pts[r_hi - 1] : 0.0;
+    const double h = r_hi - r_lo > 1 ? (tb - ta) / (double)(r_hi - 1 - r_lo) : 0.0;
     for (int i = r_lo + threadIdx.x; i < r_hi; i += blockDim.x) {
       const double t = pts[i];
       tmin = fmin(tmin, t);
       tmax = fmax(tmax, t);
       bad |= t != t;
+      dev = fmax(dev, fabs(t - fma((double)(i - r_lo), h, ta)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
       tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) nan_s = 1;
     if (lane == 0) {
       red_s[0][warp] = tmin;
       red_s[1][warp] = tmax;
+      red_s[2][warp] = dev;
+    }
+    if (threadIdx.x == 0) {
+      hstep_s = h;
+      hstep_ta_s = ta;
     }
   }
   __syncthreads();
   if (warp == 0) {
-    double tmin = INFINITY, tmax = -INFINITY;
+    double tmin = INFINITY, tmax = -INFINITY, dev = 0.0;
     for (int w = 0; w < nwarps; ++w) {
       tmin = fmin(tmin, red_s[0][w]);
       tmax = fmax(tmax, red_s[1][w]);
+      dev = fmax(dev, red_s[2][w]);
     }
+    // 8 ulp of the largest |t|; NaN deviations fail the test
+    const double tol = 8.0 * 2.220446049250313e-16 * fmax(fabs(tmin), fabs(tmax));
+    if (lane == 0 && !(dev <= tol && nan_s == 0 && hstep_s > 0.0)) hstep_s = 0.0;
     const unsigned long long live =
         live_blocks(blo_s, bhi_s, NB, special, tmin, tmax, nan_s != 0, kDeadRatio * sigma2);
     for (int h = 0; h < 2; ++h) {   // compact the live blocks in ascending order
@@ -261,22 +316,132 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int L = __popcll(live_s);
   const int T = (L + kRT - 1) / kRT;
   const int ntask = T * (T + 1) / 2;
+  __shared__ signed char wtask_s[kWarps], wrep_s[kWarps], wR_s[kWarps], genw_s[64];
   int R = 1, npass = (ntask + nwarps - 1) / nwarps;
-  if (ntask <= nwarps) {
-    R = min(nwarps / ntask, kTileKs);
+  if (ntask <= nwarps) {   // R replicas per super-tile; warp c generates block c
+    if (threadIdx.x < 64) {
+      const int Ru = min(nwarps / ntask, kTileKs), x = threadIdx.x;
+      if (x < nwarps) {
+        wtask_s[x] = (signed char)(x < ntask * Ru ? x / Ru : -1);
+        wrep_s[x] = (signed char)(x % Ru);
+        wR_s[x] = (signed char)Ru;
+      }
+      genw_s[x] = (signed char)(x % nwarps);
+    }
+    __syncthreads();
+    R = wR_s[warp];
     npass = 1;
+  } else if (threadIdx.x < 64) {
+    genw_s[threadIdx.x] = (signed char)(threadIdx.x % nwarps);
   }
+  __syncthreads();
+  int Rmax = 1;
+  for (int x = 0; x < nwarps && npass == 1; ++x) Rmax = max(Rmax, (int)wR_s[x]);
   const int cw = nwarps - 1;   // warp that prepares row coefficients
+  RowRaw<P> raw;
+  const double H = 4.0 * hstep_s;   // 0: non-uniform grid -> exp() per entry
+  const bool rec = H > 0.0 && NYS_LARGE_REC && ntask <= nwarps && L <= kGenMax * nwarps;
+  // Q^{j(j-1)/2}, j < kAnchorTiles * kTileKs (rows since the anchor)
+  __shared__ double qtri_s[kAnchorTiles * kTileKs];
+  if (rec && threadIdx.x < kAnchorTiles * kTileKs)
+    qtri_s[threadIdx.x] = exp(-H * H * inv * (double)(threadIdx.x * (threadIdx.x - 1)));
+  // recurrence state of this warp's generated blocks (rec path only): landmark,
+  // anchor exponential and ratio, rho_A^{8t}, and the next anchor
+  const int rsub = lane & 3, csub = lane >> 2;
+  int gc[kGenMax], ng = 0;
+  double gl[kGenMax], geA[kGenMax], grA[kGenMax], gP[kGenMax], geN[kGenMax], grN[kGenMax];
+#pragma unroll
+  for (int g = 0; g < kGenMax; ++g) {
+    gc[g] = -1;
+    gl[g] = geA[g] = grA[g] = gP[g] = geN[g] = grN[g] = 0.0;
+  }
+  if (rec) {
+    for (int c = 0; c < L; ++c)
+      if (genw_s[c] == warp && ng < kGenMax) gc[ng++] = c;
+#pragma unroll
+    for (int g = 0; g < kGenMax; ++g)
+      if (g < ng) {
+        const int s = lb_s[gc[g]] * 8 + csub;
+        gl[g] = s < m ? __ldg(lm + s) : 0.0;
+      }
+  }
+  const double ta = hstep_ta_s;
+  // anchor for the lane's first row of CTA tile kt (ideal grid position)
+  auto anchor = [&](int kt) {
+    const double t = fma((double)(kt * 32 + rsub), hstep_s, ta);
+#pragma unroll
+    for (int g = 0; g < kGenMax; ++g)
+      if (g < ng) {
+        const double d = gl[g] - t;
+        geN[g] = exp(neg_div(d * d, sigma2, inv));
+        grN[g] = exp(fma(2.0 * H, d, -H * H) * inv);
+      }
+  };
+  // rows j = 8u + i since the anchor: e_j = e_A rho_A^j Q^{j(j-1)/2}, with
+  // rho_A^{8u} carried and rho_A^i by a depth-3 product tree (no serial chain)
+  auto gen_rec = [&](int kt, const double* rc, double* Xd) {
+    const int u = kt % kAnchorTiles;
+    if (u == 0) {
+#pragma unroll
+      for (int g = 0; g < kGenMax; ++g) {
+        geA[g] = geN[g];
+        grA[g] = grN[g];
+        gP[g] = 1.0;
+      }
+    }
+    const double* qt = qtri_s + u * kTileKs;
+#pragma unroll
+    for (int g = 0; g < kGenMax; ++g)
+      if (g < ng) {
+        const int s = lb_s[gc[g]] * 8 + csub;
+        double* Xo = Xd + (size_t)gc[g] * 32 + lane;
+        if (s < m) {
+          double rp[kTileKs + 1];
+          rp[0] = 1.0;
+          rp[1] = grA[g];
+          rp[2] = rp[1] * rp[1];
+          rp[3] = rp[2] * rp[1];
+          rp[4] = rp[2] * rp[2];
+          rp[5] = rp[4] * rp[1];
+          rp[6] = rp[4] * rp[2];
+          rp[7] = rp[4] * rp[3];
+          rp[8] = rp[4] * rp[4];
+          const double base = geA[g] * gP[g];
+#pragma unroll
+          for (int ks = 0; ks < kTileKs; ++ks) {
+            const double* r = rc + (ks * 4 + rsub) * 8;
+            const double d = gl[g] - r[0];
+            double poly = r[1 + P];
+#pragma unroll
+            for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, r[1 + j]);
+            Xo[(size_t)ks * NBpad * 32] = poly * ((base * rp[ks]) * qt[ks]);
+          }
+          gP[g] *= rp[8];
+        } else {
+#pragma unroll
+          for (int ks = 0; ks < kTileKs; ++ks) {
+            const double* r = rc + (ks * 4 + rsub) * 8;
+            Xo[(size_t)ks * NBpad * 32] = (s == m) ? r[6] : (s == m + 1) ? r[7] : 0.0;
+          }
+        }
+      }
+    if (u == kAnchorTiles - 1) anchor(kt + 1);
+  };
+  auto gen = [&](int kt, const double* rc, double* Xd) {
+    if (rec)
+      gen_rec(kt, rc, Xd);
+    else
+      gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rc, Xd, warp, nwarps);
+  };
+  if (rec) anchor(0);
   double* const slab = slabs + (size_t)blockIdx.x * ld * ld;
 
   for (int pass = 0; pass < npass; ++pass) {
     // ---- this warp's super-tile (p, q) of the compacted triangle, replica rep
     int task = -1, rep = 0;
-    if (R > 1) {
-      if (warp < ntask * R) {
-        task = warp / R;
-        rep = warp % R;
-      }
+    if (npass == 1 && ntask <= nwarps) {
+      task = wtask_s[warp];
+      rep = wrep_s[warp];
     } else {
       task = pass * nwarps + warp;
       if (task >= ntask) task = -1;
@@ -305,22 +470,28 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 
     if (tile0 < tile1) {
       if (warp == cw) {
-        row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, rowc);
-        if (tile0 + 1 < tile1)
-          row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end,
-                        rowc + 256);
+        row_load<P>(pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, raw);
+        row_store<P>(hc_s, raw, rowc);
+        if (tile0 + 1 < tile1) {
+          row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end, raw);
+          row_store<P>(hc_s, raw, rowc + 256);
+        }
+        if (tile0 + 2 < tile1)
+          row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 2) * 32, row_end, raw);
       }
       __syncthreads();
-      gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rowc, X0, warp, nwarps);
+      gen(0, rowc, X0);
       __syncthreads();
     }
     const bool full = valid == 0xFFFFu;
+    const bool diag = valid == 0x8CEFu;   // bits i * 4 + j, i <= j
     const int offa = p * kRT * 32 + lane, offb = q * kRT * 32 + lane;
     for (int tile = tile0; tile < tile1; ++tile) {
       const int k = tile - tile0;
       const double* X = (k & 1) ? X1 : X0;
       double* const Xn = ((k + 1) & 1) ? X1 : X0;
       const double* const rcn = rowc + ((k + 1) % 3) * 256;
+      // half the warps generate before their DMMAs, half after (overlap)
       const bool gen_first = nbuf == 2 && ((warp >> 2) & 1);
 #if NYS_LARGE_PROBE == 3
       long long TT[6];
@@ -330,7 +501,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #define NYS_T(i)
 #endif
       if (NYS_LARGE_PROBE != 2 && gen_first && tile + 1 < tile1)
-        gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rcn, Xn, warp, nwarps);
+        gen(k + 1, rcn, Xn);
       NYS_T(1);
       if (NYS_LARGE_PROBE != 1 && task >= 0) {
 #pragma unroll 1
@@ -346,6 +517,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             for (int i = 0; i < kRT; ++i)
 #pragma unroll
               for (int j = 0; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
+          } else if (diag) {
+            // complete diagonal super-tile: the i <= j pattern at compile time (a
+            // predicated mma.sync costs a WARPSYNC + NOP per DMMA in SASS)
+#pragma unroll
+            for (int i = 0; i < kRT; ++i)
+#pragma unroll
+              for (int j = i; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
           } else {
 #pragma unroll
             for (int i = 0; i < kRT; ++i)
@@ -359,16 +537,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       NYS_T(2);
       if (nbuf == 1) __syncthreads();
       if (NYS_LARGE_PROBE != 2 && !gen_first && tile + 1 < tile1)
-        gen_tile<P>(lm, m, L, lb_s, NBpad, sigma2, inv, rcn, Xn, warp, nwarps);
+        gen(k + 1, rcn, Xn);
       NYS_T(3);
-      if (warp == cw && tile + 2 < tile1)
-        row_coeffs<P>(hc_s, pts, coef, forcing, n_c, row_begin + (tile + 2) * 32, row_end,
-                      rowc + ((k + 2) % 3) * 256);
+      if (warp == cw && tile + 2 < tile1) {
+        row_store<P>(hc_s, raw, rowc + ((k + 2) % 3) * 256);
+        if (tile + 3 < tile1)
+          row_load<P>(pts, coef, forcing, n_c, row_begin + (tile + 3) * 32, row_end, raw);
+      }
       NYS_T(4);
       __syncthreads();
 #if NYS_LARGE_PROBE == 3
       NYS_T(5);
-      if (blockIdx.x == 5 && (k == 20 || k == 21) && lane == 0)
+      if (blockIdx.x == 70 && (k == 20 || k == 21) && lane == 0)
         printf("k=%d w=%2d task=%d rep=%d/%d L=%d | gen1 %6lld dmma %6lld gen2 %6lld rc %6lld "
                "bar %6lld\n",
                k, warp, task, rep, R, L, TT[1] - TT[0], TT[2] - TT[1], TT[3] - TT[2],
@@ -376,7 +556,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #endif
     }
     // ---- slab write: replicas of one super-tile are added in replica order
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < Rmax; ++r) {
       if (task >= 0 && rep == r) {
 #pragma unroll
         for (int i = 0; i < kRT; ++i)

@@ -148,11 +148,13 @@ def test_row_range_partials_sum_to_full_gram(name):
     np.testing.assert_allclose(parts, full, rtol=0, atol=1e-11 * np.abs(full).max())
 
 
+@pytest.mark.parametrize("uniform", [False, True])
 @pytest.mark.parametrize("m", [80, 94, 134, 150, 256])
-def test_large_m_kspace_gram_matches_oracle(m):
+def test_large_m_kspace_gram_matches_oracle(m, uniform):
     """Large-m kernel (gram_large.cu) for every super-block shape: NB % 4 in
     {3, 0, 1 (stub + corner), 3, 1} -- E = W_ext^T [G g r]^T [G g r] W_ext
-    with G built by the oracle's rbf_block (kernel.py:75-92)."""
+    with G built by the oracle's rbf_block (kernel.py:75-92).  Random points
+    take the per-entry exp() path, a linspace grid the exp recurrence."""
     import torch
 
     from paper_2510_04094_b200 import linear as L
@@ -163,6 +165,8 @@ def test_large_m_kspace_gram_matches_oracle(m):
     rng = np.random.default_rng(m)
     lm = np.linspace(0.0, 0.39 * (m - 1), m)
     pts = np.sort(rng.uniform(lm[0], lm[-1], n))
+    if uniform:
+        pts = np.linspace(lm[0] - 0.3, lm[-1] + 0.2, n)
     coef = rng.normal(size=(p, n))
     forcing = rng.normal(size=n)
     fm = N.build_feature_map(RbfKernel(sigma2), lm)
