@@ -260,9 +260,10 @@ def setup_c2(args, ctx):
     vals_h = torch.from_numpy(bt.cond_values).pin_memory()
     x_h = torch.empty((B, side), dtype=torch.float64).pin_memory()
     info_h = torch.empty(B, dtype=torch.int32).pin_memory()
-    bufs = (torch.empty_like(coef_d), torch.empty_like(forc_d), torch.empty_like(vals_d),
-            torch.empty((B, side), dtype=torch.float64, device=dev),
-            torch.empty(B, dtype=torch.int32, device=dev))
+    # two device staging sets in rotation: step k+1's H2D overlaps step k's solve
+    bufs = [(torch.empty_like(coef_d), torch.empty_like(forc_d), torch.empty_like(vals_d),
+             torch.empty((B, side), dtype=torch.float64, device=dev),
+             torch.empty(B, dtype=torch.int32, device=dev)) for _ in range(2)]
 
     def step():
         pipe.run_device(coef_d, forc_d, vals_d)
@@ -382,16 +383,35 @@ def setup_single(args, ctx):
     coef_h = torch.from_numpy(bt.coef[0]).pin_memory()
     forc_h = torch.from_numpy(bt.forcing[0]).pin_memory()
     x_h = torch.empty(res["x"].shape, dtype=torch.float64).pin_memory()
-    stage = (torch.empty_like(pts_d), torch.empty_like(coef_d), torch.empty_like(forc_d))
+    # two persistent staging sets (the pipeline's graphs stay keyed on the same
+    # buffers) filled on a copy stream: call k+1's H2D overlaps call k's solve
+    stages = [(torch.empty_like(pts_d), torch.empty_like(coef_d), torch.empty_like(forc_d))
+              for _ in range(2)]
+    copy_stream = torch.cuda.Stream(device=dev)
+    free_ev = [None, None]
+    calls = [0]
 
     def step():
         solve(pts_d, coef_d, forc_d)
 
     def e2e():
-        stage[0].copy_(pts_h, non_blocking=True)    # persistent staging: the pipeline's
-        stage[1].copy_(coef_h, non_blocking=True)   # graph stays keyed on the same buffers
-        stage[2].copy_(forc_h, non_blocking=True)
+        k = calls[0] % 2
+        calls[0] += 1
+        stage = stages[k]
+        cur = torch.cuda.current_stream(dev)
+        with torch.cuda.stream(copy_stream):
+            if free_ev[k] is not None:     # the solve that last read this set
+                copy_stream.wait_event(free_ev[k])
+            stage[0].copy_(pts_h, non_blocking=True)
+            stage[1].copy_(coef_h, non_blocking=True)
+            stage[2].copy_(forc_h, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(copy_stream)
+        cur.wait_event(ready)
         r = solve(*stage)
+        done = torch.cuda.Event()
+        done.record(cur)
+        free_ev[k] = done
         x_h.copy_(r["x"], non_blocking=True)
 
     fm = Ac_cache["fm"]
@@ -514,7 +534,7 @@ def main():
     kms = T.kernel_ms(S["kernel"], max(3, min(args.steps, 10)))
     peak, peak_src = _fp64_peak()
     achieved = S["flops_kernel"] / (kms / 1e3) / 1e12
-    for _ in range(2):
+    for _ in range(6):   # every (staging set, eigendecomposition set) pair: graphs captured
         S["e2e"]()
     e2e_ms = T.time(S["e2e"], args.steps)
     if not S["check"]():

@@ -278,10 +278,25 @@ class SharedGridPipeline:
     def run_host(self, coef_h, forcing_h, values_h, x_h, info_h, chunks: int = 4,
                  dev_bufs=None):
         """Pinned host in -> pinned host out.  dev_bufs: optional preallocated
-        device staging (coef, forcing, values, x, info) for the full batch."""
+        device staging (coef, forcing, values, x, info) for the full batch, or a
+        list of such sets used in rotation: the copy stream then refills a set as
+        soon as the solve that last read it has finished, so this call's H2D
+        overlaps the previous call's solve (otherwise it waits for all earlier
+        work on the current stream)."""
         torch = _lib.require_device()[1]
         dev = torch.device(self.device or "cuda")
         B = coef_h.shape[0]
+        free_ev = None
+        if isinstance(dev_bufs, list):
+            k = getattr(self, "_host_calls", 0)
+            self._host_calls = k + 1
+            if not hasattr(self, "_host_free") or len(self._host_free) != len(dev_bufs):
+                self._host_free = [None] * len(dev_bufs)
+            slot = k % len(dev_bufs)
+            free_ev = self._host_free[slot]
+            dev_bufs = dev_bufs[slot]
+        else:
+            slot = None
         if dev_bufs is None:
             dev_bufs = (torch.empty(coef_h.shape, dtype=torch.float64, device=dev),
                         torch.empty(forcing_h.shape, dtype=torch.float64, device=dev),
@@ -292,7 +307,10 @@ class SharedGridPipeline:
         copy = getattr(self, "_copy_stream", None)
         if copy is None:
             copy = self._copy_stream = torch.cuda.Stream(device=dev)
-        copy.wait_stream(comp)
+        if slot is None:
+            copy.wait_stream(comp)
+        elif free_ev is not None:
+            copy.wait_event(free_ev)
         bounds = np.linspace(0, B, chunks + 1).astype(int)
         ready = []
         with torch.cuda.stream(copy):
@@ -316,6 +334,10 @@ class SharedGridPipeline:
             a, b = bounds[c], bounds[c + 1]
             comp.wait_event(ready[c])
             solver.solve_device(dc[a:b], df[a:b], dv[a:b], dx[a:b], di[a:b])
+        if slot is not None:
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            self._host_free[slot] = ev
         x_h.copy_(dx, non_blocking=True)
         info_h.copy_(di, non_blocking=True)
         return x_h, info_h

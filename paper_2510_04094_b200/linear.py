@@ -298,12 +298,15 @@ class SingleSolvePipeline:
     condition points, nys_feature_matrix_f64), the fused feature+Gram kernel and
     the KKT LU + refinement.  Inputs are device tensors; x / info come back in
     buffers owned by the pipeline (overwritten by the next call).  The
-    eigendecomposition runs on its own stream with two alternating buffer sets,
-    so a call's eigensolver overlaps the previous call's Gram and KKT
+    eigendecomposition runs on NYS_EIG_STREAMS (default 2) side streams in
+    rotation with one buffer set per call in flight, so consecutive calls'
+    eigensolvers run concurrently and overlap the previous calls' Gram and KKT
     (NYS_EIG_OVERLAP=0 turns this off); with m_eff + 2 > 72 the kernel-space
-    Gram also runs concurrently with it on a second side stream.
+    Gram also runs concurrently with it on another side stream.
     NYS_GRAPHS=0 runs everything eagerly.
     """
+
+    EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "2"))
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
                  drop_tol: float = 1e-16, device=None):
@@ -339,7 +342,8 @@ class SingleSolvePipeline:
         if self._kspace:
             self._side = torch.cuda.Stream(device=self.device)
             self._kev = torch.cuda.Event()
-            self._kctas = torch.cuda.get_device_properties(self.device).multi_processor_count - 1
+            self._kctas = (torch.cuda.get_device_properties(self.device).multi_processor_count
+                           - max(self.EIG_STREAMS, 1))   # one SM per concurrent eigensolver
             self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
             self._kn_c = None
 
@@ -427,25 +431,30 @@ class SingleSolvePipeline:
             self._kspace_launch(pts, coef, forcing)
         par = None
         if graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0":
-            # the eigendecomposition (one SM) runs on its own stream with two
-            # alternating buffer sets, so this call's eigensolver overlaps the
-            # previous call's Gram/KKT (a set is rewritten only after the
-            # main-stream work that last read it: event)
+            # the eigendecomposition (one CTA, FP64-latency bound) runs on
+            # EIG_STREAMS side streams in rotation, each call with its own buffer
+            # set (EIG_STREAMS + 1 sets), so consecutive calls' eigensolvers run
+            # concurrently on different SMs and overlap the Gram/KKT of earlier
+            # calls; a set is rewritten only after the main-stream work that last
+            # read it (event)
             if self._eigbufs is None:
                 from .nystrom import EigBuffers
-                self._eigbufs = [self.eig, EigBuffers(self.landmarks, self.device)]
-                self._eig_done = [None, None]
-                self._eig_stream = torch.cuda.Stream(device=self.device)
-                self._parity = 0
-            par = self._parity
-            self._parity ^= 1
+                ns = self.EIG_STREAMS
+                self._eigbufs = [self.eig] + [EigBuffers(self.landmarks, self.device)
+                                              for _ in range(ns)]
+                self._eig_done = [None] * (ns + 1)
+                self._eig_streams = [torch.cuda.Stream(device=self.device) for _ in range(ns)]
+                self._calls = 0
+            par = self._calls % len(self._eigbufs)
+            es = self._eig_streams[self._calls % len(self._eig_streams)]
+            self._calls += 1
             if self._eig_done[par] is not None:
-                self._eig_stream.wait_event(self._eig_done[par])
-            self._verify_pending(keep=1)
+                es.wait_event(self._eig_done[par])
+            self._verify_pending(keep=len(self._eig_streams))
             buf = self._eigbufs[par]
             if self._me_known is None:
                 # first call: synchronous build (m_eff, degenerate check, cond gate)
-                with torch.cuda.stream(self._eig_stream):
+                with torch.cuda.stream(es):
                     fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol,
                                            buffers=buf)
                 self._me_known = fm.m_eff
@@ -454,13 +463,13 @@ class SingleSolvePipeline:
                 # steady state: the same landmarks give the same m_eff (deterministic
                 # kernels), so the host does not wait for the eigensolver; this
                 # call's m_eff / info are checked at the start of the next call
-                ev = launch_eig_async(self.kernel, buf, self.drop_tol, self._eig_stream)
+                ev = launch_eig_async(self.kernel, buf, self.drop_tol, es)
                 self._pending.append((ev, buf, self._me_known))
                 fm = NystromFeatureMap(kernel=self.kernel, landmarks=self.landmarks,
                                        m_eff=self._me_known, device=self.device,
                                        d_landmarks=buf.d_lm, d_W=buf.W, d_eigvals=buf.s,
                                        d_eigvecs=buf.V)
-            torch.cuda.current_stream(self.device).wait_stream(self._eig_stream)
+            torch.cuda.current_stream(self.device).wait_stream(es)
             self.eig = buf
         else:
             fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
