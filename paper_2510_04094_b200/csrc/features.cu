@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(kFeatThreads)
       const double* kr = kt + ii * m;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int s = 0;
+#pragma unroll 4
       for (; s + 3 < m; s += 4) {
         a0 = fma(kr[s], W[(size_t)s * ldw + k], a0);
         a1 = fma(kr[s + 1], W[(size_t)(s + 1) * ldw + k], a1);

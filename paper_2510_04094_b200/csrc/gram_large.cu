@@ -47,6 +47,7 @@ constexpr int kRT = 4;             // super-tile edge (blocks)
 #endif
 constexpr int kWarps = NYS_LARGE_WARPS;   // warps per CTA (1 CTA / SM; 12: 3 per SMSP, 168 registers)
 constexpr int kTileKs = 8;         // 4-row k-steps per row tile (32 rows)
+constexpr int kRowStride = 10;     // doubles per row-coefficient record (conflict-free, 16 B aligned)
 constexpr int kMaxSmem = 227 * 1024;
 constexpr double kDeadRatio = 747.0;   // d^2 / sigma2 beyond which exp() is exactly 0
 
@@ -66,7 +67,7 @@ struct LargePlan {
     L.nrr = nrr;
     L.tiles_per_cta = (L.ntiles + nrr - 1) / nrr;
     const size_t xbuf = (size_t)kTileKs * L.NBpad * 32 * sizeof(double);
-    const size_t rowc = 3 * 32 * 8 * sizeof(double);
+    const size_t rowc = 3 * 32 * kRowStride * sizeof(double);
     L.nbuf = (2 * xbuf + rowc <= (size_t)kMaxSmem) ? 2 : 1;
     L.smem = L.nbuf * xbuf + rowc;
     return L;
@@ -122,7 +123,7 @@ NYS_DEV void row_load(const double* __restrict__ pts, const double* __restrict__
 
 template <int P>
 NYS_DEV void row_store(const double (*hc)[nys::kMaxOrder + 1], const RowRaw<P>& w, double* rowc) {
-  double* rc = rowc + (threadIdx.x & 31) * 8;
+  double* rc = rowc + (threadIdx.x & 31) * kRowStride;
   rc[0] = w.t;
 #pragma unroll
   for (int j = 0; j <= P; ++j) {
@@ -167,8 +168,8 @@ NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int L, const int* lb
     const int c = u >> 2, ks = (u & 3) * 2;
     const int s = lb[c] * 8 + csub;
     double* Xo = X + ((size_t)ks * NBpad + c) * 32 + lane;
-    const double* r0 = rowc + (ks * 4 + rsub) * 8;   // rows ks*4 + rsub and +4
-    const double* r1 = r0 + 32;
+    const double* r0 = rowc + (ks * 4 + rsub) * kRowStride;   // rows ks*4 + rsub and +4
+    const double* r1 = r0 + 4 * kRowStride;
     double v0, v1;
     if (s < m) {
       const double l = __ldg(lm + s);
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const size_t xsz = (size_t)kTileKs * NBpad * 32;
   double* const X0 = sm;
   double* const X1 = sm + (nbuf - 1) * xsz;
-  double* const rowc = sm + nbuf * xsz;   // [3][32][8]
+  double* const rowc = sm + nbuf * xsz;   // [3][32][kRowStride]
   __shared__ double blo_s[64], bhi_s[64];
   __shared__ double red_s[3][kWarps];
   __shared__ int nan_s;
@@ -326,8 +327,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         wrep_s[x] = (signed char)(x % Ru);
         wR_s[x] = (signed char)Ru;
       }
-      genw_s[x] = (signed char)(x % nwarps);
     }
+    __syncthreads();
+    if (threadIdx.x < 64) genw_s[threadIdx.x] = (signed char)(threadIdx.x % nwarps);
     __syncthreads();
     R = wR_s[warp];
     npass = 1;
@@ -409,18 +411,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           const double base = geA[g] * gP[g];
 #pragma unroll
           for (int ks = 0; ks < kTileKs; ++ks) {
-            const double* r = rc + (ks * 4 + rsub) * 8;
-            const double d = gl[g] - r[0];
-            double poly = r[1 + P];
+            const double* r = rc + (ks * 4 + rsub) * kRowStride;
+            double rv[(P + 3) & ~1];   // t, q_0..q_P by 16-byte loads
 #pragma unroll
-            for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, r[1 + j]);
+            for (int j = 0; j < ((P + 3) & ~1); j += 2) {
+              const double2 v2 = *reinterpret_cast<const double2*>(r + j);
+              rv[j] = v2.x;
+              rv[j + 1] = v2.y;
+            }
+            const double d = gl[g] - rv[0];
+            double poly = rv[1 + P];
+#pragma unroll
+            for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, rv[1 + j]);
             Xo[(size_t)ks * NBpad * 32] = poly * ((base * rp[ks]) * qt[ks]);
           }
           gP[g] *= rp[8];
         } else {
 #pragma unroll
           for (int ks = 0; ks < kTileKs; ++ks) {
-            const double* r = rc + (ks * 4 + rsub) * 8;
+            const double* r = rc + (ks * 4 + rsub) * kRowStride;
             Xo[(size_t)ks * NBpad * 32] = (s == m) ? r[6] : (s == m + 1) ? r[7] : 0.0;
           }
         }
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         row_store<P>(hc_s, raw, rowc);
         if (tile0 + 1 < tile1) {
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end, raw);
-          row_store<P>(hc_s, raw, rowc + 256);
+          row_store<P>(hc_s, raw, rowc + 32 * kRowStride);
         }
         if (tile0 + 2 < tile1)
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 2) * 32, row_end, raw);
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const int k = tile - tile0;
       const double* X = (k & 1) ? X1 : X0;
       double* const Xn = ((k + 1) & 1) ? X1 : X0;
-      const double* const rcn = rowc + ((k + 1) % 3) * 256;
+      const double* const rcn = rowc + ((k + 1) % 3) * 32 * kRowStride;
       // half the warps generate before their DMMAs, half after (overlap)
       const bool gen_first = nbuf == 2 && ((warp >> 2) & 1);
 #if NYS_LARGE_PROBE == 3
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         gen(k + 1, rcn, Xn);
       NYS_T(3);
       if (warp == cw && tile + 2 < tile1) {
-        row_store<P>(hc_s, raw, rowc + ((k + 2) % 3) * 256);
+        row_store<P>(hc_s, raw, rowc + ((k + 2) % 3) * 32 * kRowStride);
         if (tile + 3 < tile1)
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile + 3) * 32, row_end, raw);
       }
@@ -580,6 +589,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 }
 
 // K[r][c] = sum over CTAs (fixed order) of their slabs where both blocks are live
+// (dead slab entries are never written: their loads are predicated off, and
+// the select adds an exact 0); loads unrolled 8 deep so they are in flight
+// together instead of one L2 round trip per CTA
 __global__ void large_reduce_kernel(const double* __restrict__ slabs,
                                     const unsigned long long* __restrict__ live, int nrr, int ld,
                                     int Pe, double* __restrict__ K) {
@@ -588,44 +600,98 @@ __global__ void large_reduce_kernel(const double* __restrict__ slabs,
   const int r = e / Pe, c = e % Pe;
   if (c < r) return;
   const unsigned long long need = (1ull << (r / 8)) | (1ull << (c / 8));
+  const double* p = slabs + (size_t)r * ld + c;
+  const size_t step = (size_t)ld * ld;
   double s = 0.0;
-  for (int rr = 0; rr < nrr; ++rr)
-    if ((live[rr] & need) == need) s += slabs[((size_t)rr * ld + r) * ld + c];
+  int rr = 0;
+  for (; rr + 8 <= nrr; rr += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = ((__ldg(live + rr + u) & need) == need) ? __ldg(p + (rr + u) * step) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; rr < nrr; ++rr)
+    if ((live[rr] & need) == need) s += p[rr * step];
   K[(size_t)r * Pe + c] = s;
   K[(size_t)c * Pe + r] = s;
 }
 
-// T = K W_ext  (Pe x Pw), then E = W_ext^T T (Pw x Pw);  W_ext = diag(W, 1, 1)
-__global__ void proj_right_kernel(const double* __restrict__ K, int Pe, const double* __restrict__ W,
-                                  int ldw, int m, int m_eff, double* __restrict__ T) {
-  const int Pw = m_eff + 2;
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= Pe * Pw) return;
-  int r = e / Pw, c = e % Pw;
-  double acc = 0.0;
-  if (c < m_eff) {
-    for (int s = 0; s < m; ++s) acc += K[(size_t)r * Pe + s] * W[(size_t)s * ldw + c];
-  } else {
-    acc = K[(size_t)r * Pe + m + (c - m_eff)];
+// T = K W_ext (Pe x Pw), then E = W_ext^T T (Pw x Pw);  W_ext = diag(W, 1, 1).
+// One warp per 8 x 8 output tile, DMMA.8x8x4 over the landmark index s with
+// the fragments read straight from L2 (K, W, T are <= 0.6 MB).  E is
+// computed on the upper tile triangle and mirrored, so it is exactly symmetric.
+constexpr int kProjWarps = 4;
+__global__ void __launch_bounds__(kProjWarps * 32)
+    proj_right_kernel(const double* __restrict__ K, int Pe, const double* __restrict__ W,
+                      int ldw, int m, int m_eff, double* __restrict__ T) {
+  const int Pw = m_eff + 2, lane = threadIdx.x & 31;
+  const int tiles_c = (Pw + 7) / 8;
+  const int t = blockIdx.x * kProjWarps + (threadIdx.x >> 5);
+  const int r0 = (t / tiles_c) * 8, c0 = (t % tiles_c) * 8;
+  if (r0 >= Pe) return;
+  const int ar = r0 + (lane >> 2), bc = c0 + (lane >> 2), kq = lane & 3;
+  double c_0 = 0.0, c_1 = 0.0;
+  if (c0 < m_eff) {
+    for (int s = 0; s < m; s += 4) {
+      const int ks = s + kq;
+      const double a = (ar < Pe && ks < m) ? K[(size_t)ar * Pe + ks] : 0.0;
+      const double b = (bc < m_eff && ks < m) ? W[(size_t)ks * ldw + bc] : 0.0;
+      nys::dmma(c_0, c_1, a, b);
+    }
   }
-  T[e] = acc;
+  const int rr = r0 + (lane >> 2);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int cc = c0 + 2 * (lane & 3) + j;
+    if (rr >= Pe || cc >= Pw) continue;
+    T[(size_t)rr * Pw + cc] = cc < m_eff ? (j ? c_1 : c_0) : K[(size_t)rr * Pe + m + (cc - m_eff)];
+  }
 }
 
-__global__ void proj_left_kernel(const double* __restrict__ T, int Pe, const double* __restrict__ W,
-                                 int ldw, int m, int m_eff, double* __restrict__ E) {
-  const int Pw = m_eff + 2;
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= Pw * Pw) return;
-  int r = e / Pw, c = e % Pw;
-  if (c < r) return;
-  double acc = 0.0;
-  if (r < m_eff) {
-    for (int s = 0; s < m; ++s) acc += W[(size_t)s * ldw + r] * T[(size_t)s * Pw + c];
-  } else {
-    acc = T[(size_t)(m + (r - m_eff)) * Pw + c];
+__global__ void __launch_bounds__(kProjWarps * 32)
+    proj_left_kernel(const double* __restrict__ T, int Pe, const double* __restrict__ W,
+                     int ldw, int m, int m_eff, double* __restrict__ E) {
+  const int Pw = m_eff + 2, lane = threadIdx.x & 31;
+  const int nt = (Pw + 7) / 8;
+  int t = blockIdx.x * kProjWarps + (threadIdx.x >> 5);
+  if (t >= nt * (nt + 1) / 2) return;
+  int I = 0;   // upper tile triangle, row-major
+  while (t >= nt - I) {
+    t -= nt - I;
+    ++I;
   }
-  E[(size_t)r * Pw + c] = acc;
-  E[(size_t)c * Pw + r] = acc;
+  const int r0 = I * 8, c0 = (I + t) * 8;
+  const int ar = r0 + (lane >> 2), bc = c0 + (lane >> 2), kq = lane & 3;
+  double c_0 = 0.0, c_1 = 0.0;
+  if (r0 < m_eff) {
+    for (int s = 0; s < m; s += 4) {
+      const int ks = s + kq;
+      const double a = (ar < m_eff && ks < m) ? W[(size_t)ks * ldw + ar] : 0.0;
+      const double b = (bc < Pw && ks < m) ? T[(size_t)ks * Pw + bc] : 0.0;
+      nys::dmma(c_0, c_1, a, b);
+    }
+  }
+  const int rr = r0 + (lane >> 2);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int cc = c0 + 2 * (lane & 3) + j;
+    if (rr >= Pw || cc >= Pw || cc < rr) continue;
+    const double v = rr < m_eff ? (j ? c_1 : c_0) : T[(size_t)(m + (rr - m_eff)) * Pw + cc];
+    E[(size_t)rr * Pw + cc] = v;
+    E[(size_t)cc * Pw + rr] = v;
+  }
+}
+
+void launch_proj(const double* K, int Pe, const double* W, int ldw, int m, int m_eff, double* T,
+                 double* E, cudaStream_t st) {
+  const int Pw = m_eff + 2, tr = (Pe + 7) / 8, tc = (Pw + 7) / 8;
+  proj_right_kernel<<<(tr * tc + kProjWarps - 1) / kProjWarps, kProjWarps * 32, 0, st>>>(
+      K, Pe, W, ldw, m, m_eff, T);
+  proj_left_kernel<<<(tc * (tc + 1) / 2 + kProjWarps - 1) / kProjWarps, kProjWarps * 32, 0, st>>>(
+      T, Pe, W, ldw, m, m_eff, E);
+  nys_host::count_launches(2);
 }
 
 }  // namespace
@@ -671,10 +737,7 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
   large_reduce_kernel<<<(L.Pe * L.Pe + 255) / 256, 256, 0, st>>>(slabs, live, L.nrr, L.ld, L.Pe,
                                                                  K);
   nys_host::count_launches(1);
-  proj_right_kernel<<<(L.Pe * Pw + 127) / 128, 128, 0, st>>>(K, L.Pe, W, ldw, m, m_eff, T);
-  nys_host::count_launches(1);
-  proj_left_kernel<<<(Pw * Pw + 127) / 128, 128, 0, st>>>(T, L.Pe, W, ldw, m, m_eff, gram_ext);
-  nys_host::count_launches(1);
+  launch_proj(K, L.Pe, W, ldw, m, m_eff, T, gram_ext, st);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
@@ -737,11 +800,9 @@ extern "C" int nys_kspace_project_f64(const double* K, int m, const double* W, i
   if (m < 1 || m_eff < 1 || m_eff > m || ldw < m_eff) return NYS_EINVAL;
   if (ws == nullptr || ws_bytes < nys_kspace_project_workspace_bytes(m, m_eff)) return NYS_EWORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int Pe = m + 2, Pw = m_eff + 2;
+  const int Pe = m + 2;
   double* T = static_cast<double*>(ws);
-  proj_right_kernel<<<(Pe * Pw + 127) / 128, 128, 0, st>>>(K, Pe, W, ldw, m, m_eff, T);
-  proj_left_kernel<<<(Pw * Pw + 127) / 128, 128, 0, st>>>(T, Pe, W, ldw, m, m_eff, gram_ext);
-  nys_host::count_launches(2);
+  launch_proj(K, Pe, W, ldw, m, m_eff, T, gram_ext, st);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }
