@@ -23,6 +23,9 @@
 #include "common.cuh"
 
 namespace nys_host {
+int launch_kkt_chol_dense(const double* dense, int m_eff, int n_cond, const double* Ac,
+                          const double* beta, const double* values, double gamma, int B,
+                          double* x, int* info, cudaStream_t st);
 int launch_kkt_big(const double* E, int m_eff, int n_cond, const double* Ac, const double* beta,
                    const double* values, double gamma, double* x, int* info, void* ws,
                    size_t ws_bytes, cudaStream_t st);
@@ -457,6 +460,18 @@ int launch_kkt(const double* gram, int m_eff, int ncond, const double* Ac, const
                double* rhs, void* ws, size_t ws_bytes, cudaStream_t st,
                bool only_flagged = false) {
   const int n = m_eff + 1 + ncond;
+  if (B == 1 && M == nullptr && rhs == nullptr && !only_flagged && n <= kWarpKktMaxN &&
+      getenv("NYS_KKT_LU") == nullptr) {
+    // single solve (SingleSolvePipeline): Cholesky of the SPD omega block + Schur
+    // for bias and conditions (kkt_chol.cu, the batched solver's algorithm); the
+    // LU below re-solves it only if the Cholesky broke down
+    const int rc = launch_kkt_chol_dense(gram, m_eff, ncond, Ac, beta, values, gamma, B, x, info,
+                                         st);
+    if (rc == NYS_OK)
+      return launch_kkt(gram, m_eff, ncond, Ac, beta, values, gamma, B, x, info, M, rhs, ws,
+                        ws_bytes, st, true);
+    if (rc != NYS_EUNSUPPORTED) return rc;
+  }
   if (n <= kWarpKktMaxN) {
     size_t dyn = ((size_t)n * n + 3 * (size_t)n) * sizeof(double);
     if (dyn > 48 * 1024) {

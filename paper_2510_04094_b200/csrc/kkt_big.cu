@@ -254,6 +254,14 @@ __global__ void __launch_bounds__(kBigThreads, 1)
   int badS = 0;
 #pragma unroll
   for (int a = 0; a < Q; ++a) piv[a] = a;
+  // pivots lost to cancellation (duplicated conditions: S singular up to
+  // rounding) go to the LU, which decides singularity as the reference does
+  double smax = 0.0;
+#pragma unroll
+  for (int a = 0; a < Q; ++a)
+#pragma unroll
+    for (int c = 0; c < Q; ++c) smax = fmax(smax, fabs(S[a][c]));
+  const double piv_floor = 64.0 * 2.220446049250313e-16 * smax;
 #pragma unroll
   for (int k = 0; k < Q; ++k) {
     int pr = k;
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(kBigThreads, 1)
         best = fabs(S[r][k]);
         pr = r;
       }
-    if (!(best > 0.0)) badS = 1;
+    if (!(best > piv_floor)) badS = 1;
 #pragma unroll
     for (int r = k + 1; r < Q; ++r)
       if (r == pr) {

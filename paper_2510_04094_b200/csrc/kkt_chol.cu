@@ -199,9 +199,12 @@ __global__ void __launch_bounds__(32)
 #pragma unroll
   for (int a = 0; a < P; ++a) {
     double d = S[a][a];
+    const double d0 = d;
 #pragma unroll
     for (int c = 0; c < a; ++c) d -= S[a][c] * S[a][c];
-    if (!(d > 0.0)) bad = 1;
+    // a pivot lost to cancellation (e.g. duplicated conditions: S singular up to
+    // rounding) goes to the LU, which decides singularity as the reference does
+    if (!(d > 64.0 * 2.220446049250313e-16 * d0)) bad = 1;
     S[a][a] = sqrt(d > 0.0 ? d : 1.0);
 #pragma unroll
     for (int r = a + 1; r < P; ++r) {
@@ -357,6 +360,25 @@ int launch_chol(const double* dense, int m_eff, const double* Ac, const double* 
 }
 
 }  // namespace
+
+namespace nys_host {
+// dense extended Grams (B x Pe x Pe) -> Cholesky + Schur (blocked DMMA when m_eff
+// is a multiple of 8 in [32, 64]); instances whose Cholesky breaks down are
+// flagged for the LU (caller re-runs launch_kkt with only_flagged)
+int launch_kkt_chol_dense(const double* dense, int m_eff, int n_cond, const double* Ac,
+                          const double* beta, const double* values, double gamma, int B,
+                          double* x, int* info, cudaStream_t st) {
+  if (m_eff < 1 || n_cond < 1 || n_cond > 4 || m_eff + 1 > kMaxNh) return NYS_EUNSUPPORTED;
+  int rc = launch_kkt_blocked(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, st);
+  if (rc != NYS_EUNSUPPORTED) return rc;
+  switch (n_cond) {
+    case 1: return launch_chol<1>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+    case 2: return launch_chol<2>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+    case 3: return launch_chol<3>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+    default: return launch_chol<4>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+  }
+}
+}  // namespace nys_host
 
 extern "C" int nys_batch_kkt_solve_f64(const void* batch_workspace, int n_c, int m_eff, int p,
                                        int n_cond, const double* Ac, const double* beta,
