@@ -127,24 +127,47 @@ __global__ void __launch_bounds__(kFusedWarps * 32)
 }
 
 // CTA partials -> dense E (Pe x Pe), fixed summation order
+// partials -> dense E.  Eight lanes per output entry, each summing a fixed
+// contiguous range of the CTA partials (8 loads in flight), combined by a
+// fixed shuffle tree: deterministic, and 8x the parallelism of one thread per
+// entry (config 1: 28 x 64 entries over ~300 partials)
+constexpr int kFinSub = 8;
 __global__ void fused_finalize_kernel(const double* __restrict__ part, int nparts, int NB, int Pe,
                                       double* __restrict__ gram) {
   const int npair = NB * (NB + 1) / 2;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < npair * 64; e += gridDim.x * blockDim.x) {
-    int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
-    int I = 0, rem = q;
-    while (rem >= NB - I) {
-      rem -= NB - I;
-      ++I;
+  const int g = threadIdx.x & (kFinSub - 1);
+  const int e = (blockIdx.x * blockDim.x + threadIdx.x) / kFinSub;
+  const bool ok = e < npair * 64;
+  const int chunk = (nparts + kFinSub - 1) / kFinSub;
+  const int p0 = min(nparts, g * chunk), p1 = min(nparts, p0 + chunk);
+  const size_t step = (size_t)npair * 64;
+  const double* src = part + (ok ? e : 0);
+  double s = 0.0;
+  int p = p0;
+  if (ok) {
+    for (; p + 8 <= p1; p += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(src + (p + u) * step);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
     }
-    int J = I + rem;
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * npair * 64 + e];
-    int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
-    if (r < Pe && c < Pe) {
-      gram[(size_t)r * Pe + c] = s;
-      gram[(size_t)c * Pe + r] = s;
-    }
+    for (; p < p1; ++p) s += src[p * step];
+  }
+#pragma unroll
+  for (int o = 1; o < kFinSub; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (!ok || g != 0) return;
+  const int q = e >> 6, w = e & 63, lane = w >> 1, j = w & 1;
+  int I = 0, rem = q;
+  while (rem >= NB - I) {
+    rem -= NB - I;
+    ++I;
+  }
+  const int J = I + rem;
+  const int r = I * 8 + (lane >> 2), c = J * 8 + 2 * (lane & 3) + j;
+  if (r < Pe && c < Pe) {
+    gram[(size_t)r * Pe + c] = s;
+    gram[(size_t)c * Pe + r] = s;
   }
 }
 
@@ -244,8 +267,8 @@ extern "C" int nys_fused_gram_f64(const double* landmarks, int m, const double* 
     default: rc = dispatch_fused<4>(F, landmarks, m, W, ldw, m_eff, sigma2, pts, coef, forcing, n_c, row_begin, row_end, part, st); break;
   }
   if (rc) return rc;
-  fused_finalize_kernel<<<(F.npair * 64 + 255) / 256, 256, 0, st>>>(part, F.nctas, F.NB, m_eff + 2,
-                                                                    gram_ext);
+  fused_finalize_kernel<<<(F.npair * 64 * kFinSub + 255) / 256, 256, 0, st>>>(
+      part, F.nctas, F.NB, m_eff + 2, gram_ext);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
