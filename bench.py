@@ -438,9 +438,11 @@ def setup_single(args, ctx):
                "step": "eig + fused feature/Gram + KKT LU" + (" + all-reduce" if shard else "")},
         note="algorithmic F of SURVEY.md 8(d)" + (
             "; config 4 accumulates the Gram in kernel space (cond(Omega)=28, SURVEY A1 "
-            "1.3e-13) and skips landmark blocks whose exp() underflows to exactly 0 for a CTA's "
-            "rows (bit-identical sums), so the dense F overstates the work: executed_* counts "
-            "the DMMA flops actually issued" if kspace else ""),
+            "1.3e-13), skips landmark blocks whose exp() underflows to exactly 0 for a CTA's "
+            "rows, and on the uniform grid forms the exponentials by a multiplicative "
+            "recurrence (two exp() per lane per 4 tiles, ~1e-14 relative), so the dense F "
+            "overstates the work: executed_* counts the DMMA flops actually issued"
+            if kspace else ""),
         per_rank_units=False)
 
 

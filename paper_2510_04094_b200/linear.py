@@ -298,7 +298,7 @@ class SingleSolvePipeline:
     condition points, nys_feature_matrix_f64), the fused feature+Gram kernel and
     the KKT LU + refinement.  Inputs are device tensors; x / info come back in
     buffers owned by the pipeline (overwritten by the next call).  The
-    eigendecomposition runs on NYS_EIG_STREAMS (default 2) side streams in
+    eigendecomposition runs on 2-3 (NYS_EIG_STREAMS) side streams in
     rotation with one buffer set per call in flight, so consecutive calls'
     eigensolvers run concurrently and overlap the previous calls' Gram and KKT
     (NYS_EIG_OVERLAP=0 turns this off); with m_eff + 2 > 72 the kernel-space
@@ -306,7 +306,16 @@ class SingleSolvePipeline:
     NYS_GRAPHS=0 runs everything eagerly.
     """
 
-    EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "2"))
+    # concurrent eigendecompositions: enough that the one-CTA eigensolver
+    # (B200, D&C: 0.14 ms at m = 20, 0.30 ms at m = 50, 3.7 ms at m = 256) keeps
+    # up with the rest of a call (0.1 ms, 0.14 ms, 3.0 ms): 3 for mid-size
+    # landmark sets, else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
+    EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "0"))
+
+    def _eig_streams(self) -> int:
+        if self.EIG_STREAMS > 0:
+            return self.EIG_STREAMS
+        return 3 if 32 < self.landmarks.size <= 128 else 2
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
                  drop_tol: float = 1e-16, device=None):
@@ -343,7 +352,7 @@ class SingleSolvePipeline:
             self._side = torch.cuda.Stream(device=self.device)
             self._kev = torch.cuda.Event()
             self._kctas = (torch.cuda.get_device_properties(self.device).multi_processor_count
-                           - max(self.EIG_STREAMS, 1))   # one SM per concurrent eigensolver
+                           - self._eig_streams())   # one SM per concurrent eigensolver
             self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
             self._kn_c = None
 
@@ -439,7 +448,7 @@ class SingleSolvePipeline:
             # read it (event)
             if self._eigbufs is None:
                 from .nystrom import EigBuffers
-                ns = self.EIG_STREAMS
+                ns = self._eig_streams()
                 self._eigbufs = [self.eig] + [EigBuffers(self.landmarks, self.device)
                                               for _ in range(ns)]
                 self._eig_done = [None] * (ns + 1)
