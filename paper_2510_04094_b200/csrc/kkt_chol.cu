@@ -359,6 +359,278 @@ int launch_chol(const double* dense, int m_eff, const double* Ac, const double* 
   return launch_chol_nc<P, 3, 3>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
 }
 
+
+// Single (or few) small systems: the same Cholesky + Schur algorithm as
+// kkt_chol_kernel, spread over one CTA of 8 warps so a lone system is not bound
+// by one warp's latency chains (config 1: 86 us with one warp).  H is dense in
+// shared memory with an odd leading dimension (column walks are conflict-free);
+// the Cholesky runs right-looking with the forward elimination of Y = [C^T | r]
+// folded into every step (warps take rows, lanes columns, two barriers per
+// column); S = W^T W by block reductions in fixed order; the triangular sweeps
+// of the solve / refinement run in warp 0 (per-row dependency, __syncwarp
+// only); the refinement residual is a CTA-wide GEMV over E.
+constexpr int kSmallThreads = 256;
+template <int P>
+__global__ void __launch_bounds__(kSmallThreads)
+    kkt_small_cta_kernel(const double* __restrict__ gram, int m_eff, const double* __restrict__ Ac,
+                         const double* __restrict__ beta, const double* __restrict__ values,
+                         double gamma, double* __restrict__ xout, int* __restrict__ info) {
+  extern __shared__ __align__(16) double dsm[];
+  constexpr int R = P + 1;
+  constexpr int NW = kSmallThreads / 32;
+  constexpr int NS = P * (P + 1) / 2;
+  __shared__ double red[NW][NS > R ? NS : R];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, b = blockIdx.x;
+  const int nh = m_eff + 1, me = m_eff, Pe = m_eff + 2, ld = nh | 1;
+  const double* E = gram + (size_t)b * Pe * Pe;
+  const double* vals = values + (size_t)b * P;
+  double* L = dsm;                          // nh x ld, lower triangle
+  double* dinv = L + (size_t)nh * ld;       // nh
+  double* Y = dinv + nh;                    // nh x R
+  double* xs = Y + (size_t)nh * R;          // nh + P
+  const double inv_gamma = 1.0 / gamma;
+  for (int e = tid; e < nh * nh; e += kSmallThreads) {
+    const int i = e / nh, j = e % nh;
+    if (j <= i) {
+      const double v = __ldg(E + (size_t)i * Pe + j);
+      L[i * ld + j] = (i == j && i < me) ? inv_gamma + v : v;
+    }
+  }
+  for (int i = tid; i < nh; i += kSmallThreads) {
+#pragma unroll
+    for (int mu = 0; mu < P; ++mu) Y[i * R + mu] = i < me ? Ac[(size_t)mu * me + i] : beta[mu];
+    Y[i * R + P] = E[(size_t)i * Pe + me + 1];
+  }
+  __syncthreads();
+  // ---- H = L L^T with Y <- L^{-1} Y folded in
+  int chol_bad = 0;
+  for (int k = 0; k < nh; ++k) {
+    const double akk = L[k * ld + k];
+    if (!(akk > 0.0) || !isfinite(akk)) {   // uniform: every thread reads the same value
+      chol_bad = 1;
+      break;
+    }
+    const double inv = rsqrt(akk);
+    for (int i = k + 1 + tid; i < nh; i += kSmallThreads) L[i * ld + k] *= inv;
+    if (tid == 0) {
+      L[k * ld + k] = akk * inv;
+      dinv[k] = inv;
+    }
+    if (tid < R) Y[k * R + tid] *= inv;
+    __syncthreads();
+    for (int i = k + 1 + warp; i < nh; i += NW) {
+      const double li = L[i * ld + k];
+      for (int j = k + 1 + lane; j <= i; j += 32) L[i * ld + j] -= li * L[j * ld + k];
+      if (lane < R) Y[i * R + lane] -= li * Y[k * R + lane];
+    }
+    __syncthreads();
+  }
+  if (chol_bad) {
+    if (tid == 0) info[b] = kNeedsLu;
+    return;
+  }
+  // ---- S = W^T W (W = Y[:, :P]); every thread gets the same sums (fixed order)
+  {
+    double a[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) a[q] = 0.0;
+    for (int i = tid; i < nh; i += kSmallThreads) {
+      int q = 0;
+#pragma unroll
+      for (int x = 0; x < P; ++x)
+#pragma unroll
+        for (int c = 0; c <= x; ++c, ++q) a[q] = fma(Y[i * R + x], Y[i * R + c], a[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+      if (lane == 0) red[warp][q] = a[q];
+    }
+  }
+  __syncthreads();
+  double S[P][P];
+  {
+    int q = 0;
+#pragma unroll
+    for (int x = 0; x < P; ++x)
+#pragma unroll
+      for (int c = 0; c <= x; ++c, ++q) {
+        double v = 0.0;
+        for (int w = 0; w < NW; ++w) v += red[w][q];
+        S[x][c] = v;
+      }
+  }
+  int bad = 0;
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    double d = S[a][a];
+    const double d0 = d;
+#pragma unroll
+    for (int c = 0; c < a; ++c) d -= S[a][c] * S[a][c];
+    if (!(d > 64.0 * 2.220446049250313e-16 * d0)) bad = 1;
+    S[a][a] = sqrt(d > 0.0 ? d : 1.0);
+#pragma unroll
+    for (int r = a + 1; r < P; ++r) {
+      double t = S[r][a];
+#pragma unroll
+      for (int c = 0; c < a; ++c) t -= S[r][c] * S[a][c];
+      S[r][a] = t / S[a][a];
+    }
+  }
+  if (bad) {
+    if (tid == 0) info[b] = kNeedsLu;
+    return;
+  }
+  __syncthreads();   // red reused below
+
+  for (int pass = 0; pass < 2; ++pass) {
+    double rv[P];
+    if (pass == 0) {
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) rv[mu] = vals[mu];
+    } else {
+      // r1 = rhs1 - H x - C^T lambda (rows by thread, E symmetric: coalesced)
+      for (int i = tid; i < nh; i += kSmallThreads) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int j = 0;
+        for (; j + 4 <= nh; j += 4) {
+          const double e0 = __ldg(E + (size_t)j * Pe + i), e1 = __ldg(E + (size_t)(j + 1) * Pe + i);
+          const double e2 = __ldg(E + (size_t)(j + 2) * Pe + i), e3 = __ldg(E + (size_t)(j + 3) * Pe + i);
+          a0 = fma(e0, xs[j], a0);
+          a1 = fma(e1, xs[j + 1], a1);
+          a2 = fma(e2, xs[j + 2], a2);
+          a3 = fma(e3, xs[j + 3], a3);
+        }
+        for (; j < nh; ++j) a0 = fma(__ldg(E + (size_t)j * Pe + i), xs[j], a0);
+        double a = (a0 + a1) + (a2 + a3);
+        if (i < me) a = fma(inv_gamma, xs[i], a);
+#pragma unroll
+        for (int mu = 0; mu < P; ++mu) a += (i < me ? Ac[(size_t)mu * me + i] : beta[mu]) * xs[nh + mu];
+        Y[i * R + P] = E[(size_t)i * Pe + me + 1] - a;
+      }
+      double c[P];
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) c[mu] = 0.0;
+      for (int i = tid; i < me; i += kSmallThreads)
+#pragma unroll
+        for (int mu = 0; mu < P; ++mu) c[mu] = fma(Ac[(size_t)mu * me + i], xs[i], c[mu]);
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) c[mu] += __shfl_xor_sync(0xffffffffu, c[mu], o);
+        if (lane == 0) red[warp][mu] = c[mu];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) {
+        double v = 0.0;
+        for (int w = 0; w < NW; ++w) v += red[w][mu];
+        rv[mu] = vals[mu] - (v + beta[mu] * xs[me]);
+      }
+      // forward sweep of the r column (warp 0; L^{-1} C^T is unchanged)
+      if (warp == 0) {
+        for (int j = 0; j < nh; ++j) {
+          const double yj = Y[j * R + P] * dinv[j];
+          __syncwarp();
+          if (lane == 0) Y[j * R + P] = yj;
+          for (int i = j + 1 + lane; i < nh; i += 32) Y[i * R + P] -= L[i * ld + j] * yj;
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    }
+    // lambda = S^{-1} (W^T y1 - v)
+    {
+      double a[P];
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) a[mu] = 0.0;
+      for (int i = tid; i < nh; i += kSmallThreads)
+#pragma unroll
+        for (int mu = 0; mu < P; ++mu) a[mu] = fma(Y[i * R + mu], Y[i * R + P], a[mu]);
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) a[mu] += __shfl_xor_sync(0xffffffffu, a[mu], o);
+        if (lane == 0) red[warp][mu] = a[mu];
+      }
+    }
+    __syncthreads();
+    double t[P];
+#pragma unroll
+    for (int mu = 0; mu < P; ++mu) {
+      double v = 0.0;
+      for (int w = 0; w < NW; ++w) v += red[w][mu];
+      t[mu] = v - rv[mu];
+    }
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      double v = t[a];
+#pragma unroll
+      for (int c = 0; c < a; ++c) v -= S[a][c] * t[c];
+      t[a] = v / S[a][a];
+    }
+#pragma unroll
+    for (int a = P - 1; a >= 0; --a) {
+      double v = t[a];
+#pragma unroll
+      for (int c = a + 1; c < P; ++c) v -= S[c][a] * t[c];
+      t[a] = v / S[a][a];
+    }
+    // z = y1 - W lambda ; x = L^{-T} z (warp 0)
+    for (int i = tid; i < nh; i += kSmallThreads) {
+      double v = Y[i * R + P];
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) v -= Y[i * R + mu] * t[mu];
+      Y[i * R + P] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      for (int j = nh - 1; j >= 0; --j) {
+        const double xj = Y[j * R + P] * dinv[j];
+        __syncwarp();
+        if (lane == 0) Y[j * R + P] = xj;
+        for (int i = lane; i < j; i += 32) Y[i * R + P] -= L[j * ld + i] * xj;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < nh; i += kSmallThreads) {
+      const double v = Y[i * R + P];
+      xs[i] = pass == 0 ? v : xs[i] + v;
+    }
+    if (tid == 0)
+#pragma unroll
+      for (int mu = 0; mu < P; ++mu) xs[nh + mu] = pass == 0 ? t[mu] : xs[nh + mu] + t[mu];
+    __syncthreads();
+  }
+  const int n = nh + P;
+  int nonfinite = 0;
+  for (int i = tid; i < n; i += kSmallThreads) {
+    const double v = xs[i];
+    if (!isfinite(v)) nonfinite = 1;
+    xout[(size_t)b * n + i] = v;
+  }
+  nonfinite = __syncthreads_or(nonfinite);
+  if (tid == 0) info[b] = nonfinite ? kNeedsLu : NYS_INFO_OK;
+}
+
+template <int P>
+int launch_small_cta(const double* dense, int m_eff, const double* Ac, const double* beta,
+                     const double* values, double gamma, int B, double* x, int* info,
+                     cudaStream_t st) {
+  const int nh = m_eff + 1, ld = nh | 1;
+  const size_t dyn = ((size_t)nh * ld + nh + (size_t)nh * (P + 1) + nh + P) * sizeof(double);
+  auto kern = kkt_small_cta_kernel<P>;
+  if (dyn > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+  }
+  kern<<<B, kSmallThreads, dyn, st>>>(dense, m_eff, Ac, beta, values, gamma, x, info);
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
 }  // namespace
 
 namespace nys_host {
@@ -369,6 +641,14 @@ int launch_kkt_chol_dense(const double* dense, int m_eff, int n_cond, const doub
                           const double* beta, const double* values, double gamma, int B,
                           double* x, int* info, cudaStream_t st) {
   if (m_eff < 1 || n_cond < 1 || n_cond > 4 || m_eff + 1 > kMaxNh) return NYS_EUNSUPPORTED;
+  if (B <= 8 && getenv("NYS_KKT_WARP") == nullptr) {   // few systems: one CTA each
+    switch (n_cond) {
+      case 1: return launch_small_cta<1>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+      case 2: return launch_small_cta<2>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+      case 3: return launch_small_cta<3>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+      default: return launch_small_cta<4>(dense, m_eff, Ac, beta, values, gamma, B, x, info, st);
+    }
+  }
   int rc = launch_kkt_blocked(dense, m_eff, n_cond, Ac, beta, values, gamma, B, x, info, st);
   if (rc != NYS_EUNSUPPORTED) return rc;
   switch (n_cond) {
