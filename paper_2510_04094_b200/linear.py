@@ -312,7 +312,7 @@ class SingleSolvePipeline:
     # landmark sets, else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
     EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "0"))
 
-    def _eig_streams(self) -> int:
+    def _n_eig_streams(self) -> int:
         if self.EIG_STREAMS > 0:
             return self.EIG_STREAMS
         return 3 if 32 < self.landmarks.size <= 128 else 2
@@ -352,7 +352,7 @@ class SingleSolvePipeline:
             self._side = torch.cuda.Stream(device=self.device)
             self._kev = torch.cuda.Event()
             self._kctas = (torch.cuda.get_device_properties(self.device).multi_processor_count
-                           - self._eig_streams())   # one SM per concurrent eigensolver
+                           - self._n_eig_streams())   # one SM per concurrent eigensolver
             self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
             self._kn_c = None
 
@@ -448,7 +448,7 @@ class SingleSolvePipeline:
             # read it (event)
             if self._eigbufs is None:
                 from .nystrom import EigBuffers
-                ns = self._eig_streams()
+                ns = self._n_eig_streams()
                 self._eigbufs = [self.eig] + [EigBuffers(self.landmarks, self.device)
                                               for _ in range(ns)]
                 self._eig_done = [None] * (ns + 1)

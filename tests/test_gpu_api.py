@@ -56,6 +56,53 @@ def test_single_pipeline_matches_reference_and_replays(name):
         assert float(torch.max(torch.abs(xs - x1))) <= 1e-9 * float(torch.max(torch.abs(xs)))
 
 
+@pytest.mark.parametrize("name", ["c1_seed0", "c4_n16384"])
+def test_single_pipeline_rotating_buffers(name):
+    """Eigendecompositions on rotating side streams with one buffer set per call
+    in flight, inputs alternating between two staging sets (the e2e path):
+    every call reproduces the first bit for bit."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden(name)
+    pipe = L.SingleSolvePipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                 float(g["gamma"]), int(g["order"]), conditions(g, 0))
+    ins = [tuple(torch.as_tensor(a, device="cuda").clone() for a in
+                 (g["pts"], g["coef"][0], g["forcing"][0])) for _ in range(2)]
+    xs = [pipe.run_device(*ins[k % 2])[0].clone() for k in range(9)]
+    assert len(pipe._eigbufs) == pipe._n_eig_streams() + 1
+    assert all(torch.equal(xs[0], x) for x in xs[1:])
+
+
+def test_shared_pipeline_host_staging_rotation():
+    """SharedGridPipeline.run_host with two device staging sets in rotation
+    (this call's H2D overlaps the previous call's solve) == run_device."""
+    import torch
+
+    from paper_2510_04094_b200 import batch as BT
+    g = load_golden("c2_seed0_i0-7")
+    cond = conditions(g, 0)
+    pipe = BT.SharedGridPipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                 float(g["gamma"]), 2, cond, 8)
+    coef = torch.as_tensor(g["coef"], device="cuda")
+    forc = torch.as_tensor(g["forcing"], device="cuda")
+    vals = torch.as_tensor(g["cond_values"], device="cuda")
+    xd = pipe.run_device(coef, forc, vals)[0].cpu()
+    side = xd.shape[1]
+    hs = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+          for a in (g["coef"], g["forcing"], g["cond_values"])]
+    bufs = [(torch.empty_like(coef), torch.empty_like(forc), torch.empty_like(vals),
+             torch.empty((8, side), dtype=torch.float64, device="cuda"),
+             torch.empty(8, dtype=torch.int32, device="cuda")) for _ in range(2)]
+    for _ in range(3):
+        x_h = torch.empty((8, side), dtype=torch.float64).pin_memory()
+        i_h = torch.empty(8, dtype=torch.int32).pin_memory()
+        pipe.run_host(*hs, x_h, i_h, chunks=2, dev_bufs=bufs)
+        torch.cuda.synchronize()
+        assert (i_h.numpy() == 0).all()
+        assert torch.equal(x_h, xd)
+
+
 def test_shared_pipeline_graph_equals_eager():
     import torch
 

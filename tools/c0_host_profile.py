@@ -1,0 +1,27 @@
+import cProfile, pstats, sys, os, time
+sys.path.insert(0, ".")
+import torch
+from paper_2510_04094_b200 import linear as L, workloads as W
+from paper_2510_04094_b200.problems import ivp
+cfg = W.CONFIGS[0]
+bt = W.linear_batch(cfg, 0, 1)
+cond = ivp(bt.instances[0].conditions())
+pipe = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond, device="cuda")
+p = torch.as_tensor(bt.pts, device="cuda"); c = torch.as_tensor(bt.coef[0], device="cuda"); f = torch.as_tensor(bt.forcing[0], device="cuda")
+for _ in range(20):
+    pipe.run_device(p, c, f)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(500):
+    pipe.run_device(p, c, f)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"host {1e6*(t1-t0)/500:.1f} us/call, wall {1e6*(t2-t0)/500:.1f} us/call")
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(500):
+    pipe.run_device(p, c, f)
+pr.disable()
+torch.cuda.synchronize()
+pstats.Stats(pr).sort_stats("tottime").print_stats(18)
