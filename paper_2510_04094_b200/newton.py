@@ -340,6 +340,11 @@ class NewtonBatch:
             alphas.append(alphas[-1] * shrink)   # the loop's repeated products
         out = {b: alphas[halvings] for b in ids}
         left = list(range(len(ids)))
+        key = (shrink, halvings)
+        cache = self.__dict__.setdefault("_alpha_cache", {})
+        al_all = cache.get(key)
+        if al_all is None:   # the ladder on the device once (no H2D per chunk)
+            al_all = cache[key] = torch.tensor(alphas, dtype=torch.float64, device=self.dev)
         k0, c = 0, 0
         while left and k0 < halvings:
             # growing chunks: most steps are accepted at alpha = 1 or after a few
@@ -350,7 +355,7 @@ class NewtonBatch:
             idx_t = self._idx(sub)
             nb = len(sub)
             norms = torch.empty((kk, nb), dtype=torch.float64, device=self.dev)
-            al_t = torch.tensor(alphas[k0:k0 + kk], dtype=torch.float64, device=self.dev)
+            al_t = al_all[k0:k0 + kk]
             sb = self.lib.nys_newton_trial_scratch_bytes(self.me, self.n_c, nb, kk)
             scratch = _lib.WORKSPACE.get(sb, self.dev) if sb else None
             _lib.call("nys_newton_trial_norms_f64", _lib.ptr(self.S0T), _lib.ptr(self.S1T),
@@ -361,14 +366,13 @@ class NewtonBatch:
                       _lib.ptr(al_t), kk, _lib.ptr(norms), _lib.ptr(scratch) if sb else None, sb,
                       _lib.stream_ptr())
             nh = norms.cpu().numpy()
-            nxt = []
-            for c, r in enumerate(left):
-                ok = np.flatnonzero(np.isfinite(nh[:, c]) & (nh[:, c] <= ref[r]))
-                if ok.size:
-                    out[ids[r]] = alphas[k0 + int(ok[0])]
-                else:
-                    nxt.append(r)
-            left = nxt
+            # first accepted trial per instance (vectorised over the instances)
+            ok = np.isfinite(nh) & (nh <= np.asarray([ref[r] for r in left])[None, :])
+            hit = ok.any(axis=0)
+            first = ok.argmax(axis=0)
+            for c in np.flatnonzero(hit):
+                out[ids[left[c]]] = alphas[k0 + int(first[c])]
+            left = [left[c] for c in np.flatnonzero(~hit)]
             k0 += kk
         return out
 
@@ -462,36 +466,30 @@ class NewtonBatch:
         its = np.zeros(nid, dtype=int)
         bad0 = ~np.isfinite(norm)
         status[bad0] = DIVERGED           # _residual raised at the initial state
-        active = [b for b in ids if status[pos[b]] < 0]
-        while active:
-            keep = []
-            for b in active:
-                r = pos[b]
-                if norm[r] <= tol[r]:
-                    status[r] = OK
-                elif its[r] >= max_iters:
-                    status[r] = MAXITERS
-                elif norm[r] > 1e12:
-                    status[r] = DIVERGED
-                else:
-                    keep.append(b)
-            active = keep
-            if not active:
+        ids_a = np.asarray(ids)
+        act = np.flatnonzero(status < 0)          # positions r of the active instances
+        while act.size:
+            # the per-iteration checks of newton.py:296-303, vectorised over r
+            nr = norm[act]
+            ok = nr <= tol[act]
+            mx = ~ok & (its[act] >= max_iters)
+            dv = ~ok & ~mx & (nr > 1e12)
+            status[act[ok]] = OK
+            status[act[mx]] = MAXITERS
+            status[act[dv]] = DIVERGED
+            act = act[~(ok | mx | dv)]
+            if not act.size:
                 break
-            info = self.direction(active)
-            step = []
-            for b, inf in zip(active, info):
-                if inf != _lib.INFO_OK:
-                    status[pos[b]] = SINGULAR
-                else:
-                    step.append(b)
-            active = step
-            if not active:
+            info = np.asarray(self.direction(ids_a[act].tolist()))
+            sing = info != _lib.INFO_OK
+            status[act[sing]] = SINGULAR
+            act = act[~sing]
+            if not act.size:
                 break
+            active = ids_a[act].tolist()
             if damping:
                 if self.specs is None:
-                    alpha = self._line_search(active, [norm[pos[b]] for b in active], shrink,
-                                              halvings)
+                    alpha = self._line_search(active, norm[act].tolist(), shrink, halvings)
                 else:
                     alpha = {b: 1.0 for b in active}
                     searching = list(active)
@@ -512,18 +510,14 @@ class NewtonBatch:
                 self.candidate(active, [1.0] * len(active))
             act_t = self._idx(active)
             self.X[act_t] = self.Xc[act_t]
-            newn = self.residual(self.X, active, act_t)
-            still = []
-            for b, v in zip(active, newn):
-                r = pos[b]
-                its[r] += 1
-                norm[r] = v
+            newn = np.asarray(self.residual(self.X, active, act_t))
+            its[act] += 1
+            norm[act] = newn
+            for r, v in zip(act.tolist(), newn.tolist()):
                 traces[r].append(float(v))
-                if not np.isfinite(v):
-                    status[r] = DIVERGED        # _residual raised after the update
-                else:
-                    still.append(b)
-            active = still
+            fin = np.isfinite(newn)
+            status[act[~fin]] = DIVERGED        # _residual raised after the update
+            act = act[fin]
         # loop ended: converged check after exhausting iterations (newton.py:331-333)
         for r in range(nid):
             if status[r] == MAXITERS and norm[r] <= tol[r]:
