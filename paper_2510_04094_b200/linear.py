@@ -365,7 +365,7 @@ class SingleSolvePipeline:
 
     def _check(self, ev, buf, me):
         ev.synchronize()
-        m_eff, info = (int(v) for v in buf.meta_h)
+        m_eff, info = int(buf.meta_np[0]), int(buf.meta_np[1])
         if (info & 0xFF) == _lib.INFO_DEGENERATE:
             from .nystrom import DegenerateLandmarksError
             raise DegenerateLandmarksError("two landmarks coincide within 1e-12")
@@ -432,9 +432,10 @@ class SingleSolvePipeline:
         """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info)."""
         import os
 
-        from .nystrom import build_feature_map, launch_eig_async
+        from .nystrom import build_feature_map, launch_eig_pinned
 
         torch = self.torch
+        cur = torch.cuda.current_stream()
         graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
         if self._kspace:
             self._kspace_launch(pts, coef, forcing)
@@ -452,6 +453,9 @@ class SingleSolvePipeline:
                 self._eigbufs = [self.eig] + [EigBuffers(self.landmarks, self.device)
                                               for _ in range(ns)]
                 self._eig_done = [None] * (ns + 1)
+                self._eig_ev = [torch.cuda.Event() for _ in range(ns + 1)]
+                self._post_ev = [torch.cuda.Event() for _ in range(ns + 1)]
+                self._fm_cache = {}
                 self._eig_streams = [torch.cuda.Stream(device=self.device) for _ in range(ns)]
                 self._calls = 0
             par = self._calls % len(self._eigbufs)
@@ -468,17 +472,20 @@ class SingleSolvePipeline:
                                            buffers=buf)
                 self._me_known = fm.m_eff
                 self._cond_known = fm.condition
+                cur.wait_stream(es)
             else:
                 # steady state: the same landmarks give the same m_eff (deterministic
                 # kernels), so the host does not wait for the eigensolver; this
                 # call's m_eff / info are checked at the start of the next call
-                ev = launch_eig_async(self.kernel, buf, self.drop_tol, es)
+                ev = launch_eig_pinned(self.kernel, buf, self.drop_tol, es, self._eig_ev[par])
                 self._pending.append((ev, buf, self._me_known))
-                fm = NystromFeatureMap(kernel=self.kernel, landmarks=self.landmarks,
-                                       m_eff=self._me_known, device=self.device,
-                                       d_landmarks=buf.d_lm, d_W=buf.W, d_eigvals=buf.s,
-                                       d_eigvecs=buf.V)
-            torch.cuda.current_stream(self.device).wait_stream(es)
+                fm = self._fm_cache.get(par)
+                if fm is None:
+                    fm = self._fm_cache[par] = NystromFeatureMap(
+                        kernel=self.kernel, landmarks=self.landmarks, m_eff=self._me_known,
+                        device=self.device, d_landmarks=buf.d_lm, d_W=buf.W, d_eigvals=buf.s,
+                        d_eigvecs=buf.V)
+                cur.wait_event(ev)
             self.eig = buf
         else:
             fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
@@ -512,8 +519,8 @@ class SingleSolvePipeline:
                 self._post(fm, pts, coef, forcing, use_k)
             self._graph[key] = (g, self.lib.nys_launch_count() - n0)
         if par is not None:
-            ev = torch.cuda.Event()
-            ev.record(torch.cuda.current_stream(self.device))
+            ev = self._post_ev[par]
+            ev.record(cur)
             self._eig_done[par] = ev
         return self.x, self.info
 

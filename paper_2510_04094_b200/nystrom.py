@@ -218,6 +218,7 @@ class EigBuffers:
         self.W = torch.empty((m, m), **f64)
         self.meta = torch.zeros(2, dtype=torch.int32, device=self.device)   # m_eff, info
         self.meta_h = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self.meta_np = self.meta_h.numpy()   # host view (no tensor iteration on checks)
         self.s_h = torch.zeros(m, dtype=torch.float64).pin_memory()   # eigenvalues, same sync
         self.wsb = lib.nys_landmark_eig_workspace_bytes(m)
         self.ws = torch.empty(self.wsb, dtype=torch.uint8, device=self.device) if self.wsb else None
@@ -239,6 +240,20 @@ def launch_eig_async(k: RbfKernel, buffers: EigBuffers, drop_tol: float, stream)
         ev = torch.cuda.Event()
         ev.record(stream)
     return ev
+
+
+def launch_eig_pinned(k: RbfKernel, buffers: EigBuffers, drop_tol: float, stream, event):
+    """Steady-state form of launch_eig_async for pipelines: the eigensolver
+    writes m_eff / info straight into the pinned host words (device-visible
+    under unified addressing: no D2H copy op), on ``stream`` by handle (no
+    stream context switch), and ``event`` (reused) is recorded after it."""
+    m = buffers.landmarks.size
+    _lib.call("nys_landmark_eig_f64", _lib.ptr(buffers.d_lm), m, float(k.sigma2),
+              float(drop_tol), _lib.ptr(buffers.s), _lib.ptr(buffers.V), _lib.ptr(buffers.W),
+              _lib.ptr(buffers.meta_h), _lib.ptr(buffers.meta_h) + 4, _lib.ptr(buffers.ws),
+              buffers.wsb, stream.cuda_stream)
+    event.record(stream)
+    return event
 
 
 def build_feature_map(k: RbfKernel, landmarks, drop_tol: float = DEFAULT_DROP_TOL,

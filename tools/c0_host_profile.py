@@ -25,3 +25,24 @@ for _ in range(500):
 pr.disable()
 torch.cuda.synchronize()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+
+# graph replay alone (host time of the launch)
+g = next(iter(pipe._graph.values()))[0]
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(500):
+    g.replay()
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"graph replay host {1e6*(t1-t0)/500:.1f} us, wall {1e6*(t2-t0)/500:.1f} us per replay")
+from paper_2510_04094_b200 import nystrom as N
+buf = pipe._eigbufs[0]
+es = torch.cuda.Stream()
+t0 = time.perf_counter()
+for _ in range(500):
+    N.launch_eig_async(pipe.kernel, buf, pipe.drop_tol, es)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print(f"eig launch host {1e6*(t1-t0)/500:.1f} us, wall {1e6*(t2-t0)/500:.1f} us per eig")
