@@ -308,14 +308,14 @@ class SingleSolvePipeline:
 
     # concurrent eigendecompositions: enough that the one-CTA eigensolver
     # (B200, D&C: 0.14 ms at m = 20, 0.30 ms at m = 50, 3.7 ms at m = 256) keeps
-    # up with the rest of a call (0.1 ms, 0.14 ms, 3.0 ms): 3 for mid-size
-    # landmark sets, else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
+    # up with the rest of a call (~0.05 ms, 0.14 ms, 3.0 ms): 3 up to m = 128,
+    # else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
     EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "0"))
 
     def _n_eig_streams(self) -> int:
         if self.EIG_STREAMS > 0:
             return self.EIG_STREAMS
-        return 3 if 32 < self.landmarks.size <= 128 else 2
+        return 3 if self.landmarks.size <= 128 else 2
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
                  drop_tol: float = 1e-16, device=None):
@@ -428,6 +428,14 @@ class SingleSolvePipeline:
                   _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
                   _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
 
+    def _capture(self, fm, pts, coef, forcing, use_k):
+        torch = self.torch
+        n0 = self.lib.nys_launch_count()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            self._post(fm, pts, coef, forcing, use_k)
+        return g, self.lib.nys_launch_count() - n0
+
     def run_device(self, pts, coef, forcing):
         """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info)."""
         import os
@@ -513,11 +521,23 @@ class SingleSolvePipeline:
             _lib.note_graph_launches(hit[1])
         else:
             self._post(fm, pts, coef, forcing, use_k)   # eager: this call's result + attributes
-            n0 = self.lib.nys_launch_count()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, capture_error_mode="thread_local"):
-                self._post(fm, pts, coef, forcing, use_k)
-            self._graph[key] = (g, self.lib.nys_launch_count() - n0)
+            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k)
+            if par is not None:
+                # the other eigendecomposition buffer sets will come round with
+                # the same inputs: capture theirs now (capture does not execute),
+                # so steady-state calls only replay
+                for q, b2 in enumerate(self._eigbufs):
+                    if q == par:
+                        continue
+                    f2 = self._fm_cache.get(q)
+                    if f2 is None:
+                        f2 = self._fm_cache[q] = NystromFeatureMap(
+                            kernel=self.kernel, landmarks=self.landmarks, m_eff=me,
+                            device=self.device, d_landmarks=b2.d_lm, d_W=b2.W, d_eigvals=b2.s,
+                            d_eigvecs=b2.V)
+                    k2 = key[:-1] + (f2.d_W.data_ptr(),)
+                    if k2 not in self._graph:
+                        self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k)
         if par is not None:
             ev = self._post_ev[par]
             ev.record(cur)
