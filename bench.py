@@ -379,14 +379,18 @@ def setup_single(args, ctx):
     torch.cuda.synchronize()
     if int(res["info"][0]) != 0:
         raise SystemExit(f"config {cid}: singular KKT system")
-    pts_h = torch.from_numpy(bt.pts).pin_memory()
-    coef_h = torch.from_numpy(bt.coef[0]).pin_memory()
-    forc_h = torch.from_numpy(bt.forcing[0]).pin_memory()
+    # the step's host inputs in one pinned block (one H2D per call); views give
+    # the API's three arrays
+    n_p, n_k = pts_d.numel(), coef_d.numel()
+    blk_h = torch.from_numpy(np.concatenate([bt.pts, bt.coef[0].reshape(-1),
+                                             bt.forcing[0]])).pin_memory()
+    pts_h, coef_h, forc_h = (blk_h[:n_p], blk_h[n_p:n_p + n_k].view(coef_d.shape),
+                             blk_h[n_p + n_k:])
     x_h = torch.empty(res["x"].shape, dtype=torch.float64).pin_memory()
     # two persistent staging sets (the pipeline's graphs stay keyed on the same
     # buffers) filled on a copy stream: call k+1's H2D overlaps call k's solve
-    stages = [(torch.empty_like(pts_d), torch.empty_like(coef_d), torch.empty_like(forc_d))
-              for _ in range(2)]
+    blk_d = [torch.empty_like(blk_h, device=dev) for _ in range(2)]
+    stages = [(d[:n_p], d[n_p:n_p + n_k].view(coef_d.shape), d[n_p + n_k:]) for d in blk_d]
     copy_stream = torch.cuda.Stream(device=dev)
     free_ev = [None, None]
     calls = [0]
@@ -402,9 +406,7 @@ def setup_single(args, ctx):
         with torch.cuda.stream(copy_stream):
             if free_ev[k] is not None:     # the solve that last read this set
                 copy_stream.wait_event(free_ev[k])
-            stage[0].copy_(pts_h, non_blocking=True)
-            stage[1].copy_(coef_h, non_blocking=True)
-            stage[2].copy_(forc_h, non_blocking=True)
+            blk_d[k].copy_(blk_h, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(copy_stream)
         cur.wait_event(ready)
