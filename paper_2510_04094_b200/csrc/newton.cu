@@ -24,6 +24,8 @@
 // arrays (host-evaluated reference callables: the generic drop-in path).
 #include <cmath>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace nys_host {
@@ -548,6 +550,108 @@ __global__ void __launch_bounds__(32)
   if (lane == 0) info[s] = bad ? NYS_INFO_NONFINITE : NYS_INFO_OK;
 }
 
+// the same LU (first max wins, identical per-element operation order, so the
+// results are bit-identical) with the trailing rows spread over the 8 warps of
+// a CTA: a lone Newton system is no longer bound by one warp walking all rows
+constexpr int kLuCtaThreads = 256;
+__global__ void __launch_bounds__(kLuCtaThreads)
+    lu_solve_cta_kernel(double* __restrict__ Mg, double* __restrict__ rg, int n,
+                        double* __restrict__ out, int* __restrict__ info) {
+  extern __shared__ double sm[];
+  __shared__ int sing_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, s = blockIdx.x;
+  constexpr int NW = kLuCtaThreads / 32;
+  double* LU = sm;
+  double* ys = LU + (size_t)n * n;
+  int* perm = reinterpret_cast<int*>(ys + n);
+  const double* M = Mg + (size_t)s * n * n;
+  for (int e = tid; e < n * n; e += kLuCtaThreads) LU[e] = M[e];
+  for (int i = tid; i < n; i += kLuCtaThreads) ys[i] = rg[(size_t)s * n + i];
+  if (tid == 0) sing_s = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {   // pivot search (first max wins), row swap
+      double bv = -1.0;
+      int bi = n;
+#pragma unroll
+      for (int c = 0; c < kLuNC; ++c) {
+        const int i = k + lane + 32 * c;
+        if (i < n) {
+          const double a = fabs(LU[(size_t)i * n + k]);
+          if (a > bv) {
+            bv = a;
+            bi = i;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (!(bv > 0.0)) {
+        if (lane == 0) sing_s = 1;
+      } else {
+        if (lane == 0) perm[k] = bi;
+        if (bi != k)
+          for (int j = lane; j < n; j += 32) {
+            const double a = LU[(size_t)k * n + j], p = LU[(size_t)bi * n + j];
+            LU[(size_t)bi * n + j] = a;
+            LU[(size_t)k * n + j] = p;
+          }
+      }
+    }
+    __syncthreads();
+    if (sing_s) {
+      if (tid == 0) info[s] = NYS_INFO_SINGULAR;
+      return;
+    }
+    const double inv = 1.0 / LU[(size_t)k * n + k];
+    for (int i = k + 1 + tid; i < n; i += kLuCtaThreads) LU[(size_t)i * n + k] *= inv;
+    __syncthreads();
+    for (int i = k + 1 + warp; i < n; i += NW) {
+      const double l = LU[(size_t)i * n + k];
+      for (int j = k + 1 + lane; j < n; j += 32) LU[(size_t)i * n + j] -= l * LU[(size_t)k * n + j];
+    }
+    __syncthreads();
+  }
+  if (warp != 0) return;
+  if (lane == 0)
+    for (int k = 0; k < n; ++k) {
+      const int pr = perm[k];
+      if (pr != k) {
+        const double t = ys[k];
+        ys[k] = ys[pr];
+        ys[pr] = t;
+      }
+    }
+  __syncwarp();
+  for (int j = 0; j < n - 1; ++j) {
+    const double yj = ys[j];
+    for (int i = j + 1 + lane; i < n; i += 32) ys[i] -= LU[(size_t)i * n + j] * yj;
+    __syncwarp();
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    const double zj = ys[j] / LU[(size_t)j * n + j];
+    __syncwarp();
+    if (lane == 0) ys[j] = zj;
+    for (int i = lane; i < j; i += 32) ys[i] -= LU[(size_t)i * n + j] * zj;
+    __syncwarp();
+  }
+  int bad = 0;
+  for (int i = lane; i < n; i += 32) {
+    const double v = ys[i];
+    if (!isfinite(v)) bad = 1;
+    out[(size_t)s * n + i] = v;
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) info[s] = bad ? NYS_INFO_NONFINITE : NYS_INFO_OK;
+}
+
 // ---------------------------------------------------------------------------
 // delta_y and the damped update Xc = X + alpha * delta (per instance alpha);
 // delta is stored as [B][ldx] (z part from the reduced solve, y part here)
@@ -805,12 +909,14 @@ extern "C" int nys_lu_solve_f64(double* M, double* rhs, int n, int nb, double* o
   if (n < 1 || n > kLuMaxN || nb < 0) return NYS_EINVAL;
   if (nb == 0) return NYS_OK;
   const size_t smem = ((size_t)n * n + 2 * (size_t)n) * sizeof(double);
+  const bool warp_lu = getenv("NYS_LU_WARP") != nullptr;   // A/B: one warp per system
+  auto kern = warp_lu ? lu_solve_warp_kernel : lu_solve_cta_kernel;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(lu_solve_warp_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return nys_host::record_cuda(e);
   }
-  lu_solve_warp_kernel<<<nb, 32, smem, static_cast<cudaStream_t>(stream)>>>(M, rhs, n, out, info);
+  kern<<<nb, warp_lu ? 32 : kLuCtaThreads, smem, static_cast<cudaStream_t>(stream)>>>(M, rhs, n, out,
+                                                                                    info);
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
