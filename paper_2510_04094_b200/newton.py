@@ -244,13 +244,15 @@ class NewtonBatch:
             host[5, r] = np.asarray(sec(1, 1)(*a), dtype=float)
         self.samples[:, idx_t] = self.torch.as_tensor(host, device=self.dev)
 
-    def residual(self, X, ids, idx_t=None) -> np.ndarray:
-        """F(X[b]) for b in ids; returns max|F| per id (NaN = non-finite rhs)."""
+    def residual(self, X, ids, idx_t=None, read: bool = True):
+        """F(X[b]) for b in ids; returns max|F| per id (NaN = non-finite rhs),
+        or None without the read-back (read=False: F / aux for the next
+        direction only)."""
         if self.specs is not None:
             self._sample_host(X, ids)
         idx_t = self._idx(ids) if idx_t is None else idx_t
         self._residual_launch(X, idx_t, len(ids))
-        return self.norm[idx_t].cpu().numpy()
+        return self.norm[idx_t].cpu().numpy() if read else None
 
     def _ws2(self, nb):
         wsb = self.lib.nys_newton2_workspace_bytes(self.me, self.n_c, nb)
@@ -274,9 +276,10 @@ class NewtonBatch:
                   _lib.ptr(self.F), _lib.ptr(self.norm), _lib.ptr(self.aux), _lib.ptr(self.work),
                   _lib.stream_ptr())
 
-    def direction(self, ids) -> np.ndarray:
+    def direction(self, ids, sync: bool = True):
         """Newton direction D[b] at X[b] (aux/F from the last residual at X);
-        returns LU info per id."""
+        returns LU info per id (sync=False: the device tensor, read later
+        together with the line search's first trial norms)."""
         idx_t = self._idx(ids)
         nb, st = len(ids), _lib.stream_ptr()
         if self.p == 2:
@@ -297,7 +300,7 @@ class NewtonBatch:
         bad = ~self.torch.isfinite(self.D[idx_t]).all(dim=1)
         both = self.torch.where(bad, self.torch.full_like(self.info[:nb], _lib.INFO_NONFINITE),
                                 self.info[:nb])
-        return both.cpu().numpy()
+        return both.cpu().numpy() if sync else both
 
     def _direction2(self, idx_t, nb, st):
         ws, wsb = self._ws2(nb)
@@ -320,14 +323,20 @@ class NewtonBatch:
     def candidate(self, ids, alphas):
         """Xc[b] = X[b] + alpha_b D[b]."""
         idx_t = self._idx(ids)
-        self.alpha[idx_t] = self.torch.as_tensor(np.asarray(alphas, dtype=float), device=self.dev)
+        pin = self.__dict__.get("_alpha_pin")
+        if pin is None:   # pinned staging: the upload is asynchronous (no host sync)
+            pin = self._alpha_pin = self.torch.empty(self.B, dtype=self.torch.float64).pin_memory()
+        n = len(ids)
+        pin.numpy()[:n] = np.asarray(alphas, dtype=float)
+        self.alpha[idx_t] = pin[:n].to(self.dev, non_blocking=True)
         _lib.call("nys_newton_step_f64", _lib.ptr(self.S0), _lib.ptr(self.S1), self.me, self.n_c,
                   self.nk, _lib.ptr(self.aux), _lib.ptr(self.F), _lib.ptr(self.dz),
                   _lib.ptr(self.gam), _lib.ptr(self.X), _lib.ptr(self.D), _lib.ptr(self.Xc),
                   _lib.ptr(self.alpha), self.ldx, _lib.ptr(idx_t), len(ids), 0,
                   _lib.stream_ptr())
 
-    def _line_search(self, ids, ref, shrink, halvings, chunks=(1, 3)):
+    def _line_search(self, ids, ref, shrink, halvings, chunks=(1, 3), with_norms=False,
+                     info_d=None):
         """Step halving of newton.py:305-318 with the trial steps evaluated in
         batches: alpha_k = shrink^k for a chunk of k at once (one host sync per
         chunk instead of per halving), then the first accepted k per instance --
@@ -339,6 +348,8 @@ class NewtonBatch:
         for _ in range(halvings):
             alphas.append(alphas[-1] * shrink)   # the loop's repeated products
         out = {b: alphas[halvings] for b in ids}
+        tn = {}   # accepted trial norms: bit-identical to the residual at the candidate
+        info = np.full(len(ids), _lib.INFO_OK, dtype=np.int64)
         left = list(range(len(ids)))
         key = (shrink, halvings)
         cache = self.__dict__.setdefault("_alpha_cache", {})
@@ -365,15 +376,31 @@ class NewtonBatch:
                       _lib.ptr(self.X), _lib.ptr(self.D), self.ldx, _lib.ptr(idx_t), nb,
                       _lib.ptr(al_t), kk, _lib.ptr(norms), _lib.ptr(scratch) if sb else None, sb,
                       _lib.stream_ptr())
-            nh = norms.cpu().numpy()
+            if info_d is not None:
+                # the direction's LU info rides on the first read-back; instances
+                # it flags leave the search (newton.py:307-310: no step for them)
+                both = self.torch.cat([norms.reshape(-1), info_d.to(norms.dtype)]).cpu().numpy()
+                nh = both[:kk * nb].reshape(kk, nb)
+                info = both[kk * nb:].astype(np.int64)
+                info_d = None
+                keep = np.flatnonzero(info[left] == _lib.INFO_OK)
+                nh = nh[:, keep]
+                left = [left[c] for c in keep]
+            else:
+                nh = norms.cpu().numpy()
             # first accepted trial per instance (vectorised over the instances)
             ok = np.isfinite(nh) & (nh <= np.asarray([ref[r] for r in left])[None, :])
             hit = ok.any(axis=0)
             first = ok.argmax(axis=0)
             for c in np.flatnonzero(hit):
                 out[ids[left[c]]] = alphas[k0 + int(first[c])]
+                tn[ids[left[c]]] = float(nh[first[c], c])
             left = [left[c] for c in np.flatnonzero(~hit)]
             k0 += kk
+        if info_d is not None:   # no trial chunk ran (halvings == 0)
+            info = info_d.cpu().numpy().astype(np.int64)
+        if with_norms:
+            return out, tn, info
         return out
 
     # -------------------------------------------------------------- states
@@ -480,17 +507,30 @@ class NewtonBatch:
             act = act[~(ok | mx | dv)]
             if not act.size:
                 break
-            info = np.asarray(self.direction(ids_a[act].tolist()))
-            sing = info != _lib.INFO_OK
-            status[act[sing]] = SINGULAR
-            act = act[~sing]
-            if not act.size:
-                break
-            active = ids_a[act].tolist()
-            if damping:
-                if self.specs is None:
-                    alpha = self._line_search(active, norm[act].tolist(), shrink, halvings)
-                else:
+            known = None
+            if damping and self.specs is None:
+                # direction, then the batched line search; the LU info is read back
+                # with the first trial norms (one host sync instead of two)
+                active = ids_a[act].tolist()
+                info_d = self.direction(active, sync=False)
+                alpha, known, info = self._line_search(active, norm[act].tolist(), shrink,
+                                                       halvings, with_norms=True, info_d=info_d)
+                sing = info != _lib.INFO_OK
+                status[act[sing]] = SINGULAR
+                act = act[~sing]
+                if not act.size:
+                    break
+                active = ids_a[act].tolist()
+                self.candidate(active, [alpha[b] for b in active])
+            else:
+                info = np.asarray(self.direction(ids_a[act].tolist()))
+                sing = info != _lib.INFO_OK
+                status[act[sing]] = SINGULAR
+                act = act[~sing]
+                if not act.size:
+                    break
+                active = ids_a[act].tolist()
+                if damping:   # sampled specs: halving through the host-sampled residual
                     alpha = {b: 1.0 for b in active}
                     searching = list(active)
                     for _ in range(halvings):
@@ -505,12 +545,18 @@ class NewtonBatch:
                             alpha[b] *= shrink
                             nxt.append(b)
                         searching = nxt
-                self.candidate(active, [alpha[b] for b in active])
-            else:
-                self.candidate(active, [1.0] * len(active))
+                    self.candidate(active, [alpha[b] for b in active])
+                else:
+                    self.candidate(active, [1.0] * len(active))
             act_t = self._idx(active)
             self.X[act_t] = self.Xc[act_t]
-            newn = np.asarray(self.residual(self.X, active, act_t))
+            if known is not None and len(known) == len(active):
+                # every step was accepted by a trial whose norm is bit-identical
+                # to the residual at the new point: no read-back needed
+                self.residual(self.X, active, act_t, read=False)
+                newn = np.array([known[b] for b in active])
+            else:
+                newn = np.asarray(self.residual(self.X, active, act_t))
             its[act] += 1
             norm[act] = newn
             for r, v in zip(act.tolist(), newn.tolist()):
