@@ -418,10 +418,39 @@ __global__ void __launch_bounds__(kSmallThreads)
     }
     if (tid < R) Y[k * R + tid] *= inv;
     __syncthreads();
-    for (int i = k + 1 + warp; i < nh; i += NW) {
-      const double li = L[i * ld + k];
-      for (int j = k + 1 + lane; j <= i; j += 32) L[i * ld + j] -= li * L[j * ld + k];
-      if (lane < R) Y[i * R + lane] -= li * Y[k * R + lane];
+    // column k's multipliers for this lane's columns j = k+1+lane (+32, +64),
+    // then rows four at a time per warp with every load issued before the FMAs
+    double lj[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int j = k + 1 + lane + 32 * c;
+      lj[c] = j < nh ? L[j * ld + k] : 0.0;
+    }
+    const double yk = lane < R ? Y[k * R + lane] : 0.0;
+    for (int i0 = k + 1 + warp; i0 < nh; i0 += 4 * NW) {
+      double li[4], a[4][3], yv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + r * NW;
+        li[r] = i < nh ? L[i * ld + k] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int j = k + 1 + lane + 32 * c;
+          a[r][c] = (i < nh && j <= i) ? L[i * ld + j] : 0.0;
+        }
+        yv[r] = (i < nh && lane < R) ? Y[i * R + lane] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int i = i0 + r * NW;
+        if (i >= nh) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const int j = k + 1 + lane + 32 * c;
+          if (j <= i) L[i * ld + j] = a[r][c] - li[r] * lj[c];
+        }
+        if (lane < R) Y[i * R + lane] = yv[r] - li[r] * yk;
+      }
     }
     __syncthreads();
   }
@@ -494,13 +523,18 @@ __global__ void __launch_bounds__(kSmallThreads)
       for (int i = tid; i < nh; i += kSmallThreads) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int j = 0;
-        for (; j + 4 <= nh; j += 4) {
-          const double e0 = __ldg(E + (size_t)j * Pe + i), e1 = __ldg(E + (size_t)(j + 1) * Pe + i);
-          const double e2 = __ldg(E + (size_t)(j + 2) * Pe + i), e3 = __ldg(E + (size_t)(j + 3) * Pe + i);
-          a0 = fma(e0, xs[j], a0);
-          a1 = fma(e1, xs[j + 1], a1);
-          a2 = fma(e2, xs[j + 2], a2);
-          a3 = fma(e3, xs[j + 3], a3);
+        for (; j + 8 <= nh; j += 8) {   // eight L2 loads in flight
+          double e[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) e[u] = __ldg(E + (size_t)(j + u) * Pe + i);
+          a0 = fma(e[0], xs[j], a0);
+          a1 = fma(e[1], xs[j + 1], a1);
+          a2 = fma(e[2], xs[j + 2], a2);
+          a3 = fma(e[3], xs[j + 3], a3);
+          a0 = fma(e[4], xs[j + 4], a0);
+          a1 = fma(e[5], xs[j + 5], a1);
+          a2 = fma(e[6], xs[j + 6], a2);
+          a3 = fma(e[7], xs[j + 7], a3);
         }
         for (; j < nh; ++j) a0 = fma(__ldg(E + (size_t)j * Pe + i), xs[j], a0);
         double a = (a0 + a1) + (a2 + a3);

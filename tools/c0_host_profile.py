@@ -1,9 +1,12 @@
 import cProfile, pstats, sys, os, time
 sys.path.insert(0, ".")
+if os.environ.get("NYS_PROBE_LIB"):
+    from paper_2510_04094_b200 import _lib
+    _lib.load(os.environ["NYS_PROBE_LIB"])
 import torch
 from paper_2510_04094_b200 import linear as L, workloads as W
 from paper_2510_04094_b200.problems import ivp
-cfg = W.CONFIGS[0]
+cfg = W.CONFIGS[int(os.environ.get("CFG", "0"))]
 bt = W.linear_batch(cfg, 0, 1)
 cond = ivp(bt.instances[0].conditions())
 pipe = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond, device="cuda")
@@ -46,3 +49,16 @@ t1 = time.perf_counter()
 torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(f"eig launch host {1e6*(t1-t0)/500:.1f} us, wall {1e6*(t2-t0)/500:.1f} us per eig")
+
+# warm per-kernel durations of the replayed post graph
+from torch.profiler import ProfilerActivity, profile
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+agg = {}
+for e in ev:
+    agg.setdefault(e.name[:60], []).append(e.time_range.end - e.time_range.start)
+for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+    print(f"{sum(v) / len(v):8.1f} us x{len(v)}  {k}")
