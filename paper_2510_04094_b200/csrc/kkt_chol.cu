@@ -402,58 +402,61 @@ __global__ void __launch_bounds__(kSmallThreads)
     Y[i * R + P] = E[(size_t)i * Pe + me + 1];
   }
   __syncthreads();
-  // ---- H = L L^T with Y <- L^{-1} Y folded in
-  int chol_bad = 0;
-  for (int k = 0; k < nh; ++k) {
-    const double akk = L[k * ld + k];
-    if (!(akk > 0.0) || !isfinite(akk)) {   // uniform: every thread reads the same value
-      chol_bad = 1;
-      break;
-    }
-    const double inv = rsqrt(akk);
-    for (int i = k + 1 + tid; i < nh; i += kSmallThreads) L[i * ld + k] *= inv;
-    if (tid == 0) {
-      L[k * ld + k] = akk * inv;
-      dinv[k] = inv;
-    }
-    if (tid < R) Y[k * R + tid] *= inv;
-    __syncthreads();
-    // column k's multipliers for this lane's columns j = k+1+lane (+32, +64),
-    // then rows four at a time per warp with every load issued before the FMAs
-    double lj[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int j = k + 1 + lane + 32 * c;
-      lj[c] = j < nh ? L[j * ld + k] : 0.0;
-    }
-    const double yk = lane < R ? Y[k * R + lane] : 0.0;
-    for (int i0 = k + 1 + warp; i0 < nh; i0 += 4 * NW) {
-      double li[4], a[4][3], yv[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = i0 + r * NW;
-        li[r] = i < nh ? L[i * ld + k] : 0.0;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int j = k + 1 + lane + 32 * c;
-          a[r][c] = (i < nh && j <= i) ? L[i * ld + j] : 0.0;
+  // ---- H = L L^T with Y <- L^{-1} Y folded in, by 8-column panels: warp 0
+  // factors a panel (column scale, in-panel updates and the elimination of Y,
+  // __syncwarp only), then all warps apply its rank-8 update to the trailing
+  // matrix in column order (a = a - l_ik l_jk for k = c0, c0+1, ...: the same
+  // per-element operations as the unblocked right-looking loop)
+  __shared__ int chol_bad_s;
+  if (tid == 0) chol_bad_s = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < nh; c0 += 8) {
+    const int c1 = min(c0 + 8, nh);
+    if (warp == 0) {
+      for (int k = c0; k < c1; ++k) {
+        const double akk = L[k * ld + k];
+        if (!(akk > 0.0) || !isfinite(akk)) {   // warp-uniform
+          if (lane == 0) chol_bad_s = 1;
+          break;
         }
-        yv[r] = (i < nh && lane < R) ? Y[i * R + lane] : 0.0;
+        const double inv = rsqrt(akk);
+        for (int i = k + 1 + lane; i < nh; i += 32) L[i * ld + k] *= inv;
+        if (lane == 0) {
+          L[k * ld + k] = akk * inv;
+          dinv[k] = inv;
+        }
+        if (lane < R) Y[k * R + lane] *= inv;
+        __syncwarp();
+        for (int i = k + 1 + lane; i < nh; i += 32) {
+          const double li = L[i * ld + k];
+          for (int j = k + 1; j < c1 && j <= i; ++j) L[i * ld + j] -= li * L[j * ld + k];
+#pragma unroll
+          for (int q = 0; q < R; ++q) Y[i * R + q] -= li * Y[k * R + q];
+        }
+        __syncwarp();
       }
+    }
+    __syncthreads();
+    if (chol_bad_s) break;
+    if (c1 < nh) {
+      const int w = c1 - c0;
+      for (int i = c1 + warp; i < nh; i += NW) {
+        double li[8];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int i = i0 + r * NW;
-        if (i >= nh) continue;
+        for (int t = 0; t < 8; ++t) li[t] = t < w ? L[i * ld + c0 + t] : 0.0;
+        for (int j = c1 + lane; j <= i; j += 32) {
+          double a = L[i * ld + j];
+          const double* lj = L + j * ld + c0;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const int j = k + 1 + lane + 32 * c;
-          if (j <= i) L[i * ld + j] = a[r][c] - li[r] * lj[c];
+          for (int t = 0; t < 8; ++t)
+            if (t < w) a -= li[t] * lj[t];
+          L[i * ld + j] = a;
         }
-        if (lane < R) Y[i * R + lane] = yv[r] - li[r] * yk;
       }
     }
     __syncthreads();
   }
+  const int chol_bad = chol_bad_s;
   if (chol_bad) {
     if (tid == 0) info[b] = kNeedsLu;
     return;
