@@ -355,27 +355,21 @@ def setup_single(args, ctx):
     forc_d = torch.as_tensor(bt.forcing[0], device=dev)
     shard = cid == 4 and world > 1
     Ac_cache = {}
-    pipe = None if shard else L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma,
-                                                    cfg.order, cond, device=dev)
+    # c4 on N GPUs: this rank's row slab in the pipeline's kernel-space Gram +
+    # one all-reduce of K (dist.py); configs 0/1 are replicas
+    pipe = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond,
+                                 device=dev,
+                                 rows=DI.row_ranges(bt.pts.size, world)[rank] if shard else None)
 
     def solve(pts, coef, forc):
-        if pipe is not None:   # eig -> (CUDA graph) condition rows, fused Gram, KKT
-            x, info = pipe.run_device(pts, coef, forc)
-            if "fm" in Ac_cache:   # the feature map handle is only for the kernel timing
-                return dict(x=x, info=info)
+        # eig (side streams) -> (CUDA graph) condition rows, Gram, KKT
+        x, info = pipe.run_device(pts, coef, forc)
+        if "fm" not in Ac_cache:   # the feature map handle is only for the kernel timing
             Ac_cache["fm"] = N.NystromFeatureMap(
                 kernel=pipe.kernel, landmarks=pipe.landmarks, m_eff=pipe._shape[0], device=dev,
                 d_landmarks=pipe.eig.d_lm, d_W=pipe.eig.W, d_eigvals=pipe.eig.s,
                 d_eigvecs=pipe.eig.V)
-            return dict(x=x, info=info)
-        fm = N.build_feature_map(RbfKernel(cfg.sigma2), bt.landmarks, device=dev)
-        E = DI.sharded_gram_ext(fm, cfg.order, pts, coef, forc, rank, world)
-        Ac, beta, vals = L.condition_rows(cond, fm)
-        sy = L.AssembledSystem(bt.pts, cfg.gamma, None, None, None,
-                               Ac.reshape(len(cond.entries), -1), beta, vals, fm, cfg.order, E)
-        res = L._kkt_solve(sy)
-        Ac_cache["fm"] = fm
-        return res
+        return dict(x=x, info=info)
 
     res = solve(pts_d, coef_d, forc_d)
     torch.cuda.synchronize()

@@ -315,10 +315,17 @@ class SingleSolvePipeline:
     def _n_eig_streams(self) -> int:
         if self.EIG_STREAMS > 0:
             return self.EIG_STREAMS
+        if getattr(self, "_rows", None) is not None:
+            return 4   # row shards make the Gram short: more eigensolvers in flight
         return 3 if self.landmarks.size <= 128 else 2
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
-                 drop_tol: float = 1e-16, device=None):
+                 drop_tol: float = 1e-16, device=None, rows=None, group=None):
+        """rows=(lo, hi): row-sharded mode (config 4 on several GPUs, dist.py):
+        this rank's kernel-space Gram covers collocation rows [lo, hi) and one
+        all-reduce(SUM) of K (before the projection; (m+2)^2 doubles) over
+        ``group`` (default: the world) completes it; every rank then runs the
+        identical projection and KKT.  Requires the kernel-space path."""
         from .kernel import RbfKernel
         from .nystrom import EigBuffers
 
@@ -327,6 +334,7 @@ class SingleSolvePipeline:
         if gamma <= 0:
             raise ValueError(f"gamma must be positive, got {gamma}")
         self.kernel = RbfKernel(float(sigma2))
+        self._rows, self._group = (None if rows is None else tuple(int(v) for v in rows)), group
         self.landmarks = np.asarray(landmarks, dtype=float).reshape(-1)
         self.gamma, self.order, self.cond, self.drop_tol = float(gamma), int(order), cond, drop_tol
         self.eig = EigBuffers(self.landmarks, device)
@@ -355,6 +363,9 @@ class SingleSolvePipeline:
                            - self._n_eig_streams())   # one SM per concurrent eigensolver
             self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
             self._kn_c = None
+        if rows is not None and not self._kspace:
+            raise NotImplementedError("row-sharded SingleSolvePipeline needs the kernel-space "
+                                      "Gram (m + 2 > 72 landmarks)")
 
     def _verify_pending(self, keep: int = 0):
         """Check steady-state eigendecompositions (m_eff, info) once their
@@ -386,7 +397,8 @@ class SingleSolvePipeline:
         cur = torch.cuda.current_stream(self.device)
         self._side.wait_stream(cur)
         _lib.call("nys_kspace_gram_f64", _lib.ptr(self.eig.d_lm), m, float(self.kernel.sigma2),
-                  self.order, _lib.ptr(pts), _lib.ptr(coef), _lib.ptr(forcing), n_c, 0, n_c,
+                  self.order, _lib.ptr(pts), _lib.ptr(coef), _lib.ptr(forcing), n_c,
+                  *((0, n_c) if self._rows is None else self._rows),
                   self._kctas, _lib.ptr(self.K), _lib.ptr(self.kgws), self.kgws_b,
                   self._side.cuda_stream)
         self._kev.record(self._side)
@@ -501,6 +513,9 @@ class SingleSolvePipeline:
         big = (me + 2 + 7) // 8 > SMALL_NB_MAX
         if self._kspace:   # inputs and K are shared with the side stream
             self.torch.cuda.current_stream(self.device).wait_event(self._kev)
+            if self._rows is not None:   # partial K of this rank's rows -> full K
+                from .dist import allreduce_sum
+                allreduce_sum(self.K, self._group)
         cond_omega = self._cond_known if par is not None else fm.condition
         if big and cond_omega > KSPACE_MAX_COND:
             raise IllConditionedLargeMapError(

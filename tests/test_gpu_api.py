@@ -74,6 +74,33 @@ def test_single_pipeline_rotating_buffers(name):
     assert all(torch.equal(xs[0], x) for x in xs[1:])
 
 
+def test_single_pipeline_row_shards_sum_to_full():
+    """Row-sharded SingleSolvePipeline (config 4 on N GPUs): the kernel-space
+    Grams of two row slabs add up to the single-GPU one (the all-reduce is the
+    identity at world size 1, so the slabs are summed here)."""
+    import torch
+
+    from paper_2510_04094_b200 import dist as D
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden("c4_n16384")
+    args = (g["landmarks"], float(g["sigma2"]), g["grid"], float(g["gamma"]), int(g["order"]),
+            conditions(g, 0))
+    ins = tuple(torch.as_tensor(a, device="cuda") for a in (g["pts"], g["coef"][0], g["forcing"][0]))
+    full = L.SingleSolvePipeline(*args)
+    full.run_device(*ins)
+    Ks = []
+    for lo, hi in D.row_ranges(g["pts"].size, 2):
+        p = L.SingleSolvePipeline(*args, rows=(lo, hi))
+        assert p._n_eig_streams() == 4
+        p._kspace_launch(*ins)
+        torch.cuda.synchronize()
+        Ks.append(p.K.clone())
+    torch.cuda.synchronize()
+    Kf = full.K
+    scale = float(torch.max(torch.abs(Kf)))
+    assert float(torch.max(torch.abs(Ks[0] + Ks[1] - Kf))) <= 1e-12 * scale
+
+
 def test_shared_pipeline_host_staging_rotation():
     """SharedGridPipeline.run_host with two device staging sets in rotation
     (this call's H2D overlaps the previous call's solve) == run_device."""
