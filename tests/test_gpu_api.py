@@ -195,6 +195,27 @@ def test_large_kkt_cholesky_matches_lu():
     assert rel_l2(y1, g["yhat"][0]) <= 1e-6
 
 
+@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0", "cat_p12", "cat_p16"])
+def test_small_kkt_cholesky_matches_lu(name):
+    """Single small systems (one CTA: Cholesky + Schur, kkt_chol.cu) against
+    the reference's LU on the same assembled system; P12 / P16 are a BVP and a
+    fourth-order problem (more conditions, other side lengths)."""
+    from gpu_util import solve_golden_instance
+
+    g = load_golden(name)
+    fm = fmap_from_golden(g)
+    _, m_chol = solve_golden_instance(g, fm, 0)
+    os.environ["NYS_KKT_LU"] = "1"
+    try:
+        _, m_lu = solve_golden_instance(g, fm, 0)
+    finally:
+        del os.environ["NYS_KKT_LU"]
+    y1 = m_chol.predict(0, g["grid"])
+    y2 = m_lu.predict(0, g["grid"])
+    assert rel_l2(y1, y2) <= 1e-9
+    assert rel_l2(y1, g["yhat"][0]) <= 1e-6
+
+
 def test_singular_system_raises():
     """Two identical conditions make M singular: linear.solve raises
     SingularSystemError like linear.py:148-151 (and so does the batch path)."""
