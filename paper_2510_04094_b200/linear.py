@@ -440,6 +440,34 @@ class SingleSolvePipeline:
                   _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
                   _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
 
+    def _run_fast(self, plan):
+        """Steady-state call for inputs whose graphs exist for every buffer set
+        (configs 0/1): rotate the set and the eigensolver stream, launch the
+        eigendecomposition with pre-bound arguments, replay the set's graph --
+        the same work as the general path with a fraction of its host cost."""
+        n = len(self._eigbufs)
+        par = self._calls % n
+        es = self._eig_streams[self._calls % len(self._eig_streams)]
+        self._calls += 1
+        es.wait_event(self._post_ev[par])   # the set's last reader has finished
+        self._verify_pending(keep=len(self._eig_streams))
+        buf = self._eigbufs[par]
+        rc = self.lib.nys_landmark_eig_f64(*self._eig_args[par], es.cuda_stream)
+        if rc:
+            _lib.check(rc, "nys_landmark_eig_f64")
+        ev = self._eig_ev[par]
+        ev.record(es)
+        self._pending.append((ev, buf, self._me_known))
+        ev.wait()   # current stream
+        g, nl = plan[par]
+        g.replay()
+        _lib.note_graph_launches(nl)
+        post = self._post_ev[par]
+        post.record()
+        self._eig_done[par] = post
+        self.eig = buf
+        return self.x, self.info
+
     def _capture(self, fm, pts, coef, forcing, use_k):
         torch = self.torch
         n0 = self.lib.nys_launch_count()
@@ -455,6 +483,11 @@ class SingleSolvePipeline:
         from .nystrom import build_feature_map, launch_eig_pinned
 
         torch = self.torch
+        fast = self.__dict__.get("_fast")
+        if fast:
+            plan = fast.get((pts.data_ptr(), coef.data_ptr(), forcing.data_ptr()))
+            if plan is not None:
+                return self._run_fast(plan)
         cur = torch.cuda.current_stream()
         graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
         if self._kspace:
@@ -553,6 +586,14 @@ class SingleSolvePipeline:
                     k2 = key[:-1] + (f2.d_W.data_ptr(),)
                     if k2 not in self._graph:
                         self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k)
+                if not self._kspace:   # steady state for these inputs: _run_fast
+                    plan = [self._graph[key[:-1] + (b2.W.data_ptr(),)] for b2 in self._eigbufs]
+                    self.__dict__.setdefault("_fast", {})[key[1:4]] = plan
+                    self._eig_args = [
+                        (_lib.ptr(b2.d_lm), self.landmarks.size, float(self.kernel.sigma2),
+                         float(self.drop_tol), _lib.ptr(b2.s), _lib.ptr(b2.V), _lib.ptr(b2.W),
+                         _lib.ptr(b2.meta_h), _lib.ptr(b2.meta_h) + 4, _lib.ptr(b2.ws), b2.wsb)
+                        for b2 in self._eigbufs]
         if par is not None:
             ev = self._post_ev[par]
             ev.record(cur)
