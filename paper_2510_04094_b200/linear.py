@@ -421,12 +421,29 @@ class SingleSolvePipeline:
         self._shape = (me, n_c)
         self._graph = None
 
-    def _post(self, fm, pts, coef, forcing, use_k=False):
+    def _rows_args(self, fm, Ac):
+        """Argument tuples of the condition-row launches (linear.py:56-63) into Ac."""
+        me = fm.m_eff
+        return [(_lib.ptr(fm.d_landmarks), fm.m, _lib.ptr(fm.d_W), fm.ldw, me,
+                 float(fm.kernel.sigma2), int(bc.order), _lib.ptr(self.cond_pts) + 8 * mu, 1,
+                 _lib.ptr(Ac) + 8 * mu * me, me) for mu, bc in enumerate(self.cond.entries)]
+
+    def _ac_for(self, par, me):
+        """Condition rows of buffer set par: they depend on W only, so the
+        overlapped path computes them on the eigensolver's stream."""
+        sets = self.__dict__.setdefault("_Ac_sets", {})
+        a = sets.get(par)
+        if a is None or a.shape[1] != me:
+            a = sets[par] = self.torch.zeros((max(self.nk, 1), me), dtype=self.torch.float64,
+                                             device=self.device)
+        return a
+
+    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
-        for mu, bc in enumerate(self.cond.entries):   # linear.py:56-63, on the device
-            _lib.call("nys_feature_matrix_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw,
-                      me, float(fm.kernel.sigma2), int(bc.order), _lib.ptr(self.cond_pts) + 8 * mu,
-                      1, _lib.ptr(self.Ac) + 8 * mu * me, me, st)
+        if Ac is None:   # rows here (otherwise already computed on the eig stream)
+            Ac = self.Ac
+            for args in self._rows_args(fm, Ac):
+                _lib.call("nys_feature_matrix_f64", *args, st)
         n_c = pts.numel()
         if use_k:
             _lib.call("nys_kspace_project_f64", _lib.ptr(self.K), m, _lib.ptr(fm.d_W), fm.ldw, me,
@@ -436,7 +453,7 @@ class SingleSolvePipeline:
                       float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
                       _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
                       self.gws_b, st)
-        _lib.call("nys_kkt_solve_f64", _lib.ptr(self.E), me, self.nk, _lib.ptr(self.Ac),
+        _lib.call("nys_kkt_solve_f64", _lib.ptr(self.E), me, self.nk, _lib.ptr(Ac),
                   _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
                   _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
 
@@ -452,9 +469,14 @@ class SingleSolvePipeline:
         es.wait_event(self._post_ev[par])   # the set's last reader has finished
         self._verify_pending(keep=len(self._eig_streams))
         buf = self._eigbufs[par]
-        rc = self.lib.nys_landmark_eig_f64(*self._eig_args[par], es.cuda_stream)
+        sh = es.cuda_stream
+        rc = self.lib.nys_landmark_eig_f64(*self._eig_args[par], sh)
         if rc:
             _lib.check(rc, "nys_landmark_eig_f64")
+        for args in self._rows_bound[par]:   # condition rows need W only: same stream
+            rc = self.lib.nys_feature_matrix_f64(*args, sh)
+            if rc:
+                _lib.check(rc, "nys_feature_matrix_f64")
         ev = self._eig_ev[par]
         ev.record(es)
         self._pending.append((ev, buf, self._me_known))
@@ -468,12 +490,12 @@ class SingleSolvePipeline:
         self.eig = buf
         return self.x, self.info
 
-    def _capture(self, fm, pts, coef, forcing, use_k):
+    def _capture(self, fm, pts, coef, forcing, use_k, Ac=None):
         torch = self.torch
         n0 = self.lib.nys_launch_count()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            self._post(fm, pts, coef, forcing, use_k)
+            self._post(fm, pts, coef, forcing, use_k, Ac)
         return g, self.lib.nys_launch_count() - n0
 
     def run_device(self, pts, coef, forcing):
@@ -525,19 +547,25 @@ class SingleSolvePipeline:
                                            buffers=buf)
                 self._me_known = fm.m_eff
                 self._cond_known = fm.condition
+                for args in self._rows_args(fm, self._ac_for(par, fm.m_eff)):
+                    _lib.call("nys_feature_matrix_f64", *args, es.cuda_stream)
                 cur.wait_stream(es)
             else:
                 # steady state: the same landmarks give the same m_eff (deterministic
                 # kernels), so the host does not wait for the eigensolver; this
                 # call's m_eff / info are checked at the start of the next call
-                ev = launch_eig_pinned(self.kernel, buf, self.drop_tol, es, self._eig_ev[par])
-                self._pending.append((ev, buf, self._me_known))
                 fm = self._fm_cache.get(par)
                 if fm is None:
                     fm = self._fm_cache[par] = NystromFeatureMap(
                         kernel=self.kernel, landmarks=self.landmarks, m_eff=self._me_known,
                         device=self.device, d_landmarks=buf.d_lm, d_W=buf.W, d_eigvals=buf.s,
                         d_eigvecs=buf.V)
+                launch_eig_pinned(self.kernel, buf, self.drop_tol, es, self._eig_ev[par])
+                for args in self._rows_args(fm, self._ac_for(par, self._me_known)):
+                    _lib.call("nys_feature_matrix_f64", *args, es.cuda_stream)
+                ev = self._eig_ev[par]
+                ev.record(es)
+                self._pending.append((ev, buf, self._me_known))
                 cur.wait_event(ev)
             self.eig = buf
         else:
@@ -568,8 +596,9 @@ class SingleSolvePipeline:
             hit[0].replay()
             _lib.note_graph_launches(hit[1])
         else:
-            self._post(fm, pts, coef, forcing, use_k)   # eager: this call's result + attributes
-            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k)
+            Ac = None if par is None else self._ac_for(par, me)
+            self._post(fm, pts, coef, forcing, use_k, Ac)   # eager: result + attributes
+            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac)
             if par is not None:
                 # the other eigendecomposition buffer sets will come round with
                 # the same inputs: capture theirs now (capture does not execute),
@@ -585,7 +614,8 @@ class SingleSolvePipeline:
                             d_eigvecs=b2.V)
                     k2 = key[:-1] + (f2.d_W.data_ptr(),)
                     if k2 not in self._graph:
-                        self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k)
+                        self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k,
+                                                        self._ac_for(q, me))
                 if not self._kspace:   # steady state for these inputs: _run_fast
                     plan = [self._graph[key[:-1] + (b2.W.data_ptr(),)] for b2 in self._eigbufs]
                     self.__dict__.setdefault("_fast", {})[key[1:4]] = plan
@@ -594,6 +624,9 @@ class SingleSolvePipeline:
                          float(self.drop_tol), _lib.ptr(b2.s), _lib.ptr(b2.V), _lib.ptr(b2.W),
                          _lib.ptr(b2.meta_h), _lib.ptr(b2.meta_h) + 4, _lib.ptr(b2.ws), b2.wsb)
                         for b2 in self._eigbufs]
+                    self._fm_cache.setdefault(par, fm)
+                    self._rows_bound = [self._rows_args(self._fm_cache[q], self._ac_for(q, me))
+                                        for q in range(len(self._eigbufs))]
         if par is not None:
             ev = self._post_ev[par]
             ev.record(cur)
