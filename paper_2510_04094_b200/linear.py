@@ -359,9 +359,10 @@ class SingleSolvePipeline:
         if self._kspace:
             self._side = torch.cuda.Stream(device=self.device)
             self._kev = torch.cuda.Event()
+            # one SM per concurrent eigensolver and one for the previous call's
+            # KKT, which may overlap this call's Gram (input_event)
             self._kctas = (torch.cuda.get_device_properties(self.device).multi_processor_count
-                           - self._n_eig_streams())   # one SM per concurrent eigensolver
-            self.K = torch.empty((m + 2, m + 2), dtype=torch.float64, device=self.device)
+                           - self._n_eig_streams() - 1)
             self._kn_c = None
         if rows is not None and not self._kspace:
             raise NotImplementedError("row-sharded SingleSolvePipeline needs the kernel-space "
@@ -384,7 +385,23 @@ class SingleSolvePipeline:
             raise RuntimeError(f"landmark eigendecomposition changed m_eff {me} -> {m_eff} "
                                "between calls on the same landmarks")
 
-    def _kspace_launch(self, pts, coef, forcing):
+    def _calls_next(self) -> int:
+        """Buffer set the next overlapped call will use."""
+        n = self._n_eig_streams() + 1
+        return self.__dict__.get("_calls", 0) % n
+
+    def _k_for(self, par):
+        """Kernel-space Gram buffer of buffer set par (one per set, so the next
+        call's Gram never overwrites a K the previous projection still reads)."""
+        ks = self.__dict__.setdefault("_K_sets", {})
+        k = ks.get(par)
+        if k is None:
+            m = self.landmarks.size
+            k = ks[par] = self.torch.empty((m + 2, m + 2), dtype=self.torch.float64,
+                                           device=self.device)
+        return k
+
+    def _kspace_launch(self, pts, coef, forcing, kpar=0, input_event=None):
         torch, lib = self.torch, self.lib
         n_c = int(pts.numel())
         m = self.landmarks.size
@@ -394,12 +411,20 @@ class SingleSolvePipeline:
             self.kpws_b = lib.nys_kspace_project_workspace_bytes(m, m)
             self.kpws = torch.empty(self.kpws_b, dtype=torch.uint8, device=self.device)
             self._kn_c = n_c
-        cur = torch.cuda.current_stream(self.device)
-        self._side.wait_stream(cur)
+        if input_event is not None:
+            # the caller's event marks its inputs final: the Gram need not wait
+            # for the caller's earlier work (the previous call's KKT)
+            self._side.wait_event(input_event)
+        else:
+            self._side.wait_stream(torch.cuda.current_stream(self.device))
+        done = self.__dict__.get("_eig_done")
+        if done is not None and done[kpar] is not None:
+            self._side.wait_event(done[kpar])   # the last projection that read K_kpar
+        K = self._kcur = self._k_for(kpar)
         _lib.call("nys_kspace_gram_f64", _lib.ptr(self.eig.d_lm), m, float(self.kernel.sigma2),
                   self.order, _lib.ptr(pts), _lib.ptr(coef), _lib.ptr(forcing), n_c,
                   *((0, n_c) if self._rows is None else self._rows),
-                  self._kctas, _lib.ptr(self.K), _lib.ptr(self.kgws), self.kgws_b,
+                  self._kctas, _lib.ptr(K), _lib.ptr(self.kgws), self.kgws_b,
                   self._side.cuda_stream)
         self._kev.record(self._side)
 
@@ -438,7 +463,7 @@ class SingleSolvePipeline:
                                              device=self.device)
         return a
 
-    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None):
+    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
         if Ac is None:   # rows here (otherwise already computed on the eig stream)
             Ac = self.Ac
@@ -446,7 +471,8 @@ class SingleSolvePipeline:
                 _lib.call("nys_feature_matrix_f64", *args, st)
         n_c = pts.numel()
         if use_k:
-            _lib.call("nys_kspace_project_f64", _lib.ptr(self.K), m, _lib.ptr(fm.d_W), fm.ldw, me,
+            _lib.call("nys_kspace_project_f64", _lib.ptr(self._kcur if K is None else K), m,
+                      _lib.ptr(fm.d_W), fm.ldw, me,
                       _lib.ptr(self.E), _lib.ptr(self.kpws), self.kpws_b, st)
         else:
             _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw, me,
@@ -490,16 +516,21 @@ class SingleSolvePipeline:
         self.eig = buf
         return self.x, self.info
 
-    def _capture(self, fm, pts, coef, forcing, use_k, Ac=None):
+    def _capture(self, fm, pts, coef, forcing, use_k, Ac=None, K=None):
         torch = self.torch
         n0 = self.lib.nys_launch_count()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            self._post(fm, pts, coef, forcing, use_k, Ac)
+            self._post(fm, pts, coef, forcing, use_k, Ac, K)
         return g, self.lib.nys_launch_count() - n0
 
-    def run_device(self, pts, coef, forcing):
-        """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info)."""
+    def run_device(self, pts, coef, forcing, input_event=None):
+        """pts (n_c,), coef (p, n_c), forcing (n_c,) device float64 -> (x (1, side), info).
+
+        input_event: optional CUDA event after which the inputs are final (e.g.
+        the caller's H2D, or recorded once for static inputs); the kernel-space
+        Gram then waits on it instead of on all earlier work of the current
+        stream, so it can overlap the previous call's KKT."""
         import os
 
         from .nystrom import build_feature_map, launch_eig_pinned
@@ -512,10 +543,12 @@ class SingleSolvePipeline:
                 return self._run_fast(plan)
         cur = torch.cuda.current_stream()
         graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
+        overlap = graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0"
         if self._kspace:
-            self._kspace_launch(pts, coef, forcing)
+            kpar = self._calls_next() if overlap else 0
+            self._kspace_launch(pts, coef, forcing, kpar, input_event)
         par = None
-        if graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0":
+        if overlap:
             # the eigendecomposition (one CTA, FP64-latency bound) runs on
             # EIG_STREAMS side streams in rotation, each call with its own buffer
             # set (EIG_STREAMS + 1 sets), so consecutive calls' eigensolvers run
@@ -576,7 +609,7 @@ class SingleSolvePipeline:
             self.torch.cuda.current_stream(self.device).wait_event(self._kev)
             if self._rows is not None:   # partial K of this rank's rows -> full K
                 from .dist import allreduce_sum
-                allreduce_sum(self.K, self._group)
+                allreduce_sum(self._kcur, self._group)
         cond_omega = self._cond_known if par is not None else fm.condition
         if big and cond_omega > KSPACE_MAX_COND:
             raise IllConditionedLargeMapError(
@@ -597,8 +630,9 @@ class SingleSolvePipeline:
             _lib.note_graph_launches(hit[1])
         else:
             Ac = None if par is None else self._ac_for(par, me)
-            self._post(fm, pts, coef, forcing, use_k, Ac)   # eager: result + attributes
-            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac)
+            Kp = (self._k_for(par) if par is not None else self._kcur) if use_k else None
+            self._post(fm, pts, coef, forcing, use_k, Ac, Kp)   # eager: result + attributes
+            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac, Kp)
             if par is not None:
                 # the other eigendecomposition buffer sets will come round with
                 # the same inputs: capture theirs now (capture does not execute),
@@ -615,7 +649,8 @@ class SingleSolvePipeline:
                     k2 = key[:-1] + (f2.d_W.data_ptr(),)
                     if k2 not in self._graph:
                         self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k,
-                                                        self._ac_for(q, me))
+                                                        self._ac_for(q, me),
+                                                        self._k_for(q) if use_k else None)
                 if not self._kspace:   # steady state for these inputs: _run_fast
                     plan = [self._graph[key[:-1] + (b2.W.data_ptr(),)] for b2 in self._eigbufs]
                     self.__dict__.setdefault("_fast", {})[key[1:4]] = plan
