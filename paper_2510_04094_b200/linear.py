@@ -308,8 +308,8 @@ class SingleSolvePipeline:
 
     # concurrent eigendecompositions: enough that the one-CTA eigensolver
     # (B200, D&C: 0.14 ms at m = 20, 0.30 ms at m = 50, 3.7 ms at m = 256) keeps
-    # up with the rest of a call (~0.05 ms, 0.14 ms, 3.0 ms): 3 up to m = 128,
-    # else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
+    # up with the rest of a call (measured ~0.06, ~0.07 and 2.4 ms): 3 up to
+    # m = 32, 5 up to 128, else 2 (each one holds an SM); NYS_EIG_STREAMS overrides
     EIG_STREAMS = int(os.environ.get("NYS_EIG_STREAMS", "0"))
 
     def _n_eig_streams(self) -> int:
@@ -317,7 +317,8 @@ class SingleSolvePipeline:
             return self.EIG_STREAMS
         if getattr(self, "_rows", None) is not None:
             return 4   # row shards make the Gram short: more eigensolvers in flight
-        return 3 if self.landmarks.size <= 128 else 2
+        m = self.landmarks.size
+        return 3 if m <= 32 else (5 if m <= 128 else 2)
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
                  drop_tol: float = 1e-16, device=None, rows=None, group=None):
@@ -463,27 +464,80 @@ class SingleSolvePipeline:
                                              device=self.device)
         return a
 
-    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None):
+    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None, E=None, part="all"):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
-        if Ac is None:   # rows here (otherwise already computed on the eig stream)
-            Ac = self.Ac
-            for args in self._rows_args(fm, Ac):
-                _lib.call("nys_feature_matrix_f64", *args, st)
-        n_c = pts.numel()
-        if use_k:
-            _lib.call("nys_kspace_project_f64", _lib.ptr(self._kcur if K is None else K), m,
-                      _lib.ptr(fm.d_W), fm.ldw, me,
-                      _lib.ptr(self.E), _lib.ptr(self.kpws), self.kpws_b, st)
-        else:
-            _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W), fm.ldw, me,
-                      float(fm.kernel.sigma2), self.order, _lib.ptr(pts), _lib.ptr(coef),
-                      _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(self.E), _lib.ptr(self.gws),
-                      self.gws_b, st)
-        _lib.call("nys_kkt_solve_f64", _lib.ptr(self.E), me, self.nk, _lib.ptr(Ac),
-                  _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
-                  _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
+        E = self.E if E is None else E
+        if part != "kkt":
+            if Ac is None:   # rows here (otherwise already computed on the eig stream)
+                Ac = self.Ac
+                for args in self._rows_args(fm, Ac):
+                    _lib.call("nys_feature_matrix_f64", *args, st)
+            n_c = pts.numel()
+            if use_k:
+                _lib.call("nys_kspace_project_f64", _lib.ptr(self._kcur if K is None else K), m,
+                          _lib.ptr(fm.d_W), fm.ldw, me,
+                          _lib.ptr(E), _lib.ptr(self.kpws), self.kpws_b, st)
+            else:
+                _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W),
+                          fm.ldw, me, float(fm.kernel.sigma2), self.order, _lib.ptr(pts),
+                          _lib.ptr(coef), _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(E),
+                          _lib.ptr(self.gws), self.gws_b, st)
+        if part != "gram":
+            _lib.call("nys_kkt_solve_f64", _lib.ptr(E), me, self.nk, _lib.ptr(Ac),
+                      _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
+                      _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
 
-    def _run_fast(self, plan):
+    def _e_for(self, par, me):
+        es = self.__dict__.setdefault("_E_sets", {})
+        e = es.get(par)
+        if e is None or e.shape[0] != me + 2:
+            e = es[par] = self.torch.empty((me + 2, me + 2), dtype=self.torch.float64,
+                                           device=self.device)
+        return e
+
+    def _split_capture(self, fm, pts, coef, forcing, Ac, E):
+        """Two graphs for the fused-Gram path: the Gram (replayed on a side
+        stream that waits only for the inputs and W) and the KKT (on the
+        caller's stream), so call k+1's Gram overlaps call k's KKT."""
+        torch = self.torch
+        out = []
+        for part in ("gram", "kkt"):
+            n0 = self.lib.nys_launch_count()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._post(fm, pts, coef, forcing, False, Ac, None, E, part)
+            out += [g, self.lib.nys_launch_count() - n0]
+        return tuple(out)
+
+    def _gram_side(self):
+        side = self.__dict__.get("_gside")
+        if side is None:
+            side = self._gside = self.torch.cuda.Stream(device=self.device)
+            self._gram_ev = [self.torch.cuda.Event() for _ in self._eigbufs]
+        return side
+
+    def _replay_split(self, plan_par, par, input_event, cur):
+        """Gram graph on the side stream (inputs + W + this set's E free), KKT
+        graph on the caller's stream after it."""
+        torch = self.torch
+        gg, nlg, gk, nlk = plan_par
+        side = self._gram_side()
+        if input_event is not None:
+            side.wait_event(input_event)
+        else:
+            side.wait_stream(cur)
+        side.wait_event(self._eig_ev[par])
+        if self._eig_done[par] is not None:
+            side.wait_event(self._eig_done[par])   # E of this set: its last KKT is done
+        with torch.cuda.stream(side):
+            gg.replay()
+        gev = self._gram_ev[par]
+        gev.record(side)
+        cur.wait_event(gev)
+        gk.replay()
+        _lib.note_graph_launches(nlg + nlk)
+
+    def _run_fast(self, plan, input_event=None):
         """Steady-state call for inputs whose graphs exist for every buffer set
         (configs 0/1): rotate the set and the eigensolver stream, launch the
         eigendecomposition with pre-bound arguments, replay the set's graph --
@@ -506,12 +560,16 @@ class SingleSolvePipeline:
         ev = self._eig_ev[par]
         ev.record(es)
         self._pending.append((ev, buf, self._me_known))
-        ev.wait()   # current stream
-        g, nl = plan[par]
-        g.replay()
-        _lib.note_graph_launches(nl)
+        cur = self.torch.cuda.current_stream()
+        p = plan[par]
+        if len(p) == 4:
+            self._replay_split(p, par, input_event, cur)
+        else:
+            cur.wait_event(ev)
+            p[0].replay()
+            _lib.note_graph_launches(p[1])
         post = self._post_ev[par]
-        post.record()
+        post.record(cur)
         self._eig_done[par] = post
         self.eig = buf
         return self.x, self.info
@@ -540,7 +598,7 @@ class SingleSolvePipeline:
         if fast:
             plan = fast.get((pts.data_ptr(), coef.data_ptr(), forcing.data_ptr()))
             if plan is not None:
-                return self._run_fast(plan)
+                return self._run_fast(plan, input_event)
         cur = torch.cuda.current_stream()
         graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
         overlap = graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0"
@@ -624,42 +682,63 @@ class SingleSolvePipeline:
                fm.d_W.data_ptr())
         if self._graph is None:
             self._graph = {}
+        # split Gram / KKT graphs (call k+1's Gram overlaps call k's KKT) pay off
+        # once the KKT is long; for tiny systems the extra stream hops cost more
+        split = (not use_k) and par is not None and me >= 32
+        if split:
+            key = key + ("split",)
         hit = self._graph.get(key)
         if hit is not None:
-            hit[0].replay()
-            _lib.note_graph_launches(hit[1])
+            if split:
+                self._replay_split(hit, par, input_event, cur)
+            else:
+                hit[0].replay()
+                _lib.note_graph_launches(hit[1])
         else:
             Ac = None if par is None else self._ac_for(par, me)
             Kp = (self._k_for(par) if par is not None else self._kcur) if use_k else None
-            self._post(fm, pts, coef, forcing, use_k, Ac, Kp)   # eager: result + attributes
-            self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac, Kp)
+            Ep = self._e_for(par, me) if split else None
+            # eager: this call's result + the kernels' one-time attribute setup
+            self._post(fm, pts, coef, forcing, use_k, Ac, Kp, Ep)
+            if split:
+                self._graph[key] = self._split_capture(fm, pts, coef, forcing, Ac, Ep)
+                # the eager Gram ran on this stream: later side-stream Grams (shared
+                # workspace) must follow it
+                self._gram_side().wait_stream(cur)
+            else:
+                self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac, Kp)
             if par is not None:
                 # the other eigendecomposition buffer sets will come round with
                 # the same inputs: capture theirs now (capture does not execute),
                 # so steady-state calls only replay
+                self._fm_cache.setdefault(par, fm)
                 for q, b2 in enumerate(self._eigbufs):
-                    if q == par:
-                        continue
                     f2 = self._fm_cache.get(q)
                     if f2 is None:
                         f2 = self._fm_cache[q] = NystromFeatureMap(
                             kernel=self.kernel, landmarks=self.landmarks, m_eff=me,
                             device=self.device, d_landmarks=b2.d_lm, d_W=b2.W, d_eigvals=b2.s,
                             d_eigvecs=b2.V)
-                    k2 = key[:-1] + (f2.d_W.data_ptr(),)
-                    if k2 not in self._graph:
+                    k2 = key[:6] + (f2.d_W.data_ptr(),) + key[7:]
+                    if k2 in self._graph:
+                        continue
+                    if split:
+                        self._graph[k2] = self._split_capture(f2, pts, coef, forcing,
+                                                              self._ac_for(q, me),
+                                                              self._e_for(q, me))
+                    else:
                         self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k,
                                                         self._ac_for(q, me),
                                                         self._k_for(q) if use_k else None)
                 if not self._kspace:   # steady state for these inputs: _run_fast
-                    plan = [self._graph[key[:-1] + (b2.W.data_ptr(),)] for b2 in self._eigbufs]
+                    plan = [self._graph[key[:6] + (b2.W.data_ptr(),) + key[7:]]
+                            for b2 in self._eigbufs]
                     self.__dict__.setdefault("_fast", {})[key[1:4]] = plan
                     self._eig_args = [
                         (_lib.ptr(b2.d_lm), self.landmarks.size, float(self.kernel.sigma2),
                          float(self.drop_tol), _lib.ptr(b2.s), _lib.ptr(b2.V), _lib.ptr(b2.W),
                          _lib.ptr(b2.meta_h), _lib.ptr(b2.meta_h) + 4, _lib.ptr(b2.ws), b2.wsb)
                         for b2 in self._eigbufs]
-                    self._fm_cache.setdefault(par, fm)
                     self._rows_bound = [self._rows_args(self._fm_cache[q], self._ac_for(q, me))
                                         for q in range(len(self._eigbufs))]
         if par is not None:
