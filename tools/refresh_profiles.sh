@@ -9,12 +9,12 @@ for c in 2 0 1 3 4; do
   timeout 600 python bench.py --config $c > $O/bench_c$c.log 2>&1
 done
 timeout 600 python bench.py --impl reference > $O/bench_reference.log 2>&1
-for s in 1 3; do
+for s in 1 3 5; do
   for c in 0 1; do
     echo "c$c streams=$s $(NYS_EIG_STREAMS=$s timeout 300 python bench.py --config $c --no-cpu-baseline 2>&1 | tail -1)" >> $O/streams.log
   done
 done
-for c in 2 4; do
+for c in 1 2 4; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
       --log-file $O/launches_c$c.csv python bench.py --config $c --no-cpu-baseline --steps 3 --warmup 3 > $O/ncu_launch_c$c.log 2>&1
 done
