@@ -435,18 +435,23 @@ class NewtonBatch:
         b0 = x0[:, self.me]
         t = self.pts_host
         p = self.p
-        coef = np.empty((len(ids), p, self.n_c))
-        forcing = np.empty((len(ids), self.n_c))
-        if self.family is not None:   # vectorised over the instances (family mode)
+        if self.family is not None:   # vectorised over the instances, on the device
             # y = b0 is constant along t, so the y-dependent terms are one scalar
-            # per instance (the same numbers the elementwise form produces)
+            # per instance; forcing = (g + c) - d elementwise, the same two
+            # roundings the host form makes
             fam = self.family
+            torch = self.torch
             ida = np.asarray(ids)
             a, be = fam.alpha[ida], fam.beta[ida]
-            f0 = fam.g[ida] + (a * b0 * b0 + be * np.sin(b0))[:, None]
+            c = a * b0 * b0 + be * np.sin(b0)
             fy = 2.0 * a * b0 + be * np.cos(b0)
-            coef[:, 0] = fy[:, None]
-            forcing[:] = f0 - (fy * b0)[:, None]
+            sc = torch.as_tensor(np.stack([c, fy, fy * b0]), device=self.dev)
+            idx_t = self._idx(ids)
+            coef = sc[1][:, None, None].expand(len(ids), 1, self.n_c).contiguous()
+            forcing = (self.g.index_select(0, idx_t.long()) + sc[0][:, None]) - sc[2][:, None]
+        else:
+            coef = np.empty((len(ids), p, self.n_c))
+            forcing = np.empty((len(ids), self.n_c))
         for r, b in enumerate(ids if self.family is None else ()):
             yb = np.full_like(t, b0[r])
             if p == 2:   # args (t, b0, 0); f_k = df/dy^(p-k) (newton.py:256-266)
