@@ -45,13 +45,17 @@ __global__ void __launch_bounds__(32)
   const double* vals = values + (size_t)b * P;
   double* L = dsm;                  // NBLK blocks x 64
   double* dinv = L + NBLK * 64;     // me
-  double* Yb = dinv + me;           // me x 8: [block][row][column], columns >= R zero
-  double* xs = Yb + me * 8;         // me
+  // Y in CW columns per row (4 when R <= 4: 2 KB less shared memory per
+  // system, 10 instead of 9 systems per SM at m_eff = 64); the DMMA operands
+  // read the columns >= CW as zeros
+  constexpr int CW = R <= 4 ? 4 : 8;
+  double* Yb = dinv + me;           // me x CW: [block][row][column], columns >= R zero
+  double* xs = Yb + me * CW;        // me
   const double inv_gamma = 1.0 / gamma;
   auto at = [&](int i, int j) -> double& {   // element (i, j), j <= i
     return L[blk(i >> 3, j >> 3) * 64 + swz(i & 7, j & 7)];
   };
-  auto Y = [&](int i, int q) -> double& { return Yb[(i >> 3) * 64 + (i & 7) * 8 + q]; };
+  auto Y = [&](int i, int q) -> double& { return Yb[(i >> 3) * 8 * CW + (i & 7) * CW + q]; };
 
   // ---- A = E[0:me, 0:me] into the lower blocks: asynchronous global->shared
   // copies (all of them in flight at once, no registers), then + I / gamma
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(32)
     for (int mu = 0; mu < P; ++mu) Y(i, 1 + mu) = Ac[(size_t)mu * me + i];
     Y(i, Q) = E[(size_t)i * Pe + me + 1];
 #pragma unroll
-    for (int q = R; q < 8; ++q) Y(i, q) = 0.0;
+    for (int q = R; q < CW; ++q) Y(i, q) = 0.0;
   }
   __syncwarp();
   // Blocked triangular solves.  A lane holds the 8 x 8 block's MMA accumulator
@@ -150,12 +154,13 @@ __global__ void __launch_bounds__(32)
   auto forward = [&](unsigned cols) {   // Y <- L^{-1} Y
 #pragma unroll 1
     for (int I = 0; I < NBK; ++I) {
-      double2 cv = *reinterpret_cast<const double2*>(Yb + I * 64 + fr * 8 + 2 * fc);
+      double2 cv = 2 * fc < CW ? *reinterpret_cast<const double2*>(Yb + I * 8 * CW + fr * CW + 2 * fc)
+                                : make_double2(0.0, 0.0);
       for (int J = 0; J < I; ++J) {
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const double a = -L[blk(I, J) * 64 + swz(fr, 4 * kk + fc)];
-          const double bq = Yb[J * 64 + (4 * kk + fc) * 8 + fr];
+          const double bq = fr < CW ? Yb[J * 8 * CW + (4 * kk + fc) * CW + fr] : 0.0;
           nys::dmma(cv.x, cv.y, a, bq);
         }
       }
@@ -174,21 +179,22 @@ __global__ void __launch_bounds__(32)
           cv.y = fma(-l, yy, cv.y);
         }
       }
-      double* dst = Yb + I * 64 + fr * 8 + 2 * fc;
-      if ((cols >> (2 * fc)) & 1u) dst[0] = cv.x;
-      if ((cols >> (2 * fc + 1)) & 1u) dst[1] = cv.y;
+      double* dst = Yb + I * 8 * CW + fr * CW + 2 * fc;
+      if (2 * fc < CW && ((cols >> (2 * fc)) & 1u)) dst[0] = cv.x;
+      if (2 * fc + 1 < CW && ((cols >> (2 * fc + 1)) & 1u)) dst[1] = cv.y;
       __syncwarp();
     }
   };
   auto backward = [&](unsigned cols) {   // Y <- L^{-T} Y
 #pragma unroll 1
     for (int I = NBK - 1; I >= 0; --I) {
-      double2 cv = *reinterpret_cast<const double2*>(Yb + I * 64 + fr * 8 + 2 * fc);
+      double2 cv = 2 * fc < CW ? *reinterpret_cast<const double2*>(Yb + I * 8 * CW + fr * CW + 2 * fc)
+                                : make_double2(0.0, 0.0);
       for (int J = I + 1; J < NBK; ++J) {
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
           const double a = -L[blk(J, I) * 64 + swz(4 * kk + fc, fr)];   // (L_JI)^T
-          const double bq = Yb[J * 64 + (4 * kk + fc) * 8 + fr];
+          const double bq = fr < CW ? Yb[J * 8 * CW + (4 * kk + fc) * CW + fr] : 0.0;
           nys::dmma(cv.x, cv.y, a, bq);
         }
       }
@@ -207,9 +213,9 @@ __global__ void __launch_bounds__(32)
           cv.y = fma(-l, yy, cv.y);
         }
       }
-      double* dst = Yb + I * 64 + fr * 8 + 2 * fc;
-      if ((cols >> (2 * fc)) & 1u) dst[0] = cv.x;
-      if ((cols >> (2 * fc + 1)) & 1u) dst[1] = cv.y;
+      double* dst = Yb + I * 8 * CW + fr * CW + 2 * fc;
+      if (2 * fc < CW && ((cols >> (2 * fc)) & 1u)) dst[0] = cv.x;
+      if (2 * fc + 1 < CW && ((cols >> (2 * fc + 1)) & 1u)) dst[1] = cv.y;
       __syncwarp();
     }
   };
@@ -386,7 +392,8 @@ template <int P, int NBK>
 int launch_block(const double* dense, const double* Ac, const double* beta, const double* values,
                  double gamma, int B, double* x, int* info, cudaStream_t st) {
   constexpr int me = NBK * 8;
-  const size_t dyn = ((size_t)NBK * (NBK + 1) / 2 * 64 + me + (size_t)me * 8 + me) *
+  constexpr int CW = P + 2 <= 4 ? 4 : 8;   // Y columns (kernel: R = P + 2)
+  const size_t dyn = ((size_t)NBK * (NBK + 1) / 2 * 64 + me + (size_t)me * CW + me) *
                      sizeof(double);
   auto kern = kkt_block_kernel<P, NBK>;
   if (dyn > 48 * 1024) {
