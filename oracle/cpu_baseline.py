@@ -134,3 +134,42 @@ def c4_solve_seconds_estimate(sample_rows: int = 1 << 18, seed: int = 0):
     scale = (g.size - 1) / sample_rows
     return t_eig + t_asm * scale + t_solve, dict(t_eig=t_eig, t_asm_sample=t_asm, scale=scale,
                                                  t_solve=t_solve)
+
+
+def _yhat_range(args):
+    cid, seed, indices, cfg_over = args
+    from oracle import nys_port as O
+    from paper_2510_04094_b200 import workloads as W
+
+    cfg = _cfg(cid, cfg_over)
+    g = W.grid(cfg)
+    lm = O.equidistant(g, cfg.m)
+    s, v = O.eig_landmarks(cfg.sigma2, lm)
+    Wb = O.scaled_basis(s, v)
+    me = Wb.shape[1]
+    out = []
+    for i in indices:
+        inst = W.instance(cid, seed, i, cfg)
+        sy = O.assemble(cfg.order, inst.coeff_fns(), inst.forcing_fn, inst.conditions(), g,
+                        cfg.gamma, cfg.sigma2, lm, Wb)
+        x = O.solve_kkt(sy["M"], sy["rhs"])
+        y = O.predict(cfg.sigma2, lm, Wb, x[:me], float(x[me]), 0, g)
+        ys = inst.sol(g)
+        out.append((i, y, float(np.linalg.norm(y - ys) / np.linalg.norm(ys))))
+    return out
+
+
+def reference_yhat(cid: int, indices, workers: int | None = None, seed: int = 0,
+                   cfg_over=None) -> dict:
+    """Oracle y_hat on the grid (and its error vs y*) for the given linear
+    instances -- the checker bench.py runs beside its cpu_baseline leg to
+    compare the timed batch's solutions with (never the thing measured)."""
+    import multiprocessing as mp
+
+    indices = list(indices)
+    workers = max(1, min(workers or os.cpu_count() or 1, len(indices)))
+    parts = [indices[w::workers] for w in range(workers)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_worker_init) as pool:
+        res = pool.map(_yhat_range, [(cid, seed, p, cfg_over) for p in parts if p])
+    return {i: (y, e) for part in res for i, y, e in part}

@@ -15,12 +15,13 @@ import time
 import numpy as np
 
 from . import linear, newton, nystrom
+from ._refcompat import ref_base
 from .kernel import RbfKernel
 
 FULL_FEATURE_MAX_N = 5000       # baselines.py:167
 
 
-class MemoryGuardError(ValueError):
+class MemoryGuardError(*ref_base("baselines", "MemoryGuardError", ValueError)):
     """n above the full-feature cap (baselines.py:170-171)."""
 
 

@@ -7,10 +7,12 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+from ._refcompat import ref_base
+
 MAX_DERIV_ORDER = 4          # kernel.py:19
 
 
-class UnsupportedOrderError(ValueError):
+class UnsupportedOrderError(*ref_base("kernel", "UnsupportedOrderError", ValueError)):
     """Derivative order outside 0..4 (kernel.py:22-23)."""
 
 

@@ -22,6 +22,7 @@ import os
 
 import numpy as np
 
+from ._refcompat import ref_base
 from . import _lib
 from .nystrom import NystromFeatureMap
 
@@ -32,7 +33,7 @@ KSPACE_MAX_COND = 1e6
 SMALL_NB_MAX = 9                 # register-resident fused kernel: m_eff + 2 <= 72
 
 
-class SingularSystemError(np.linalg.LinAlgError):
+class SingularSystemError(*ref_base("linear", "SingularSystemError", np.linalg.LinAlgError)):
     """Direct solve failed or produced non-finite entries (linear.py:36-37)."""
 
 

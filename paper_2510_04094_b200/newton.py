@@ -33,26 +33,30 @@ from typing import Optional, Sequence
 
 import numpy as np
 
+from ._refcompat import ref_base
 from . import _lib
 from .linear import PrimalModel, condition_rows, constraint_points, predict_batch
 from .nystrom import NystromFeatureMap
 
 
-class PartialsMissingError(ValueError):
+class PartialsMissingError(*ref_base("newton", "PartialsMissingError", ValueError)):
     pass
 
 
-class SingularJacobianError(np.linalg.LinAlgError):
+class SingularJacobianError(*ref_base("newton", "SingularJacobianError",
+                                     np.linalg.LinAlgError)):
     pass
 
 
-class DivergenceError(RuntimeError):
+class DivergenceError(*ref_base("newton", "DivergenceError", RuntimeError)):
     pass
 
 
-class MaxItersExceeded(RuntimeError):
+class MaxItersExceeded(*ref_base("newton", "MaxItersExceeded", RuntimeError)):
     def __init__(self, message: str, model: PrimalModel, trace: "NewtonTrace"):
-        super().__init__(message)
+        # the reference's __init__ (newton.py:42-45) only stores the same two
+        # attributes; RuntimeError's works for both bases
+        RuntimeError.__init__(self, message)
         self.model = model
         self.trace = trace
 

@@ -19,6 +19,7 @@ from typing import Any, Optional
 
 import numpy as np
 
+from ._refcompat import ref_base
 from . import _lib
 from .kernel import RbfKernel, check_order
 
@@ -26,11 +27,11 @@ DEFAULT_DROP_TOL = 1e-16     # nystrom.py:21
 _LEVERAGE_EXACT_LIMIT = 4000  # nystrom.py:25
 
 
-class DegenerateLandmarksError(ValueError):
+class DegenerateLandmarksError(*ref_base("nystrom", "DegenerateLandmarksError", ValueError)):
     """Two landmarks coincide within 1e-12 (nystrom.py:29-30)."""
 
 
-class InvalidCountError(ValueError):
+class InvalidCountError(*ref_base("nystrom", "InvalidCountError", ValueError)):
     """Landmark count outside 2..n (nystrom.py:33-34)."""
 
 

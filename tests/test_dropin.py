@@ -1,0 +1,108 @@
+"""Drop-in boundary: exception identity with the reference and the unmodified
+``nysode.harness.run`` under the monkeypatch of INTEGRATION.md §2.
+
+``nysode`` is found in ``baseline/_ref`` (the reference installed by pip,
+git-ignored, travels to the GPU box) or in ``/root/reference/pkg/src`` (build
+container only); without either these tests skip.  Everything runs in a
+subprocess so the package's exception bases are resolved with ``nysode`` on
+the path from the start.
+"""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+_CANDIDATES = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
+NYSODE = next((p for p in _CANDIDATES if os.path.isdir(os.path.join(p, "nysode"))), None)
+needs_nysode = pytest.mark.skipif(NYSODE is None, reason="nysode (reference) not importable")
+
+
+def _env():
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([NYSODE, ROOT]),
+               PYTHONDONTWRITEBYTECODE="1")
+    env.pop("NYSB200_NO_NYSODE", None)
+    return env
+
+
+# (our module, class, reference module) -- reference file:line of each class:
+# newton.py:29-45, linear.py:36, nystrom.py:28-33, kernel.py:22, baselines.py:166
+_CLASSES = [
+    ("newton", "MaxItersExceeded", "newton"), ("newton", "DivergenceError", "newton"),
+    ("newton", "SingularJacobianError", "newton"), ("newton", "PartialsMissingError", "newton"),
+    ("linear", "SingularSystemError", "linear"), ("nystrom", "DegenerateLandmarksError", "nystrom"),
+    ("nystrom", "InvalidCountError", "nystrom"), ("kernel", "UnsupportedOrderError", "kernel"),
+    ("baselines", "MemoryGuardError", "baselines"),
+]
+
+
+@needs_nysode
+def test_exceptions_subclass_reference_classes():
+    code = (
+        "import importlib, json\n"
+        f"pairs = {_CLASSES!r}\n"
+        "out = {}\n"
+        "for ours, cls, ref in pairs:\n"
+        "    a = getattr(importlib.import_module('paper_2510_04094_b200.' + ours), cls)\n"
+        "    b = getattr(importlib.import_module('nysode.' + ref), cls)\n"
+        "    out[cls] = issubclass(a, b)\n"
+        "import paper_2510_04094_b200.newton as W1, nysode.newton as W0\n"
+        "try:\n"
+        "    raise W1.MaxItersExceeded('x', None, None)\n"
+        "except W0.MaxItersExceeded as exc:\n"
+        "    out['caught'] = exc.model is None and exc.trace is None\n"
+        "print(json.dumps(out))\n")
+    r = subprocess.run([sys.executable, "-c", code], env=_env(), capture_output=True,
+                       text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(out.values()), out
+
+
+@needs_nysode
+def test_patch_and_undo_rebind_reference_entry_points():
+    code = (
+        "import json, nysode.linear as L0, nysode.newton as W0, nysode.nystrom as N0\n"
+        "import nysode.baselines as B0\n"
+        "from paper_2510_04094_b200 import dropin, linear as L1, newton as W1, nystrom as N1\n"
+        "from paper_2510_04094_b200 import baselines as B1\n"
+        "orig = (L0.assemble, L0.solve, W0.solve_nonlinear, N0.build_feature_map)\n"
+        "undo = dropin.patch_nysode()\n"
+        "patched = (L0.assemble is L1.assemble and L0.solve is L1.solve and\n"
+        "           L0.check_kkt is L1.check_kkt and W0.solve_nonlinear is W1.solve_nonlinear\n"
+        "           and N0.build_feature_map is N1.build_feature_map and\n"
+        "           N0.select_landmarks is N1.select_landmarks and\n"
+        "           B0.full_feature_baseline is B1.full_feature_baseline)\n"
+        "undo()\n"
+        "restored = orig == (L0.assemble, L0.solve, W0.solve_nonlinear, N0.build_feature_map)\n"
+        "print(json.dumps([patched, restored]))\n")
+    r = subprocess.run([sys.executable, "-c", code], env=_env(), capture_output=True,
+                       text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert json.loads(r.stdout.strip().splitlines()[-1]) == [True, True]
+
+
+@pytest.mark.gpu
+@needs_nysode
+def test_unmodified_harness_under_patch():
+    """harness.run on P3, P12, P4 and a P4 MaxIters outcome: same results as
+    the reference (y_hat within 1e-6 relative L2, MAE within 1 %), and the
+    MaxIters outcome is caught by harness.py:173 instead of crashing."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "harness_dropin.py")],
+                       env=_env(), capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-4000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["maxiters_is_subclass"]
+    for name in ("P3", "P12", "P4"):
+        c = out[name]
+        assert c["dev_m_eff"] == c["ref_m_eff"], (name, c)
+        assert c["yhat_rel_l2"] <= 1e-6, (name, c)
+        assert abs(c["dev_mae"] - c["ref_mae"]) <= 0.01 * c["ref_mae"], (name, c)
+        assert c["dev_model_type"].startswith("paper_2510_04094_b200"), (name, c)
+    assert out["P4"]["dev_converged"] is True and out["P4"]["ref_converged"] is True
+    mi = out["P4_maxiters"]
+    assert mi["ref_converged"] is False and mi["dev_converged"] is False, mi
+    assert mi["dev_trace_len"] == mi["ref_trace_len"], mi
