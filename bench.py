@@ -806,9 +806,10 @@ def main():
         for cid in (0, 1, 3, 4):
             torch.cuda.empty_cache()
             r = measure(cid, args, ctx, T, with_cpu=(world == 1))
-            sub[f"c{cid}"] = {k: r[k] for k in ("value", "unit", "ms_per_step", "scaling",
+            sub[f"c{cid}"] = {k: r[k] for k in ("value", "unit", "ms_per_step",
+                                                 "latency_ms_l2_flushed", "scaling",
                                                  "gpu_launches", "e2e", "roofline", "config",
-                                                 "clocks") if k in r}
+                                                 "details", "clocks") if k in r}
             for k in ("cpu_baseline", "parity"):
                 if k in r:
                     sub[f"c{cid}"][k] = r[k]

@@ -85,6 +85,15 @@ NYS_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// shared-memory atomic add with acquire-release semantics at CTA scope
+NYS_DEV int atomic_add_acq_rel_cta(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;\n"
+               : "=r"(old)
+               : "r"(smem_u32(p)), "r"(v)
+               : "memory");
+  return old;
+}
 // global -> shared bulk copy, completion signalled on `bar` (bytes % 16 == 0).
 NYS_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -146,12 +146,16 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
       rr = rr_n;
     }
     // release the stage without a CTA barrier: the last warp to finish it
-    // refills it with chunk c + NS (warps drift up to NS - 1 chunks apart)
+    // refills it with chunk c + NS (warps drift up to NS - 1 chunks apart).
+    // Ordering: __syncwarp orders the warp's shared-memory reads of the stage
+    // before lane 0's release (acq_rel atomic); the last arriver's acquire
+    // sees every warp's reads complete, then fence.proxy.async orders them
+    // before the async-proxy refill.  The counter only grows (one WARPS-sized
+    // round per use of the stage), so no reset store races the next round.
     __syncwarp();
     if (lane == 0) {
-      const int done = atomicAdd(&cnt[stage], 1);
-      if (done == WARPS - 1) {
-        cnt[stage] = 0;
+      const int done = nys::atomic_add_acq_rel_cta(&cnt[stage], 1);
+      if (done % WARPS == WARPS - 1) {
         if (c + NS < nchunks) {
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           nys::mbar_expect_tx(&bar[stage], kChunkBytes);

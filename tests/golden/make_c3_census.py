@@ -1,10 +1,11 @@
 """Config-3 census: run the LIVE reference (``nysode``) on all 256 bench
 instances (seed 0) and store each outcome -- status, iteration count, the
 solution vector x and its error vs the manufactured solution -- plus the
-reference's landmark eigenpairs (x is expressed in that basis).  The fixture's
-status_dsyev column (the reference re-run with scipy's dsyev driver for the
-landmark eigenproblem, /tmp-free variant of this script with driver="ev") is the
-reference's own outcome sensitivity that the GPU test uses as its yardstick.
+reference's landmark eigenpairs (x is expressed in that basis).  A second pass
+re-runs the reference with only its landmark eigensolver driver swapped
+(scipy's dsyev for numpy's dsyevd) and stores that outcome as status_dsyev /
+iterations_dsyev: the reference's own outcome sensitivity, the yardstick of
+the GPU census test.
 
 Build container only (``/root/reference`` is absent on the GPU box):
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_c3_census.py
@@ -31,6 +32,13 @@ def _init():
     sys.path.insert(0, ROOT)
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
+
+
+def _solve_dsyev(i):
+    import scipy.linalg as sl
+
+    np.linalg.eigh = lambda A: sl.eigh(A, driver="ev")   # worker process only
+    return _solve(i)
 
 
 def _solve(i):
@@ -68,6 +76,8 @@ def main():
     n = 256
     with ProcessPoolExecutor(max_workers=os.cpu_count(), initializer=_init) as ex:
         res = sorted(ex.map(_solve, range(n)))
+    with ProcessPoolExecutor(max_workers=os.cpu_count(), initializer=_init) as ex:
+        res_ev = sorted(ex.map(_solve_dsyev, range(n)))
     me = next(r[3].size for r in res if r[3] is not None)
     X = np.full((n, me), np.nan)
     for i, st, its, x, err in res:
@@ -85,9 +95,13 @@ def main():
                         eigvals=fmap.eigenvalues, eigvecs=fmap.eigenvectors,
                         status=np.array([r[1] for r in res], np.int32),
                         iterations=np.array([r[2] for r in res], np.int32),
-                        x=X, err_vs_exact=np.array([r[4] for r in res]))
+                        x=X, err_vs_exact=np.array([r[4] for r in res]),
+                        status_dsyev=np.array([r[1] for r in res_ev], np.int32),
+                        iterations_dsyev=np.array([r[2] for r in res_ev], np.int32))
     st = np.bincount([r[1] for r in res], minlength=4)
-    print(f"c3 census: status counts {st.tolist()} in {time.time() - t0:.1f}s")
+    st_ev = np.bincount([r[1] for r in res_ev], minlength=4)
+    print(f"c3 census: status counts {st.tolist()} (dsyev driver {st_ev.tolist()}) "
+          f"in {time.time() - t0:.1f}s")
 
 
 if __name__ == "__main__":
