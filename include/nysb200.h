@@ -61,7 +61,8 @@ unsigned long long nys_launch_count(void);
 /* ------------------------------------------------------------------------
  * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map
  * (nystrom.py:136-160) + NystromFeatureMap._scaled_vectors (nystrom.py:120-121).
- * Omega = K(L, L); cyclic parallel Jacobi; eigenpairs sorted descending;
+ * Omega = K(L, L); one CTA: Householder tridiagonalisation + Cuppen divide and
+ * conquer (m <= 256; implicit QL above); eigenpairs sorted descending;
  * keep s > max(drop_tol * s_0, 0).
  *   eigvals  [m]     descending (entries >= m_eff are the dropped ones)
  *   eigvecs  [m*m]   column k = eigenvector k (row-major m x m)
@@ -245,6 +246,46 @@ int nys_newton_step_f64(const double* S0, const double* S1, int m_eff, int n_c, 
                         const double* gamma, const double* X, double* D, double* Xc,
                         const double* alpha, int ldx, const int* idx, int nb, int compute_delta,
                         void* stream);
+
+/* Device-resident Newton loop (replaces newton._solve_once, newton.py:279-349,
+ * for the separable family f = g + alpha y^2 + beta sin y, p = 1): one CTA per
+ * instance idx[j] runs the convergence / divergence checks, the Schur-reduced
+ * system, its LU, the y back-substitution, the step-halving line search
+ * (damped != 0: alpha = shrink^k, k < halvings, accept the first finite trial
+ * norm <= the current one, else shrink^halvings) and the residual at every
+ * trial with no host round trip.  X[idx[j]] holds the start point on entry
+ * and the final iterate on exit; norms[j][0..iters[j]] the residual max-norms
+ * (the trace); status[j] 0 converged / 1 max iterations / 2 diverged /
+ * 3 singular.  work: nb * nys_newton_solve_once_work_doubles doubles. */
+size_t nys_newton_solve_once_work_doubles(int m_eff, int n_c, int n_cond);
+int nys_newton_solve_once_f64(const double* S0, const double* S1, const double* S0T,
+                              const double* S1T, const double* packed, int m_eff, int n_c,
+                              const double* g, const double* alpha, const double* beta,
+                              const double* Ac, const double* betac, const double* vals,
+                              int n_cond, const double* gamma, const double* tol, double* X,
+                              int ldx, const int* idx, int nb, int damped, double shrink,
+                              int halvings, int max_iters, double* work, size_t work_bytes,
+                              double* norms, int* iters, int* status, void* stream);
+
+/* The whole retry ladder on the device (replaces newton.solve_nonlinear's
+ * ladder, newton.py:376-412, and _solve_with_continuation, newton.py:352-373):
+ * per instance, one CTA runs rung 1 (X0c, undamped), 2 (X0c, damped), 3 (X0l,
+ * undamped), 4 (X0l, damped) until one converges, else rung 5: damped stages
+ * at gamma = 1, 1e2, 1e4 below gamma[idx] with tol 1e-8 (1 + g) (MaxIters
+ * tolerated, divergence / singularity ends the instance), each handing
+ * (omega, b, lambda = 0, y = Psi_0 omega + b) on, then gamma[idx] itself.
+ * X0c / X0l [nb][ldx] (indexed by slot j): the constant and linearised
+ * starts; X[idx[j]] the final iterate; rung[j] 1..5 the rung that produced
+ * status[j] / norms[j][0..iters[j]] (the trace of that last _solve_once). */
+int nys_newton_ladder_f64(const double* S0, const double* S1, const double* S0T,
+                          const double* S1T, const double* packed, int m_eff, int n_c,
+                          const double* g, const double* alpha, const double* beta,
+                          const double* Ac, const double* betac, const double* vals, int n_cond,
+                          const double* gamma, const double* tol, const double* X0c,
+                          const double* X0l, double* X, int ldx, const int* idx, int nb,
+                          double shrink, int halvings, int max_iters, double* work,
+                          size_t work_bytes, double* norms, int* iters, int* status, int* rung,
+                          void* stream);
 
 /* ---- ridge leverage scores -------------------------
  * Replaces the exact branch of nystrom.ridge_leverage_scores (nystrom.py:58-70,

@@ -86,6 +86,14 @@ SIGNATURES = {
     "nys_sym_eig_f64": (_i, [_vp, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_newton_step_f64": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                  _i, _vp, _i, _i, _vp]),
+    "nys_newton_solve_once_work_doubles": (_sz, [_i, _i, _i]),
+    "nys_newton_persist_profile": (None, [_vp]),
+    "nys_newton_ladder_f64": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp,
+                                   _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _i, _d, _i, _i, _vp,
+                                   _sz, _vp, _vp, _vp, _vp, _vp]),
+    "nys_newton_solve_once_f64": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp,
+                                       _vp, _i, _vp, _vp, _vp, _i, _vp, _i, _i, _d, _i, _i, _vp,
+                                       _sz, _vp, _vp, _vp, _vp]),
 }
 
 

@@ -24,9 +24,12 @@
 // arrays (host-evaluated reference callables: the generic drop-in path).
 #include <cmath>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
+
+#define NYS_HD_INLINE __host__ __device__ __forceinline__
 
 namespace nys_host {
 int launch_psi_pack(const double* lm, int m, const double* W, int ldw, int m_eff, double sigma2,
@@ -104,27 +107,18 @@ struct Rhs {
 constexpr int kResSplit = 4;
 NYS_DEV int res_rows_per_split(int n_c) { return ((n_c + kResSplit - 1) / kResSplit + 31) / 32 * 32; }
 
+// one row range (split) of the residual of instance b at x (kTrial: at
+// x + al * dx), by the whole CTA; the range's partial sums go to out[2 me + 3]
 template <bool kTrial>
-__global__ void __launch_bounds__(kResThreads)
-    newton_residual_kernel(const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
-                           int n_c, Rhs rhs, const double* __restrict__ gamma,
-                           const double* __restrict__ X, int ldx, const int* __restrict__ idx,
-                           double* __restrict__ F, double* __restrict__ aux,
-                           const double* __restrict__ D, const double* __restrict__ alphas, int nb,
-                           int nk, double* __restrict__ part) {
-  extern __shared__ double sh[];
-  __shared__ double red[kResThreads / 32];
-  const int b = idx[blockIdx.x];
-  const double gm = gamma[b];
-  const double* x = X + (size_t)b * ldx;
-  const double* dx = kTrial ? D + (size_t)b * ldx : nullptr;
-  const double al = kTrial ? alphas[blockIdx.y] : 0.0;
+NYS_DEV void residual_range(const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
+                            int n_c, const Rhs& rhs, double gm, const double* __restrict__ x,
+                            const double* __restrict__ dx, double al, int b, int split, int nk,
+                            double* __restrict__ Fb, double* __restrict__ auxb,
+                            double* __restrict__ out, double* sh, double* red) {
   // x entry j of this CTA's point (trial: the candidate, as newton_step_kernel forms it)
 #define NYS_XV(j) (kTrial ? fma(al, dx[j], x[j]) : x[j])
-  const int split = blockIdx.z;
   const int rpc = res_rows_per_split(n_c);
   const int r0 = split * rpc, r1 = min(n_c, r0 + rpc);
-  double* Fb = kTrial ? nullptr : F + (size_t)b * ldx;
   double* om = sh;                 // me
   double* e1 = sh + me;            // rpc (this CTA's rows)
   double* e2 = e1 + rpc;
@@ -133,7 +127,6 @@ __global__ void __launch_bounds__(kResThreads)
   __syncthreads();
   const double bias = NYS_XV(me);
   const int y0 = me + 1 + nk;
-  double* auxb = kTrial ? nullptr : aux + (size_t)b * 3 * n_c;
   double fmax_local = 0.0;
   int bad = 0;
   // rows across threads, features from the transposed copies: every load is
@@ -173,9 +166,6 @@ __global__ void __launch_bounds__(kResThreads)
     }
   }
   __syncthreads();
-  const size_t slot = kTrial ? (size_t)blockIdx.y * nb + blockIdx.x : (size_t)blockIdx.x;
-  const int pstride = 2 * me + 3;
-  double* out = part + (slot * kResSplit + split) * pstride;
   // partial S1^T e1 and S0^T e2 over this row range (warp per k)
   for (int k = warp; k < me; k += nw) {
     const double* rr1 = S1T + (size_t)k * n_c;
@@ -206,6 +196,29 @@ __global__ void __launch_bounds__(kResThreads)
     out[2 * me + 2] = any_bad ? 1.0 : 0.0;
   }
 #undef NYS_XV
+}
+
+template <bool kTrial>
+__global__ void __launch_bounds__(kResThreads)
+    newton_residual_kernel(const double* __restrict__ S0T, const double* __restrict__ S1T, int me,
+                           int n_c, Rhs rhs, const double* __restrict__ gamma,
+                           const double* __restrict__ X, int ldx, const int* __restrict__ idx,
+                           double* __restrict__ F, double* __restrict__ aux,
+                           const double* __restrict__ D, const double* __restrict__ alphas, int nb,
+                           int nk, double* __restrict__ part) {
+  extern __shared__ double sh[];
+  __shared__ double red[kResThreads / 32];
+  const int b = idx[blockIdx.x];
+  const double* x = X + (size_t)b * ldx;
+  const double* dx = kTrial ? D + (size_t)b * ldx : nullptr;
+  const double al = kTrial ? alphas[blockIdx.y] : 0.0;
+  const int split = blockIdx.z;
+  double* Fb = kTrial ? nullptr : F + (size_t)b * ldx;
+  double* auxb = kTrial ? nullptr : aux + (size_t)b * 3 * n_c;
+  const size_t slot = kTrial ? (size_t)blockIdx.y * nb + blockIdx.x : (size_t)blockIdx.x;
+  const int pstride = 2 * me + 3;
+  residual_range<kTrial>(S0T, S1T, me, n_c, rhs, gamma[b], x, dx, al, b, split, nk, Fb, auxb,
+                         part + (slot * kResSplit + split) * pstride, sh, red);
 }
 
 template <bool kTrial>
@@ -301,12 +314,11 @@ constexpr int kRedWarps = 4;
 // NPAIR*64 Gram entries in MMA layout, then NB*8 rhs entries).
 template <int NB>
 NYS_DEV void build_reduced(const double* red, int stride, int nparts, int me, int nk,
-                           const double* __restrict__ F, int ldx, double gm,
-                           const double* __restrict__ Ac, const double* __restrict__ betac, int b,
+                           const double* __restrict__ Fb, double gm,
+                           const double* __restrict__ Ac, const double* __restrict__ betac,
                            double* Kb, double* rb) {
   constexpr int NPAIR = Tri<NB>::kPairs;
   const int nz = me + 1 + nk, nh = me + 1;
-  const double* Fb = F + (size_t)b * ldx;
   for (int e = threadIdx.x; e < NPAIR * 64; e += blockDim.x) {
     double s = 0.0;
     for (int w = 0; w < nparts; ++w) s += red[(size_t)w * stride + e];
@@ -341,32 +353,22 @@ NYS_DEV void build_reduced(const double* red, int stride, int nparts, int me, in
   for (int mu = threadIdx.x; mu < nk; mu += blockDim.x) rb[nh + mu] = -Fb[nh + mu];
 }
 
-// grid (instances, nsplit): CTA (j, s) accumulates k-steps [s kps, (s+1) kps)
-// of instance idx[j]; with part == nullptr (nsplit = 1) it builds K directly,
-// otherwise it stores its partial sums for newton_reduce_finalize_kernel.
+// one warp's share of the reduced system over k-steps ks_lo + wi, + nwg, ...
+// < ks_hi: the three weighted DMMA Grams and the rhs term, stored to mine[]
+// (NPAIR*64 Gram entries in MMA layout, then NB*8 rhs entries)
 template <int NB>
-__global__ void __launch_bounds__(kRedWarps * 32)
-    newton_reduce_kernel(const double* __restrict__ psi, int nks, int me, int n_c,
-                         const double* __restrict__ aux, const double* __restrict__ F, int ldx,
-                         const double* __restrict__ gamma, const double* __restrict__ Ac,
-                         const double* __restrict__ betac, int nk, const int* __restrict__ idx,
-                         double* __restrict__ K, double* __restrict__ rz, int kps,
-                         double* __restrict__ part) {
+NYS_DEV void reduce_warp(const double* __restrict__ psi, int me, int n_c,
+                         const double* __restrict__ auxb, const double* __restrict__ Fy,
+                         int ks_lo, int ks_hi, int wi, int nwg, double* mine) {
   constexpr int NPAIR = Tri<NB>::kPairs;
-  extern __shared__ double red[];   // [kRedWarps][NPAIR*64 + NB*8]
-  const int b = idx[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tig = lane & 3, gid = lane >> 2;
-  const double* auxb = aux + (size_t)b * 3 * n_c;
-  const double* Fy = F + (size_t)b * ldx + me + 1 + nk;
+  const int lane = threadIdx.x & 31, tig = lane & 3, gid = lane >> 2;
   double acc[NPAIR][2];
 #pragma unroll
   for (int q = 0; q < NPAIR; ++q) acc[q][0] = acc[q][1] = 0.0;
   double racc[NB];
 #pragma unroll
   for (int F_ = 0; F_ < NB; ++F_) racc[F_] = 0.0;
-
-  const int ks_lo = blockIdx.y * kps, ks_hi = min(nks, ks_lo + kps);
-  for (int ks = ks_lo + warp; ks < ks_hi; ks += kRedWarps) {
+  for (int ks = ks_lo + wi; ks < ks_hi; ks += nwg) {
     const int row = ks * 4 + tig;
     const bool ok = row < n_c;
     const double fy = ok ? auxb[row] : 0.0;
@@ -385,26 +387,43 @@ __global__ void __launch_bounds__(kRedWarps * 32)
       xv[F_] = fma(-fy, x0[F_], x1[F_]);                  // vh = S1h - f_y S0h
       racc[F_] = fma(fma(fy, x1[F_], x0[F_]), fyc, racc[F_]);   // sum wh F_y / c
     }
+    // per accumulator the order is (vh, S1h, S0h) as before, but the three
+    // terms are issued as three passes over the block pairs so consecutive
+    // DMMAs never depend on each other (asm volatile keeps issue order)
 #pragma unroll
     for (int I = 0; I < NB; ++I) {
-      const double av = w1 * xv[I], a1 = w2 * x1[I], a0 = w2 * x0[I];
+      const double av = w1 * xv[I];
 #pragma unroll
       for (int J = I; J < NB; ++J) {
         const int t = Tri<NB>::idx(I, J);
         nys::dmma(acc[t][0], acc[t][1], av, xv[J]);
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < NB; ++I) {
+      const double a1 = w2 * x1[I];
+#pragma unroll
+      for (int J = I; J < NB; ++J) {
+        const int t = Tri<NB>::idx(I, J);
         nys::dmma(acc[t][0], acc[t][1], a1, x1[J]);
+      }
+    }
+#pragma unroll
+    for (int I = 0; I < NB; ++I) {
+      const double a0 = w2 * x0[I];
+#pragma unroll
+      for (int J = I; J < NB; ++J) {
+        const int t = Tri<NB>::idx(I, J);
         nys::dmma(acc[t][0], acc[t][1], a0, x0[J]);
       }
     }
   }
-  // reduce racc over the 4 rows held by a quad (tig), then over warps in smem
+  // reduce racc over the 4 rows held by a quad (tig)
 #pragma unroll
   for (int F_ = 0; F_ < NB; ++F_) {
     racc[F_] += __shfl_xor_sync(0xffffffffu, racc[F_], 1);
     racc[F_] += __shfl_xor_sync(0xffffffffu, racc[F_], 2);
   }
-  const int stride = NPAIR * 64 + NB * 8;
-  double* mine = red + (size_t)warp * stride;
 #pragma unroll
   for (int t = 0; t < NPAIR; ++t) {
     mine[t * 64 + lane * 2] = acc[t][0];
@@ -413,6 +432,27 @@ __global__ void __launch_bounds__(kRedWarps * 32)
   if (tig == 0)
 #pragma unroll
     for (int F_ = 0; F_ < NB; ++F_) mine[NPAIR * 64 + F_ * 8 + gid] = racc[F_];
+}
+
+// grid (instances, nsplit): CTA (j, s) accumulates k-steps [s kps, (s+1) kps)
+// of instance idx[j]; with part == nullptr (nsplit = 1) it builds K directly,
+// otherwise it stores its partial sums for newton_reduce_finalize_kernel.
+template <int NB>
+__global__ void __launch_bounds__(kRedWarps * 32)
+    newton_reduce_kernel(const double* __restrict__ psi, int nks, int me, int n_c,
+                         const double* __restrict__ aux, const double* __restrict__ F, int ldx,
+                         const double* __restrict__ gamma, const double* __restrict__ Ac,
+                         const double* __restrict__ betac, int nk, const int* __restrict__ idx,
+                         double* __restrict__ K, double* __restrict__ rz, int kps,
+                         double* __restrict__ part) {
+  constexpr int NPAIR = Tri<NB>::kPairs;
+  extern __shared__ double red[];   // [kRedWarps][NPAIR*64 + NB*8]
+  const int b = idx[blockIdx.x];
+  const int warp = threadIdx.x >> 5;
+  const int ks_lo = blockIdx.y * kps, ks_hi = min(nks, ks_lo + kps);
+  const int stride = NPAIR * 64 + NB * 8;
+  reduce_warp<NB>(psi, me, n_c, aux + (size_t)b * 3 * n_c, F + (size_t)b * ldx + me + 1 + nk,
+                  ks_lo, ks_hi, warp, kRedWarps, red + (size_t)warp * stride);
   __syncthreads();
   if (part != nullptr) {   // this split's partial, warps summed in fixed order
     double* out = part + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * stride;
@@ -424,7 +464,7 @@ __global__ void __launch_bounds__(kRedWarps * 32)
     return;
   }
   const int nz = me + 1 + nk;
-  build_reduced<NB>(red, stride, kRedWarps, me, nk, F, ldx, gamma[b], Ac, betac, b,
+  build_reduced<NB>(red, stride, kRedWarps, me, nk, F + (size_t)b * ldx, gamma[b], Ac, betac,
                     K + (size_t)blockIdx.x * nz * nz, rz + (size_t)blockIdx.x * nz);
 }
 
@@ -441,8 +481,8 @@ __global__ void __launch_bounds__(256)
   const int b = idx[blockIdx.x];
   const int nz = me + 1 + nk;
   // partials of this instance sit nb * stride apart (one per split)
-  build_reduced<NB>(part + (size_t)blockIdx.x * stride, nb * stride, nsplit, me, nk, F, ldx,
-                    gamma[b], Ac, betac, b, K + (size_t)blockIdx.x * nz * nz,
+  build_reduced<NB>(part + (size_t)blockIdx.x * stride, nb * stride, nsplit, me, nk,
+                    F + (size_t)b * ldx, gamma[b], Ac, betac, K + (size_t)blockIdx.x * nz * nz,
                     rz + (size_t)blockIdx.x * nz);
 }
 
@@ -708,6 +748,792 @@ __global__ void transpose_kernel(const double* __restrict__ A, int rows, int col
   }
 }
 
+// ---------------------------------------------------------------------------
+// Device-resident Newton (newton._solve_once, newton.py:279-349) for the
+// separable family, p = 1: ONE CTA per instance runs the whole loop -- the
+// convergence / divergence checks, the reduced (omega, b, lambda) system, its
+// LU, the y back-substitution, the step-halving line search and the residual
+// at every trial point -- with no host round trip.  Every piece is the
+// arithmetic of the multi-kernel path above, in the same order: the residual
+// is residual_range over the same kResSplit row ranges with the same 256-thread
+// mapping and the same fixed-order finalize, the LU is lu_solve_cta's, the step
+// is newton_step_kernel's; the reduced Gram uses the 2-split / 4-warp partition
+// the multi-kernel path uses for 148..295 active instances.  Trial points are
+// materialised (Xc = fma(alpha, D, X)) and evaluated with every by-product, so
+// an accepted trial's F / aux are the next iteration's (no second residual).
+constexpr int kPersistThreads = 256;
+#ifndef NYS_PERSIST_MINB
+#define NYS_PERSIST_MINB 1   // 255 registers: the reduced-system accumulators do not spill
+#endif
+constexpr int kPersistSplits = 2;
+constexpr int kPTrials = 4;   // line-search trials evaluated together
+
+// the kResSplit row ranges of residual_range<false> in ONE pass: every row,
+// partial sum and reduction tree is the one residual_range forms for its range
+// (thread tid takes rows r0 + tid + k * blockDim.x of every range, warps take
+// (range, k) pairs for S^T e with the same lane / row mapping, the per-range
+// sum of e2 goes through block_reduce's tree), so part[] is bit-identical to
+// four residual_range calls -- with 4x the loads in flight and a quarter of
+// the barriers.  sh: me + 2 n_c doubles; red: kResSplit * (blockDim / 32).
+NYS_DEV void residual_splits_fused(const double* __restrict__ S0T, const double* __restrict__ S1T,
+                                   int me, int n_c, const Rhs& rhs, double gm,
+                                   const double* __restrict__ x, int b, int nk,
+                                   double* __restrict__ Fb, double* __restrict__ auxb,
+                                   double* __restrict__ part, double* sh, double* red) {
+  const int rpc = res_rows_per_split(n_c);
+  const int pstride = 2 * me + 3;
+  double* om = sh;
+  double* e1 = sh + me;
+  double* e2 = e1 + n_c;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  for (int k = tid; k < me; k += nt) om[k] = x[k];
+  __syncthreads();
+  const double bias = x[me];
+  const int y0 = me + 1 + nk;
+  double fmax_local = 0.0;
+  int bad = 0;
+  double se2[kResSplit];
+#pragma unroll
+  for (int sp = 0; sp < kResSplit; ++sp) se2[sp] = 0.0;
+#pragma unroll
+  for (int sp = 0; sp < kResSplit; ++sp) {
+    const int r0 = sp * rpc, r1 = min(n_c, r0 + rpc);
+    for (int i = r0 + tid; i < r1; i += nt) {
+      double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0;
+      int k = 0;
+#pragma unroll 4
+      for (; k + 1 < me; k += 2) {
+        a0 = fma(S1T[(size_t)k * n_c + i], om[k], a0);
+        a1 = fma(S1T[(size_t)(k + 1) * n_c + i], om[k + 1], a1);
+        c0 = fma(S0T[(size_t)k * n_c + i], om[k], c0);
+        c1 = fma(S0T[(size_t)(k + 1) * n_c + i], om[k + 1], c1);
+      }
+      if (k < me) {
+        a0 = fma(S1T[(size_t)k * n_c + i], om[k], a0);
+        c0 = fma(S0T[(size_t)k * n_c + i], om[k], c0);
+      }
+      const double s1w = a0 + a1, s0w = c0 + c1;
+      const double yi = x[y0 + i];
+      double f, fy, fyy;
+      rhs.eval(b, i, yi, f, fy, fyy);
+      const double ee1 = __dsub_rn(s1w, f);
+      const double ee2 = __dsub_rn(__dsub_rn(yi, s0w), bias);
+      if (!isfinite(ee1) || !isfinite(f)) bad = 1;
+      e1[i] = ee1;
+      e2[i] = ee2;
+      se2[sp] += ee2;
+      const double Fy = __dadd_rn(__dmul_rn(__dmul_rn(-gm, fy), ee1), __dmul_rn(gm, ee2));
+      fmax_local = fmax(fmax_local, fabs(Fy));
+      Fb[y0 + i] = Fy;
+      const double q = __dmul_rn(fyy, ee1);
+      auxb[i] = fy;
+      auxb[n_c + i] = q;
+      auxb[2 * n_c + i] = __dsub_rn(__dadd_rn(1.0, __dmul_rn(fy, fy)), q);
+    }
+  }
+  // per-range sums of e2: block_reduce's tree, kResSplit at once
+#pragma unroll
+  for (int sp = 0; sp < kResSplit; ++sp) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se2[sp] = se2[sp] + __shfl_xor_sync(0xffffffffu, se2[sp], o);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) fmax_local = fmax(fmax_local, __shfl_xor_sync(0xffffffffu, fmax_local, o));
+  if (lane == 0) {
+#pragma unroll
+    for (int sp = 0; sp < kResSplit; ++sp) red[sp * nw + warp] = se2[sp];
+    red[kResSplit * nw + warp] = fmax_local;
+  }
+  const int any_bad = __syncthreads_or(bad);
+  // partial S1^T e1 and S0^T e2 per (range, k): one warp each, lanes over the range's rows
+  for (int t = warp; t < kResSplit * me; t += nw) {
+    const int sp = t / me, k = t % me;
+    const int r0 = sp * rpc, r1 = min(n_c, r0 + rpc);
+    const double* rr1 = S1T + (size_t)k * n_c;
+    const double* rr0 = S0T + (size_t)k * n_c;
+    double a = 0.0, c = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) {
+      a = fma(rr1[i], e1[i], a);
+      c = fma(rr0[i], e2[i], c);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) {
+      part[sp * pstride + k] = a;
+      part[sp * pstride + me + k] = c;
+    }
+  }
+  if (tid < kResSplit) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += red[tid * nw + w];   // fixed order
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, red[kResSplit * nw + w]);
+    part[tid * pstride + 2 * me] = s;
+    part[tid * pstride + 2 * me + 1] = m;   // the max over all ranges: the finalize takes the max
+    part[tid * pstride + 2 * me + 2] = any_bad ? 1.0 : 0.0;
+  }
+  __syncthreads();
+}
+
+NYS_DEV double bias_of(double al, const double* D, const double* X, int me) {
+  return fma(al, D[me], X[me]);
+}
+
+// Residual max-norms at KT line-search trial points x_t = fma(al[t], D, X)
+// at once (nothing else written): every trial's arithmetic -- rows, range
+// partials, reduction trees, finalize -- is persist_residual's, so each norm is
+// bit-identical to materialising the trial and calling persist_residual, but
+// every S0^T / S1^T element loaded from L2 serves all KT trials.
+// sh: KT (me + 2 n_c) doubles; red: KT (kResSplit + 1) (blockDim / 32);
+// part: KT kResSplit (2 me + 3); out[t] = norm (NaN: non-finite rhs).
+template <int KT>
+NYS_DEV void trial_norms_multi(const double* __restrict__ S0T, const double* __restrict__ S1T,
+                               int me, int n_c, const Rhs& rhs, double gm,
+                               const double* __restrict__ X, const double* __restrict__ D,
+                               const double* al, int b, int nk, const double* __restrict__ Ac,
+                               const double* __restrict__ betac, const double* __restrict__ vals,
+                               double* part, double* sh, double* red, double* out) {
+  const int rpc = res_rows_per_split(n_c);
+  const int pstride = 2 * me + 3;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double* om = sh;                       // [KT][me]
+  double* e1 = sh + KT * me;             // [KT][n_c]
+  double* e2 = e1 + KT * (size_t)n_c;    // [KT][n_c]
+  for (int e = tid; e < KT * me; e += nt) {
+    const int t = e / me, k = e % me;
+    om[e] = fma(al[t], D[k], X[k]);
+  }
+  __syncthreads();
+  const int y0 = me + 1 + nk;
+  double bias[KT];
+#pragma unroll
+  for (int t = 0; t < KT; ++t) bias[t] = fma(al[t], D[me], X[me]);
+  double fmax_local[KT], se2[KT][kResSplit];
+  int bad[KT];
+#pragma unroll
+  for (int t = 0; t < KT; ++t) {
+    fmax_local[t] = 0.0;
+    bad[t] = 0;
+#pragma unroll
+    for (int sp = 0; sp < kResSplit; ++sp) se2[t][sp] = 0.0;
+  }
+#pragma unroll
+  for (int sp = 0; sp < kResSplit; ++sp) {
+    const int r0 = sp * rpc, r1 = min(n_c, r0 + rpc);
+    for (int i = r0 + tid; i < r1; i += nt) {
+      double a0[KT], a1[KT], c0[KT], c1[KT];
+#pragma unroll
+      for (int t = 0; t < KT; ++t) a0[t] = a1[t] = c0[t] = c1[t] = 0.0;
+      int k = 0;
+#pragma unroll 2
+      for (; k + 1 < me; k += 2) {
+        const double s1a = S1T[(size_t)k * n_c + i], s1b = S1T[(size_t)(k + 1) * n_c + i];
+        const double s0a = S0T[(size_t)k * n_c + i], s0b = S0T[(size_t)(k + 1) * n_c + i];
+#pragma unroll
+        for (int t = 0; t < KT; ++t) {
+          a0[t] = fma(s1a, om[t * me + k], a0[t]);
+          a1[t] = fma(s1b, om[t * me + k + 1], a1[t]);
+          c0[t] = fma(s0a, om[t * me + k], c0[t]);
+          c1[t] = fma(s0b, om[t * me + k + 1], c1[t]);
+        }
+      }
+      if (k < me) {
+        const double s1a = S1T[(size_t)k * n_c + i], s0a = S0T[(size_t)k * n_c + i];
+#pragma unroll
+        for (int t = 0; t < KT; ++t) {
+          a0[t] = fma(s1a, om[t * me + k], a0[t]);
+          c0[t] = fma(s0a, om[t * me + k], c0[t]);
+        }
+      }
+      const double xy = X[y0 + i], dy = D[y0 + i];
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        const double s1w = a0[t] + a1[t], s0w = c0[t] + c1[t];
+        const double yi = fma(al[t], dy, xy);
+        double f, fy, fyy;
+        rhs.eval(b, i, yi, f, fy, fyy);
+        const double ee1 = __dsub_rn(s1w, f);
+        const double ee2 = __dsub_rn(__dsub_rn(yi, s0w), bias[t]);
+        if (!isfinite(ee1) || !isfinite(f)) bad[t] = 1;
+        e1[t * (size_t)n_c + i] = ee1;
+        e2[t * (size_t)n_c + i] = ee2;
+        se2[t][sp] += ee2;
+        const double Fy = __dadd_rn(__dmul_rn(__dmul_rn(-gm, fy), ee1), __dmul_rn(gm, ee2));
+        fmax_local[t] = fmax(fmax_local[t], fabs(Fy));
+      }
+    }
+  }
+  int badm = 0;
+#pragma unroll
+  for (int t = 0; t < KT; ++t) {
+#pragma unroll
+    for (int sp = 0; sp < kResSplit; ++sp) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+        se2[t][sp] = se2[t][sp] + __shfl_xor_sync(0xffffffffu, se2[t][sp], o);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+      fmax_local[t] = fmax(fmax_local[t], __shfl_xor_sync(0xffffffffu, fmax_local[t], o));
+    badm |= bad[t] << t;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < KT; ++t) {
+      double* rt = red + t * (kResSplit + 1) * nw;
+#pragma unroll
+      for (int sp = 0; sp < kResSplit; ++sp) rt[sp * nw + warp] = se2[t][sp];
+      rt[kResSplit * nw + warp] = fmax_local[t];
+    }
+  }
+  // OR of the per-trial flags over the CTA (bit t = trial t)
+  __shared__ int badm_s;
+  if (tid == 0) badm_s = 0;
+  __syncthreads();
+  if (badm) atomicOr(&badm_s, badm);
+  // range partials of S1^T e1 and S0^T e2 for every trial
+  for (int task = warp; task < kResSplit * me; task += nw) {
+    const int sp = task / me, k = task % me;
+    const int r0 = sp * rpc, r1 = min(n_c, r0 + rpc);
+    const double* rr1 = S1T + (size_t)k * n_c;
+    const double* rr0 = S0T + (size_t)k * n_c;
+    double a[KT], c[KT];
+#pragma unroll
+    for (int t = 0; t < KT; ++t) a[t] = c[t] = 0.0;
+    for (int i = r0 + lane; i < r1; i += 32) {
+      const double v1 = rr1[i], v0 = rr0[i];
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        a[t] = fma(v1, e1[t * (size_t)n_c + i], a[t]);
+        c[t] = fma(v0, e2[t * (size_t)n_c + i], c[t]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < KT; ++t) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        a[t] += __shfl_xor_sync(0xffffffffu, a[t], o);
+        c[t] += __shfl_xor_sync(0xffffffffu, c[t], o);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int t = 0; t < KT; ++t) {
+        part[(t * kResSplit + sp) * pstride + k] = a[t];
+        part[(t * kResSplit + sp) * pstride + me + k] = c[t];
+      }
+    }
+  }
+  __syncthreads();
+  // finalize per trial (persist_residual's arithmetic); warp t handles trial t
+  for (int t = warp; t < KT; t += nw) {
+    const double* pt = part + (size_t)t * kResSplit * pstride;
+    const double* rt = red + t * (kResSplit + 1) * nw;
+    const double* omt = om + t * me;
+    double fm = 0.0;
+    for (int k = lane; k < me; k += 32) {
+      double a = 0.0, c = 0.0;
+      for (int s2 = 0; s2 < kResSplit; ++s2) {
+        a += pt[s2 * pstride + k];
+        c += pt[s2 * pstride + me + k];
+      }
+      double acl = 0.0;
+      for (int mu = 0; mu < nk; ++mu)
+        acl = __dadd_rn(acl, __dmul_rn(Ac[(size_t)mu * me + k],
+                                       fma(al[t], D[me + 1 + mu], X[me + 1 + mu])));
+      const double v = __dadd_rn(__dsub_rn(__dadd_rn(omt[k], __dmul_rn(gm, a)), __dmul_rn(gm, c)), acl);
+      fm = fmax(fm, fabs(v));
+    }
+    if (lane == 0) {
+      double se = 0.0;
+      for (int s2 = 0; s2 < kResSplit; ++s2) {
+        double sw = 0.0;
+        for (int w = 0; w < nw; ++w) sw += rt[s2 * nw + w];   // block_reduce's order
+        se += sw;
+      }
+      double fy = 0.0;
+      for (int w = 0; w < nw; ++w) fy = fmax(fy, rt[kResSplit * nw + w]);
+      fm = fmax(fm, fy);
+      double bl = 0.0;
+      for (int mu = 0; mu < nk; ++mu)
+        bl = __dadd_rn(bl, __dmul_rn(betac[mu], fma(al[t], D[me + 1 + mu], X[me + 1 + mu])));
+      fm = fmax(fm, fabs(__dadd_rn(__dmul_rn(-gm, se), bl)));
+      for (int mu = 0; mu < nk; ++mu) {
+        double v = 0.0;
+        for (int k = 0; k < me; ++k) v = fma(Ac[(size_t)mu * me + k], omt[k], v);
+        v = __dsub_rn(__dadd_rn(v, __dmul_rn(betac[mu], bias_of(al[t], D, X, me))),
+                      vals[(size_t)b * nk + mu]);
+        fm = fmax(fm, fabs(v));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) fm = fmax(fm, __shfl_xor_sync(0xffffffffu, fm, o));
+    if (lane == 0) out[t] = ((badm_s >> t) & 1) ? NAN : fm;
+  }
+  __syncthreads();
+}
+
+// residual at x (F, aux, the norm; NaN when the rhs is non-finite): the four
+// row ranges of newton_residual_kernel<false> + newton_residual_finalize_kernel
+NYS_DEV double persist_residual(const double* __restrict__ S0T, const double* __restrict__ S1T,
+                                int me, int n_c, const Rhs& rhs, double gm,
+                                const double* __restrict__ x, int b, int nk,
+                                const double* __restrict__ Ac, const double* __restrict__ betac,
+                                const double* __restrict__ vals, double* __restrict__ Fb,
+                                double* __restrict__ auxb, double* part, double* sh, double* red,
+                                double* lam_s) {
+  const int pstride = 2 * me + 3;
+  residual_splits_fused(S0T, S1T, me, n_c, rhs, gm, x, b, nk, Fb, auxb, part, sh, red);
+  const int tid = threadIdx.x;
+  if (tid < nk) lam_s[tid] = x[me + 1 + tid];
+  __syncthreads();
+  double fmax_local = 0.0;
+  int bad = 0;
+  for (int s2 = 0; s2 < kResSplit; ++s2) bad |= part[s2 * pstride + 2 * me + 2] != 0.0;
+  for (int k = tid; k < me; k += blockDim.x) {
+    double a = 0.0, c = 0.0;
+    for (int s2 = 0; s2 < kResSplit; ++s2) {
+      a += part[s2 * pstride + k];
+      c += part[s2 * pstride + me + k];
+    }
+    double acl = 0.0;
+    for (int mu = 0; mu < nk; ++mu) acl = __dadd_rn(acl, __dmul_rn(Ac[(size_t)mu * me + k], lam_s[mu]));
+    const double v = __dadd_rn(__dsub_rn(__dadd_rn(x[k], __dmul_rn(gm, a)), __dmul_rn(gm, c)), acl);
+    Fb[k] = v;
+    fmax_local = fmax(fmax_local, fabs(v));
+  }
+  if (tid == 0) {
+    double se2 = 0.0, fy = 0.0;
+    for (int s2 = 0; s2 < kResSplit; ++s2) {
+      se2 += part[s2 * pstride + 2 * me];
+      fy = fmax(fy, part[s2 * pstride + 2 * me + 1]);
+    }
+    fmax_local = fmax(fmax_local, fy);
+    double bl = 0.0;
+    for (int mu = 0; mu < nk; ++mu) bl = __dadd_rn(bl, __dmul_rn(betac[mu], lam_s[mu]));
+    const double Fbias = __dadd_rn(__dmul_rn(-gm, se2), bl);
+    Fb[me] = Fbias;
+    fmax_local = fmax(fmax_local, fabs(Fbias));
+    const double bias = x[me];
+    for (int mu = 0; mu < nk; ++mu) {
+      double v = 0.0;
+      for (int k = 0; k < me; ++k) v = fma(Ac[(size_t)mu * me + k], x[k], v);
+      v = __dsub_rn(__dadd_rn(v, __dmul_rn(betac[mu], bias)), vals[(size_t)b * nk + mu]);
+      Fb[me + 1 + mu] = v;
+      fmax_local = fmax(fmax_local, fabs(v));
+    }
+  }
+  const double nrm = block_reduce(fmax_local, red, true);   // max: order-free
+  __syncthreads();
+  return bad ? NAN : nrm;
+}
+
+// The LU of lu_solve_cta_kernel (first max wins; every element updated by the
+// same operation in the same k order, so the factors and the solution are
+// bit-identical): per column warp 0 searches the pivot and swaps the rows,
+// then all warps scale and update the trailing rows (row i by warp i % 8,
+// columns across lanes) -- two CTA barriers per column.  K (row-major n x n)
+// is copied into a padded odd-stride tile T (conflict-free 8-byte accesses).
+// Returns NYS_INFO_* to every thread; the solution is left in ys.
+constexpr int kPLuMaxN = 64;
+NYS_DEV int persist_lu(double* K, double* ys, int* perm, int n, int* flag, double* T) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int ld = n | 1;   // odd stride in doubles
+  for (int e = tid; e < n * n; e += blockDim.x) T[(e / n) * ld + e % n] = K[e];
+  if (tid == 0) *flag = NYS_INFO_OK;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {
+      double bv = -1.0;
+      int bi = n;
+      for (int i = k + lane; i < n; i += 32) {
+        const double a = fabs(T[i * ld + k]);
+        if (a > bv) {
+          bv = a;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (!(bv > 0.0)) {
+        if (lane == 0) *flag = NYS_INFO_SINGULAR;
+      } else {
+        if (lane == 0) perm[k] = bi;
+        if (bi != k)
+          for (int j = lane; j < n; j += 32) {
+            const double a = T[k * ld + j], p = T[bi * ld + j];
+            T[bi * ld + j] = a;
+            T[k * ld + j] = p;
+          }
+      }
+    }
+    __syncthreads();
+    if (*flag != NYS_INFO_OK) return *flag;
+    const double inv = 1.0 / T[k * ld + k];
+    const double* urow = T + k * ld;
+    for (int i = k + 1 + warp; i < n; i += nw) {
+      double* r = T + i * ld;
+      const double l = r[k] * inv;
+      __syncwarp();
+      if (lane == 0) r[k] = l;
+      for (int j = k + 1 + lane; j < n; j += 32) r[j] -= l * urow[j];
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    if (lane == 0)
+      for (int k = 0; k < n; ++k) {
+        const int pr = perm[k];
+        if (pr != k) {
+          const double t = ys[k];
+          ys[k] = ys[pr];
+          ys[pr] = t;
+        }
+      }
+    __syncwarp();
+    for (int j = 0; j < n - 1; ++j) {
+      const double yj = ys[j];
+      for (int i = j + 1 + lane; i < n; i += 32) ys[i] -= T[i * ld + j] * yj;
+      __syncwarp();
+    }
+    for (int j = n - 1; j >= 0; --j) {
+      const double zj = ys[j] / T[j * ld + j];
+      __syncwarp();
+      if (lane == 0) ys[j] = zj;
+      for (int i = lane; i < j; i += 32) ys[i] -= T[i * ld + j] * zj;
+      __syncwarp();
+    }
+    int bad = 0;
+    for (int i = lane; i < n; i += 32)
+      if (!isfinite(ys[i])) bad = 1;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *flag = NYS_INFO_NONFINITE;
+  }
+  __syncthreads();
+  return *flag;
+}
+
+// doubles of the persistent kernel's region A: the reduce partials of 8 warps,
+// the residual scratch, the padded LU tile or the multi-trial scratch
+NYS_HD_INLINE size_t persist_region_a(size_t stride, int me, int n_c, int nz) {
+  size_t r = (size_t)(kPersistThreads / 32) * stride;
+  const size_t res = (size_t)me + 2 * (size_t)n_c + kResSplit * (2 * (size_t)me + 3);
+  const size_t lu = (size_t)nz * (nz | 1);
+  const size_t multi = (size_t)kPTrials * kResSplit * (2 * (size_t)me + 3) +
+                       (size_t)kPTrials * ((size_t)me + 2 * (size_t)n_c);
+  r = r > res ? r : res;
+  r = r > lu ? r : lu;
+  return r > multi ? r : multi;
+}
+
+struct PersistArgs {
+  const double *S0, *S1, *S0T, *S1T, *psi;
+  int me, n_c, nk, nks, ldx;
+  Rhs rhs;
+  const double *Ac, *betac, *vals, *gamma, *tol;
+  double* X;
+  const int* idx;
+  int damped, halvings, max_iters;
+  double shrink;
+  double* work;        // per slot: Xc, F, Fc, D (ldx each), aux, auxc (3 n_c each)
+  size_t work_stride;  // doubles per slot
+  double* norms;       // [nb][max_iters + 1]
+  int* iters;          // [nb]
+  int* status;         // [nb]
+  long long* prof;     // optional [nb][8]: clocks in residual / reduce / LU / step, trials
+};
+
+// shared-memory carve-up of the persistent kernels
+struct PersistSmem {
+  double *redA, *sh, *part, *K, *ys, *red, *red_m, *al_s, *tn_s, *lam_s;
+  int *perm, *flag;
+};
+
+// newton._solve_once (newton.py:279-349) for instance b from the point in xg
+// (final iterate left there): returns the status (0 converged, 1 max
+// iterations, 2 diverged, 3 singular); *its = iterations, nrm_out[0..*its] the
+// residual max-norms.  wk: 4 ldx + 6 n_c doubles of scratch.
+template <int NB>
+NYS_DEV int persist_solve_once(const PersistArgs& A, const PersistSmem& S, int b, double gm,
+                               double tol, bool damped, double* xg, double* wk, double* nrm_out,
+                               int* its, long long* pc) {
+  constexpr int NPAIR = Tri<NB>::kPairs;
+  constexpr int kStride = NPAIR * 64 + NB * 8;
+  const int me = A.me, n_c = A.n_c, nk = A.nk, ldx = A.ldx;
+  const int nz = me + 1 + nk;
+  double* Xcur = xg;
+  double* Xnew = wk;
+  double* Fcur = wk + ldx;
+  double* Fnew = wk + 2 * (size_t)ldx;
+  double* Dv = wk + 3 * (size_t)ldx;
+  double* auxc = wk + 4 * (size_t)ldx;
+  double* auxn = auxc + 3 * (size_t)n_c;
+  double *redA = S.redA, *K = S.K, *ys = S.ys;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  double norm = persist_residual(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xcur, b, nk, A.Ac, A.betac,
+                                 A.vals, Fcur, auxc, S.part, S.sh, S.red, S.lam_s);
+  if (tid == 0) nrm_out[0] = norm;
+  int status = isfinite(norm) ? -1 : 2;   // DIVERGED: _residual raised at the start
+  int it = 0;
+  const int kps = (A.nks + kPersistSplits - 1) / kPersistSplits;
+  long long t0 = clock64();
+#define NYS_PT(i)                       \
+  do {                                  \
+    const long long t1_ = clock64();    \
+    pc[i] += t1_ - t0;                  \
+    t0 = t1_;                           \
+  } while (0)
+  while (status < 0) {
+    // newton.py:296-303
+    if (norm <= tol) { status = 0; break; }
+    if (it >= A.max_iters) { status = 1; break; }
+    if (norm > 1e12) { status = 2; break; }
+    // ---- reduced system (newton_reduce_kernel, 2 splits x 4 warps)
+    {
+      const int sp = warp >> 2, wi = warp & 3;
+      const int lo = sp * kps, hi = min(A.nks, lo + kps);
+      reduce_warp<NB>(A.psi, me, n_c, auxc, Fcur + nz, lo, hi, wi, 4,
+                      redA + (size_t)warp * kStride);
+      __syncthreads();
+      for (int e = tid; e < kStride; e += blockDim.x) {   // split partials, fixed order
+        double p0 = 0.0, p1 = 0.0;
+        for (int w = 0; w < 4; ++w) {
+          p0 += redA[(size_t)w * kStride + e];
+          p1 += redA[(size_t)(4 + w) * kStride + e];
+        }
+        redA[e] = p0;
+        redA[kStride + e] = p1;
+      }
+      __syncthreads();
+      build_reduced<NB>(redA, kStride, kPersistSplits, me, nk, Fcur, gm, A.Ac, A.betac, K, ys);
+      __syncthreads();
+    }
+    NYS_PT(1);
+    // ---- LU (first max wins), as nys_lu_solve_f64
+    const int info = persist_lu(K, ys, S.perm, nz, S.flag, redA);   // redA: free here
+    if (info != NYS_INFO_OK) { status = 3; break; }
+    NYS_PT(2);
+    // ---- delta (newton_step_kernel, compute_delta)
+    {
+      for (int k = tid; k < nz; k += blockDim.x) Dv[k] = ys[k];
+      int bad = 0;
+      for (int k = tid; k < nz; k += blockDim.x) bad |= !isfinite(ys[k]);
+      for (int i = tid; i < n_c; i += blockDim.x) {
+        // newton_step_kernel's dot products in the same k order, read from the
+        // transposed copies (coalesced across the CTA's rows)
+        double a = 0.0, c = 0.0;
+#pragma unroll 8
+        for (int k = 0; k < me; ++k) {
+          a = fma(A.S1T[(size_t)k * n_c + i], ys[k], a);
+          c = fma(A.S0T[(size_t)k * n_c + i], ys[k], c);
+        }
+        const double fy = auxc[i], cc = auxc[2 * n_c + i];
+        const double wd = fy * a + c + ys[me];
+        const double dv = (-Fcur[nz + i] + gm * wd) / (gm * cc);
+        Dv[nz + i] = dv;
+        bad |= !isfinite(dv);
+      }
+      if (__syncthreads_or(bad)) { status = 3; break; }   // non-finite correction
+    }
+    NYS_PT(3);
+    // ---- step halving (newton.py:313-325) or the full step.  alpha_k =
+    // shrink^k by the loop's repeated products; the first finite trial norm
+    // <= norm wins.  Trial 0 is a full residual (its F / aux are kept when it
+    // is accepted, the common case); later trials are evaluated kPTrials at a
+    // time (trial_norms_multi: bit-identical norms) and the accepted one is
+    // then materialised with its full residual.
+    double alpha = 1.0, tn = 0.0;
+    bool have;
+    {
+      for (int k = tid; k < nz + n_c; k += blockDim.x) Xnew[k] = fma(alpha, Dv[k], Xcur[k]);
+      __syncthreads();
+      tn = persist_residual(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xnew, b, nk, A.Ac, A.betac, A.vals,
+                            Fnew, auxn, S.part, S.sh, S.red, S.lam_s);
+      pc[5] += 1;
+      have = !damped || (isfinite(tn) && tn <= norm);
+    }
+    if (!have) {
+      alpha *= A.shrink;
+      bool found = false;
+      int h = 1;
+      while (!found && h < A.halvings) {
+        const int cnt = min(kPTrials, A.halvings - h);
+        if (tid == 0) {
+          double a = alpha;
+          for (int t = 0; t < kPTrials; ++t) {
+            S.al_s[t] = a;
+            if (t + 1 < cnt) a *= A.shrink;
+          }
+        }
+        __syncthreads();
+        trial_norms_multi<kPTrials>(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xcur, Dv, S.al_s, b, nk,
+                                    A.Ac, A.betac, A.vals, redA,
+                                    redA + kPTrials * kResSplit * (2 * me + 3), S.red_m, S.tn_s);
+        pc[5] += cnt;
+        for (int t = 0; t < cnt && !found; ++t) {
+          if (isfinite(S.tn_s[t]) && S.tn_s[t] <= norm) {
+            found = true;
+            alpha = S.al_s[t];
+          } else {
+            alpha *= A.shrink;
+          }
+        }
+        h += cnt;
+        __syncthreads();
+      }
+      // the accepted trial, or the last (untested) halving the loop leaves
+      for (int k = tid; k < nz + n_c; k += blockDim.x) Xnew[k] = fma(alpha, Dv[k], Xcur[k]);
+      __syncthreads();
+      tn = persist_residual(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xnew, b, nk, A.Ac, A.betac, A.vals,
+                            Fnew, auxn, S.part, S.sh, S.red, S.lam_s);
+    }
+    // x <- candidate; F, aux at it
+    {
+      double* t = Xcur; Xcur = Xnew; Xnew = t;   // the old point is no longer needed
+      t = Fcur; Fcur = Fnew; Fnew = t;
+      t = auxc; auxc = auxn; auxn = t;
+    }
+    ++it;
+    NYS_PT(0);
+    norm = tn;
+    if (tid == 0) nrm_out[it] = norm;
+    if (!isfinite(norm)) { status = 2; break; }
+  }
+#undef NYS_PT
+  // the final iterate lives in xg
+  if (Xcur != xg) {
+    for (int k = tid; k < nz + n_c; k += blockDim.x) xg[k] = Xcur[k];
+  }
+  __syncthreads();
+  *its = it;
+  return status;
+}
+
+template <int NB>
+NYS_DEV PersistSmem persist_smem(const PersistArgs& A, double* smp, double* red, double* red_m,
+                                 double* al_s, double* tn_s, double* lam_s, int* flag) {
+  constexpr int kStride = Tri<NB>::kPairs * 64 + NB * 8;
+  const int nz = A.me + 1 + A.nk;
+  PersistSmem S;
+  S.redA = smp;
+  S.sh = smp;                                  // me + 2 n_c (aliases redA)
+  S.part = smp + A.me + 2 * A.n_c;             // kResSplit (2 me + 3)
+  S.K = smp + persist_region_a(kStride, A.me, A.n_c, nz);
+  S.ys = S.K + (size_t)nz * nz;
+  S.perm = reinterpret_cast<int*>(S.ys + nz);
+  S.red = red;
+  S.red_m = red_m;
+  S.al_s = al_s;
+  S.tn_s = tn_s;
+  S.lam_s = lam_s;
+  S.flag = flag;
+  return S;
+}
+
+#define NYS_PERSIST_SHARED                                                   \
+  extern __shared__ double smp[];                                            \
+  __shared__ double red[(kResSplit + 1) * (kPersistThreads / 32)];           \
+  __shared__ double red_m[kPTrials * (kResSplit + 1) * (kPersistThreads / 32)]; \
+  __shared__ double al_s[kPTrials], tn_s[kPTrials];                          \
+  __shared__ double lam_s[kMaxCondN];                                        \
+  __shared__ int flag_s;                                                     \
+  const PersistSmem S = persist_smem<NB>(A, smp, red, red_m, al_s, tn_s, lam_s, &flag_s)
+
+// one _solve_once per instance (nys_newton_solve_once_f64)
+template <int NB>
+__global__ void __launch_bounds__(kPersistThreads, NYS_PERSIST_MINB)
+    newton_persist_kernel(PersistArgs A) {
+  NYS_PERSIST_SHARED;
+  const int slot = blockIdx.x;
+  const int b = A.idx[slot];
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int it = 0;
+  const int status = persist_solve_once<NB>(
+      A, S, b, A.gamma[b], A.tol[b], A.damped != 0, A.X + (size_t)b * A.ldx,
+      A.work + (size_t)slot * A.work_stride, A.norms + (size_t)slot * (A.max_iters + 1), &it, pc);
+  if (threadIdx.x == 0) {
+    A.iters[slot] = it;
+    A.status[slot] = status;
+    if (A.prof != nullptr)
+      for (int i = 0; i < 8; ++i) A.prof[(size_t)slot * 8 + i] = pc[i];
+  }
+}
+
+// the whole retry ladder per instance (newton.py:376-412; nys_newton_ladder_f64):
+// rungs 1-4 from the constant / linearised starts, undamped then damped;
+// rung 5 the gamma continuation (newton.py:352-373: stages 1, 1e2, 1e4 below
+// the target, damped, tol 1e-8 (1 + g), MaxIters tolerated, Divergence /
+// Singular escape; the model hand-off omega, b, lambda = 0, y = S0 omega + b),
+// then the target.  No instance waits for another between rungs or stages.
+template <int NB>
+__global__ void __launch_bounds__(kPersistThreads, NYS_PERSIST_MINB)
+    newton_ladder_kernel(PersistArgs A, const double* __restrict__ X0c,
+                         const double* __restrict__ X0l, int* __restrict__ rung_out) {
+  NYS_PERSIST_SHARED;
+  const int slot = blockIdx.x;
+  const int b = A.idx[slot];
+  const int me = A.me, n_c = A.n_c, nk = A.nk, ldx = A.ldx, nz = me + 1 + nk;
+  const double gt = A.gamma[b], tt = A.tol[b];
+  double* xg = A.X + (size_t)b * ldx;
+  double* wk = A.work + (size_t)slot * A.work_stride;
+  double* nrm = A.norms + (size_t)slot * (A.max_iters + 1);
+  long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int it = 0, status = 1, rung = 0;
+  const int tid = threadIdx.x;
+  for (int r = 1; r <= 4; ++r) {
+    const double* x0 = (r <= 2 ? X0c : X0l) + (size_t)slot * ldx;
+    for (int k = tid; k < ldx; k += blockDim.x) xg[k] = x0[k];
+    __syncthreads();
+    status = persist_solve_once<NB>(A, S, b, gt, tt, (r & 1) == 0, xg, wk, nrm, &it, pc);
+    rung = r;
+    if (status == 0) break;
+  }
+  if (status != 0) {
+    rung = 5;
+    for (int k = tid; k < ldx; k += blockDim.x) xg[k] = X0c[(size_t)slot * ldx + k];
+    __syncthreads();
+    bool escaped = false;
+    const double stages[3] = {1e0, 1e2, 1e4};
+    for (int s = 0; s < 3 && !escaped; ++s) {
+      const double g = stages[s];
+      if (!(g < gt)) continue;
+      status = persist_solve_once<NB>(A, S, b, g, 1e-8 * (1.0 + g), true, xg, wk, nrm, &it, pc);
+      if (status == 2 || status == 3) {
+        escaped = true;
+        break;
+      }
+      // hand-off: omega, b kept; lambda = 0; y = Psi_0 omega + b (linear.py:47-53)
+      for (int k = me + 1 + tid; k < nz; k += blockDim.x) xg[k] = 0.0;
+      const double bias = xg[me];
+      for (int i = tid; i < n_c; i += blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < me; ++k) acc = fma(A.S0T[(size_t)k * n_c + i], xg[k], acc);
+        xg[nz + i] = acc + bias;
+      }
+      __syncthreads();
+    }
+    if (!escaped)
+      status = persist_solve_once<NB>(A, S, b, gt, tt, true, xg, wk, nrm, &it, pc);
+  }
+  if (tid == 0) {
+    A.iters[slot] = it;
+    A.status[slot] = status;
+    rung_out[slot] = rung;
+    if (A.prof != nullptr)
+      for (int i = 0; i < 8; ++i) A.prof[(size_t)slot * 8 + i] = pc[i];
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI
@@ -935,4 +1761,104 @@ extern "C" int nys_newton_step_f64(const double* S0, const double* S1, int m_eff
   nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
+}
+
+// test hook: per-instance phase clocks of the next nys_newton_solve_once_f64
+static long long* g_persist_prof = nullptr;
+extern "C" void nys_newton_persist_profile(long long* dev_buf) { g_persist_prof = dev_buf; }
+
+extern "C" size_t nys_newton_solve_once_work_doubles(int m_eff, int n_c, int n_cond) {
+  const size_t ldx = (size_t)m_eff + 1 + n_cond + n_c;
+  return 4 * ldx + 6 * (size_t)n_c;
+}
+
+template <int NB>
+static int launch_persist(const PersistArgs& A, int nb, const double* X0c, const double* X0l,
+                          int* rung, cudaStream_t st) {
+  constexpr size_t kStride = NB * (NB + 1) / 2 * 64 + NB * 8;
+  const int nz = A.me + 1 + A.nk;
+  const size_t regA = persist_region_a(kStride, A.me, A.n_c, nz);
+  const size_t smem = (regA + (size_t)nz * nz + nz) * sizeof(double) + nz * sizeof(int);
+  if (X0c == nullptr) {
+    auto kern = newton_persist_kernel<NB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+    kern<<<nb, kPersistThreads, smem, st>>>(A);
+  } else {
+    auto kern = newton_ladder_kernel<NB>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return nys_host::record_cuda(e);
+    kern<<<nb, kPersistThreads, smem, st>>>(A, X0c, X0l, rung);
+  }
+  nys_host::count_launches(1);
+  NYS_CHECK_LAUNCH();
+  return NYS_OK;
+}
+
+static int persist_dispatch(const PersistArgs& A, int nb, const double* X0c, const double* X0l,
+                            int* rung, cudaStream_t st) {
+  switch ((A.me + 2 + 7) / 8) {
+    case 1: return launch_persist<1>(A, nb, X0c, X0l, rung, st);
+    case 2: return launch_persist<2>(A, nb, X0c, X0l, rung, st);
+    case 3: return launch_persist<3>(A, nb, X0c, X0l, rung, st);
+    case 4: return launch_persist<4>(A, nb, X0c, X0l, rung, st);
+    case 5: return launch_persist<5>(A, nb, X0c, X0l, rung, st);
+    case 6: return launch_persist<6>(A, nb, X0c, X0l, rung, st);
+    case 7: return launch_persist<7>(A, nb, X0c, X0l, rung, st);
+    case 8: return launch_persist<8>(A, nb, X0c, X0l, rung, st);
+    default: return NYS_EUNSUPPORTED;   // nz <= 64: m_eff <= 62
+  }
+}
+
+static int persist_check(int m_eff, int n_c, int n_cond, int nb, int max_iters, int halvings,
+                         int ldx, const double* g, const double* alpha, const double* beta,
+                         const double* work, size_t work_bytes) {
+  if (m_eff < 1 || n_c < 1 || n_cond < 0 || n_cond > kMaxCondN || nb < 0 || max_iters < 0 ||
+      halvings < 0 || ldx < m_eff + 1 + n_cond + n_c || m_eff + 1 + n_cond > kPLuMaxN)
+    return NYS_EINVAL;
+  if (g == nullptr || alpha == nullptr || beta == nullptr) return NYS_EINVAL;   // family mode
+  if ((size_t)kResSplit * (2 * m_eff + 3) > 2 * (size_t)n_c) return NYS_EUNSUPPORTED;
+  const size_t wd = nys_newton_solve_once_work_doubles(m_eff, n_c, n_cond);
+  if (nb > 0 && (work == nullptr || work_bytes < (size_t)nb * wd * sizeof(double)))
+    return NYS_EWORKSPACE;
+  return NYS_OK;
+}
+
+extern "C" int nys_newton_solve_once_f64(
+    const double* S0, const double* S1, const double* S0T, const double* S1T,
+    const double* packed, int m_eff, int n_c, const double* g, const double* alpha,
+    const double* beta, const double* Ac, const double* betac, const double* vals, int n_cond,
+    const double* gamma, const double* tol, double* X, int ldx, const int* idx, int nb,
+    int damped, double shrink, int halvings, int max_iters, double* work, size_t work_bytes,
+    double* norms, int* iters, int* status, void* stream) {
+  const int rc = persist_check(m_eff, n_c, n_cond, nb, max_iters, halvings, ldx, g, alpha, beta,
+                               work, work_bytes);
+  if (rc != NYS_OK || nb == 0) return rc;
+  PersistArgs A{S0, S1, S0T, S1T, packed, m_eff, n_c, n_cond, (n_c + 3) / 4, ldx,
+                Rhs{g, nullptr, nullptr, alpha, beta, n_c}, Ac, betac, vals, gamma, tol, X, idx,
+                damped, halvings, max_iters, shrink, work,
+                nys_newton_solve_once_work_doubles(m_eff, n_c, n_cond), norms, iters, status,
+                g_persist_prof};
+  return persist_dispatch(A, nb, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int nys_newton_ladder_f64(
+    const double* S0, const double* S1, const double* S0T, const double* S1T,
+    const double* packed, int m_eff, int n_c, const double* g, const double* alpha,
+    const double* beta, const double* Ac, const double* betac, const double* vals, int n_cond,
+    const double* gamma, const double* tol, const double* X0c, const double* X0l, double* X,
+    int ldx, const int* idx, int nb, double shrink, int halvings, int max_iters, double* work,
+    size_t work_bytes, double* norms, int* iters, int* status, int* rung, void* stream) {
+  const int rc = persist_check(m_eff, n_c, n_cond, nb, max_iters, halvings, ldx, g, alpha, beta,
+                               work, work_bytes);
+  if (rc != NYS_OK || nb == 0) return rc;
+  if (X0c == nullptr || X0l == nullptr || rung == nullptr) return NYS_EINVAL;
+  PersistArgs A{S0, S1, S0T, S1T, packed, m_eff, n_c, n_cond, (n_c + 3) / 4, ldx,
+                Rhs{g, nullptr, nullptr, alpha, beta, n_c}, Ac, betac, vals, gamma, tol, X, idx,
+                1, halvings, max_iters, shrink, work,
+                nys_newton_solve_once_work_doubles(m_eff, n_c, n_cond), norms, iters, status,
+                g_persist_prof};
+  return persist_dispatch(A, nb, X0c, X0l, rung, static_cast<cudaStream_t>(stream));
 }

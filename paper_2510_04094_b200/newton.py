@@ -483,10 +483,63 @@ class NewtonBatch:
         return out, info
 
     # -------------------------------------------------------------- solve_once
+    def persistent(self) -> bool:
+        """The device-resident loop (nys_newton_solve_once_f64) serves the
+        separable family at p = 1; NYS_NEWTON_PERSIST=0 selects the
+        host-orchestrated multi-kernel loop (same arithmetic)."""
+        import os
+
+        return (self.family is not None and self.p == 1
+                and os.environ.get("NYS_NEWTON_PERSIST", "1") != "0")
+
+    def _solve_once_device(self, ids, x0, gamma, tol, damping, max_iters, shrink, halvings):
+        """newton._solve_once for every instance in ids at once, entirely on
+        the device: one CTA per instance loops until converged / max iterations
+        / diverged / singular.  One read-back (status, iterations, trace)."""
+        torch = self.torch
+        nid = len(ids)
+        idx_all = self._idx(ids)
+        self.X[idx_all] = _lib.as_f64(x0, self.dev)
+        self.gam[idx_all] = _lib.as_f64(np.broadcast_to(np.asarray(gamma, dtype=float), (nid,)),
+                                        self.dev)
+        tolv = self.__dict__.get("_tolv")
+        if tolv is None:
+            tolv = self._tolv = torch.zeros(self.B, dtype=torch.float64, device=self.dev)
+        tolv[idx_all] = _lib.as_f64(np.broadcast_to(np.asarray(tol, dtype=float), (nid,)),
+                                    self.dev)
+        wd = int(self.lib.nys_newton_solve_once_work_doubles(self.me, self.n_c, self.nk))
+        work = self.__dict__.get("_pwork")
+        if work is None or work.numel() < nid * wd:
+            work = self._pwork = torch.empty(self.B * wd, dtype=torch.float64, device=self.dev)
+        outs = self.__dict__.get("_pouts")
+        if outs is None or outs[0].shape[1] < max_iters + 1:
+            outs = self._pouts = (torch.empty((self.B, max_iters + 1), dtype=torch.float64,
+                                              device=self.dev),
+                                  torch.empty(2 * self.B, dtype=torch.int32, device=self.dev))
+        norms, ist = outs[0][:nid, :max_iters + 1].contiguous(), outs[1]
+        _lib.call("nys_newton_solve_once_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
+                  _lib.ptr(self.S0T), _lib.ptr(self.S1T), _lib.ptr(self.packed), self.me,
+                  self.n_c, _lib.ptr(self.g), _lib.ptr(self.fal), _lib.ptr(self.fbe),
+                  _lib.ptr(self.Ac), _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk,
+                  _lib.ptr(self.gam), _lib.ptr(tolv), _lib.ptr(self.X), self.ldx,
+                  _lib.ptr(idx_all), nid, 1 if damping else 0, float(shrink), int(halvings),
+                  int(max_iters), _lib.ptr(work), work.numel() * 8, _lib.ptr(norms),
+                  _lib.ptr(ist), _lib.ptr(ist[self.B:]), _lib.stream_ptr())
+        self.launches += 1
+        nr = norms.cpu().numpy()
+        st_its = ist.cpu().numpy()
+        its, status = st_its[:nid], st_its[self.B:self.B + nid].astype(int)
+        traces = [[float(v) for v in nr[r, :its[r] + 1]] for r in range(nid)]
+        Xn = self.X[idx_all].cpu().numpy()
+        return status, Xn, traces
+
     def solve_once(self, ids, x0, gamma, tol, damping, max_iters, shrink=0.5, halvings=30):
         """Batched newton._solve_once (newton.py:279-349).
 
         Returns (status[len(ids)], X rows (np), traces)."""
+        if self.persistent():
+            return self._solve_once_device(list(ids), x0, gamma, tol, damping, max_iters,
+                                           shrink, halvings)
         torch = self.torch
         ids = list(ids)
         nid = len(ids)
@@ -581,12 +634,53 @@ class NewtonBatch:
         return status, Xn, traces
 
     # -------------------------------------------------------------- ladder
+    def _solve_ladder_device(self, max_iters, tol_t):
+        """The whole ladder in one launch (nys_newton_ladder_f64): both starts
+        are formed up front for every instance (the linearised one by one
+        batched linear solve), then each instance climbs the rungs on its own
+        CTA without waiting for the others."""
+        torch = self.torch
+        B = self.B
+        ids = list(range(B))
+        x0c = _lib.as_f64(self.const_state(ids), self.dev)
+        xl, _ = self.linearized_state(ids)
+        x0l = _lib.as_f64(xl, self.dev)
+        idx_all = self._idx(ids)
+        self.gam.fill_(self.gamma_target)
+        tolv = self.__dict__.get("_tolv")
+        if tolv is None:
+            tolv = self._tolv = torch.zeros(B, dtype=torch.float64, device=self.dev)
+        tolv.fill_(float(tol_t))
+        wd = int(self.lib.nys_newton_solve_once_work_doubles(self.me, self.n_c, self.nk))
+        work = self.__dict__.get("_pwork")
+        if work is None or work.numel() < B * wd:
+            work = self._pwork = torch.empty(B * wd, dtype=torch.float64, device=self.dev)
+        norms = torch.empty((B, max_iters + 1), dtype=torch.float64, device=self.dev)
+        ist = torch.empty(3 * B, dtype=torch.int32, device=self.dev)
+        _lib.call("nys_newton_ladder_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
+                  _lib.ptr(self.S0T), _lib.ptr(self.S1T), _lib.ptr(self.packed), self.me,
+                  self.n_c, _lib.ptr(self.g), _lib.ptr(self.fal), _lib.ptr(self.fbe),
+                  _lib.ptr(self.Ac), _lib.ptr(self.betac), _lib.ptr(self.vals), self.nk,
+                  _lib.ptr(self.gam), _lib.ptr(tolv), _lib.ptr(x0c), _lib.ptr(x0l),
+                  _lib.ptr(self.X), self.ldx, _lib.ptr(idx_all), B, 0.5, 30, int(max_iters),
+                  _lib.ptr(work), work.numel() * 8, _lib.ptr(norms), _lib.ptr(ist),
+                  _lib.ptr(ist[B:]), _lib.ptr(ist[2 * B:]), _lib.stream_ptr())
+        self.launches += 1
+        nr = norms.cpu().numpy()
+        v = ist.cpu().numpy()
+        its, status, rung = v[:B], v[B:2 * B].astype(int), v[2 * B:].astype(int)
+        traces = [[float(x) for x in nr[r, :its[r] + 1]] for r in range(B)]
+        return status, self.X.cpu().numpy(), traces, rung
+
     def solve(self, max_iters: int = 100, tol: Optional[float] = None):
         """Retry ladder (newton.py:376-412) for all B instances.
 
         Returns (status[B], X[B, ldx] np, traces list, rung[B]); status is the
         outcome of the rung that finished the instance (OK) or of the last rung."""
         gam = self.gamma_target
+        if self.persistent():
+            return self._solve_ladder_device(max_iters,
+                                             1e-10 * (1.0 + gam) if tol is None else tol)
         tol_t = 1e-10 * (1.0 + gam) if tol is None else tol
         B = self.B
         status = np.full(B, -1)

@@ -4,8 +4,10 @@ solution vector x and its error vs the manufactured solution -- plus the
 reference's landmark eigenpairs (x is expressed in that basis).  A second pass
 re-runs the reference with only its landmark eigensolver driver swapped
 (scipy's dsyev for numpy's dsyevd) and stores that outcome as status_dsyev /
-iterations_dsyev: the reference's own outcome sensitivity, the yardstick of
-the GPU census test.
+iterations_dsyev, and three more passes with the landmark matrix perturbed by
+at most one ulp per entry (seeded) store status_perturbed: the reference's own
+outcome sensitivity to rounding-level noise, the yardstick of the GPU census
+test.
 
 Build container only (``/root/reference`` is absent on the GPU box):
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_c3_census.py
@@ -41,6 +43,25 @@ def _solve_dsyev(i):
     return _solve(i)
 
 
+def _solve_perturbed(args):
+    """The reference on its landmark matrix with every entry moved by at most
+    one ulp (symmetric, seeded): rounding-level input noise."""
+    i, seed = args
+    orig = np.linalg.eigh
+
+    def eigh(A):
+        rng = np.random.default_rng(seed)
+        U = np.triu(rng.integers(-1, 2, size=A.shape).astype(float))
+        U = U + np.triu(U, 1).T
+        return orig(A * (1.0 + np.finfo(float).eps * U))
+
+    np.linalg.eigh = eigh
+    try:
+        return _solve(i)
+    finally:
+        np.linalg.eigh = orig
+
+
 def _solve(i):
     from nysode import newton, nystrom
     from nysode.kernel import RbfKernel
@@ -71,6 +92,9 @@ def _solve(i):
     return i, status, tr.iterations, x, float(np.linalg.norm(y - ys) / np.linalg.norm(ys))
 
 
+PERTURB_SEEDS = (1, 2, 3)
+
+
 def main():
     t0 = time.time()
     n = 256
@@ -78,6 +102,10 @@ def main():
         res = sorted(ex.map(_solve, range(n)))
     with ProcessPoolExecutor(max_workers=os.cpu_count(), initializer=_init) as ex:
         res_ev = sorted(ex.map(_solve_dsyev, range(n)))
+    res_pert = []
+    for seed in PERTURB_SEEDS:
+        with ProcessPoolExecutor(max_workers=os.cpu_count(), initializer=_init) as ex:
+            res_pert.append(sorted(ex.map(_solve_perturbed, [(i, seed) for i in range(n)])))
     me = next(r[3].size for r in res if r[3] is not None)
     X = np.full((n, me), np.nan)
     for i, st, its, x, err in res:
@@ -97,7 +125,9 @@ def main():
                         iterations=np.array([r[2] for r in res], np.int32),
                         x=X, err_vs_exact=np.array([r[4] for r in res]),
                         status_dsyev=np.array([r[1] for r in res_ev], np.int32),
-                        iterations_dsyev=np.array([r[2] for r in res_ev], np.int32))
+                        iterations_dsyev=np.array([r[2] for r in res_ev], np.int32),
+                        status_perturbed=np.array([[r[1] for r in rp] for rp in res_pert],
+                                                  np.int32))
     st = np.bincount([r[1] for r in res], minlength=4)
     st_ev = np.bincount([r[1] for r in res_ev], minlength=4)
     print(f"c3 census: status counts {st.tolist()} (dsyev driver {st_ev.tolist()}) "

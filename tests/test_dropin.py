@@ -93,12 +93,11 @@ def test_unmodified_harness_under_patch():
 
     * y_hat within 1e-6 relative L2 of the unpatched reference (north star);
     * the reference's acceptance gate holds on the device result;
-    * error vs the exact solution within 1 % of the reference's -- except in
-      the rounding regime (reference MAE < 1e-8: P12 5e-9, P3 7e-10), where
-      the error is set by eigenpairs at the drop_tol = 1e-16 noise floor: the
-      reference's own MAE moves 2-3x and its m_eff by 5-10 under a 16-ulp
-      perturbation of the landmark matrix, so there the
-      acceptance gate is the bar;
+    * error vs the exact solution within 1 % of the reference's, or within 3x
+      the reference's own move when its landmark matrix is perturbed by 16 ulps
+      of its largest entry (the catalog spectra run into the drop_tol = 1e-16
+      noise floor: P16's MAE moves 60 %, m_eff by 2-10), or 1e-8 absolute in
+      the rounding regime (P12 MAE 5e-9, P3 7e-10; DESIGN.md §7);
     * Newton: same converged flag and trace length; the MaxIters outcome is
       caught by harness.py:173 instead of crashing.
     """
@@ -114,8 +113,11 @@ def test_unmodified_harness_under_patch():
         assert c["yhat_rel_l2"] <= 1e-6, (name, c)
         if c["acceptance_gate"] is not None:
             assert c["dev_mae"] <= c["acceptance_gate"], (name, c)
-        if c["ref_mae"] >= 1e-8:
-            assert abs(c["dev_mae"] - c["ref_mae"]) <= 0.01 * c["ref_mae"], (name, c)
+        # 1 % of the reference's error, widened to 3x the reference's own move
+        # under a 16-ulp perturbation of its landmark matrix (P16: 60 %) and to
+        # 1e-8 absolute in the rounding regime (P3, P12)
+        tol = max(0.01 * c["ref_mae"], 3 * abs(c["perturbed16_mae"] - c["ref_mae"]), 1e-8)
+        assert abs(c["dev_mae"] - c["ref_mae"]) <= tol, (name, c)
         assert c["dev_converged"] == c["ref_converged"], (name, c)
         assert c["dev_trace_len"] == c["ref_trace_len"], (name, c)
     assert out["P4"]["dev_converged"] is True and out["P15"]["dev_converged"] is True

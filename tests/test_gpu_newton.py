@@ -172,13 +172,14 @@ def test_config3_census_matches_reference():
     assert not bad, bad
     # Outcome flips sit on knife-edge trajectories.  Yardstick: the reference
     # against itself with only LAPACK's eigensolver driver swapped (dsyev for
-    # dsyevd, status_dsyev in the fixture) loses 6 of its converged instances
-    # and gains 9; allow three times that self-sensitivity.
+    # dsyevd; status_dsyev, written by make_c3_census.py) loses 6 of its
+    # converged instances and agrees on 240 of 256 outcomes.  The device must
+    # do at least as well as that.
     self_lost = int(((ref["status"] == 0) & (ref["status_dsyev"] != 0)).sum())
     self_agree = int((ref["status"] == ref["status_dsyev"]).sum())
     print("reference self-sensitivity: agreement", self_agree, "lost", self_lost)
-    assert len(lost) <= 3 * self_lost, lost
-    assert B - agree <= 3 * (B - self_agree), (agree, self_agree)
+    assert len(lost) <= self_lost, lost
+    assert agree >= self_agree, (agree, self_agree)
 
 
 # ---------------------------------------------------------------- p = 2
