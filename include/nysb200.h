@@ -258,6 +258,10 @@ int nys_newton_step_f64(const double* S0, const double* S1, int m_eff, int n_c, 
  * (the trace); status[j] 0 converged / 1 max iterations / 2 diverged /
  * 3 singular.  work: nb * nys_newton_solve_once_work_doubles doubles. */
 size_t nys_newton_solve_once_work_doubles(int m_eff, int n_c, int n_cond);
+/* diagnostics: when dev_buf != NULL, later persistent Newton launches write
+ * per-instance phase clocks there ([nb][8]: residual + line search, reduced
+ * system, LU, step, -, trials); NULL turns it off */
+void nys_newton_persist_profile(long long* dev_buf);
 int nys_newton_solve_once_f64(const double* S0, const double* S1, const double* S0T,
                               const double* S1T, const double* packed, int m_eff, int n_c,
                               const double* g, const double* alpha, const double* beta,
