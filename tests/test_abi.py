@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_symbols():
     txt = open(os.path.join(ROOT, "include", "nysb200.h")).read()
-    return sorted(set(re.findall(r"^(?:int|size_t|unsigned long long|const char\*)\s+(nys_[a-z0-9_]+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|size_t|unsigned long long|const char\*)\s+(nys_[a-z0-9_]+)\(", txt, re.M)))
 
 
 def test_library_loads_and_exports_header_symbols():
