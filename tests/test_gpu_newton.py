@@ -171,13 +171,17 @@ def test_config3_census_matches_reference():
           len(both), "| y_hat mismatches", bad)
     assert not bad, bad
     # Outcome flips sit on knife-edge trajectories.  Yardstick: the reference
-    # against itself with only LAPACK's eigensolver driver swapped (dsyev for
-    # dsyevd; status_dsyev, written by make_c3_census.py) loses 6 of its
-    # converged instances and agrees on 240 of 256 outcomes.  The device must
-    # do at least as well as that.
+    # against itself (make_c3_census.py) -- with only LAPACK's eigensolver
+    # driver swapped (status_dsyev) it loses 6 of its converged instances and
+    # agrees on 240 of 256 outcomes; with its landmark matrix moved by at most
+    # one ulp per entry (status_perturbed, 3 seeds) it agrees on 237-243 and
+    # loses 4-9.  The device must do at least as well as the driver swap.
     self_lost = int(((ref["status"] == 0) & (ref["status_dsyev"] != 0)).sum())
     self_agree = int((ref["status"] == ref["status_dsyev"]).sum())
-    print("reference self-sensitivity: agreement", self_agree, "lost", self_lost)
+    pert = [(int((ref["status"] == p).sum()), int(((ref["status"] == 0) & (p != 0)).sum()))
+            for p in ref["status_perturbed"]]
+    print("reference self-sensitivity: dsyev agreement", self_agree, "lost", self_lost,
+          "| 1-ulp perturbations (agreement, lost)", pert)
     assert len(lost) <= self_lost, lost
     assert agree >= self_agree, (agree, self_agree)
 
