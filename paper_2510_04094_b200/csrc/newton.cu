@@ -775,11 +775,15 @@ constexpr int kPTrials = 4;   // line-search trials evaluated together
 // sum of e2 goes through block_reduce's tree), so part[] is bit-identical to
 // four residual_range calls -- with 4x the loads in flight and a quarter of
 // the barriers.  sh: me + 2 n_c doubles; red: kResSplit * (blockDim / 32).
-NYS_DEV void residual_splits_fused(const double* __restrict__ S0T, const double* __restrict__ S1T,
+// bound: when the rows alone already give max|F_y| > bound (or a non-finite
+// rhs), the S^T e pass is skipped and true returned -- a line-search trial
+// rejected exactly as the full norm would reject it.
+NYS_DEV bool residual_splits_fused(const double* __restrict__ S0T, const double* __restrict__ S1T,
                                    int me, int n_c, const Rhs& rhs, double gm,
                                    const double* __restrict__ x, int b, int nk,
                                    double* __restrict__ Fb, double* __restrict__ auxb,
-                                   double* __restrict__ part, double* sh, double* red) {
+                                   double* __restrict__ part, double* sh, double* red,
+                                   double bound, double* early) {
   const int rpc = res_rows_per_split(n_c);
   const int pstride = 2 * me + 3;
   double* om = sh;
@@ -845,6 +849,14 @@ NYS_DEV void residual_splits_fused(const double* __restrict__ S0T, const double*
     red[kResSplit * nw + warp] = fmax_local;
   }
   const int any_bad = __syncthreads_or(bad);
+  {
+    double m = 0.0;
+    for (int w = 0; w < nw; ++w) m = fmax(m, red[kResSplit * nw + w]);
+    if (any_bad || m > bound) {   // uniform across the CTA
+      *early = any_bad ? NAN : m;
+      return true;
+    }
+  }
   // partial S1^T e1 and S0^T e2 per (range, k): one warp each, lanes over the range's rows
   for (int t = warp; t < kResSplit * me; t += nw) {
     const int sp = t / me, k = t % me;
@@ -876,6 +888,7 @@ NYS_DEV void residual_splits_fused(const double* __restrict__ S0T, const double*
     part[tid * pstride + 2 * me + 2] = any_bad ? 1.0 : 0.0;
   }
   __syncthreads();
+  return false;
 }
 
 NYS_DEV double bias_of(double al, const double* D, const double* X, int me) {
@@ -895,7 +908,7 @@ NYS_DEV void trial_norms_multi(const double* __restrict__ S0T, const double* __r
                                const double* __restrict__ X, const double* __restrict__ D,
                                const double* al, int b, int nk, const double* __restrict__ Ac,
                                const double* __restrict__ betac, const double* __restrict__ vals,
-                               double* part, double* sh, double* red, double* out) {
+                               double* part, double* sh, double* red, double* out, double ref) {
   const int rpc = res_rows_per_split(n_c);
   const int pstride = 2 * me + 3;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
@@ -994,6 +1007,28 @@ NYS_DEV void trial_norms_multi(const double* __restrict__ S0T, const double* __r
   if (tid == 0) badm_s = 0;
   __syncthreads();
   if (badm) atomicOr(&badm_s, badm);
+  __syncthreads();
+  {
+    // every trial already rejected by its rows (non-finite rhs or max|F_y| >
+    // ref): the S^T e pass cannot change that -- report the lower bounds
+    bool all_rej = true;
+    for (int t = 0; t < KT; ++t) {
+      const double* rt = red + t * (kResSplit + 1) * nw;
+      double m = 0.0;
+      for (int w = 0; w < nw; ++w) m = fmax(m, rt[kResSplit * nw + w]);
+      if (!((badm_s >> t) & 1) && !(m > ref)) all_rej = false;
+    }
+    if (all_rej) {
+      if (tid < KT) {
+        const double* rt = red + tid * (kResSplit + 1) * nw;
+        double m = 0.0;
+        for (int w = 0; w < nw; ++w) m = fmax(m, rt[kResSplit * nw + w]);
+        out[tid] = ((badm_s >> tid) & 1) ? NAN : m;
+      }
+      __syncthreads();
+      return;
+    }
+  }
   // range partials of S1^T e1 and S0^T e2 for every trial
   for (int task = warp; task < kResSplit * me; task += nw) {
     const int sp = task / me, k = task % me;
@@ -1084,9 +1119,12 @@ NYS_DEV double persist_residual(const double* __restrict__ S0T, const double* __
                                 const double* __restrict__ Ac, const double* __restrict__ betac,
                                 const double* __restrict__ vals, double* __restrict__ Fb,
                                 double* __restrict__ auxb, double* part, double* sh, double* red,
-                                double* lam_s) {
+                                double* lam_s, double bound = INFINITY) {
   const int pstride = 2 * me + 3;
-  residual_splits_fused(S0T, S1T, me, n_c, rhs, gm, x, b, nk, Fb, auxb, part, sh, red);
+  double early;
+  if (residual_splits_fused(S0T, S1T, me, n_c, rhs, gm, x, b, nk, Fb, auxb, part, sh, red, bound,
+                            &early))
+    return early;   // > bound or NaN: F / aux incomplete, the caller rejects the point
   const int tid = threadIdx.x;
   if (tid < nk) lam_s[tid] = x[me + 1 + tid];
   __syncthreads();
@@ -1358,7 +1396,7 @@ NYS_DEV int persist_solve_once(const PersistArgs& A, const PersistSmem& S, int b
       for (int k = tid; k < nz + n_c; k += blockDim.x) Xnew[k] = fma(alpha, Dv[k], Xcur[k]);
       __syncthreads();
       tn = persist_residual(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xnew, b, nk, A.Ac, A.betac, A.vals,
-                            Fnew, auxn, S.part, S.sh, S.red, S.lam_s);
+                            Fnew, auxn, S.part, S.sh, S.red, S.lam_s, damped ? norm : INFINITY);
       pc[5] += 1;
       have = !damped || (isfinite(tn) && tn <= norm);
     }
@@ -1378,7 +1416,8 @@ NYS_DEV int persist_solve_once(const PersistArgs& A, const PersistSmem& S, int b
         __syncthreads();
         trial_norms_multi<kPTrials>(A.S0T, A.S1T, me, n_c, A.rhs, gm, Xcur, Dv, S.al_s, b, nk,
                                     A.Ac, A.betac, A.vals, redA,
-                                    redA + kPTrials * kResSplit * (2 * me + 3), S.red_m, S.tn_s);
+                                    redA + kPTrials * kResSplit * (2 * me + 3), S.red_m, S.tn_s,
+                                    norm);
         pc[5] += cnt;
         for (int t = 0; t < cnt && !found; ++t) {
           if (isfinite(S.tn_s[t]) && S.tn_s[t] <= norm) {
