@@ -279,8 +279,9 @@ int nys_newton_solve_once_f64(const double* S0, const double* S1, const double* 
  * tolerated, divergence / singularity ends the instance), each handing
  * (omega, b, lambda = 0, y = Psi_0 omega + b) on, then gamma[idx] itself.
  * X0c / X0l [nb][ldx] (indexed by slot j): the constant and linearised
- * starts; X[idx[j]] the final iterate; rung[j] 1..5 the rung that produced
- * status[j] / norms[j][0..iters[j]] (the trace of that last _solve_once). */
+ * starts; X[idx[j]] the final iterate; rung[2 nb]: rung[j] 1..5 the rung that
+ * produced status[j] / norms[j][0..iters[j]] (the trace of that last
+ * _solve_once), rung[nb + j] the Newton iterations over every rung and stage. */
 int nys_newton_ladder_f64(const double* S0, const double* S1, const double* S0T,
                           const double* S1T, const double* packed, int m_eff, int n_c,
                           const double* g, const double* alpha, const double* beta,

@@ -1288,6 +1288,7 @@ struct PersistArgs {
   int* iters;          // [nb]
   int* status;         // [nb]
   long long* prof;     // optional [nb][8]: clocks in residual / reduce / LU / step, trials
+  int* tot_iters;      // optional [nb]: Newton iterations over every rung / stage (ladder)
 };
 
 // shared-memory carve-up of the persistent kernels
@@ -1527,13 +1528,14 @@ __global__ void __launch_bounds__(kPersistThreads, NYS_PERSIST_MINB)
   double* wk = A.work + (size_t)slot * A.work_stride;
   double* nrm = A.norms + (size_t)slot * (A.max_iters + 1);
   long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  int it = 0, status = 1, rung = 0;
+  int it = 0, status = 1, rung = 0, tot = 0;
   const int tid = threadIdx.x;
   for (int r = 1; r <= 4; ++r) {
     const double* x0 = (r <= 2 ? X0c : X0l) + (size_t)slot * ldx;
     for (int k = tid; k < ldx; k += blockDim.x) xg[k] = x0[k];
     __syncthreads();
     status = persist_solve_once<NB>(A, S, b, gt, tt, (r & 1) == 0, xg, wk, nrm, &it, pc);
+    tot += it;
     rung = r;
     if (status == 0) break;
   }
@@ -1547,6 +1549,7 @@ __global__ void __launch_bounds__(kPersistThreads, NYS_PERSIST_MINB)
       const double g = stages[s];
       if (!(g < gt)) continue;
       status = persist_solve_once<NB>(A, S, b, g, 1e-8 * (1.0 + g), true, xg, wk, nrm, &it, pc);
+      tot += it;
       if (status == 2 || status == 3) {
         escaped = true;
         break;
@@ -1561,13 +1564,16 @@ __global__ void __launch_bounds__(kPersistThreads, NYS_PERSIST_MINB)
       }
       __syncthreads();
     }
-    if (!escaped)
+    if (!escaped) {
       status = persist_solve_once<NB>(A, S, b, gt, tt, true, xg, wk, nrm, &it, pc);
+      tot += it;
+    }
   }
   if (tid == 0) {
     A.iters[slot] = it;
     A.status[slot] = status;
     rung_out[slot] = rung;
+    if (A.tot_iters != nullptr) A.tot_iters[slot] = tot;
     if (A.prof != nullptr)
       for (int i = 0; i < 8; ++i) A.prof[(size_t)slot * 8 + i] = pc[i];
   }
@@ -1879,7 +1885,7 @@ extern "C" int nys_newton_solve_once_f64(
                 Rhs{g, nullptr, nullptr, alpha, beta, n_c}, Ac, betac, vals, gamma, tol, X, idx,
                 damped, halvings, max_iters, shrink, work,
                 nys_newton_solve_once_work_doubles(m_eff, n_c, n_cond), norms, iters, status,
-                g_persist_prof};
+                g_persist_prof, nullptr};
   return persist_dispatch(A, nb, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
@@ -1898,6 +1904,6 @@ extern "C" int nys_newton_ladder_f64(
                 Rhs{g, nullptr, nullptr, alpha, beta, n_c}, Ac, betac, vals, gamma, tol, X, idx,
                 1, halvings, max_iters, shrink, work,
                 nys_newton_solve_once_work_doubles(m_eff, n_c, n_cond), norms, iters, status,
-                g_persist_prof};
+                g_persist_prof, rung + nb};
   return persist_dispatch(A, nb, X0c, X0l, rung, static_cast<cudaStream_t>(stream));
 }

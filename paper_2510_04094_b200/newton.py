@@ -634,18 +634,21 @@ class NewtonBatch:
         return status, Xn, traces
 
     # -------------------------------------------------------------- ladder
-    def _solve_ladder_device(self, max_iters, tol_t):
-        """The whole ladder in one launch (nys_newton_ladder_f64): both starts
-        are formed up front for every instance (the linearised one by one
-        batched linear solve), then each instance climbs the rungs on its own
-        CTA without waiting for the others."""
-        torch = self.torch
-        B = self.B
-        ids = list(range(B))
+    def ladder_starts(self):
+        """Constant and linearised starts of every instance on the device (the
+        latter by one batched linear solve)."""
+        ids = list(range(self.B))
         x0c = _lib.as_f64(self.const_state(ids), self.dev)
         xl, _ = self.linearized_state(ids)
-        x0l = _lib.as_f64(xl, self.dev)
-        idx_all = self._idx(ids)
+        return x0c, _lib.as_f64(xl, self.dev)
+
+    def ladder_launch(self, x0c, x0l, max_iters, tol_t):
+        """One nys_newton_ladder_f64 launch over all B instances; device
+        outputs (norms[B, max_iters + 1], ints[4 B]: iterations, status, rung,
+        iterations over all rungs), X updated in place.  No host sync."""
+        torch = self.torch
+        B = self.B
+        idx_all = self._idx(list(range(B)))
         self.gam.fill_(self.gamma_target)
         tolv = self.__dict__.get("_tolv")
         if tolv is None:
@@ -655,8 +658,12 @@ class NewtonBatch:
         work = self.__dict__.get("_pwork")
         if work is None or work.numel() < B * wd:
             work = self._pwork = torch.empty(B * wd, dtype=torch.float64, device=self.dev)
-        norms = torch.empty((B, max_iters + 1), dtype=torch.float64, device=self.dev)
-        ist = torch.empty(3 * B, dtype=torch.int32, device=self.dev)
+        outs = self.__dict__.get("_louts")
+        if outs is None or outs[0].shape[1] != max_iters + 1:
+            outs = self._louts = (torch.empty((B, max_iters + 1), dtype=torch.float64,
+                                              device=self.dev),
+                                  torch.empty(4 * B, dtype=torch.int32, device=self.dev))
+        norms, ist = outs
         _lib.call("nys_newton_ladder_f64", _lib.ptr(self.S0), _lib.ptr(self.S1),
                   _lib.ptr(self.S0T), _lib.ptr(self.S1T), _lib.ptr(self.packed), self.me,
                   self.n_c, _lib.ptr(self.g), _lib.ptr(self.fal), _lib.ptr(self.fbe),
@@ -666,9 +673,18 @@ class NewtonBatch:
                   _lib.ptr(work), work.numel() * 8, _lib.ptr(norms), _lib.ptr(ist),
                   _lib.ptr(ist[B:]), _lib.ptr(ist[2 * B:]), _lib.stream_ptr())
         self.launches += 1
+        return norms, ist
+
+    def _solve_ladder_device(self, max_iters, tol_t):
+        """The whole ladder in one launch (nys_newton_ladder_f64): both starts
+        are formed up front for every instance, then each instance climbs the
+        rungs on its own CTA without waiting for the others."""
+        B = self.B
+        norms, ist = self.ladder_launch(*self.ladder_starts(), max_iters, tol_t)
         nr = norms.cpu().numpy()
         v = ist.cpu().numpy()
-        its, status, rung = v[:B], v[B:2 * B].astype(int), v[2 * B:].astype(int)
+        its, status, rung = v[:B], v[B:2 * B].astype(int), v[2 * B:3 * B].astype(int)
+        self.total_iterations = v[3 * B:4 * B].astype(int)
         traces = [[float(x) for x in nr[r, :its[r] + 1]] for r in range(B)]
         return status, self.X.cpu().numpy(), traces, rung
 
