@@ -635,12 +635,42 @@ class NewtonBatch:
 
     # -------------------------------------------------------------- ladder
     def ladder_starts(self):
-        """Constant and linearised starts of every instance on the device (the
-        latter by one batched linear solve)."""
+        """Constant and linearised starts of every instance, formed on the
+        device without a host round trip (the latter by one batched linear
+        solve and the model hand-off y = Psi_0 omega + b; the same roundings
+        as const_state / linearized_state)."""
+        torch = self.torch
         ids = list(range(self.B))
-        x0c = _lib.as_f64(self.const_state(ids), self.dev)
-        xl, _ = self.linearized_state(ids)
-        return x0c, _lib.as_f64(xl, self.dev)
+        if self.family is None:
+            x0c = _lib.as_f64(self.const_state(ids), self.dev)
+            xl, _ = self.linearized_state(ids)
+            return x0c, _lib.as_f64(xl, self.dev)
+        from .batch import LinearBatchSolver
+
+        B, me, nz = self.B, self.me, self.nz
+        j0 = [j for j, bc in enumerate(self.cond.entries) if bc.order == 0]
+        b0 = (self.values[:, j0[0]] if self.cond.kind == "ivp"
+              else self.values[:, j0].mean(axis=1))
+        fam = self.family
+        a, be = fam.alpha, fam.beta
+        c = a * b0 * b0 + be * np.sin(b0)
+        fy = 2.0 * a * b0 + be * np.cos(b0)
+        sc = torch.as_tensor(np.stack([b0, c, fy, fy * b0]), device=self.dev)
+        x0c = torch.zeros((B, self.ldx), dtype=torch.float64, device=self.dev)
+        x0c[:, me] = sc[0]
+        x0c[:, nz:] = sc[0][:, None]
+        coef = sc[2][:, None, None].expand(B, 1, self.n_c).contiguous()
+        forcing = (self.g + sc[1][:, None]) - sc[3][:, None]
+        solver = self.__dict__.get("_lin_solver")
+        if solver is None:
+            solver = LinearBatchSolver(self.fmap, self.grid, self.gamma_target, self.p, self.cond,
+                                       self.B)
+            self._lin_solver = solver
+        xl, _ = solver.solve_device(coef, forcing, self.vals)
+        x0l = torch.zeros((B, self.ldx), dtype=torch.float64, device=self.dev)
+        x0l[:, :me + 1] = xl[:, :me + 1]
+        x0l[:, nz:] = predict_batch(self.fmap, xl[:, :me + 1].contiguous(), 0, self.pts)
+        return x0c, x0l
 
     def ladder_launch(self, x0c, x0l, max_iters, tol_t):
         """One nys_newton_ladder_f64 launch over all B instances; device
