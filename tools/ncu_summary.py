@@ -9,8 +9,11 @@ import sys
 
 rep, kre, label = sys.argv[1], sys.argv[2], sys.argv[3]
 algo = float(sys.argv[4]) if len(sys.argv) > 4 else None
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+if rep.endswith(".csv"):   # a `ncu -i REPORT --page raw --csv` export
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
 pick = None
