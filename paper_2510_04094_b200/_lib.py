@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnysb200.so")
+LIB_PATH = os.environ.get("NYS_LIB_PATH") or os.path.join(HERE, "libnysb200.so")   # override: A/B builds (tools/)
 
 NYS_OK, NYS_EINVAL, NYS_ECUDA, NYS_EWORKSPACE, NYS_EUNSUPPORTED = range(5)
 INFO_OK, INFO_SINGULAR, INFO_NONFINITE, INFO_DIVERGED, INFO_MAXITERS, INFO_DEGENERATE = range(6)

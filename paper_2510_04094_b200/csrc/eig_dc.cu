@@ -484,6 +484,8 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
     if (tid == 0) {
       *info = NYS_INFO_DEGENERATE;
       *m_eff_out = 0;
+      if (!kSmem)   // the split epilogue reads the verdict from the buffer tail
+        reinterpret_cast<int*>(gbuf + (size_t)n * ld + 3 * (size_t)n * n + 2 * n)[1] = 1;
     }
     return;
   }
@@ -927,14 +929,21 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   tc3 = clock64();
   if (!kSmem) {
     // large n: the back-transform and the epilogue run as separate kernels
-    // (dc_backtransform_kernel: one warp per column of Q in registers, all SMs)
+    // (dc_backT_out_kernel: columns of Q in registers, reflectors staged in smem)
     double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;   // lam | beta | qsel
     for (int i = tid; i < n; i += nt) {
       tail[i] = S.lam[i];
       tail[n + i] = S.beta[i];
     }
-    if (tid == 0) reinterpret_cast<int*>(tail + 2 * n)[0] = (Q == base + (size_t)n * ld) ? 0 : 1;
-    if (debug && tid == 0) printf("[nys dc] n=%d tridiag=%lld leaves=%lld merges=%lld (backT split)\n", n, tc1 - tc0, tc2 - tc1, tc3 - tc2);
+    if (tid == 0) {
+      reinterpret_cast<int*>(tail + 2 * n)[0] = (Q == base + (size_t)n * ld) ? 0 : 1;
+      reinterpret_cast<int*>(tail + 2 * n)[1] = 0;
+    }
+    if (debug && tid == 0) {
+      printf("[nys dc] merge phases: pre %lld M1 %lld M2 %lld M3 %lld M4 %lld M5 %lld M6 %lld M7+ %lld\n",
+             tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], tm[6], tm[7]);
+      printf("[nys dc] n=%d tridiag=%lld leaves=%lld merges=%lld (backT split)\n", n, tc1 - tc0, tc2 - tc1, tc3 - tc2);
+    }
     return;
   }
   // ---------------- back-transform Z = H_0 ... H_{n-3} Q (reflectors in A)
@@ -1031,111 +1040,156 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
   }
 }
 
-// Back-transform for large n: Z = H_0 H_1 ... H_{n-3} Q, one warp per column of
-// Q held in registers (kRows rows per lane), reflectors applied in reverse order
-// straight from the Householder vectors in A (the next one prefetched).  No
-// block-level synchronisation: every column is independent.
+// Back-transform Z = H_0 H_1 ... H_{n-3} Q fused with the epilogue (descending
+// order, ties: higher index first, nystrom.py:151; drop rule; W = V / sqrt(s)).
+// Each warp owns kCpw columns of Q in registers (kRows rows per lane); the CTA
+// stages the Householder vectors through shared memory kRefl at a time (zeros
+// above the diagonal written explicitly), the next chunk prefetched into
+// registers while this one is applied, so every reflector costs shared-memory
+// loads and one warp reduction instead of an L2 round trip.  A column's rank in
+// the sorted spectrum is counted by its own warp, which then writes its
+// eigenvector and W column straight to their final place.
+constexpr int kRefl = 8, kBtWarps = 8, kCpw = 2;
 template <int kRows>
-__global__ void __launch_bounds__(256)
-    dc_backtransform_kernel(const double* __restrict__ gbuf, int n) {
+__global__ void __launch_bounds__(kBtWarps * 32)
+    dc_backT_out_kernel(const double* __restrict__ gbuf, int n, double drop_tol,
+                        double* __restrict__ eigvals, double* __restrict__ eigvecs,
+                        double* __restrict__ Wout, int* __restrict__ m_eff_out,
+                        int* __restrict__ info) {
+  __shared__ double vs[2][kRefl][kDcMaxN];
+  __shared__ double bs[kDcMaxN];
   const int ld = dc_ld(n);
   const double* A = gbuf;
   const double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;
-  const double* beta = tail + n;
-  const int qsel = reinterpret_cast<const int*>(tail + 2 * n)[0];
-  double* Q = const_cast<double*>(gbuf) + (size_t)n * ld + (qsel ? (size_t)n * n : 0);
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= n) return;
-  double z[kRows];
-#pragma unroll
-  for (int t = 0; t < kRows; ++t) {
-    const int i = lane + 32 * t;
-    z[t] = i < n ? Q[(size_t)i * n + c] : 0.0;
+  const double* lam = tail;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (reinterpret_cast<const int*>(tail + 2 * n)[1] != 0) {   // degenerate landmarks
+    if (blockIdx.x == 0 && tid == 0) {
+      *m_eff_out = 0;
+      *info = NYS_INFO_DEGENERATE;
+    }
+    return;
   }
-  double vn[kRows];
-  auto loadv = [&](int k, double* v) {
+  const int qsel = reinterpret_cast<const int*>(tail + 2 * n)[0];
+  const double* Q = gbuf + (size_t)n * ld + (qsel ? (size_t)n * n : 0);
+  for (int i = tid; i < n; i += blockDim.x) bs[i] = tail[n + i];
+  int col[kCpw];
+  double z[kCpw][kRows];
+#pragma unroll
+  for (int w = 0; w < kCpw; ++w) {
+    col[w] = (blockIdx.x * kBtWarps + warp) * kCpw + w;
 #pragma unroll
     for (int t = 0; t < kRows; ++t) {
       const int i = lane + 32 * t;
-      v[t] = (i > k && i < n) ? A[(size_t)i * ld + k] : 0.0;
+      z[w][t] = (col[w] < n && i < n) ? Q[(size_t)i * n + col[w]] : 0.0;
+    }
+  }
+  // chunks of reflectors [k_lo, k_lo + kRefl), applied from the last one down
+  const int nk = n - 2;                          // reflectors 0 .. n-3
+  const int nchunk = (nk + kRefl - 1) / kRefl;
+  constexpr int kPer = (kRefl * kDcMaxN) / (kBtWarps * 32);   // staged entries per thread
+  double pre[kPer];
+  auto fetch = [&](int c) {   // chunk c into registers: entry e = kk * n + i
+    const int k_lo = c * kRefl;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kBtWarps * 32, kk = e / kDcMaxN, i = e % kDcMaxN, k = k_lo + kk;
+      pre[u] = (k < nk && i > k && i < n) ? A[(size_t)i * ld + k] : 0.0;
     }
   };
-  if (n >= 3) loadv(n - 3, vn);
-  for (int k = n - 3; k >= 0; --k) {
-    double v[kRows];
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int t = 0; t < kRows; ++t) v[t] = vn[t];
-    if (k > 0) loadv(k - 1, vn);
-    const double bk = beta[k];
-    if (bk == 0.0) continue;
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int t = 0; t < kRows; t += 2) {
-      a0 = fma(v[t], z[t], a0);
-      if (t + 1 < kRows) a1 = fma(v[t + 1], z[t + 1], a1);
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kBtWarps * 32;
+      vs[buf][e / kDcMaxN][e % kDcMaxN] = pre[u];
     }
-    double d = a0 + a1;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    const double w = bk * d;
-#pragma unroll
-    for (int t = 0; t < kRows; ++t) z[t] = fma(-v[t], w, z[t]);
+  };
+  if (nchunk > 0) {
+    fetch(nchunk - 1);
+    stash(0);
   }
-#pragma unroll
-  for (int t = 0; t < kRows; ++t) {
-    const int i = lane + 32 * t;
-    if (i < n) Q[(size_t)i * n + c] = z[t];
-  }
-}
-
-// descending order (ties: higher index first, nystrom.py:151), drop rule, W
-__global__ void __launch_bounds__(1024)
-    dc_epilogue_kernel(const double* __restrict__ gbuf, int n, double drop_tol,
-                       double* __restrict__ eigvals, double* __restrict__ eigvecs,
-                       double* __restrict__ Wout, int* __restrict__ m_eff_out,
-                       int* __restrict__ info) {
-  __shared__ int perm[kDcMaxN];
-  __shared__ double lam[kDcMaxN];
-  const int ld = dc_ld(n);
-  const double* tail = gbuf + (size_t)n * ld + 3 * (size_t)n * n;
-  const int qsel = reinterpret_cast<const int*>(tail + 2 * n)[0];
-  const double* Q = gbuf + (size_t)n * ld + (qsel ? (size_t)n * n : 0);
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < n; i += nt) lam[i] = tail[i];
   __syncthreads();
-  for (int i = tid; i < n; i += nt) {
-    const double di = lam[i];
+  for (int c = nchunk - 1, buf = 0; c >= 0; --c, buf ^= 1) {
+    if (c > 0) fetch(c - 1);
+    const int k_lo = c * kRefl;
+    for (int kk = min(kRefl, nk - k_lo) - 1; kk >= 0; --kk) {
+      const double bk = bs[k_lo + kk];
+      if (bk == 0.0) continue;
+      double v[kRows];
+#pragma unroll
+      for (int t = 0; t < kRows; ++t) v[t] = vs[buf][kk][lane + 32 * t];
+      double d[kCpw];
+#pragma unroll
+      for (int w = 0; w < kCpw; ++w) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < kRows; t += 2) {
+          a0 = fma(v[t], z[w][t], a0);
+          if (t + 1 < kRows) a1 = fma(v[t + 1], z[w][t + 1], a1);
+        }
+        d[w] = a0 + a1;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int w = 0; w < kCpw; ++w) d[w] += __shfl_xor_sync(0xffffffffu, d[w], o);
+#pragma unroll
+      for (int w = 0; w < kCpw; ++w) {
+        const double wk = bk * d[w];
+#pragma unroll
+        for (int t = 0; t < kRows; ++t) z[w][t] = fma(-v[t], wk, z[w][t]);
+      }
+    }
+    if (c > 0) stash(buf ^ 1);
+    __syncthreads();
+  }
+  // epilogue: s_0, the cut, this column's rank; m_eff and the eigenvalues
+  double smax = -INFINITY;
+  for (int j = lane; j < n; j += 32) smax = fmax(smax, lam[j]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  const double cut = fmax(drop_tol * smax, 0.0);
+  if (blockIdx.x == 0 && warp == 0) {
+    int cnt = 0;
+    for (int j = lane; j < n; j += 32) cnt += lam[j] > cut;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) {
+      *m_eff_out = cnt;
+      *info = NYS_INFO_OK;
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < kCpw; ++w) {
+    if (col[w] >= n) continue;
+    const double lc = lam[col[w]];
     int rank = 0;
-    for (int j = 0; j < n; ++j) {
-      const double dj = lam[j];
-      rank += (dj > di) || (dj == di && j > i);
+    for (int j = lane; j < n; j += 32) {
+      const double lj = lam[j];
+      rank += (lj > lc) || (lj == lc && j > col[w]);
     }
-    perm[rank] = i;
-  }
-  __syncthreads();
-  const double s0 = lam[perm[0]];
-  const double cut = fmax(drop_tol * s0, 0.0);
-  for (int k = tid; k < n; k += nt) eigvals[k] = lam[perm[k]];
-  if (tid == 0) {
-    int me = 0;
-    while (me < n && lam[perm[me]] > cut) ++me;
-    *m_eff_out = me;
-    *info = NYS_INFO_OK;
-  }
-  for (int e = tid; e < n * n; e += nt) {
-    const int i = e / n, k = e % n;
-    const int src = perm[k];
-    const double v = Q[(size_t)i * n + src];
-    eigvecs[e] = v;
-    const double sk = lam[src];
-    Wout[e] = (sk > cut) ? v / sqrt(sk) : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) eigvals[rank] = lc;
+    const bool keep = lc > cut;
+    const double rs = keep ? 1.0 / sqrt(lc) : 0.0;
+#pragma unroll
+    for (int t = 0; t < kRows; ++t) {
+      const int i = lane + 32 * t;
+      if (i < n) {
+        eigvecs[(size_t)i * n + rank] = z[w][t];
+        Wout[(size_t)i * n + rank] = keep ? z[w][t] * rs : 0.0;
+      }
+    }
   }
 }
 
 }  // namespace
 
 namespace nys_host {
+bool dcc_fits(int n);
+int launch_dcc_eig(const double* lm, const double* Ain, int n, double sigma2, double* gbuf,
+                   int debug, cudaStream_t st);
 size_t dc_buffer_bytes(int n) {
   // A (n x ld) | Q | Qn | DL (n x n each) | lam, beta (n each) | qsel
   return ((size_t)n * dc_ld(n) + 3 * (size_t)n * n + 2 * (size_t)n + 2) * sizeof(double);
@@ -1164,23 +1218,29 @@ int launch_dc_eig(const double* lm, const double* Ain, int n, double sigma2, dou
     return NYS_OK;
   };
   int rc;
-  if (use_smem)
+  // 64 < n <= 256: the cluster kernel (eig_cluster.cu); NYS_EIG_ALGO=dc1 keeps the
+  // one-CTA kernel (A/B tests)
+  const char* algo = getenv("NYS_EIG_ALGO");
+  const bool one_cta = algo && algo[0] == 'd' && algo[1] == 'c' && algo[2] == '1';
+  if (!use_smem && !one_cta && dcc_fits(n))
+    rc = launch_dcc_eig(lm, Ain, n, sigma2, static_cast<double*>(ws), dbg, st);
+  else if (use_smem)
     rc = n <= 64 ? launch(dc_eig_kernel<true, 2>) : launch(dc_eig_kernel<true, kDcMaxN / 32>);
   else
     rc = n <= 64 ? launch(dc_eig_kernel<false, 2>) : launch(dc_eig_kernel<false, kDcMaxN / 32>);
   if (rc) return rc;
-  count_launches(1);
+  if (use_smem || one_cta || !dcc_fits(n)) count_launches(1);
   NYS_CHECK_LAUNCH();
   if (!use_smem) {
     double* g = static_cast<double*>(ws);
-    const int warps = 8;
-    const int grid = (n + warps - 1) / warps;
+    const int grid = (n + kBtWarps * kCpw - 1) / (kBtWarps * kCpw);
     if (n <= 128)
-      dc_backtransform_kernel<4><<<grid, 32 * warps, 0, st>>>(g, n);
+      dc_backT_out_kernel<4><<<grid, 32 * kBtWarps, 0, st>>>(g, n, drop_tol, eigvals, eigvecs, W,
+                                                             m_eff, info);
     else
-      dc_backtransform_kernel<kDcMaxN / 32><<<grid, 32 * warps, 0, st>>>(g, n);
-    dc_epilogue_kernel<<<1, 1024, 0, st>>>(g, n, drop_tol, eigvals, eigvecs, W, m_eff, info);
-    count_launches(2);
+      dc_backT_out_kernel<kDcMaxN / 32><<<grid, 32 * kBtWarps, 0, st>>>(g, n, drop_tol, eigvals,
+                                                                        eigvecs, W, m_eff, info);
+    count_launches(1);
     NYS_CHECK_LAUNCH();
   }
   return NYS_OK;
