@@ -29,12 +29,13 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 1) probe(int va
   double acc = 0.0;
   for (int k = 0; k < K; ++k) {
     const int jj = 15, prow = rk * 16;
-    const uint32_t bytes = (variant == 2) ? 0 : 8u * (256 + 8);
-    if (tid == 0 && variant != 2)
+    const bool local = variant == 2 || variant >= 4;
+    const uint32_t bytes = 8u * (256 + 8);
+    if (tid == 0 && !local)
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su32(&bar[xe & 1])), "r"(bytes) : "memory");
     if (warp == 0) {
       double c = 1.0 + acc;
-      if (variant != 1 && variant != 3) {
+      if (variant != 1 && variant != 3 && variant != 4 && variant != 5) {
         const double* Vi = V + (prow + (lane & 15)) * 17; const double* Wi = W + (prow + (lane & 15)) * 17;
         const double* Vj = V + 37 * 17; const double* Wj = W + 37 * 17;
         double c1 = 0, c2 = 0, c3 = 0, c4 = 0;
@@ -45,16 +46,16 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 1) probe(int va
         }
         c = c - ((c1 + c3) + (c2 + c4));
       }
-      if (variant != 2) {
+      if (!local) {
         const uint32_t la = su32(V + (prow + (lane & 15)) * 17 + (k & 15)), lb = su32(&bar[xe & 1]);
 #pragma unroll
         for (int r = 0; r < 8; ++r)
           asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" :: "r"(mapa(la, r)), "d"(c), "r"(mapa(lb, r)) : "memory");
       }
       double part = c * c;
-      if (variant != 3)
+      if (variant != 3 && variant != 4 && variant != 6)
         for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0 && variant != 2) {
+      if (lane == 0 && !local) {
         const uint32_t la = su32(&slot[xe & 1][rk]), lb = su32(&bar[xe & 1]);
 #pragma unroll
         for (int r = 0; r < 8; ++r)
@@ -62,7 +63,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 1) probe(int va
       }
       acc += part * 1e-30;
     }
-    if (variant != 2) {
+    if (!local) {
       if (tid == 0) {
         const uint32_t b = su32(&bar[xe & 1]), par = (xe >> 1) & 1;
         asm volatile("{ .reg .pred p; W_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1; @!p bra W_%=; }" :: "r"(b), "r"(par) : "memory");
@@ -73,17 +74,18 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(512, 1) probe(int va
   }
   long long t1 = clock64();
   if (tid == 0 && rk == 0) out[variant] = (t1 - t0) / K;
-  if (acc == 12345.0) out[7] = 1;
+  if (acc == 12345.0) out[15] = 1;
   cl.sync();
 }
 
 int main() {
-  long long* d; cudaMalloc(&d, 8 * sizeof(long long));
-  const char* names[] = {"full (q-loop + push + reduce + wait)", "no q-loop", "no push/wait (local)", "push + wait only"};
-  for (int v = 0; v < 4; ++v) {
+  long long* d; cudaMalloc(&d, 16 * sizeof(long long));
+  const char* names[] = {"full (q-loop + push + reduce + wait)", "no q-loop", "no push/wait (local)", "push + wait only",
+                         "syncthreads only", "reduce + syncthreads", "q-loop + syncthreads"};
+  for (int v = 0; v < 7; ++v) {
     probe<<<8, 512>>>(v, 2000, d);
     cudaError_t e = cudaDeviceSynchronize();
-    long long h[8]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    long long h[16]; cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     printf("variant %d %-40s %lld cycles/round  (%s)\n", v, names[v], h[v], cudaGetErrorString(e));
   }
   return 0;
