@@ -368,13 +368,43 @@ def setup_c2(args, ctx):
                            "tests/test_oracle_golden.py)",
                 "ok": bool(max(rel) <= YHAT_TOL and max(derr) <= ERR_TOL)}
 
+    def callable_e2e():
+        """The reference-style callable API (batch.solve_many: spec callables
+        sampled on host threads, upload, solve, PrimalModels back) on the timed
+        batch's specs: host wall clock per call, median of 3 after one warm call."""
+        import time as _t
+        from paper_2510_04094_b200.problems import BoundaryCondition, Conditions, LinearOdeSpec
+
+        specs = [LinearOdeSpec(p, inst.coeff_fns(), inst.forcing_fn, inst.domain)
+                 for inst in bt.instances]
+        conds = [Conditions("ivp", tuple(BoundaryCondition(*c) for c in inst.conditions()))
+                 for inst in bt.instances]
+        BT.solve_many(specs, conds, fm, bt.grid, cfg.gamma)
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
+            BT.solve_many(specs, conds, fm, bt.grid, cfg.gamma)
+            ts.append(_t.perf_counter() - t0)
+        t0 = _t.perf_counter()
+        BT._sample_specs(specs, solver.pts.cpu().numpy(), p,
+                         np.empty((B, p, n_c)), np.empty((B, n_c)), 0, B)
+        t_one = _t.perf_counter() - t0
+        wall = sorted(ts)[1]
+        return {"value": B / wall, "unit": "solves/s", "ms_per_call": wall * 1e3,
+                "api": "batch.solve_many(specs, conds, fmap, grid, gamma): reference-style "
+                       "callables (the feature map built once, outside the call)",
+                "host_threads": BT._SAMPLE_THREADS,
+                "sampling_ms_one_thread": t_one * 1e3,
+                "clock": "host wall clock (time.perf_counter), synchronised before each call"}
+
     # symmetric count of what the Gram computes: the extended Gram [D g r]^T [D g r]
     # (upper triangle, (w)(w+1)/2 entries x 2 flops per row, w = m_eff + 2) plus
     # the row combine D = Psi_2 - f_1 Psi_1 - f_2 Psi_0 (4 flops per element)
     w = me + 2
     flops_inst = n_c * (w * (w + 1) + 4.0 * me)
     return dict(
-        B=B, step=step, e2e=e2e, kernel=kernel, parity=parity,
+        B=B, step=step, e2e=e2e, kernel=kernel, parity=parity, callable_e2e=callable_e2e,
         check=lambda: int((info_h != 0).sum()) == 0,
         h2d=coef_h.numel() * 8 + forc_h.numel() * 8 + vals_h.numel() * 8,
         d2h=x_h.numel() * 8 + info_h.numel() * 4,
@@ -716,7 +746,8 @@ def measure(cid, args, ctx, T, with_cpu, batch=None):
     # solve across all ranks
     units = {2: world * S["B"], 3: world * S["B"], 0: world, 1: world, 4: 1}[cid]
     value = units / (ms / 1e3)
-    cold = T.time_flushed(S["step"], min(args.steps, 5)) if cid in (0, 1, 3) else None
+    # one call alone (synchronised on both sides, cold L2): single-solve latency
+    cold = T.time_flushed(S["step"], min(args.steps, 5))
     kms = T.kernel_ms(S["kernel"], max(3, min(args.steps, 10)))
     peak, peak_src = _fp64_peak()
     for _ in range(6):   # every (staging set, eigendecomposition set) pair: graphs captured
@@ -760,6 +791,8 @@ def measure(cid, args, ctx, T, with_cpu, batch=None):
         "latency_ms_l2_flushed": cold,
         "clocks": clk.summary(),
     }
+    if rank == 0 and S.get("callable_e2e") is not None and not args.no_parity:
+        line["e2e_callable"] = S["callable_e2e"]()
     if cpu is not None:
         line["cpu_baseline"] = cpu
     if parity is not None:

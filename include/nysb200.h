@@ -61,9 +61,10 @@ unsigned long long nys_launch_count(void);
 /* ------------------------------------------------------------------------
  * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map
  * (nystrom.py:136-160) + NystromFeatureMap._scaled_vectors (nystrom.py:120-121).
- * Omega = K(L, L); one CTA: Householder tridiagonalisation + Cuppen divide and
- * conquer (m <= 256; implicit QL above); eigenpairs sorted descending;
- * keep s > max(drop_tol * s_0, 0).
+ * Omega = K(L, L); Householder tridiagonalisation + Cuppen divide and conquer
+ * (one CTA for m <= 68; one 8-CTA thread-block cluster exchanging through
+ * DSMEM for 68 < m <= 256, then a multi-SM back-transform; implicit QL above
+ * 256); eigenpairs sorted descending; keep s > max(drop_tol * s_0, 0).
  *   eigvals  [m]     descending (entries >= m_eff are the dropped ones)
  *   eigvecs  [m*m]   column k = eigenvector k (row-major m x m)
  *   W        [m*m]   W[:, k] = eigvecs[:, k] / sqrt(s_k) for k < m_eff, 0 else

@@ -16,6 +16,7 @@ Entry points:
 """
 from __future__ import annotations
 
+import os
 from typing import Optional, Sequence
 
 import numpy as np
@@ -107,11 +108,38 @@ class LinearBatchSolver:
         return self.solve_device(coef, forcing, values)
 
 
+def _sample_specs(specs, pts, p, coef, forcing, lo, hi):
+    """Spec callables on the constraint points for specs[lo:hi] (linear.py:104-116:
+    the same non-finite checks, in the same order per spec)."""
+    for b in range(lo, hi):
+        sp = specs[b]
+        if sp.order != p:
+            raise ValueError("solve_many needs a common ODE order")
+        for k, fk in enumerate(sp.coeffs, start=1):
+            v = np.asarray(fk(pts), dtype=float)
+            if not np.all(np.isfinite(v)):
+                raise FloatingPointError(f"coefficient f_{k} non-finite on constraint points")
+            coef[b, k - 1] = v
+        r = np.asarray(sp.forcing(pts), dtype=float)
+        if not np.all(np.isfinite(r)):
+            raise FloatingPointError("forcing non-finite on constraint points")
+        forcing[b] = r
+
+
+# host threads sampling the spec callables (NumPy ufuncs release the GIL inside
+# their loops); NYS_SAMPLE_THREADS=1 samples on the calling thread
+_SAMPLE_THREADS = int(os.environ.get("NYS_SAMPLE_THREADS", "0")) or min(16, os.cpu_count() or 1)
+_POOL = None
+
+
 def solve_many(specs: Sequence, conds: Sequence, fmap: NystromFeatureMap, grid,
                gamma: float) -> list[PrimalModel]:
     """Reference-style batch: one PrimalModel per (spec, cond), same grid/fmap.
 
-    Condition points and orders must be shared (values may differ)."""
+    Condition points and orders must be shared (values may differ).  The spec
+    callables are sampled on a host thread pool in contiguous chunks (each spec's
+    checks and errors as in linear.py:104-116; the first failing chunk's error is
+    raised)."""
     if len(specs) != len(conds) or not specs:
         raise ValueError("need matching, non-empty spec and condition lists")
     grid = np.asarray(grid, dtype=float)
@@ -124,18 +152,20 @@ def solve_many(specs: Sequence, conds: Sequence, fmap: NystromFeatureMap, grid,
     pts = constraint_points(c0, grid)
     coef = np.empty((len(specs), p, pts.size))
     forcing = np.empty((len(specs), pts.size))
-    for b, sp in enumerate(specs):
-        if sp.order != p:
-            raise ValueError("solve_many needs a common ODE order")
-        for k, fk in enumerate(sp.coeffs, start=1):
-            v = np.asarray(fk(pts), dtype=float)
-            if not np.all(np.isfinite(v)):
-                raise FloatingPointError(f"coefficient f_{k} non-finite on constraint points")
-            coef[b, k - 1] = v
-        r = np.asarray(sp.forcing(pts), dtype=float)
-        if not np.all(np.isfinite(r)):
-            raise FloatingPointError("forcing non-finite on constraint points")
-        forcing[b] = r
+    nb = len(specs)
+    nt = min(_SAMPLE_THREADS, max(1, nb // 64))
+    if nt <= 1:
+        _sample_specs(specs, pts, p, coef, forcing, 0, nb)
+    else:
+        global _POOL
+        if _POOL is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _POOL = ThreadPoolExecutor(max_workers=_SAMPLE_THREADS)
+        bounds = [nb * i // nt for i in range(nt + 1)]
+        futs = [_POOL.submit(_sample_specs, specs, pts, p, coef, forcing, bounds[i], bounds[i + 1])
+                for i in range(nt)]
+        for f in futs:   # in chunk order: the lowest failing chunk's error wins
+            f.result()
     values = np.array([[bc.value for bc in c.entries] for c in conds])
     solver = LinearBatchSolver(fmap, grid, gamma, p, c0, len(specs))
     x, info = solver.solve(coef, forcing, values)

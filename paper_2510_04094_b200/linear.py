@@ -289,6 +289,13 @@ def predict(model: PrimalModel, ell: int, points) -> np.ndarray:
     return model.predict(ell, points)
 
 
+def _cluster_eig(m: int) -> bool:
+    """Landmark counts whose eigendecomposition runs on an 8-CTA cluster
+    (csrc/eig_cluster.cu: 68 < m <= 256, the sizes whose one-CTA buffers spill
+    out of shared memory)."""
+    return 68 < m <= 256 and os.environ.get("NYS_EIG_ALGO", "") != "dc1"
+
+
 class SingleSolvePipeline:
     """One linear ODE per call on a fixed grid / landmark set (configs 0, 1, 4):
     the reference's assemble + solve (linear.py:90-158) as a device pipeline.
@@ -316,10 +323,19 @@ class SingleSolvePipeline:
     def _n_eig_streams(self) -> int:
         if self.EIG_STREAMS > 0:
             return self.EIG_STREAMS
+        m = self.landmarks.size
+        if _cluster_eig(m):
+            # one 8-SM cluster eigensolver (1.4 ms at m = 256) per call: one in
+            # flight keeps up with a 2.4 ms call; two when row shards make the
+            # Gram short
+            return 2 if getattr(self, "_rows", None) is not None else 1
         if getattr(self, "_rows", None) is not None:
             return 4   # row shards make the Gram short: more eigensolvers in flight
-        m = self.landmarks.size
         return 3 if m <= 32 else (5 if m <= 128 else 2)
+
+    def _eig_sms(self) -> int:
+        """SMs one in-flight eigendecomposition holds."""
+        return 8 if _cluster_eig(self.landmarks.size) else 1
 
     def __init__(self, landmarks, sigma2: float, grid, gamma: float, order: int, cond,
                  drop_tol: float = 1e-16, device=None, rows=None, group=None):
@@ -364,7 +380,7 @@ class SingleSolvePipeline:
             # one SM per concurrent eigensolver and one for the previous call's
             # KKT, which may overlap this call's Gram (input_event)
             self._kctas = (torch.cuda.get_device_properties(self.device).multi_processor_count
-                           - self._n_eig_streams() - 1)
+                           - self._eig_sms() * self._n_eig_streams() - 1)
             self._kn_c = None
         if rows is not None and not self._kspace:
             raise NotImplementedError("row-sharded SingleSolvePipeline needs the kernel-space "
