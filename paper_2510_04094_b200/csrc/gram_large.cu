@@ -36,6 +36,7 @@
 // reduce kernel sums the slabs in fixed order (deterministic).
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -217,7 +218,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
                         const double* __restrict__ pts, const double* __restrict__ coef,
                         const double* __restrict__ forcing, int n_c, int row_begin, int row_end,
                         int NB, int NBpad, int ld, int nbuf, int tiles_per_cta,
-                        double* __restrict__ slabs, unsigned long long* __restrict__ live_out) {
+                        double* __restrict__ slabs, unsigned long long* __restrict__ live_out,
+                        int min_L) {
   extern __shared__ __align__(16) double sm[];
   const size_t xsz = (size_t)kTileKs * NBpad * 32;
   double* const X0 = sm;
@@ -315,6 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
   __syncthreads();
   const int L = __popcll(live_s);
+  if (L < min_L) return;   // large_ws_kernel covered this range
   const int T = (L + kRT - 1) / kRT;
   const int ntask = T * (T + 1) / 2;
   __shared__ signed char wtask_s[kWarps], wrep_s[kWarps], wR_s[kWarps], genw_s[64];
@@ -588,6 +591,401 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
 }
 
+// ---- Warp-specialised kernel-space Gram (live windows of at most kWsMaxL
+// blocks, config 4: 11-13).  16 warps, one CTA per SM:
+//   * 8 producer warps (two per SM sub-partition) generate the 32-row tiles of
+//     the compacted window into a kWsStages-deep shared-memory ring (warp 0 also
+//     forms the row coefficients a tile ahead; the eight meet at a named
+//     barrier), each warp its own blocks with the recurrence state in registers;
+//   * 8 consumer warps own the window's block pairs (I <= J) in equal
+//     contiguous chunks of the row-pair order (I / 2, J, I % 2), so consecutive
+//     pairs share the B fragment and each row pair's two A fragments: every warp
+//     issues the same number of DMMAs per tile (no replicas, no idle warp).
+// Stages are handed over by mbarriers (full: 8 producer arrivals, empty: 8
+// consumer arrivals): no CTA-wide barrier per tile, so the tensor pipe stays fed
+// while the producers run ahead.  Same exact-underflow window and generation
+// arithmetic as large_kspace_kernel; each pair is accumulated by one warp in k
+// order (no replica split).  A CTA whose window is wider than kWsMaxL leaves its range to
+// large_kspace_kernel (launched after this one with min_L = kWsMaxL + 1).
+#ifndef NYS_WS_PROBE
+#define NYS_WS_PROBE 0   // probe builds: 1 = consumers skip DMMA, 2 = producers skip generation
+#endif
+constexpr int kWsProd = 8, kWsCons = 8, kWsWarps = kWsProd + kWsCons;
+constexpr int kWsStages = 6, kWsMaxL = 14, kWsCols = 8, kWsGen = (kWsMaxL + kWsProd - 1) / kWsProd;
+
+NYS_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(nys::smem_u32(bar)) : "memory");
+}
+
+size_t ws_smem_bytes() {   // X ring + per-producer row records (non-uniform grids)
+  return ((size_t)kWsStages * kTileKs * kWsMaxL * 32 + kWsProd * 32 * kRowStride) * sizeof(double);
+}
+
+// consumer body for a warp owning NC columns (see large_ws_kernel): per k-step
+// the A fragments of a row pair are loaded when the row pair changes, one B
+// fragment per column, one or two DMMAs
+template <int NC>
+NYS_DEV void ws_consume(const double* Xr, int nt, uint64_t* full_b, uint64_t* empty_b,
+                        const int* offa, const int* offb, const int* Ia, const int* Jb,
+                        unsigned newrp, unsigned two, const int* lb_s, double* slab, int ld) {
+  constexpr size_t xsz = (size_t)kTileKs * kWsMaxL * 32;
+  const int lane = threadIdx.x & 31;
+  double acc[NC > 0 ? NC : 1][2][2];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c][0][0] = acc[c][0][1] = acc[c][1][0] = acc[c][1][1] = 0.0;
+  for (int k = 0; k < nt; ++k) {
+    const int st = k % kWsStages;
+    nys::mbar_wait(&full_b[st], (k / kWsStages) & 1);
+    const double* const Xs = Xr + (size_t)st * xsz + lane;
+#pragma unroll 2
+    for (int ks = 0; ks < kTileKs; ++ks) {
+      const double* Xk = Xs + (size_t)ks * kWsMaxL * 32;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if ((newrp >> c) & 1u) {
+          a0 = Xk[offa[c]];
+          a1 = Xk[offa[c] + 32];
+        }
+        const double b = Xk[offb[c]];
+        if (NYS_WS_PROBE != 1) {
+          nys::dmma(acc[c][0][0], acc[c][0][1], a0, b);
+          if ((two >> c) & 1u) nys::dmma(acc[c][1][0], acc[c][1][1], a1, b);
+        } else {
+          acc[c][0][0] += a0 * b;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_b[st]);
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int r2 = 0; r2 < 2; ++r2) {
+      if (r2 == 1 && !((two >> c) & 1u)) continue;
+      const int I = lb_s[Ia[c] + r2], J = lb_s[Jb[c]];
+      double* o = slab + (size_t)(I * 8 + (lane >> 2)) * ld + J * 8 + 2 * (lane & 3);
+      o[0] = acc[c][r2][0];
+      o[1] = acc[c][r2][1];
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kWsWarps * 32, 1)
+    large_ws_kernel(const double* __restrict__ lm, int m, double sigma2,
+                    const double* __restrict__ pts, const double* __restrict__ coef,
+                    const double* __restrict__ forcing, int n_c, int row_begin, int row_end,
+                    int NB, int ld, int tiles_per_cta, double* __restrict__ slabs,
+                    unsigned long long* __restrict__ live_out) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr size_t xsz = (size_t)kTileKs * kWsMaxL * 32;
+  double* const Xr = sm;                              // [stage][ks][c][lane]
+  double* const rowr = sm + kWsStages * xsz;          // [producer][32][kRowStride]
+  __shared__ double blo_s[64], bhi_s[64];
+  __shared__ double red_s[3][kWsWarps];
+  __shared__ int nan_s;
+  __shared__ double hstep_s, hstep_ta_s;
+  __shared__ unsigned long long live_s;
+  __shared__ int lb_s[64];
+  __shared__ double hc_s[nys::kMaxOrder + 1][nys::kMaxOrder + 1];
+  __shared__ double qtri_s[kAnchorTiles * kTileKs];
+  __shared__ __align__(8) uint64_t full_b[kWsStages], empty_b[kWsStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = kWsWarps;
+  const int ntiles = (row_end - row_begin + 31) / 32;
+  const int tile0 = blockIdx.x * tiles_per_cta;
+  const int tile1 = min(ntiles, tile0 + tiles_per_cta);
+  const int nt = max(0, tile1 - tile0);
+  const double inv = 1.0 / sigma2;
+  const unsigned long long special = (1ull << (m / 8)) | (1ull << ((m + 1) / 8));
+
+  // ---- prologue: as large_kspace_kernel (Hermite coefficients, window, grid test)
+  if (threadIdx.x == 0) {
+    nan_s = 0;
+    nys::Hermite H;
+    H.init(sigma2, P);
+    for (int a = 0; a <= nys::kMaxOrder; ++a)
+      for (int j = 0; j <= nys::kMaxOrder; ++j) hc_s[a][j] = H.c[a][j];
+    for (int s = 0; s < kWsStages; ++s) {
+      nys::mbar_init(&full_b[s], kWsProd);
+      nys::mbar_init(&empty_b[s], kWsCons);
+    }
+  }
+  if (warp == 1) {
+    for (int blk = lane; blk < NB; blk += 32) {
+      double lo = INFINITY, hi = -INFINITY;
+      for (int s = blk * 8; s < min(blk * 8 + 8, m); ++s) {
+        lo = fmin(lo, lm[s]);
+        hi = fmax(hi, lm[s]);
+      }
+      blo_s[blk] = lo;
+      bhi_s[blk] = hi;
+    }
+  }
+  __syncthreads();
+  {
+    double tmin = INFINITY, tmax = -INFINITY, dev = 0.0;
+    bool bad = false;
+    const int r_lo = row_begin + tile0 * 32, r_hi = min(row_end, row_begin + tile1 * 32);
+    const double ta = r_hi > r_lo ? pts[r_lo] : 0.0, tb = r_hi > r_lo ? pts[r_hi - 1] : 0.0;
+    const double h = r_hi - r_lo > 1 ? (tb - ta) / (double)(r_hi - 1 - r_lo) : 0.0;
+    for (int i = r_lo + threadIdx.x; i < r_hi; i += blockDim.x) {
+      const double t = pts[i];
+      tmin = fmin(tmin, t);
+      tmax = fmax(tmax, t);
+      bad |= t != t;
+      dev = fmax(dev, fabs(t - fma((double)(i - r_lo), h, ta)));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+      dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) nan_s = 1;
+    if (lane == 0) {
+      red_s[0][warp] = tmin;
+      red_s[1][warp] = tmax;
+      red_s[2][warp] = dev;
+    }
+    if (threadIdx.x == 0) {
+      hstep_s = h;
+      hstep_ta_s = ta;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double tmin = INFINITY, tmax = -INFINITY, dev = 0.0;
+    for (int w = 0; w < nwarps; ++w) {
+      tmin = fmin(tmin, red_s[0][w]);
+      tmax = fmax(tmax, red_s[1][w]);
+      dev = fmax(dev, red_s[2][w]);
+    }
+    const double tol = 8.0 * 2.220446049250313e-16 * fmax(fabs(tmin), fabs(tmax));
+    if (lane == 0 && !(dev <= tol && nan_s == 0 && hstep_s > 0.0)) hstep_s = 0.0;
+    const unsigned long long live =
+        live_blocks(blo_s, bhi_s, NB, special, tmin, tmax, nan_s != 0, kDeadRatio * sigma2);
+    for (int h = 0; h < 2; ++h) {
+      const int blk = lane + 32 * h;
+      if ((live >> blk) & 1ull) lb_s[__popcll(live & ((1ull << blk) - 1ull))] = blk;
+    }
+    if (lane == 0) {
+      live_s = live;
+      live_out[blockIdx.x] = live;
+    }
+  }
+  __syncthreads();
+  const int L = __popcll(live_s);
+  if (L > kWsMaxL) return;   // large_kspace_kernel (min_L) covers this range
+  const double H = 4.0 * hstep_s;
+  const bool rec = H > 0.0 && NYS_LARGE_REC;
+  if (rec && threadIdx.x < kAnchorTiles * kTileKs)
+    qtri_s[threadIdx.x] = exp(-H * H * inv * (double)(threadIdx.x * (threadIdx.x - 1)));
+  __syncthreads();
+  double* const slab = slabs + (size_t)blockIdx.x * ld * ld;
+  const int rsub = lane & 3, csub = lane >> 2;
+
+  if (warp < kWsProd) {
+    // ================= producers
+    const int pw = warp;
+    int gc[kWsGen], ng = 0;
+    double gl[kWsGen], geA[kWsGen], grA[kWsGen], gP[kWsGen], geN[kWsGen], grN[kWsGen];
+#pragma unroll
+    for (int g = 0; g < kWsGen; ++g) {
+      gc[g] = -1;
+      gl[g] = geA[g] = grA[g] = gP[g] = geN[g] = grN[g] = 0.0;
+    }
+    for (int c = pw; c < L && ng < kWsGen; c += kWsProd) gc[ng++] = c;
+#pragma unroll
+    for (int g = 0; g < kWsGen; ++g)
+      if (g < ng) {
+        const int s = lb_s[gc[g]] * 8 + csub;
+        gl[g] = s < m ? __ldg(lm + s) : 0.0;
+      }
+    const double ta = hstep_ta_s;
+    auto anchor = [&](int kt) {
+      const double t = fma((double)(kt * 32 + rsub), hstep_s, ta);
+#pragma unroll
+      for (int g = 0; g < kWsGen; ++g)
+        if (g < ng) {
+          const double d = gl[g] - t;
+          geN[g] = exp(neg_div(d * d, sigma2, inv));
+          grN[g] = exp(fma(2.0 * H, d, -H * H) * inv);
+        }
+    };
+    if (rec) anchor(0);
+    // every producer warp forms the row coefficients of its own tile copy in
+    // registers (lane = row; the raw samples loaded two tiles ahead) and
+    // exchanges them by shuffles: no producer waits for another
+    RowRaw<P> raw1, raw2;
+    if (nt > 0) row_load<P>(pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, raw1);
+    if (nt > 1) row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end, raw2);
+    for (int k = 0; k < nt; ++k) {
+      const int st = k % kWsStages;
+      // this lane's row record: t, q_0..q_P, g = -f_P, r (row_store's arithmetic)
+      double rt = raw1.t, rq[P + 1], rg, rr;
+#pragma unroll
+      for (int j = 0; j <= P; ++j) {
+        double v = hc_s[P][j];
+#pragma unroll
+        for (int kk = 1; kk <= P; ++kk) v = fma(-raw1.f[kk - 1], hc_s[P - kk][j], v);
+        rq[j] = raw1.ok ? v : 0.0;
+      }
+      rg = raw1.ok ? -raw1.f[P - 1] : 0.0;
+      rr = raw1.r;
+      raw1 = raw2;
+      if (k + 2 < nt)
+        row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + k + 2) * 32, row_end, raw2);
+      if (k >= kWsStages) nys::mbar_wait(&empty_b[st], ((k / kWsStages) - 1) & 1);
+      double* const Xd = Xr + (size_t)st * xsz;
+      if (NYS_WS_PROBE == 2) {
+      } else if (rec) {
+        const int u = k % kAnchorTiles;
+        if (u == 0) {
+#pragma unroll
+          for (int g = 0; g < kWsGen; ++g) {
+            geA[g] = geN[g];
+            grA[g] = grN[g];
+            gP[g] = 1.0;
+          }
+        }
+        const double* qt = qtri_s + u * kTileKs;
+        // (the shuffles stay outside the per-lane branch on s: every lane of
+        // the warp takes part in each of them)
+#pragma unroll
+        for (int g = 0; g < kWsGen; ++g)
+          if (g < ng) {
+            const int s = lb_s[gc[g]] * 8 + csub;
+            double* Xo = Xd + (size_t)gc[g] * 32 + lane;
+            double rp[kTileKs + 1];   // rho_A^i, i <= 8, by a depth-3 product tree
+            rp[0] = 1.0;
+            rp[1] = grA[g];
+            rp[2] = rp[1] * rp[1];
+            rp[3] = rp[2] * rp[1];
+            rp[4] = rp[2] * rp[2];
+            rp[5] = rp[4] * rp[1];
+            rp[6] = rp[4] * rp[2];
+            rp[7] = rp[4] * rp[3];
+            rp[8] = rp[4] * rp[4];
+            const double base = geA[g] * gP[g];
+#pragma unroll
+            for (int ks = 0; ks < kTileKs; ++ks) {
+              const int src = ks * 4 + rsub;   // this lane's row: ks * 4 + rsub
+              const double d = gl[g] - __shfl_sync(0xffffffffu, rt, src);
+              double poly = __shfl_sync(0xffffffffu, rq[P], src);
+#pragma unroll
+              for (int j = P - 1; j >= 0; --j)
+                poly = fma(poly, d, __shfl_sync(0xffffffffu, rq[j], src));
+              const double gv = __shfl_sync(0xffffffffu, rg, src);
+              const double rv = __shfl_sync(0xffffffffu, rr, src);
+              Xo[(size_t)ks * kWsMaxL * 32] = s < m ? poly * ((base * rp[ks]) * qt[ks])
+                                                    : (s == m) ? gv : (s == m + 1) ? rv : 0.0;
+            }
+            gP[g] *= rp[8];
+          }
+        if (u == kAnchorTiles - 1) anchor(k + 1);
+      } else {
+        // non-uniform grid: exp() per entry from a per-warp copy of the records
+        double* rc = rowr + (size_t)pw * 32 * kRowStride;   // written and read by this warp
+        rc[lane * kRowStride + 0] = rt;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) rc[lane * kRowStride + 1 + j] = rq[j];
+        rc[lane * kRowStride + 6] = rg;
+        rc[lane * kRowStride + 7] = rr;
+        __syncwarp();
+        for (int c = pw; c < L; c += kWsProd)
+          gen_tile<P>(lm, m, c + 1, lb_s, kWsMaxL, sigma2, inv, rc, Xd, 4 * c, 1);   // block c
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_b[st]);
+    }
+  } else {
+    // ================= consumers
+    // The window's block pairs as a sequence of columns of row pairs: item
+    // (rp, J), J >= 2 rp, holds the pairs (2 rp, J) and, when valid, (2 rp + 1, J)
+    // -- one B fragment for both.  Consumer cw takes the items whose cumulative
+    // pair count starts in [P cw / 12, P (cw + 1) / 12): equal DMMA counts, at
+    // most kWsCols columns per warp; the per-warp shape is a template (no
+    // per-pair decoding in the k loop).
+    const int cw = warp - kWsProd;
+    const int P_all = L * (L + 1) / 2;
+    const int w0 = P_all * cw / kWsCons, w1 = P_all * (cw + 1) / kWsCons;
+    int offa[kWsCols], offb[kWsCols], Ia[kWsCols], Jb[kWsCols];
+    unsigned newrp = 0u, two = 0u;
+    int nc = 0;
+    {
+      int cum = 0, prevrp = -1;
+      for (int rp = 0; 2 * rp < L; ++rp)
+        for (int J = 2 * rp; J < L; ++J) {
+          const bool tw = 2 * rp + 1 < L && 2 * rp + 1 <= J;
+          if (cum >= w0 && cum < w1 && nc < kWsCols) {
+#pragma unroll
+            for (int c = 0; c < kWsCols; ++c)
+              if (c == nc) {
+                offa[c] = 2 * rp * 32;
+                offb[c] = J * 32;
+                Ia[c] = 2 * rp;
+                Jb[c] = J;
+              }
+            if (rp != prevrp) newrp |= 1u << nc;
+            if (tw) two |= 1u << nc;
+            prevrp = rp;
+            ++nc;
+          }
+          cum += tw ? 2 : 1;
+        }
+    }
+    switch (nc) {
+      case 0: ws_consume<0>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 1: ws_consume<1>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 2: ws_consume<2>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 3: ws_consume<3>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 4: ws_consume<4>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 5: ws_consume<5>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 6: ws_consume<6>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      case 7: ws_consume<7>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+      default: ws_consume<8>(Xr, nt, full_b, empty_b, offa, offb, Ia, Jb, newrp, two, lb_s, slab, ld); break;
+    }
+  }
+}
+
+// the warp-specialised kernel for windows of <= kWsMaxL blocks, then the
+// 12-warp kernel for the CTAs whose window is wider (it returns at once for the
+// others); NYS_KSPACE_WS=0 runs the 12-warp kernel alone
+template <int PP>
+cudaError_t launch_kspace(const LargePlan& L, const double* lm, int m, double sigma2,
+                          const double* pts, const double* coef, const double* forcing, int n_c,
+                          int row_begin, int row_end, double* slabs, unsigned long long* live,
+                          cudaStream_t st) {
+  static const bool ws_on = [] {
+    const char* e = getenv("NYS_KSPACE_WS");
+    return !(e && e[0] == '0');
+  }();
+  int min_L = 0;
+  if (ws_on) {
+    auto kw = large_ws_kernel<PP>;
+    cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)ws_smem_bytes());
+    if (e != cudaSuccess) return e;
+    kw<<<L.nrr, kWsWarps * 32, ws_smem_bytes(), st>>>(lm, m, sigma2, pts, coef, forcing, n_c,
+                                                      row_begin, row_end, L.NB, L.ld,
+                                                      L.tiles_per_cta, slabs, live);
+    nys_host::count_launches(1);
+    min_L = kWsMaxL + 1;
+  }
+  auto kern = large_kspace_kernel<PP>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)L.smem);
+  if (e != cudaSuccess) return e;
+  kern<<<L.nrr, kWarps * 32, L.smem, st>>>(lm, m, sigma2, pts, coef, forcing, n_c, row_begin,
+                                           row_end, L.NB, L.NBpad, L.ld, L.nbuf, L.tiles_per_cta,
+                                           slabs, live, min_L);
+  nys_host::count_launches(1);
+  return cudaGetLastError();
+}
+
 // K[r][c] = sum over CTAs (fixed order) of their slabs where both blocks are live
 // (dead slab entries are never written: their loads are predicated off, and
 // the select adds an exact 0); loads unrolled 8 deep so they are in flight
@@ -714,25 +1112,14 @@ int fused_gram_large(const double* lm, int m, const double* W, int ldw, int m_ef
   double* T = K + (size_t)L.Pe * L.Pe;
   const int Pw = m_eff + 2;
   auto* live = reinterpret_cast<unsigned long long*>(T + (size_t)L.Pe * Pw);
-  const int nthreads = kWarps * 32;
-#define NYS_LARGE(PP)                                                                              \
-  do {                                                                                             \
-    auto kern = large_kspace_kernel<PP>;                                                           \
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                         (int)L.smem);                                             \
-    if (e != cudaSuccess) return record_cuda(e);                                                   \
-    kern<<<L.nrr, nthreads, L.smem, st>>>(lm, m, sigma2, pts, coef, forcing, n_c, row_begin,       \
-                                          row_end, L.NB, L.NBpad, L.ld, L.nbuf, L.tiles_per_cta,   \
-                                          slabs, live);                                            \
-    nys_host::count_launches(1);                                                                   \
-  } while (0)
+  cudaError_t le;
   switch (p) {
-    case 1: NYS_LARGE(1); break;
-    case 2: NYS_LARGE(2); break;
-    case 3: NYS_LARGE(3); break;
-    default: NYS_LARGE(4); break;
+    case 1: le = launch_kspace<1>(L, lm, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    case 2: le = launch_kspace<2>(L, lm, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    case 3: le = launch_kspace<3>(L, lm, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    default: le = launch_kspace<4>(L, lm, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
   }
-#undef NYS_LARGE
+  if (le != cudaSuccess) return record_cuda(le);
   NYS_CHECK_LAUNCH();
   large_reduce_kernel<<<(L.Pe * L.Pe + 255) / 256, 256, 0, st>>>(slabs, live, L.nrr, L.ld, L.Pe,
                                                                  K);
@@ -766,27 +1153,17 @@ extern "C" int nys_kspace_gram_f64(const double* landmarks, int m, double sigma2
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* slabs = static_cast<double*>(ws);
   auto* live = reinterpret_cast<unsigned long long*>(slabs + L.slab_doubles());
-  const int nthreads = kWarps * 32;
-#define NYS_LARGE(PP)                                                                              \
-  do {                                                                                             \
-    auto kern = large_kspace_kernel<PP>;                                                           \
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                                         (int)L.smem);                                             \
-    if (e != cudaSuccess) return nys_host::record_cuda(e);                                         \
-    kern<<<L.nrr, nthreads, L.smem, st>>>(landmarks, m, sigma2, pts, coef, forcing, n_c,           \
-                                          row_begin, row_end, L.NB, L.NBpad, L.ld, L.nbuf,         \
-                                          L.tiles_per_cta, slabs, live);                           \
-  } while (0)
+  cudaError_t le;
   switch (p) {
-    case 1: NYS_LARGE(1); break;
-    case 2: NYS_LARGE(2); break;
-    case 3: NYS_LARGE(3); break;
-    default: NYS_LARGE(4); break;
+    case 1: le = launch_kspace<1>(L, landmarks, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    case 2: le = launch_kspace<2>(L, landmarks, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    case 3: le = launch_kspace<3>(L, landmarks, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
+    default: le = launch_kspace<4>(L, landmarks, m, sigma2, pts, coef, forcing, n_c, row_begin, row_end, slabs, live, st); break;
   }
-#undef NYS_LARGE
+  if (le != cudaSuccess) return nys_host::record_cuda(le);
   NYS_CHECK_LAUNCH();
   large_reduce_kernel<<<(L.Pe * L.Pe + 255) / 256, 256, 0, st>>>(slabs, live, L.nrr, L.ld, L.Pe, K);
-  nys_host::count_launches(2);
+  nys_host::count_launches(1);
   NYS_CHECK_LAUNCH();
   return NYS_OK;
 }

@@ -97,7 +97,7 @@ def test_single_pipeline_row_shards_sum_to_full():
     Ks = []
     for lo, hi in D.row_ranges(g["pts"].size, 2):
         p = L.SingleSolvePipeline(*args, rows=(lo, hi))
-        assert p._n_eig_streams() == 4
+        assert p._n_eig_streams() == 2   # two 8-SM cluster eigensolvers in flight
         p._kspace_launch(*ins)
         torch.cuda.synchronize()
         Ks.append(p._kcur.clone())
