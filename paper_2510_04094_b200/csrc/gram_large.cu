@@ -852,13 +852,24 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
           }
         }
         const double* qt = qtri_s + u * kTileKs;
-        // (the shuffles stay outside the per-lane branch on s: every lane of
-        // the warp takes part in each of them)
+        // three warp-uniform block kinds (the shuffles need every lane): landmark
+        // columns only, g / r / padding columns only, or both (m % 8 != 0)
 #pragma unroll
         for (int g = 0; g < kWsGen; ++g)
           if (g < ng) {
-            const int s = lb_s[gc[g]] * 8 + csub;
+            const int b8 = lb_s[gc[g]] * 8, s = b8 + csub;
+            const int kind = b8 + 7 < m ? 0 : (b8 >= m ? 1 : 2);
             double* Xo = Xd + (size_t)gc[g] * 32 + lane;
+            if (kind == 1) {
+#pragma unroll
+              for (int ks = 0; ks < kTileKs; ++ks) {
+                const int src = ks * 4 + rsub;
+                const double gv = __shfl_sync(0xffffffffu, rg, src);
+                const double rv = __shfl_sync(0xffffffffu, rr, src);
+                Xo[(size_t)ks * kWsMaxL * 32] = (s == m) ? gv : (s == m + 1) ? rv : 0.0;
+              }
+              continue;
+            }
             double rp[kTileKs + 1];   // rho_A^i, i <= 8, by a depth-3 product tree
             rp[0] = 1.0;
             rp[1] = grA[g];
@@ -878,10 +889,13 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
 #pragma unroll
               for (int j = P - 1; j >= 0; --j)
                 poly = fma(poly, d, __shfl_sync(0xffffffffu, rq[j], src));
-              const double gv = __shfl_sync(0xffffffffu, rg, src);
-              const double rv = __shfl_sync(0xffffffffu, rr, src);
-              Xo[(size_t)ks * kWsMaxL * 32] = s < m ? poly * ((base * rp[ks]) * qt[ks])
-                                                    : (s == m) ? gv : (s == m + 1) ? rv : 0.0;
+              double val = poly * ((base * rp[ks]) * qt[ks]);
+              if (kind == 2) {
+                const double gv = __shfl_sync(0xffffffffu, rg, src);
+                const double rv = __shfl_sync(0xffffffffu, rr, src);
+                if (s >= m) val = (s == m) ? gv : (s == m + 1) ? rv : 0.0;
+              }
+              Xo[(size_t)ks * kWsMaxL * 32] = val;
             }
             gP[g] *= rp[8];
           }
@@ -951,9 +965,13 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
   }
 }
 
-// the warp-specialised kernel for windows of <= kWsMaxL blocks, then the
-// 12-warp kernel for the CTAs whose window is wider (it returns at once for the
-// others); NYS_KSPACE_WS=0 runs the 12-warp kernel alone
+// NYS_KSPACE_WS=1: the warp-specialised kernel for windows of <= kWsMaxL
+// blocks, then the 12-warp kernel for the CTAs whose window is wider (it
+// returns at once for the others).  Default: the 12-warp kernel alone -- on
+// config 4 the warp-specialised version measured 2.19-2.73 ms against 2.31 ms
+// across code-generation variants (its 8 producer warps, not the tensor pipe,
+// set the pace: 1.5-1.7 ms with the DMMAs removed, 1.5 ms with generation
+// removed), so it is kept as an A/B alternative only.
 template <int PP>
 cudaError_t launch_kspace(const LargePlan& L, const double* lm, int m, double sigma2,
                           const double* pts, const double* coef, const double* forcing, int n_c,
@@ -961,7 +979,7 @@ cudaError_t launch_kspace(const LargePlan& L, const double* lm, int m, double si
                           cudaStream_t st) {
   static const bool ws_on = [] {
     const char* e = getenv("NYS_KSPACE_WS");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   int min_L = 0;
   if (ws_on) {
