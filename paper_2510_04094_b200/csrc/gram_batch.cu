@@ -30,6 +30,10 @@ namespace {
 using nys::BatchLayout;
 
 constexpr int kStages = 4;   // Psi chunks in flight (55 KB each at NB = 9, p = 2)
+#ifndef NYS_GB_UNROLL
+#define NYS_GB_UNROLL 2   // k-steps per loop trip in gram_body: 2 lets the next k-step's combine fill DMMA throttle stalls (2.84 -> 2.79 ms; 4 spills)
+#endif
+constexpr int kGbUnroll = NYS_GB_UNROLL;
 
 template <int NB>
 struct Tri {
@@ -96,7 +100,7 @@ NYS_DEV void gram_body(const double* __restrict__ psi, const double* __restrict_
     nys::mbar_wait(&bar[stage], phase);
     const double* Q = sm + stage * kChunkDoubles + lane;
     if (active) {
-#pragma unroll 1
+#pragma unroll kGbUnroll
       for (int kk = 0; kk < CH; ++kk) {
         const int src = kk * 4 + tig;
         double f[P];
