@@ -649,8 +649,10 @@ NYS_DEV void ws_consume(const double* Xr, int nt, uint64_t* full_b, uint64_t* em
         }
         const double b = Xk[offb[c]];
         if (NYS_WS_PROBE != 1) {
+          // both DMMAs unpredicated (a predicated mma.sync costs WARPSYNC + NOP);
+          // a single-row column's second accumulator is never stored
           nys::dmma(acc[c][0][0], acc[c][0][1], a0, b);
-          if ((two >> c) & 1u) nys::dmma(acc[c][1][0], acc[c][1][1], a1, b);
+          nys::dmma(acc[c][1][0], acc[c][1][1], a1, b);
         } else {
           acc[c][0][0] += a0 * b;
         }
