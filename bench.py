@@ -510,19 +510,21 @@ def setup_single(args, ctx):
     pts_h, coef_h, forc_h = (blk_h[:n_p], blk_h[n_p:n_p + n_k].view(coef_d.shape),
                              blk_h[n_p + n_k:])
     x_h = torch.empty(res["x"].shape, dtype=torch.float64).pin_memory()
-    # two persistent staging sets (the pipeline's graphs stay keyed on the same
-    # buffers) filled on a copy stream: call k+1's H2D overlaps call k's solve
-    blk_d = [torch.empty_like(blk_h, device=dev) for _ in range(2)]
+    # NS persistent staging sets (the pipeline's graphs stay keyed on the same
+    # buffers) filled on a copy stream: later calls' H2D overlap earlier calls'
+    # solves (the pipeline keeps several independent solves in flight)
+    NS = 2
+    blk_d = [torch.empty_like(blk_h, device=dev) for _ in range(NS)]
     stages = [(d[:n_p], d[n_p:n_p + n_k].view(coef_d.shape), d[n_p + n_k:]) for d in blk_d]
     copy_stream = torch.cuda.Stream(device=dev)
-    free_ev = [None, None]
+    free_ev = [None] * NS
     calls = [0]
 
     def step():
         solve(pts_d, coef_d, forc_d)
 
     def e2e():
-        k = calls[0] % 2
+        k = calls[0] % NS
         calls[0] += 1
         stage = stages[k]
         cur = torch.cuda.current_stream(dev)

@@ -57,6 +57,13 @@ const char* nys_last_cuda_error(void);
 /* number of kernels this library has launched in the process (evidence for
  * benchmark launch counts) */
 unsigned long long nys_launch_count(void);
+/* Pipeline plumbing (no reference equivalent): replay CUDA graph A on `stream`,
+ * wait for `in_event` (or, if NULL, for the work already on `caller`, recorded
+ * into `caller_event`), replay graph B, record `done` and make `caller` wait on
+ * it.  Graph arguments are cudaGraphExec_t handles, the others cudaStream_t /
+ * cudaEvent_t. */
+int nys_replay_pair(void* stream, void* exec_a, void* in_event, void* exec_b, void* done,
+                    void* caller, void* caller_event);
 
 /* ------------------------------------------------------------------------
  * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map

@@ -54,3 +54,28 @@ extern "C" const char* nys_status_string(int status) {
 extern "C" const char* nys_last_cuda_error(void) { return g_last_err; }
 
 extern "C" unsigned long long nys_launch_count(void) { return g_launches.load(); }
+
+// One steady-state pipeline call in a single C call (linear.SingleSolvePipeline):
+// graph A (input-independent work) on `stream`, then -- after `in_event`, or
+// after everything already on `caller` when in_event is null (recorded into
+// caller_event) -- graph B, then `done` on `stream` and a wait on it in `caller`.
+// Saves the host the per-operation Python/stream-switch cost of the same five
+// CUDA calls.
+extern "C" int nys_replay_pair(void* stream, void* exec_a, void* in_event, void* exec_b,
+                               void* done, void* caller, void* caller_event) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec_a), st);
+  if (e == cudaSuccess) {
+    cudaEvent_t w = static_cast<cudaEvent_t>(in_event);
+    if (w == nullptr) {
+      w = static_cast<cudaEvent_t>(caller_event);
+      e = cudaEventRecord(w, static_cast<cudaStream_t>(caller));
+    }
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, w, 0);
+  }
+  if (e == cudaSuccess) e = cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec_b), st);
+  if (e == cudaSuccess) e = cudaEventRecord(static_cast<cudaEvent_t>(done), st);
+  if (e == cudaSuccess)
+    e = cudaStreamWaitEvent(static_cast<cudaStream_t>(caller), static_cast<cudaEvent_t>(done), 0);
+  return nys_host::record_cuda(e);
+}

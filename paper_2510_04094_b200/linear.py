@@ -331,6 +331,11 @@ class SingleSolvePipeline:
             return 2 if getattr(self, "_rows", None) is not None else 1
         if getattr(self, "_rows", None) is not None:
             return 4   # row shards make the Gram short: more eigensolvers in flight
+        if self.WHOLE and (m + 2 + 7) // 8 <= SMALL_NB_MAX:
+            # whole-call graphs: every set's call runs concurrently, so the set
+            # count is the number of solves in flight (8: c0's chain is ~0.2 ms,
+            # c1's ~0.4 ms, against 60-100 us of host time per call)
+            return 7
         return 3 if m <= 32 else (5 if m <= 128 else 2)
 
     def _eig_sms(self) -> int:
@@ -481,9 +486,12 @@ class SingleSolvePipeline:
                                              device=self.device)
         return a
 
-    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None, E=None, part="all"):
+    def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None, E=None, part="all",
+              gws=None, xi=None):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
         E = self.E if E is None else E
+        gws = self.gws if gws is None else gws
+        x, info = (self.x, self.info) if xi is None else xi
         if part != "kkt":
             if Ac is None:   # rows here (otherwise already computed on the eig stream)
                 Ac = self.Ac
@@ -498,11 +506,11 @@ class SingleSolvePipeline:
                 _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W),
                           fm.ldw, me, float(fm.kernel.sigma2), self.order, _lib.ptr(pts),
                           _lib.ptr(coef), _lib.ptr(forcing), n_c, 0, n_c, _lib.ptr(E),
-                          _lib.ptr(self.gws), self.gws_b, st)
+                          _lib.ptr(gws), self.gws_b, st)
         if part != "gram":
             _lib.call("nys_kkt_solve_f64", _lib.ptr(E), me, self.nk, _lib.ptr(Ac),
-                      _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(self.x),
-                      _lib.ptr(self.info), None, None, _lib.ptr(self.kws), self.kws_b, st)
+                      _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(x),
+                      _lib.ptr(info), None, None, _lib.ptr(self.kws), self.kws_b, st)
 
     def _e_for(self, par, me):
         es = self.__dict__.setdefault("_E_sets", {})
@@ -525,6 +533,70 @@ class SingleSolvePipeline:
                 self._post(fm, pts, coef, forcing, False, Ac, None, E, part)
             out += [g, self.lib.nys_launch_count() - n0]
         return tuple(out)
+
+    # configs 0/1 steady state: each buffer set's WHOLE call (eigendecomposition,
+    # condition rows, fused Gram, KKT) is one CUDA graph replayed on the set's own
+    # stream with the set's own workspace and outputs, so consecutive calls
+    # (independent solves) run concurrently on different SMs and the host pays one
+    # replay per call; NYS_WHOLE_GRAPH=0 keeps the per-stage replays
+    WHOLE = os.environ.get("NYS_WHOLE_GRAPH", "1") != "0"
+
+    def _capture_whole(self, q, fm, pts, coef, forcing):
+        torch, lib = self.torch, self.lib
+        me = fm.m_eff
+        gw = self.__dict__.setdefault("_gws_sets", {})
+        if q not in gw:
+            gw[q] = torch.empty(self.gws_b, dtype=torch.uint8, device=self.device)
+        xs = self.__dict__.setdefault("_X_sets", {})
+        if q not in xs:
+            xs[q] = (torch.empty_like(self.x), torch.zeros_like(self.info))
+        Ac, E = self._ac_for(q, me), self._e_for(q, me)
+        # two graphs on the set's stream: the eigendecomposition and condition rows
+        # need no inputs (they start as soon as the set is free), the Gram and KKT
+        # wait for the inputs
+        n0 = lib.nys_launch_count()
+        ge = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(ge, capture_error_mode="thread_local"):
+            st = _lib.stream_ptr()
+            rc = lib.nys_landmark_eig_f64(*self._eig_args[q], st)
+            if rc:
+                _lib.check(rc, "nys_landmark_eig_f64")
+            for args in self._rows_args(fm, Ac):
+                _lib.call("nys_feature_matrix_f64", *args, st)
+        gp = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gp, capture_error_mode="thread_local"):
+            self._post(fm, pts, coef, forcing, False, Ac, None, E, "all", gw[q], xs[q])
+        return (ge, gp, lib.nys_launch_count() - n0, ge.raw_cuda_graph_exec(),
+                gp.raw_cuda_graph_exec())
+
+    def _run_whole(self, plan, input_event):
+        torch = self.torch
+        n = len(self._eigbufs)
+        par = self._calls % n
+        self._calls += 1
+        # the set's previous call (n calls ago) is checked now; newer ones later,
+        # so the host never waits for work still in flight
+        self._verify_pending(keep=n - 1)
+        ws = self.__dict__.setdefault("_wstreams", {})
+        sd = ws.get(par)
+        if sd is None:
+            st = torch.cuda.Stream(device=self.device)
+            evs = (torch.cuda.Event(), torch.cuda.Event())
+            for e in evs:   # create the CUDA events now (lazy in torch)
+                e.record(st)
+            sd = ws[par] = (st, evs[0], evs[1], st.cuda_stream, evs[0].cuda_event,
+                            evs[1].cuda_event)
+        ge, gp, nl = plan[par][:3]
+        rc = self.lib.nys_replay_pair(
+            sd[3], plan[par][3], None if input_event is None else input_event.cuda_event,
+            plan[par][4], sd[4], _lib.stream_ptr(), sd[5])
+        if rc:
+            _lib.check(rc, "nys_replay_pair")
+        _lib.note_graph_launches(nl)
+        self._pending.append((sd[1], self._eigbufs[par], self._me_known))
+        self.eig = self._eigbufs[par]
+        self.x, self.info = self._X_sets[par]
+        return self.x, self.info
 
     def _gram_side(self):
         side = self.__dict__.get("_gside")
@@ -611,6 +683,14 @@ class SingleSolvePipeline:
         from .nystrom import build_feature_map, launch_eig_pinned
 
         torch = self.torch
+        whole = self.__dict__.get("_whole")
+        if whole:
+            plan = whole.get((pts.data_ptr(), coef.data_ptr(), forcing.data_ptr()))
+            if plan is not None:
+                return self._run_whole(plan, input_event)
+            # new input buffers: let the whole-call graphs in flight on the sets'
+            # own streams finish before the staged path reuses the sets
+            torch.cuda.synchronize(self.device)
         fast = self.__dict__.get("_fast")
         if fast:
             plan = fast.get((pts.data_ptr(), coef.data_ptr(), forcing.data_ptr()))
@@ -758,6 +838,13 @@ class SingleSolvePipeline:
                         for b2 in self._eigbufs]
                     self._rows_bound = [self._rows_args(self._fm_cache[q], self._ac_for(q, me))
                                         for q in range(len(self._eigbufs))]
+                    if self.WHOLE and self._rows is None:
+                        # every set's previous work has finished before its
+                        # whole-call graph is first replayed on its own stream
+                        torch.cuda.synchronize(self.device)
+                        self.__dict__.setdefault("_whole", {})[key[1:4]] = [
+                            self._capture_whole(q, self._fm_cache[q], pts, coef, forcing)
+                            for q in range(len(self._eigbufs))]
         if par is not None:
             ev = self._post_ev[par]
             ev.record(cur)
