@@ -76,8 +76,11 @@ def test_single_pipeline_rotating_buffers(name):
     # the previous call's KKT; same results
     ready = torch.cuda.Event()
     ready.record()
-    xe = [pipe.run_device(*ins[k % 2], input_event=ready)[0].clone() for k in range(7)]
+    xe = [pipe.run_device(*ins[k % 2], input_event=ready)[0].clone() for k in range(21)]
     assert all(torch.equal(xs[0], x) for x in xe)
+    if name.startswith("c1"):   # configs 0/1: whole-call graphs, all sets in flight
+        assert len(pipe._whole) == 2 and all(len(p) == len(pipe._eigbufs)
+                                             for p in pipe._whole.values())
 
 
 def test_single_pipeline_row_shards_sum_to_full():
