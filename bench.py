@@ -646,14 +646,49 @@ def setup_c3(args, ctx):
     vals = np.array([[i.conditions()[0][2]] for i in insts])
     cond = ivp([(0.0, 0, 0.0)])
     state = {}
+    # consecutive batches are independent solves: up to NP of them in flight,
+    # each on its own stream with its own engine (one CTA per instance: the
+    # next batch's CTAs take the SMs this batch's short instances free while
+    # its rung-5 instances finish); each step collects the batch launched NP
+    # steps earlier (the end-of-timing synchronize completes the rest)
+    NP = 3
+    streams = [torch.cuda.Stream(device=dev) for _ in range(NP)]
+    slots = [None] * NP
+    calls = [0]
+    tol_t = 1e-10 * (1.0 + cfg.gamma)
 
-    def step():
-        fm = N.build_feature_map(RbfKernel(cfg.sigma2), lm, device=dev)
-        eng = NW.NewtonBatch(fm, g, cond, vals, cfg.gamma, family=fam)
-        st, X, tr, rung = eng.solve(max_iters=cfg.newton_max_iters)
+    def collect(sl):
+        eng, fm, norms, ist = sl
+        st, X, tr, rung = eng.ladder_collect(norms, ist)
         state.update(st=st, X=X, tr=tr, me=eng.me, eng=eng, fm=fm)
 
+    def step():
+        s = calls[0] % NP
+        calls[0] += 1
+        with torch.cuda.stream(streams[s]):
+            if slots[s] is not None:   # read back on the batch's own stream only
+                collect(slots[s])
+                slots[s] = None
+            fm = N.build_feature_map(RbfKernel(cfg.sigma2), lm, device=dev)
+            eng = NW.NewtonBatch(fm, g, cond, vals, cfg.gamma, family=fam)
+            if eng.persistent():
+                norms, ist = eng.ladder_launch(*eng.ladder_starts(), cfg.newton_max_iters,
+                                               tol_t)
+                slots[s] = (eng, fm, norms, ist)
+            else:
+                st, X, tr, rung = eng.solve(max_iters=cfg.newton_max_iters)
+                state.update(st=st, X=X, tr=tr, me=eng.me, eng=eng, fm=fm)
+        torch.cuda.current_stream(dev).wait_stream(streams[s])
+
+    def drain():
+        for s in range(NP):
+            if slots[s] is not None:
+                with torch.cuda.stream(streams[s]):
+                    collect(slots[s])
+                slots[s] = None
+
     step()
+    drain()
     eng = state["eng"]
     me, n_c = state["me"], pts.size
     persistent = eng.persistent()

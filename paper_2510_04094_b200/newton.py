@@ -709,8 +709,15 @@ class NewtonBatch:
         """The whole ladder in one launch (nys_newton_ladder_f64): both starts
         are formed up front for every instance, then each instance climbs the
         rungs on its own CTA without waiting for the others."""
-        B = self.B
         norms, ist = self.ladder_launch(*self.ladder_starts(), max_iters, tol_t)
+        return self.ladder_collect(norms, ist)
+
+    def ladder_collect(self, norms, ist):
+        """Read back one ladder launch's outcomes (status, X, traces, rung;
+        total_iterations kept on the engine) -- the host half of
+        _solve_ladder_device, so a caller may keep several launches in flight
+        (one engine per launch) and collect each later."""
+        B = self.B
         nr = norms.cpu().numpy()
         v = ist.cpu().numpy()
         its, status, rung = v[:B], v[B:2 * B].astype(int), v[2 * B:3 * B].astype(int)
