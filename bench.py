@@ -651,7 +651,7 @@ def setup_c3(args, ctx):
     # next batch's CTAs take the SMs this batch's short instances free while
     # its rung-5 instances finish); each step collects the batch launched NP
     # steps earlier (the end-of-timing synchronize completes the rest)
-    NP = 3
+    NP = int(os.environ.get("NYS_C3_INFLIGHT", "3"))
     streams = [torch.cuda.Stream(device=dev) for _ in range(NP)]
     slots = [None] * NP
     calls = [0]
