@@ -699,9 +699,16 @@ class SingleSolvePipeline:
         cur = torch.cuda.current_stream()
         graphs = os.environ.get("NYS_GRAPHS", "1") != "0"
         overlap = graphs and os.environ.get("NYS_EIG_OVERLAP", "1") != "0"
-        if self._kspace:
-            kpar = self._calls_next() if overlap else 0
-            self._kspace_launch(pts, coef, forcing, kpar, input_event)
+        kpar = self._calls_next() if overlap else 0
+        if self._kspace and input_event is None:
+            # the caller's work so far (its inputs), before this call's
+            # eigendecomposition is joined into the stream: the Gram waits only
+            # for that
+            pre = self.__dict__.get("_pre_ev")
+            if pre is None:
+                pre = self._pre_ev = torch.cuda.Event()
+            pre.record(cur)
+            input_event = pre
         par = None
         if overlap:
             # the eigendecomposition (one CTA, FP64-latency bound) runs on
@@ -758,6 +765,11 @@ class SingleSolvePipeline:
             self.eig = buf
         else:
             fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
+        if self._kspace:
+            # launched after the eigendecomposition: an 8-SM cluster eigensolver
+            # (68 < m <= 256) must find its SMs in one GPC before the Gram's CTAs
+            # spread over the rest, else it waits for the whole Gram
+            self._kspace_launch(pts, coef, forcing, kpar, input_event)
         me = fm.m_eff
         big = (me + 2 + 7) // 8 > SMALL_NB_MAX
         if self._kspace:   # inputs and K are shared with the side stream
