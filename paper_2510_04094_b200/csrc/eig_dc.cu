@@ -668,60 +668,123 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
     }
     __syncthreads();
     if (debug) { long long tn = clock64(); tm[1] += tn - tlast; tlast = tn; }
-    // M2: normalise, deflate (serial scan per block)
-    for (int b = tid; b < nmerge; b += nt) {
+    // M2: normalise, deflate (the serial dlaed2-style scan's decisions).
+    // One warp per block: the norms and the type-1 tests (|rho z_i| <= tol) are
+    // lane-parallel, the close-pair Givens test is evaluated speculatively for
+    // every pair of consecutive surviving entries with their original values, and
+    // lane 0 walks the entries in order, recomputing a pair only when its left
+    // entry was itself just rotated (the sequential dependence of dlaed2).
+    for (int b = (tid >> 5); b < nmerge; b += (nt >> 5)) {
+      const int lane = tid & 31;
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
       if (mid >= end) continue;
       double zn2 = 0.0, dmax = 0.0;
-      for (int i = 0; i < N; ++i) {
-        zn2 += S.zs[s + i] * S.zs[s + i];
+      for (int i = lane; i < N; i += 32) {
+        zn2 = fma(S.zs[s + i], S.zs[s + i], zn2);
         dmax = fmax(dmax, fabs(S.ds[s + i]));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        zn2 += __shfl_xor_sync(0xffffffffu, zn2, o);
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
       }
       const double rho = fabs(S.e[mid - 1]) * zn2;
       const double inv = zn2 > 0.0 ? 1.0 / sqrt(zn2) : 0.0;
-      for (int i = 0; i < N; ++i) S.zs[s + i] *= inv;
-      S.rho[b] = rho;
       const double tol = 8.0 * kEps * fmax(dmax, rho);
-      int K = 0, nd = 0, nrot = 0, prev = -1;
       int* keep = S.keep + s;
-      // keep[] collects kept indices from the front and deflated ones from the back
-      if (rho <= tol) {
-        for (int i = 0; i < N; ++i) keep[N - 1 - i] = i;   // all deflated
-        nd = N;
-      } else {
-        for (int i = 0; i < N; ++i) {
-          if (fabs(rho * S.zs[s + i]) <= tol) {
-            keep[N - 1 - nd++] = i;
-            continue;
+      int* srot = S.col + s;                       // scratch: speculative verdicts
+      double *sc = S.hv + s, *ssn = S.hp + s, *sr = S.zh + s;
+      // surviving (not type-1) entries as a bit mask, 8 words for N <= 256
+      unsigned surv[kDcMaxN / 32];
+#pragma unroll
+      for (int wd = 0; wd < kDcMaxN / 32; ++wd) {
+        const int i = 32 * wd + lane;
+        bool sv = false;
+        if (i < N) {
+          const double z = S.zs[s + i] * inv;
+          S.zs[s + i] = z;
+          sv = !(fabs(rho * z) <= tol);
+        }
+        surv[wd] = __ballot_sync(0xffffffffu, sv);
+      }
+      __syncwarp();
+      if (!(rho <= tol)) {
+        for (int i = lane; i < N; i += 32) {
+          srot[i] = 0;
+          if (!((surv[i >> 5] >> (i & 31)) & 1u)) continue;
+          int p = -1;   // previous surviving entry
+          for (int wd = i >> 5; wd >= 0 && p < 0; --wd) {
+            unsigned m = surv[wd];
+            if (wd == (i >> 5)) m &= (i & 31) ? (0xffffffffu >> (32 - (i & 31))) : 0u;
+            if (m) p = 32 * wd + 31 - __clz(m);
           }
-          if (prev >= 0) {
-            const double zi = S.zs[s + i], zp = S.zs[s + prev];
-            const double r = hypot(zi, zp);
-            const double c = zi / r, sn = -zp / r;
-            const double t = S.ds[s + i] - S.ds[s + prev];
-            if (fabs(t * c * sn) <= tol) {
-              const double dp = S.ds[s + prev] * c * c + S.ds[s + i] * sn * sn;
-              const double di = S.ds[s + prev] * sn * sn + S.ds[s + i] * c * c;
-              S.ds[s + prev] = dp;
-              S.ds[s + i] = di;
-              S.zs[s + i] = r;
-              S.zs[s + prev] = 0.0;
-              S.roti[s + nrot] = prev;
-              S.rotj[s + nrot] = i;
-              S.rotc[s + nrot] = c;
-              S.rots[s + nrot] = sn;
-              ++nrot;
-              // prev becomes deflated: remove it from the kept list
-              --K;
-              keep[N - 1 - nd++] = prev;
-            }
-          }
-          keep[K++] = i;
-          prev = i;
+          if (p < 0) continue;
+          const double zi = S.zs[s + i], zp = S.zs[s + p];
+          const double r = hypot(zi, zp);
+          const double c = zi / r, sn = -zp / r;
+          const double t = S.ds[s + i] - S.ds[s + p];
+          srot[i] = fabs(t * c * sn) <= tol ? 1 : 0;
+          sc[i] = c;
+          ssn[i] = sn;
+          sr[i] = r;
         }
       }
-      S.K[b] = K;
-      S.nrot[b] = nrot;
+      __syncwarp();
+      if (lane == 0) {
+        S.rho[b] = rho;
+        int K = 0, nd = 0, nrot = 0, prev = -1;
+        bool prev_mod = false;
+        if (rho <= tol) {
+          for (int i = 0; i < N; ++i) keep[N - 1 - i] = i;
+        } else {
+          for (int i = 0; i < N; ++i) {
+            if (!((surv[i >> 5] >> (i & 31)) & 1u)) {
+              keep[N - 1 - nd++] = i;
+              continue;
+            }
+            bool mod = false;
+            if (prev >= 0) {
+              double c, sn, r;
+              bool rot;
+              if (!prev_mod) {
+                rot = srot[i] != 0;
+                c = sc[i];
+                sn = ssn[i];
+                r = sr[i];
+              } else {
+                const double zi = S.zs[s + i], zp = S.zs[s + prev];
+                r = hypot(zi, zp);
+                c = zi / r;
+                sn = -zp / r;
+                const double t = S.ds[s + i] - S.ds[s + prev];
+                rot = fabs(t * c * sn) <= tol;
+              }
+              if (rot) {
+                const double dp = S.ds[s + prev] * c * c + S.ds[s + i] * sn * sn;
+                const double di = S.ds[s + prev] * sn * sn + S.ds[s + i] * c * c;
+                S.ds[s + prev] = dp;
+                S.ds[s + i] = di;
+                S.zs[s + i] = r;
+                S.zs[s + prev] = 0.0;
+                S.roti[s + nrot] = prev;
+                S.rotj[s + nrot] = i;
+                S.rotc[s + nrot] = c;
+                S.rots[s + nrot] = sn;
+                ++nrot;
+                --K;
+                keep[N - 1 - nd++] = prev;
+                mod = true;
+              }
+            }
+            keep[K++] = i;
+            prev = i;
+            prev_mod = mod;
+          }
+        }
+        S.K[b] = K;
+        S.nrot[b] = nrot;
+      }
+      __syncwarp();
     }
     __syncthreads();
     if (debug) { long long tn = clock64(); tm[2] += tn - tlast; tlast = tn; }
