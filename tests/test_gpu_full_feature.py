@@ -5,8 +5,8 @@ The m x m eigendecomposition of the full-feature map reaches the 1e-16 noise
 floor of the spectrum, so the reference itself moves when only its LAPACK
 driver changes (dsyevd -> dsyev, stored as ``yhat_dsyev``): m_eff shifts by a
 few and y_hat by up to ~6e-7.  The device must agree with the reference within
-a small multiple of that yardstick (and never worse than 1e-5), and keep the
-solution quality (error vs y*) of the reference.
+a small multiple of that yardstick and within the north star's 1e-6, and keep
+the solution quality (error vs y*) of the reference.
 """
 from types import SimpleNamespace
 
@@ -51,7 +51,9 @@ def test_full_feature_matches_reference(pid):
     yard = _rel(g[f"{key}_yhat_dsyev"], ref)
     err = _rel(y, ref)
     assert abs(model.feature_map.m_eff - int(g[f"{key}_m_eff"])) <= 8
-    assert err <= max(20 * yard, 1e-7) and err <= 1e-5, (err, yard)
+    # the north star's 1e-6, and a small multiple of the reference's own
+    # driver sensitivity (observed 1.7e-7 .. 6.0e-7 against yardsticks 6e-9 .. 6e-7)
+    assert err <= max(20 * yard, 1e-7) and err <= 1e-6, (err, yard)
     # the spectrum agrees to the rounding floor eps * s_0 of a dense m x m eigh
     ev = model.feature_map.eigenvalues
     ref_ev = g[f"{key}_eigvals"]
