@@ -678,16 +678,15 @@ __global__ void __launch_bounds__(kT <= 2 ? 256 : kDcThreads, 1)
       const int lane = tid & 31;
       const int s = S.bs[b], mid = S.bmid[b], end = S.be[b], N = end - s;
       if (mid >= end) continue;
+      // ||z||^2 in index order by one lane (the serial scan's rounding, so the
+      // one-CTA eigensolver's results are unchanged), max |d| by the warp
       double zn2 = 0.0, dmax = 0.0;
-      for (int i = lane; i < N; i += 32) {
-        zn2 = fma(S.zs[s + i], S.zs[s + i], zn2);
-        dmax = fmax(dmax, fabs(S.ds[s + i]));
-      }
+      if (lane == 0)
+        for (int i = 0; i < N; ++i) zn2 += S.zs[s + i] * S.zs[s + i];
+      zn2 = __shfl_sync(0xffffffffu, zn2, 0);
+      for (int i = lane; i < N; i += 32) dmax = fmax(dmax, fabs(S.ds[s + i]));
 #pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        zn2 += __shfl_xor_sync(0xffffffffu, zn2, o);
-        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-      }
+      for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
       const double rho = fabs(S.e[mid - 1]) * zn2;
       const double inv = zn2 > 0.0 ? 1.0 / sqrt(zn2) : 0.0;
       const double tol = 8.0 * kEps * fmax(dmax, rho);
