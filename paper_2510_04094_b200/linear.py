@@ -587,9 +587,15 @@ class SingleSolvePipeline:
             sd = ws[par] = (st, evs[0], evs[1], st.cuda_stream, evs[0].cuda_event,
                             evs[1].cuda_event)
         ge, gp, nl = plan[par][:3]
+        di = self.__dict__.get("_dev_index")
+        if di is None:
+            di = self._dev_index = torch.device(self.device).index or 0
+        # the caller's current stream by its raw handle (torch.cuda.current_stream()
+        # resolves the device on every call: ~half the host cost of a call)
+        caller = torch._C._cuda_getCurrentRawStream(di)
         rc = self.lib.nys_replay_pair(
             sd[3], plan[par][3], None if input_event is None else input_event.cuda_event,
-            plan[par][4], sd[4], _lib.stream_ptr(), sd[5])
+            plan[par][4], sd[4], caller, sd[5])
         if rc:
             _lib.check(rc, "nys_replay_pair")
         _lib.note_graph_launches(nl)
