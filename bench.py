@@ -775,9 +775,9 @@ def measure(cid, args, ctx, T, with_cpu, batch=None):
     S = setup_c2(a, ctx) if cid == 2 else (setup_c3(a, ctx) if cid == 3 else setup_single(a, ctx))
     # configs 0/1 keep up to eight independent solves in flight (a step is
     # ~20-60 us) and config 3 three batches: a handful of steps would time mostly
-    # the pipeline filling up, so they are timed over at least 200 / 30 steps
+    # the pipeline filling up, so they are timed over at least 400 / 30 steps
     # (the count is in their line)
-    steps = {0: max(args.steps, 200), 1: max(args.steps, 200),
+    steps = {0: max(args.steps, 400), 1: max(args.steps, 400),
              3: max(args.steps, 30)}.get(cid, args.steps)
     for _ in range(args.warmup):
         S["step"]()

@@ -333,9 +333,9 @@ class SingleSolvePipeline:
             return 4   # row shards make the Gram short: more eigensolvers in flight
         if self.WHOLE and (m + 2 + 7) // 8 <= SMALL_NB_MAX:
             # whole-call graphs: every set's call runs concurrently, so the set
-            # count is the number of solves in flight (8: c0's chain is ~0.2 ms,
-            # c1's ~0.4 ms, against 60-100 us of host time per call)
-            return 7
+            # count is the number of solves in flight: a call's chain (c0 ~0.2 ms,
+            # c1 ~0.4 ms) over ~22 us of host time per call
+            return int(os.environ.get("NYS_INFLIGHT", "12" if m <= 32 else "16")) - 1
         return 3 if m <= 32 else (5 if m <= 128 else 2)
 
     def _eig_sms(self) -> int:
