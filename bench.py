@@ -646,12 +646,12 @@ def setup_c3(args, ctx):
     vals = np.array([[i.conditions()[0][2]] for i in insts])
     cond = ivp([(0.0, 0, 0.0)])
     state = {}
-    # consecutive batches are independent solves: up to NP of them in flight,
+    # consecutive batches are independent solves: up to NP (4) of them in flight,
     # each on its own stream with its own engine (one CTA per instance: the
     # next batch's CTAs take the SMs this batch's short instances free while
     # its rung-5 instances finish); each step collects the batch launched NP
     # steps earlier (the end-of-timing synchronize completes the rest)
-    NP = int(os.environ.get("NYS_C3_INFLIGHT", "3"))
+    NP = int(os.environ.get("NYS_C3_INFLIGHT", "4"))
     streams = [torch.cuda.Stream(device=dev) for _ in range(NP)]
     slots = [None] * NP
     calls = [0]
@@ -687,7 +687,8 @@ def setup_c3(args, ctx):
                     collect(slots[s])
                 slots[s] = None
 
-    step()
+    for _ in range(NP):   # every slot's stream, engine and allocations used once
+        step()
     drain()
     eng = state["eng"]
     me, n_c = state["me"], pts.size
