@@ -325,10 +325,16 @@ class SingleSolvePipeline:
             return self.EIG_STREAMS
         m = self.landmarks.size
         if _cluster_eig(m):
-            # one 8-SM cluster eigensolver (1.4 ms at m = 256) per call: one in
-            # flight keeps up with a 2.4 ms call; two when row shards make the
-            # Gram short
-            return 2 if getattr(self, "_rows", None) is not None else 1
+            # one 8-SM cluster eigensolver (1.3 ms at m = 256) per call: one in
+            # flight keeps up with a 2.4 ms call; with row shards the Gram is
+            # short and more run concurrently (each takes 8 of the Gram's SMs):
+            # two for half the rows, three for a quarter, four below
+            # (tools/c4_rank_model.py)
+            rows = getattr(self, "_rows", None)
+            if rows is None:
+                return 1
+            frac = (rows[1] - rows[0]) / max(1, getattr(self, "_n_grid", rows[1]))
+            return 2 if frac > 0.3 else (3 if frac > 0.15 else 4)
         if getattr(self, "_rows", None) is not None:
             return 4   # row shards make the Gram short: more eigensolvers in flight
         if self.WHOLE and (m + 2 + 7) // 8 <= SMALL_NB_MAX:
@@ -358,6 +364,7 @@ class SingleSolvePipeline:
             raise ValueError(f"gamma must be positive, got {gamma}")
         self.kernel = RbfKernel(float(sigma2))
         self._rows, self._group = (None if rows is None else tuple(int(v) for v in rows)), group
+        self._n_grid = int(np.asarray(grid).size)
         self.landmarks = np.asarray(landmarks, dtype=float).reshape(-1)
         self.gamma, self.order, self.cond, self.drop_tol = float(gamma), int(order), cond, drop_tol
         self.eig = EigBuffers(self.landmarks, device)
@@ -487,10 +494,12 @@ class SingleSolvePipeline:
         return a
 
     def _post(self, fm, pts, coef, forcing, use_k=False, Ac=None, K=None, E=None, part="all",
-              gws=None, xi=None):
+              gws=None, xi=None, kws=None, kpws=None):
         me, m, st = fm.m_eff, fm.m, _lib.stream_ptr()
         E = self.E if E is None else E
         gws = self.gws if gws is None else gws
+        kws = self.kws if kws is None else kws
+        kpws = self.__dict__.get("kpws") if kpws is None else kpws
         x, info = (self.x, self.info) if xi is None else xi
         if part != "kkt":
             if Ac is None:   # rows here (otherwise already computed on the eig stream)
@@ -501,7 +510,7 @@ class SingleSolvePipeline:
             if use_k:
                 _lib.call("nys_kspace_project_f64", _lib.ptr(self._kcur if K is None else K), m,
                           _lib.ptr(fm.d_W), fm.ldw, me,
-                          _lib.ptr(E), _lib.ptr(self.kpws), self.kpws_b, st)
+                          _lib.ptr(E), _lib.ptr(kpws), self.kpws_b, st)
             else:
                 _lib.call("nys_fused_gram_f64", _lib.ptr(fm.d_landmarks), m, _lib.ptr(fm.d_W),
                           fm.ldw, me, float(fm.kernel.sigma2), self.order, _lib.ptr(pts),
@@ -510,7 +519,34 @@ class SingleSolvePipeline:
         if part != "gram":
             _lib.call("nys_kkt_solve_f64", _lib.ptr(E), me, self.nk, _lib.ptr(Ac),
                       _lib.ptr(self.beta), _lib.ptr(self.vals), self.gamma, 1, _lib.ptr(x),
-                      _lib.ptr(info), None, None, _lib.ptr(self.kws), self.kws_b, st)
+                      _lib.ptr(info), None, None, _lib.ptr(kws), self.kws_b, st)
+
+    # kernel-space path (config 4): each buffer set's projection + KKT (one CTA,
+    # ~0.45 ms at side 259) runs on the set's own stream with the set's own E,
+    # workspaces and outputs, so consecutive calls' KKTs overlap each other (with
+    # row shards the Gram is short and one KKT per call in series would bound the
+    # step); NYS_KSPACE_SETS=0 keeps them on the caller's stream
+    KSETS = os.environ.get("NYS_KSPACE_SETS", "1") != "0"
+
+    def _set_res(self, q, me):
+        """Per-set E, (x, info), KKT and projection workspaces (kernel-space sets)."""
+        rs = self.__dict__.setdefault("_set_res_d", {})
+        r = rs.get(q)
+        if r is None or r[0] != me:
+            torch = self.torch
+            xs = (torch.empty_like(self.x), torch.zeros_like(self.info))
+            kws = (torch.empty(self.kws_b, dtype=torch.uint8, device=self.device)
+                   if self.kws_b else None)
+            kpws = torch.empty(self.kpws_b, dtype=torch.uint8, device=self.device)
+            r = rs[q] = (me, dict(E=self._e_for(q, me), xi=xs, kws=kws, kpws=kpws))
+        return r[1]
+
+    def _set_stream(self, q):
+        ss = self.__dict__.setdefault("_set_streams", {})
+        st = ss.get(q)
+        if st is None:
+            st = ss[q] = self.torch.cuda.Stream(device=self.device)
+        return st
 
     def _e_for(self, par, me):
         es = self.__dict__.setdefault("_E_sets", {})
@@ -669,12 +705,12 @@ class SingleSolvePipeline:
         self.eig = buf
         return self.x, self.info
 
-    def _capture(self, fm, pts, coef, forcing, use_k, Ac=None, K=None):
+    def _capture(self, fm, pts, coef, forcing, use_k, Ac=None, K=None, res=None):
         torch = self.torch
         n0 = self.lib.nys_launch_count()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            self._post(fm, pts, coef, forcing, use_k, Ac, K)
+            self._post(fm, pts, coef, forcing, use_k, Ac, K, **(res or {}))
         return g, self.lib.nys_launch_count() - n0
 
     def run_device(self, pts, coef, forcing, input_event=None):
@@ -716,6 +752,8 @@ class SingleSolvePipeline:
             pre.record(cur)
             input_event = pre
         par = None
+        kset = self._kspace and overlap and self.KSETS
+        post_st = cur
         if overlap:
             # the eigendecomposition (one CTA, FP64-latency bound) runs on
             # EIG_STREAMS side streams in rotation, each call with its own buffer
@@ -737,6 +775,8 @@ class SingleSolvePipeline:
             par = self._calls % len(self._eigbufs)
             es = self._eig_streams[self._calls % len(self._eig_streams)]
             self._calls += 1
+            if kset:
+                post_st = self._set_stream(par)
             if self._eig_done[par] is not None:
                 es.wait_event(self._eig_done[par])
             self._verify_pending(keep=len(self._eig_streams))
@@ -751,6 +791,8 @@ class SingleSolvePipeline:
                 for args in self._rows_args(fm, self._ac_for(par, fm.m_eff)):
                     _lib.call("nys_feature_matrix_f64", *args, es.cuda_stream)
                 cur.wait_stream(es)
+                if post_st is not cur:
+                    post_st.wait_stream(cur)
             else:
                 # steady state: the same landmarks give the same m_eff (deterministic
                 # kernels), so the host does not wait for the eigensolver; this
@@ -767,7 +809,7 @@ class SingleSolvePipeline:
                 ev = self._eig_ev[par]
                 ev.record(es)
                 self._pending.append((ev, buf, self._me_known))
-                cur.wait_event(ev)
+                post_st.wait_event(ev)
             self.eig = buf
         else:
             fm = build_feature_map(self.kernel, self.landmarks, self.drop_tol, buffers=self.eig)
@@ -779,10 +821,13 @@ class SingleSolvePipeline:
         me = fm.m_eff
         big = (me + 2 + 7) // 8 > SMALL_NB_MAX
         if self._kspace:   # inputs and K are shared with the side stream
-            self.torch.cuda.current_stream(self.device).wait_event(self._kev)
+            post_st.wait_event(self._kev)
+            if post_st is not cur:   # the fused-Gram fallback (small m_eff) reads the inputs
+                post_st.wait_event(input_event)
             if self._rows is not None:   # partial K of this rank's rows -> full K
                 from .dist import allreduce_sum
-                allreduce_sum(self._kcur, self._group)
+                with torch.cuda.stream(post_st):
+                    allreduce_sum(self._kcur, self._group)
         cond_omega = self._cond_known if par is not None else fm.condition
         if big and cond_omega > KSPACE_MAX_COND:
             raise IllConditionedLargeMapError(
@@ -793,13 +838,29 @@ class SingleSolvePipeline:
         if not graphs:
             self._post(fm, pts, coef, forcing, use_k)
             return self.x, self.info
+        with torch.cuda.stream(post_st):
+            self._post_graphs(fm, pts, coef, forcing, me, n_c, use_k, par, kset, input_event,
+                              post_st)
+        if par is not None:
+            ev = self._post_ev[par]
+            ev.record(post_st)
+            self._eig_done[par] = ev
+            if post_st is not cur:
+                cur.wait_event(ev)
+                self.x, self.info = self._set_res(par, me)["xi"]
+        return self.x, self.info
+
+    def _post_graphs(self, fm, pts, coef, forcing, me, n_c, use_k, par, kset, input_event, cur):
+        """Replay (or run eagerly and capture) the post-eigendecomposition graphs
+        of buffer set par on the current stream (``cur``)."""
+        torch = self.torch
         key = (me, pts.data_ptr(), coef.data_ptr(), forcing.data_ptr(), n_c, use_k,
                fm.d_W.data_ptr())
         if self._graph is None:
             self._graph = {}
         # split Gram / KKT graphs (call k+1's Gram overlaps call k's KKT) pay off
         # once the KKT is long; for tiny systems the extra stream hops cost more
-        split = (not use_k) and par is not None and me >= 32
+        split = (not use_k) and par is not None and me >= 32 and not kset
         if split:
             key = key + ("split",)
         hit = self._graph.get(key)
@@ -814,14 +875,18 @@ class SingleSolvePipeline:
             Kp = (self._k_for(par) if par is not None else self._kcur) if use_k else None
             Ep = self._e_for(par, me) if split else None
             # eager: this call's result + the kernels' one-time attribute setup
-            self._post(fm, pts, coef, forcing, use_k, Ac, Kp, Ep)
+            if kset:
+                self._post(fm, pts, coef, forcing, use_k, Ac, Kp, **self._set_res(par, me))
+            else:
+                self._post(fm, pts, coef, forcing, use_k, Ac, Kp, Ep)
             if split:
                 self._graph[key] = self._split_capture(fm, pts, coef, forcing, Ac, Ep)
                 # the eager Gram ran on this stream: later side-stream Grams (shared
                 # workspace) must follow it
                 self._gram_side().wait_stream(cur)
             else:
-                self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac, Kp)
+                self._graph[key] = self._capture(fm, pts, coef, forcing, use_k, Ac, Kp,
+                                                 self._set_res(par, me) if kset else None)
             if par is not None:
                 # the other eigendecomposition buffer sets will come round with
                 # the same inputs: capture theirs now (capture does not execute),
@@ -844,7 +909,8 @@ class SingleSolvePipeline:
                     else:
                         self._graph[k2] = self._capture(f2, pts, coef, forcing, use_k,
                                                         self._ac_for(q, me),
-                                                        self._k_for(q) if use_k else None)
+                                                        self._k_for(q) if use_k else None,
+                                                        self._set_res(q, me) if kset else None)
                 if not self._kspace:   # steady state for these inputs: _run_fast
                     plan = [self._graph[key[:6] + (b2.W.data_ptr(),) + key[7:]]
                             for b2 in self._eigbufs]
@@ -863,11 +929,6 @@ class SingleSolvePipeline:
                         self.__dict__.setdefault("_whole", {})[key[1:4]] = [
                             self._capture_whole(q, self._fm_cache[q], pts, coef, forcing)
                             for q in range(len(self._eigbufs))]
-        if par is not None:
-            ev = self._post_ev[par]
-            ev.record(cur)
-            self._eig_done[par] = ev
-        return self.x, self.info
 
     def model(self):
         """PrimalModel of the last call (raises the reference's errors from info)."""

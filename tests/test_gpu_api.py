@@ -78,6 +78,8 @@ def test_single_pipeline_rotating_buffers(name):
     ready.record()
     xe = [pipe.run_device(*ins[k % 2], input_event=ready)[0].clone() for k in range(21)]
     assert all(torch.equal(xs[0], x) for x in xe)
+    if name.startswith("c4"):   # each set's projection + KKT on the set's own stream
+        assert len(pipe._set_streams) == len(pipe._eigbufs)
     if name.startswith("c1"):   # configs 0/1: whole-call graphs, all sets in flight
         assert len(pipe._whole) == 2 and all(len(p) == len(pipe._eigbufs)
                                              for p in pipe._whole.values())

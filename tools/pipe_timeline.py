@@ -1,5 +1,6 @@
 """GPU timeline of steady-state SingleSolvePipeline calls (config argv[1],
-default 1; argv[2] calls, default 6): kernels with stream, start and duration."""
+default 1; argv[2] calls, default 6): kernels with start and duration.
+WORLD=N: config 4's row-sharded pipeline over rank 0's slab of N."""
 import os
 import sys
 
@@ -15,7 +16,24 @@ ncall = int(sys.argv[2]) if len(sys.argv) > 2 else 6
 cfg = W.CONFIGS[cid]
 bt = W.linear_batch(cfg, 0, 1)
 cond = ivp(bt.instances[0].conditions())
-pipe = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond)
+world = int(os.environ.get("WORLD", "1"))
+rows = None
+if world > 1:
+    from paper_2510_04094_b200 import dist as DI
+    rows = DI.row_ranges(bt.pts.size, world)[0]
+    # the K all-reduce stood in for by a copy of the full K (tools/c4_rank_model.py)
+    _f = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond)
+    _e = torch.cuda.Event()
+    _e.record()
+    _f.run_device(torch.as_tensor(bt.pts, device="cuda"),
+                  torch.as_tensor(bt.coef[0], device="cuda"),
+                  torch.as_tensor(bt.forcing[0], device="cuda"), input_event=_e)
+    torch.cuda.synchronize()
+    _K = _f._kcur.clone()
+    del _f
+    DI.allreduce_sum = lambda t, group=None: t.copy_(_K)
+pipe = L.SingleSolvePipeline(bt.landmarks, cfg.sigma2, bt.grid, cfg.gamma, cfg.order, cond,
+                             rows=rows)
 pts = torch.as_tensor(bt.pts, device="cuda")
 coef = torch.as_tensor(bt.coef[0], device="cuda")
 forc = torch.as_tensor(bt.forcing[0], device="cuda")
