@@ -122,16 +122,21 @@ NYS_DEV void row_load(const double* __restrict__ pts, const double* __restrict__
   w.r = w.ok ? forcing[i] : 0.0;
 }
 
+// qscale (exp-recurrence tiles only): per-k-step factor Q^{j(j-1)/2} folded
+// into the row's polynomial, so the generator multiplies it once per row here
+// instead of once per (row, landmark) entry
 template <int P>
-NYS_DEV void row_store(const double (*hc)[nys::kMaxOrder + 1], const RowRaw<P>& w, double* rowc) {
+NYS_DEV void row_store(const double (*hc)[nys::kMaxOrder + 1], const RowRaw<P>& w, double* rowc,
+                       const double* qscale = nullptr) {
   double* rc = rowc + (threadIdx.x & 31) * kRowStride;
+  const double qs = qscale != nullptr ? qscale[(threadIdx.x & 31) >> 2] : 1.0;
   rc[0] = w.t;
 #pragma unroll
   for (int j = 0; j <= P; ++j) {
     double v = hc[P][j];
 #pragma unroll
     for (int k = 1; k <= P; ++k) v = fma(-w.f[k - 1], hc[P - k][j], v);
-    rc[1 + j] = w.ok ? v : 0.0;
+    rc[1 + j] = w.ok ? (qscale != nullptr ? v * qs : v) : 0.0;
   }
   rc[6] = w.ok ? -w.f[P - 1] : 0.0;
   rc[7] = w.r;
@@ -350,6 +355,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   __shared__ double qtri_s[kAnchorTiles * kTileKs];
   if (rec && threadIdx.x < kAnchorTiles * kTileKs)
     qtri_s[threadIdx.x] = exp(-H * H * inv * (double)(threadIdx.x * (threadIdx.x - 1)));
+  __syncthreads();   // qtri_s is read by the row-record warp (row_store's qscale)
+  // Q^{j(j-1)/2} factors of CTA tile kt's k-steps (rec path), else none
+  auto qscale = [&](int kt) -> const double* {
+    return rec ? qtri_s + (kt % kAnchorTiles) * kTileKs : nullptr;
+  };
   // recurrence state of this warp's generated blocks (rec path only): landmark,
   // anchor exponential and ratio, rho_A^{8t}, and the next anchor
   const int rsub = lane & 3, csub = lane >> 2;
@@ -383,7 +393,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
   };
   // rows j = 8u + i since the anchor: e_j = e_A rho_A^j Q^{j(j-1)/2}, with
-  // rho_A^{8u} carried and rho_A^i by a depth-3 product tree (no serial chain)
+  // rho_A^{8u} carried (in base) and base rho_A^i by a depth-3 product tree
+  // with base folded in (no serial chain); Q^{j(j-1)/2} is already in the row
+  // record's polynomial (row_store's qscale).  11 DMULs per lane and tile for
+  // the eight Gaussians (was 25 with the per-entry Q factor and base product).
   auto gen_rec = [&](int kt, const double* rc, double* Xd) {
     const int u = kt % kAnchorTiles;
     if (u == 0) {
@@ -394,24 +407,22 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         gP[g] = 1.0;
       }
     }
-    const double* qt = qtri_s + u * kTileKs;
 #pragma unroll
     for (int g = 0; g < kGenMax; ++g)
       if (g < ng) {
         const int s = lb_s[gc[g]] * 8 + csub;
         double* Xo = Xd + (size_t)gc[g] * 32 + lane;
         if (s < m) {
-          double rp[kTileKs + 1];
-          rp[0] = 1.0;
-          rp[1] = grA[g];
-          rp[2] = rp[1] * rp[1];
-          rp[3] = rp[2] * rp[1];
-          rp[4] = rp[2] * rp[2];
-          rp[5] = rp[4] * rp[1];
-          rp[6] = rp[4] * rp[2];
-          rp[7] = rp[4] * rp[3];
-          rp[8] = rp[4] * rp[4];
-          const double base = geA[g] * gP[g];
+          const double r1 = grA[g], r2 = r1 * r1, r4 = r2 * r2;
+          double bp[kTileKs];   // base rho_A^ks
+          bp[0] = geA[g] * gP[g];
+          bp[1] = bp[0] * r1;
+          bp[2] = bp[0] * r2;
+          bp[4] = bp[0] * r4;
+          bp[3] = bp[1] * r2;
+          bp[5] = bp[1] * r4;
+          bp[6] = bp[2] * r4;
+          bp[7] = bp[3] * r4;
 #pragma unroll
           for (int ks = 0; ks < kTileKs; ++ks) {
             const double* r = rc + (ks * 4 + rsub) * kRowStride;
@@ -426,9 +437,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             double poly = rv[1 + P];
 #pragma unroll
             for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, rv[1 + j]);
-            Xo[(size_t)ks * NBpad * 32] = poly * ((base * rp[ks]) * qt[ks]);
+            Xo[(size_t)ks * NBpad * 32] = poly * bp[ks];
           }
-          gP[g] *= rp[8];
+          gP[g] *= r4 * r4;
         } else {
 #pragma unroll
           for (int ks = 0; ks < kTileKs; ++ks) {
@@ -483,10 +494,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (tile0 < tile1) {
       if (warp == cw) {
         row_load<P>(pts, coef, forcing, n_c, row_begin + tile0 * 32, row_end, raw);
-        row_store<P>(hc_s, raw, rowc);
+        row_store<P>(hc_s, raw, rowc, qscale(0));
         if (tile0 + 1 < tile1) {
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 1) * 32, row_end, raw);
-          row_store<P>(hc_s, raw, rowc + 32 * kRowStride);
+          row_store<P>(hc_s, raw, rowc + 32 * kRowStride, qscale(1));
         }
         if (tile0 + 2 < tile1)
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile0 + 2) * 32, row_end, raw);
@@ -552,7 +563,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         gen(k + 1, rcn, Xn);
       NYS_T(3);
       if (warp == cw && tile + 2 < tile1) {
-        row_store<P>(hc_s, raw, rowc + ((k + 2) % 3) * 32 * kRowStride);
+        row_store<P>(hc_s, raw, rowc + ((k + 2) % 3) * 32 * kRowStride, qscale(k + 2));
         if (tile + 3 < tile1)
           row_load<P>(pts, coef, forcing, n_c, row_begin + (tile + 3) * 32, row_end, raw);
       }
