@@ -37,6 +37,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -506,8 +507,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       gen(0, rowc, X0);
       __syncthreads();
     }
-    const bool full = valid == 0xFFFFu;
-    const bool diag = valid == 0x8CEFu;   // bits i * 4 + j, i <= j
+    // block pattern of the super-tile: only the last super-row / super-column of
+    // the compacted window is ragged, so an off-diagonal task is 4 x nj and a
+    // diagonal one n x n (i <= j)
+    static_assert(kRT == 4, "the pattern table below is written for 4 x 4 super-tiles");
+    const int nj = min(kRT, L - q * kRT);
+    const int pattern = p == q ? (nj == 4 ? 1 : nj == 3 ? 5 : nj == 2 ? 6 : 7)
+                               : (nj == 4 ? 0 : nj == 3 ? 2 : nj == 2 ? 3 : 4);
     const int offa = p * kRT * 32 + lane, offb = q * kRT * 32 + lane;
     for (int tile = tile0; tile < tile1; ++tile) {
       const int k = tile - tile0;
@@ -527,35 +533,43 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         gen(k + 1, rcn, Xn);
       NYS_T(1);
       if (NYS_LARGE_PROBE != 1 && task >= 0) {
+        // one k-step loop per block pattern, chosen once per pass: NI x NJ blocks,
+        // DIAG: i <= j only.  Ragged edge super-tiles get their own unpredicated
+        // loops too (a predicated mma.sync costs a WARPSYNC + NOP per DMMA in
+        // SASS: the (4 x 3)-block task ran at 50 cycles per DMMA and the 3-block
+        // diagonal one at 110, against 28 for the complete 4 x 4).
+        auto ks_loop = [&](auto ni_c, auto nj_c, auto diag_c) {
+          constexpr int NI = decltype(ni_c)::value, NJ = decltype(nj_c)::value;
+          constexpr bool DG = decltype(diag_c)::value;
 #pragma unroll 1
-        for (int ks = rep; ks < kTileKs; ks += R) {
-          const double* Xk = X + (size_t)ks * NBpad * 32;
-          double xa[kRT], xb[kRT];
+          for (int ks = rep; ks < kTileKs; ks += R) {
+            const double* Xk = X + (size_t)ks * NBpad * 32;
+            double xa[NI], xb[NJ];
 #pragma unroll
-          for (int i = 0; i < kRT; ++i) xa[i] = Xk[offa + i * 32];
+            for (int i = 0; i < NI; ++i) xa[i] = Xk[offa + i * 32];
 #pragma unroll
-          for (int j = 0; j < kRT; ++j) xb[j] = Xk[offb + j * 32];
-          if (full) {
+            for (int j = 0; j < NJ; ++j) xb[j] = Xk[offb + j * 32];
 #pragma unroll
-            for (int i = 0; i < kRT; ++i)
+            for (int i = 0; i < NI; ++i)
 #pragma unroll
-              for (int j = 0; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
-          } else if (diag) {
-            // complete diagonal super-tile: the i <= j pattern at compile time (a
-            // predicated mma.sync costs a WARPSYNC + NOP per DMMA in SASS)
-#pragma unroll
-            for (int i = 0; i < kRT; ++i)
-#pragma unroll
-              for (int j = i; j < kRT; ++j) nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < kRT; ++i)
-#pragma unroll
-              for (int j = 0; j < kRT; ++j)
-                if ((valid >> (i * kRT + j)) & 1u)
-                  nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
+              for (int j = DG ? i : 0; j < NJ; ++j)
+                nys::dmma(acc[i][j][0], acc[i][j][1], xa[i], xb[j]);
           }
+        };
+        using std::integral_constant;
+#define NYS_PAT(NI, NJ, DG) \
+  ks_loop(integral_constant<int, NI>{}, integral_constant<int, NJ>{}, integral_constant<bool, DG>{})
+        switch (pattern) {
+          case 0: NYS_PAT(4, 4, false); break;
+          case 1: NYS_PAT(4, 4, true); break;
+          case 2: NYS_PAT(4, 3, false); break;
+          case 3: NYS_PAT(4, 2, false); break;
+          case 4: NYS_PAT(4, 1, false); break;
+          case 5: NYS_PAT(3, 3, true); break;
+          case 6: NYS_PAT(2, 2, true); break;
+          default: NYS_PAT(1, 1, true); break;
         }
+#undef NYS_PAT
       }
       NYS_T(2);
       if (nbuf == 1) __syncthreads();
