@@ -438,8 +438,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             double poly = rv[1 + P];
 #pragma unroll
             for (int j = P - 1; j >= 0; --j) poly = fma(poly, d, rv[1 + j]);
-            Xo[(size_t)ks * NBpad * 32] = poly * bp[ks];
+            bp[ks] *= poly;
           }
+          // all eight entries are formed before the first store: a store into X
+          // between the row-record loads would order the eight chains one after
+          // the other (the compiler cannot tell X from the row records)
+#pragma unroll
+          for (int ks = 0; ks < kTileKs; ++ks) Xo[(size_t)ks * NBpad * 32] = bp[ks];
           gP[g] *= r4 * r4;
         } else {
 #pragma unroll
