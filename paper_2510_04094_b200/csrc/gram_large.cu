@@ -26,9 +26,12 @@
 // k-step; many (dense windows) run in several passes over the row range.
 // Per 32-row tile the fragment-native smem layout X[ks][c][lane] (c = compacted
 // live-block index, so every super-tile reads contiguous fragments) is double
-// buffered: iteration t issues the DMMAs of tile t and generates tile t+1
-// (half the warps of every SM sub-partition in the opposite order so the
-// exp arithmetic and the tensor pipe overlap); row coefficients are
+// buffered: iteration t issues the DMMAs of tile t and then generates tile t+1
+// (every warp in that order: with three warps per sub-partition issuing DMMAs
+// the FP64 pipe is saturated for the whole DMMA phase, ~2100-2400 cycles per
+// tile for 132 DMMAs per sub-partition, and the generation that follows runs
+// uncontended, ~950 cycles; a warp that generates while its two neighbours
+// stream DMMAs gets one FP64 issue per ~32 cycles and needs ~2250); row coefficients are
 // produced two tiles ahead (raw row data loaded three ahead).  Diagonal
 // super-tiles that are complete run an unpredicated i <= j DMMA pattern (a
 // predicated mma.sync costs a WARPSYNC + NOP in SASS).  Each CTA writes its live
@@ -447,11 +450,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           for (int ks = 0; ks < kTileKs; ++ks) Xo[(size_t)ks * NBpad * 32] = bp[ks];
           gP[g] *= r4 * r4;
         } else {
+          double v[kTileKs];   // loads first, then the stores (as above)
 #pragma unroll
           for (int ks = 0; ks < kTileKs; ++ks) {
             const double* r = rc + (ks * 4 + rsub) * kRowStride;
-            Xo[(size_t)ks * NBpad * 32] = (s == m) ? r[6] : (s == m + 1) ? r[7] : 0.0;
+            v[ks] = (s == m) ? r[6] : (s == m + 1) ? r[7] : 0.0;
           }
+#pragma unroll
+          for (int ks = 0; ks < kTileKs; ++ks) Xo[(size_t)ks * NBpad * 32] = v[ks];
         }
       }
     if (u == kAnchorTiles - 1) anchor(kt + 1);
@@ -525,8 +531,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const double* X = (k & 1) ? X1 : X0;
       double* const Xn = ((k + 1) & 1) ? X1 : X0;
       const double* const rcn = rowc + ((k + 1) % 3) * 32 * kRowStride;
-      // half the warps generate before their DMMAs, half after (overlap)
-      const bool gen_first = nbuf == 2 && ((warp >> 2) & 1);
+      // DMMAs first, then the next tile's blocks (see the header; the other
+      // orders are A/B builds: generation in the shadow of the neighbours' DMMAs
+      // is starved of FP64 issue slots)
+#ifndef NYS_LARGE_GENFIRST
+#define NYS_LARGE_GENFIRST 0   // A/B builds: 0 none (1.78 ms), 1 warps 4-7 (1.89), 2 all (2.01), 3 all but warps 4-7 (1.86)
+#endif
+      const bool gen_first =
+          nbuf == 2 && (NYS_LARGE_GENFIRST == 0   ? false
+                        : NYS_LARGE_GENFIRST == 1 ? (bool)((warp >> 2) & 1)
+                        : NYS_LARGE_GENFIRST == 2 ? true
+                                                  : !((warp >> 2) & 1));
 #if NYS_LARGE_PROBE == 3
       long long TT[6];
       TT[0] = clock64();
