@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(32)
 
   // ---- blocked right-looking Cholesky
   int bad = 0;
-#pragma unroll 1
+  // fully unrolled: the trailing update's block pattern (J > p) is then known at
+  // compile time -- with a runtime p every one of its 56 DMMAs was predicated,
+  // and a predicated mma.sync costs a WARPSYNC + NOP per DMMA in SASS
+#pragma unroll
   for (int p = 0; p < NBK; ++p) {
     const int nrows = (NBK - p) * 8;
     // panel rows R0 = lane, R1 = lane + 32 (local to the panel) in registers

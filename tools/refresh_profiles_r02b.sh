@@ -5,7 +5,7 @@
 # c2 batched Gram, the c3 ladder, the c4 kernel-space Gram and the cluster
 # eigensolver (raw + details CSV come back; the .ncu-rep stay on the box).
 set -u
-O=gpurun_out/${R02_OUT:-r02c}
+O=gpurun_out/${R02_OUT:-r02d}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
 timeout 900 python bench.py > $O/bench_default.json 2> $O/bench_default.err
