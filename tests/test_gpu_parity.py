@@ -197,6 +197,45 @@ def test_large_m_kspace_gram_matches_oracle(m, uniform):
     np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
 
 
+@pytest.mark.parametrize("sigma", [0.25, 0.3, 0.35, 0.4, 0.45, 0.5, 0.55, 0.6])
+def test_kspace_gram_every_window_width(sigma):
+    """Kernel-space Gram at m = 256 with the live window swept through every
+    width (sigma 0.25 .. 0.6 on landmarks 0.39 apart: ~6 .. 13 live blocks per
+    CTA), so each ragged super-tile pattern of large_kspace_kernel (4 x n and
+    n x n edge tiles, n = 1..3, each with its own unpredicated DMMA loop) is the
+    one that runs somewhere; uniform grid (exp recurrence), three row tiles per
+    CTA.  Checked against G built by the oracle's rbf_block (kernel.py:75-92)."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+
+    m, p, n = 256, 2, 148 * 32 * 3 + 5
+    sigma2 = sigma * sigma
+    rng = np.random.default_rng(int(sigma * 100))
+    lm = np.linspace(0.0, 0.39 * (m - 1), m)
+    pts = np.linspace(lm[0] - 0.1, lm[-1] + 0.1, n)
+    coef = rng.normal(size=(p, n))
+    forcing = rng.normal(size=n)
+    fm = N.build_feature_map(RbfKernel(sigma2), lm)
+    assert fm.m_eff == m and fm.condition < L.KSPACE_MAX_COND
+    E = L.gram_ext_device(fm, p, torch.as_tensor(pts, device="cuda"),
+                          torch.as_tensor(coef, device="cuda"),
+                          torch.as_tensor(forcing, device="cuda")).cpu().numpy()
+    G = O.rbf_block(sigma2, p, lm, pts).T.copy()
+    for k in range(1, p + 1):
+        G -= coef[k - 1][:, None] * O.rbf_block(sigma2, p - k, lm, pts).T
+    X = np.column_stack([G, -coef[p - 1], forcing])
+    K = X.T @ X
+    Wx = np.zeros((m + 2, m + 2))
+    Wx[:m, :m] = fm.d_W[:, :m].cpu().numpy()
+    Wx[m, m] = Wx[m + 1, m + 1] = 1.0
+    Eo = Wx.T @ K @ Wx
+    assert np.allclose(E, E.T, rtol=0, atol=0)
+    np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
+
+
 def test_solve_many_callables_match_array_batch():
     """Reference-style callables through solve_many (host sampling on the thread
     pool) give the same solutions as the array batch entry."""
