@@ -502,46 +502,24 @@ def setup_single(args, ctx):
     torch.cuda.synchronize()
     if int(res["info"][0]) != 0:
         raise SystemExit(f"config {cid}: singular KKT system")
-    # the step's host inputs in one pinned block (one H2D per call); views give
-    # the API's three arrays
-    n_p, n_k = pts_d.numel(), coef_d.numel()
-    blk_h = torch.from_numpy(np.concatenate([bt.pts, bt.coef[0].reshape(-1),
-                                             bt.forcing[0]])).pin_memory()
-    pts_h, coef_h, forc_h = (blk_h[:n_p], blk_h[n_p:n_p + n_k].view(coef_d.shape),
-                             blk_h[n_p + n_k:])
+    # the step's host inputs in one pinned block (one H2D per call), solved
+    # through the pipeline's host entry: NS device staging sets in rotation, the
+    # upload on a copy stream (later calls' H2D overlap earlier calls' solves --
+    # the pipeline keeps several independent solves in flight), x back into
+    # pinned host memory; two C calls + run_device per solve
+    # (config 4: three sets, so the next call's 134 MB upload never waits for the set that
+    # the call before last is still reading: 358 -> 395 solves/s, H2D alone gives 411;
+    # configs 0/1: four, a set is free again only when its solve has finished and
+    # a solve's latency is several calls long: c0 39.9K -> 51.1K, c1 16.6K -> 25.6K)
+    blk_h = pipe.host_block(bt.pts, bt.coef[0], bt.forcing[0])
     x_h = torch.empty(res["x"].shape, dtype=torch.float64).pin_memory()
-    # NS persistent staging sets (the pipeline's graphs stay keyed on the same
-    # buffers) filled on a copy stream: later calls' H2D overlap earlier calls'
-    # solves (the pipeline keeps several independent solves in flight)
-    # (config 4: three, so the next call's 134 MB upload never waits for the set that
-    # the call before last is still reading: 358 -> 395 solves/s, H2D alone gives 411)
-    NS = int(os.environ.get("NYS_E2E_STAGES", "3" if cid == 4 else "2"))
-    blk_d = [torch.empty_like(blk_h, device=dev) for _ in range(NS)]
-    stages = [(d[:n_p], d[n_p:n_p + n_k].view(coef_d.shape), d[n_p + n_k:]) for d in blk_d]
-    copy_stream = torch.cuda.Stream(device=dev)
-    free_ev = [None] * NS
-    calls = [0]
+    NS = int(os.environ.get("NYS_E2E_STAGES", "3" if cid == 4 else "4"))
 
     def step():
         solve(pts_d, coef_d, forc_d)
 
     def e2e():
-        k = calls[0] % NS
-        calls[0] += 1
-        stage = stages[k]
-        cur = torch.cuda.current_stream(dev)
-        with torch.cuda.stream(copy_stream):
-            if free_ev[k] is not None:     # the solve that last read this set
-                copy_stream.wait_event(free_ev[k])
-            blk_d[k].copy_(blk_h, non_blocking=True)
-            ready = torch.cuda.Event()
-            ready.record(copy_stream)
-        cur.wait_event(ready)
-        r = solve(*stage, ready=ready)
-        done = torch.cuda.Event()
-        done.record(cur)
-        free_ev[k] = done
-        x_h.copy_(r["x"], non_blocking=True)
+        pipe.run_host(blk_h, x_h, stages=NS)
 
     fm = Ac_cache["fm"]
     me, n_c, m = fm.m_eff, bt.pts.size, cfg.m
@@ -602,7 +580,9 @@ def setup_single(args, ctx):
         r = solve(pts_d, coef_d, forc_d)
         torch.cuda.synchronize()
         res_x["x"] = r["x"].clone()
-        return int(r["info"][0]) == 0 and bool(torch.isfinite(x_h).all())
+        # the host path's solution (pinned x_h) against the device path's
+        same = bool(torch.allclose(x_h, r["x"].cpu(), rtol=1e-9, atol=0.0))
+        return int(r["info"][0]) == 0 and bool(torch.isfinite(x_h).all()) and same
 
     if kspace:
         # kernel-space reassociation with exact-underflow skipping (banded):
@@ -617,7 +597,7 @@ def setup_single(args, ctx):
     return dict(
         B=1 if cid == 4 else world, step=step, e2e=e2e, kernel=kernel, check=check,
         parity=parity,
-        h2d=(pts_h.numel() + coef_h.numel() + forc_h.numel()) * 8, d2h=x_h.numel() * 8,
+        h2d=blk_h.numel() * 8, d2h=x_h.numel() * 8,
         flops_kernel=flops_kernel, flops_def=flops_def, flops_step=fl(n_c),
         roof_extra={"surveyed_F": fl(rows[1] - rows[0])} if kspace else {},
         kernel_name="large_kspace_kernel (kernel-space Gram, cond-gated)" if kspace

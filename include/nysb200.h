@@ -65,6 +65,17 @@ unsigned long long nys_launch_count(void);
 int nys_replay_pair(void* stream, void* exec_a, void* in_event, void* exec_b, void* done,
                     void* caller, void* caller_event);
 
+/* Host staging of one SingleSolvePipeline call (the reference's callers hold
+ * NumPy arrays: linear.py:90-137 samples the spec on the host).  Upload: on
+ * stream `copy`, after `free_ev` (null: no wait), bytes from pinned host `src`
+ * to device `dst`; `ready` is recorded behind the copy and `caller` waits on it.
+ * Download: `free_ev` (null: none) is recorded on `stream`, then bytes from
+ * device `src` to pinned host `dst_host`.  Streams / events are cudaStream_t /
+ * cudaEvent_t handles; nothing synchronises the host. */
+int nys_stage_upload(void* dst, const void* src, size_t bytes, void* copy, void* free_ev,
+                     void* ready, void* caller);
+int nys_stage_download(void* dst_host, const void* src, size_t bytes, void* stream, void* free_ev);
+
 /* ------------------------------------------------------------------------
  * (i) Landmark eigendecomposition.  Replaces nystrom.build_feature_map
  * (nystrom.py:136-160) + NystromFeatureMap._scaled_vectors (nystrom.py:120-121).

@@ -28,6 +28,8 @@ SIGNATURES = {
     "nys_last_cuda_error": (C.c_char_p, []),
     "nys_launch_count": (C.c_ulonglong, []),
     "nys_replay_pair": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "nys_stage_upload": (_i, [_vp, _vp, _sz, _vp, _vp, _vp, _vp]),
+    "nys_stage_download": (_i, [_vp, _vp, _sz, _vp, _vp]),
     "nys_landmark_eig_workspace_bytes": (_sz, [_i]),
     "nys_landmark_eig_f64": (_i, [_vp, _i, _d, _d, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "nys_feature_matrix_f64": (_i, [_vp, _i, _vp, _i, _i, _d, _i, _vp, _i, _vp, _i, _vp]),

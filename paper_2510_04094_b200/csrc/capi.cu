@@ -79,3 +79,33 @@ extern "C" int nys_replay_pair(void* stream, void* exec_a, void* in_event, void*
     e = cudaStreamWaitEvent(static_cast<cudaStream_t>(caller), static_cast<cudaEvent_t>(done), 0);
   return nys_host::record_cuda(e);
 }
+
+// Host staging of one pipeline call (linear.SingleSolvePipeline.run_host), each
+// a single C call for the same reason as nys_replay_pair.  Upload: on `copy`,
+// after `free_ev` (the solve that last read this device set; may be null), the
+// pinned host block -> device, `ready` recorded behind it, and `caller` made to
+// wait on it.
+extern "C" int nys_stage_upload(void* dst, const void* src, size_t bytes, void* copy,
+                                void* free_ev, void* ready, void* caller) {
+  if (dst == nullptr || src == nullptr || ready == nullptr) return NYS_EINVAL;
+  cudaStream_t cs = static_cast<cudaStream_t>(copy);
+  cudaError_t e = cudaSuccess;
+  if (free_ev != nullptr) e = cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(free_ev), 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cs);
+  if (e == cudaSuccess) e = cudaEventRecord(static_cast<cudaEvent_t>(ready), cs);
+  if (e == cudaSuccess)
+    e = cudaStreamWaitEvent(static_cast<cudaStream_t>(caller), static_cast<cudaEvent_t>(ready), 0);
+  return nys_host::record_cuda(e);
+}
+
+// Download: `free_ev` recorded on `stream` (everything that read the staged
+// inputs is ordered before it), then the solution -> pinned host memory.
+extern "C" int nys_stage_download(void* dst_host, const void* src, size_t bytes, void* stream,
+                                  void* free_ev) {
+  if (dst_host == nullptr || src == nullptr) return NYS_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaSuccess;
+  if (free_ev != nullptr) e = cudaEventRecord(static_cast<cudaEvent_t>(free_ev), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dst_host, src, bytes, cudaMemcpyDeviceToHost, st);
+  return nys_host::record_cuda(e);
+}

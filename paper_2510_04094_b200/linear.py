@@ -930,6 +930,70 @@ class SingleSolvePipeline:
                             self._capture_whole(q, self._fm_cache[q], pts, coef, forcing)
                             for q in range(len(self._eigbufs))]
 
+    def host_block(self, pts, coef, forcing):
+        """The samples of one call as ONE pinned host block [pts | coef (p x n_c) |
+        forcing] (one H2D per call) -- what run_host takes.  The reference's
+        callers hold these as NumPy arrays (linear.py:103-116 samples the spec
+        on the host)."""
+        blk = np.concatenate([np.asarray(pts, dtype=np.float64).reshape(-1),
+                              np.asarray(coef, dtype=np.float64).reshape(-1),
+                              np.asarray(forcing, dtype=np.float64).reshape(-1)])
+        n_c = int(np.asarray(pts).size)
+        if blk.size != n_c * (2 + self.order):
+            raise ValueError(f"expected pts (n_c,), coef ({self.order}, n_c), forcing (n_c,)")
+        return self.torch.from_numpy(blk).pin_memory()
+
+    def run_host(self, block_h, x_h, stages: int = 0):
+        """One call from pinned host memory to pinned host memory: ``block_h`` (see
+        host_block) is uploaded on a copy stream into one of ``stages`` device
+        sets used in rotation (default 3 on the kernel-space path, else 4), the
+        solve runs as in run_device with the upload's event as its input event,
+        and x lands in ``x_h`` (pinned, (1, side)) behind it on the current
+        stream.  Nothing blocks the host: call k + 1's upload overlaps call k's
+        solve, and a set is refilled only after the solve that last read it.
+        Returns (x_h, info) with info the device int32[1] of this call's buffer
+        set (0 ok; read it after synchronising).  Two C calls + run_device per
+        solve."""
+        torch = self.torch
+        hs = self.__dict__.get("_hstage")
+        n = int(block_h.numel())
+        ns = int(stages) if stages else (3 if self._kspace else 4)
+        if hs is None or hs["n"] != n or len(hs["dev"]) != ns:
+            p = self.order
+            if n % (p + 2):
+                raise ValueError(f"block of {n} doubles is not (p + 2) * n_c with p = {p}")
+            n_c = n // (p + 2)
+            if hs is not None:   # in-flight calls still read the old sets
+                torch.cuda.synchronize(self.device)
+            dev = [torch.empty(n, dtype=torch.float64, device=self.device) for _ in range(ns)]
+            evs = [(torch.cuda.Event(), torch.cuda.Event()) for _ in range(ns)]
+            copy = torch.cuda.Stream(device=self.device)
+            for r, f in evs:   # torch creates the CUDA events lazily
+                r.record(copy)
+                f.record(copy)
+            hs = self._hstage = dict(
+                n=n, dev=dev, copy=copy, evs=evs, calls=0, used=[False] * ns,
+                views=[(d[:n_c], d[n_c:n_c * (p + 1)].view(p, n_c), d[n_c * (p + 1):])
+                       for d in dev],
+                raw=[(d.data_ptr(), r.cuda_event, f.cuda_event) for d, (r, f) in zip(dev, evs)],
+                di=torch.device(self.device).index or 0)
+        if not (block_h.is_pinned() and x_h.is_pinned()):
+            raise ValueError("run_host needs pinned host tensors (host_block / pin_memory())")
+        k = hs["calls"] % ns
+        hs["calls"] += 1
+        dptr, ready, free = hs["raw"][k]
+        caller = torch._C._cuda_getCurrentRawStream(hs["di"])
+        rc = self.lib.nys_stage_upload(dptr, block_h.data_ptr(), n * 8, hs["copy"].cuda_stream,
+                                       free if hs["used"][k] else None, ready, caller)
+        if rc:
+            _lib.check(rc, "nys_stage_upload")
+        hs["used"][k] = True
+        x, info = self.run_device(*hs["views"][k], input_event=hs["evs"][k][0])
+        rc = self.lib.nys_stage_download(x_h.data_ptr(), x.data_ptr(), x.numel() * 8, caller, free)
+        if rc:
+            _lib.check(rc, "nys_stage_download")
+        return x_h, info
+
     def model(self):
         """PrimalModel of the last call (raises the reference's errors from info)."""
         self._verify_pending()

@@ -85,6 +85,35 @@ def test_single_pipeline_rotating_buffers(name):
                                              for p in pipe._whole.values())
 
 
+@pytest.mark.parametrize("name", ["c0_seed0", "c1_seed0", "c4_n16384"])
+def test_single_pipeline_run_host_matches_run_device(name):
+    """run_host (pinned host block in, pinned x out, staging sets in rotation):
+    calls alternating between two different right-hand sides, issued back to back
+    without synchronising, each return the device path's solution for ITS
+    inputs -- a stale or overwritten staging set would give the other one's."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    g = load_golden(name)
+    pipe = L.SingleSolvePipeline(g["landmarks"], float(g["sigma2"]), g["grid"],
+                                 float(g["gamma"]), int(g["order"]), conditions(g, 0))
+    forc = [g["forcing"][0], 0.5 * g["forcing"][0] + 1.0]
+    want = []
+    for f in forc:
+        ins = tuple(torch.as_tensor(a, device="cuda") for a in (g["pts"], g["coef"][0], f))
+        want.append(pipe.run_device(*ins)[0].cpu().clone())
+    assert not torch.equal(want[0], want[1])
+    blocks = [pipe.host_block(g["pts"], g["coef"][0], f) for f in forc]
+    outs = [torch.empty(want[0].shape, dtype=torch.float64).pin_memory() for _ in range(14)]
+    infos = [pipe.run_host(blocks[k % 2], outs[k])[1] for k in range(14)]
+    torch.cuda.synchronize()
+    assert all(int(i[0]) == 0 for i in infos)
+    for k, x in enumerate(outs):
+        assert torch.equal(x, want[k % 2]), k
+    with pytest.raises(ValueError):
+        pipe.run_host(torch.zeros(blocks[0].numel(), dtype=torch.float64), outs[0])
+
+
 def test_single_pipeline_row_shards_sum_to_full():
     """Row-sharded SingleSolvePipeline (config 4 on N GPUs): the kernel-space
     Grams of two row slabs add up to the single-GPU one (the all-reduce is the
