@@ -32,9 +32,11 @@
 // tile for 132 DMMAs per sub-partition, and the generation that follows runs
 // uncontended, ~950 cycles; a warp that generates while its two neighbours
 // stream DMMAs gets one FP64 issue per ~32 cycles and needs ~2250); row coefficients are
-// produced two tiles ahead (raw row data loaded three ahead).  Diagonal
-// super-tiles that are complete run an unpredicated i <= j DMMA pattern (a
-// predicated mma.sync costs a WARPSYNC + NOP in SASS).  Each CTA writes its live
+// produced two tiles ahead (raw row data loaded three ahead).  Every block
+// pattern of a super-tile (4 x 4, diagonal i <= j, the ragged 4 x n / n x n edge
+// tiles) has its own unpredicated k-step loop, chosen once per pass (a
+// predicated mma.sync costs a WARPSYNC + NOP in SASS and its predicated-off
+// slots still occupy the pipe).  Each CTA writes its live
 // block pairs to a private dense slab (replicas added in fixed order) and one
 // reduce kernel sums the slabs in fixed order (deterministic).
 #include <cstdint>

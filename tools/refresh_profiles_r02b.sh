@@ -30,4 +30,5 @@ ncu --set full --clock-control none --import-source on -k regex:dcc_eig -c 1 \
 ncu -i /tmp/r02b_eig.ncu-rep --page raw --csv > $O/ncu_full_eig.raw.csv 2>/dev/null
 ncu -i /tmp/r02b_eig.ncu-rep --page details --csv > $O/ncu_full_eig.details.csv 2>/dev/null
 NYS_EIG_DEBUG=1 python tools/eig_one.py 4 > $O/eig_phases.txt 2>&1
+python tools/c4_rank_model.py > $O/c4_rank_model.jsonl 2> $O/c4_rank_model.err
 echo done
