@@ -106,6 +106,26 @@ NYS_DEV unsigned long long live_blocks(const double* blo, const double* bhi, int
   return mk;
 }
 
+// Exp-recurrence range check (coarse grids).  Between two anchors a lane forms
+// rho_A^j for j < kRecSpan rows 4h apart, rho_A = exp((2 H d_A - H^2) / sigma2):
+// with |d| up to the distance from the CTA's rows to the far edge of its live
+// window that power must stay far from overflow (an underflowed e_A times an
+// infinite rho_A^j is NaN; n = 300 rows over the config-4 landmarks, h / sigma =
+// 0.67, produced exactly that).  Such ranges take the exp()-per-entry path.
+constexpr int kRecSpan = 4 * 8;   // kAnchorTiles * kTileKs (static_assert below)
+NYS_DEV bool rec_span_ok(const double* blo, const double* bhi, int m, unsigned long long live,
+                         double tmin, double tmax, double hstep, double inv) {
+  // live blocks that hold landmarks: the lowest and the highest bound the window
+  const int nlb = (m + 7) / 8;
+  const unsigned long long lmk = nlb >= 64 ? live : live & ((1ull << nlb) - 1ull);
+  double dwin = 0.0;
+  if (lmk != 0ull)
+    dwin = fmax(fabs(bhi[63 - __clzll((long long)lmk)] - tmin),
+                fabs(tmax - blo[__ffsll((long long)lmk) - 1]));
+  const double H = 4.0 * hstep;
+  return fma(2.0 * H, dwin, H * H) * inv * (double)kRecSpan < 600.0;
+}
+
 // per-row polynomial coefficients for one 32-row tile: t, q0..qP, g = -f_p, r
 // (one warp; rows past the end get an all-zero polynomial -> G = 0).  The raw
 // row data are loaded a tile ahead (RowRaw in registers) so the global-load
@@ -214,6 +234,7 @@ NYS_DEV void gen_tile(const double* __restrict__ lm, int m, int L, const int* lb
 // entry exceeds 1e-17).  The Hermite factor P(d) uses the exact d of every row.
 // Stores are lane-contiguous (X[ks][c][lane]).
 constexpr int kAnchorTiles = 4;
+static_assert(kRecSpan == kAnchorTiles * kTileKs, "rec_span_ok covers one anchor period");
 constexpr int kGenMax = 2;      // blocks one warp generates (register state)
 
 #ifndef NYS_LARGE_PROBE
@@ -241,6 +262,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   __shared__ int nan_s;
   __shared__ double hstep_s, hstep_ta_s;
   __shared__ unsigned long long live_s;
+  __shared__ int rec_ok_s;
   __shared__ int lb_s[64];
   __shared__ double hc_s[nys::kMaxOrder + 1][nys::kMaxOrder + 1];
 
@@ -324,6 +346,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     if (lane == 0) {
       live_s = live;
       live_out[blockIdx.x] = live;
+      rec_ok_s = rec_span_ok(blo_s, bhi_s, m, live, tmin, tmax, hstep_s, inv) ? 1 : 0;
     }
   }
   __syncthreads();
@@ -356,7 +379,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int cw = nwarps - 1;   // warp that prepares row coefficients
   RowRaw<P> raw;
   const double H = 4.0 * hstep_s;   // 0: non-uniform grid -> exp() per entry
-  const bool rec = H > 0.0 && NYS_LARGE_REC && ntask <= nwarps && L <= kGenMax * nwarps;
+  const bool rec = H > 0.0 && NYS_LARGE_REC && ntask <= nwarps && L <= kGenMax * nwarps && rec_ok_s;
   // Q^{j(j-1)/2}, j < kAnchorTiles * kTileKs (rows since the anchor)
   __shared__ double qtri_s[kAnchorTiles * kTileKs];
   if (rec && threadIdx.x < kAnchorTiles * kTileKs)
@@ -823,6 +846,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 1)
     if (lane == 0) {
       live_s = live;
       live_out[blockIdx.x] = live;
+      if (!rec_span_ok(blo_s, bhi_s, m, live, tmin, tmax, hstep_s, inv)) hstep_s = 0.0;
     }
   }
   __syncthreads();

@@ -236,6 +236,48 @@ def test_kspace_gram_every_window_width(sigma):
     np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
 
 
+@pytest.mark.parametrize("case", ["n300", "n500", "sparse"])
+def test_kspace_gram_coarse_uniform_grids(case):
+    """Uniform grids that are coarse against sigma: the exp recurrence of
+    large_kspace_kernel (e_j = e_A rho_A^j Q^{j(j-1)/2}) would overflow rho_A^j
+    within one anchor period (h / sigma = 0.67 at n = 300 gave NaN), so those
+    row ranges must take the exp()-per-entry path (rec_span_ok).  "sparse": a
+    long domain with landmarks 23 sigma apart and five row tiles per CTA."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+
+    sigma2, p = 0.25, 2
+    if case == "sparse":
+        m, n = 80, 148 * 32 * 5
+        lm = np.linspace(0.0, 924.0, m)
+    else:
+        m, n = 256, int(case[1:])
+        lm = np.linspace(0.0, 0.39 * (m - 1), m)
+    rng = np.random.default_rng(n)
+    pts = np.linspace(lm[0] - 0.1, lm[-1] + 0.1, n)
+    coef = rng.normal(size=(p, n))
+    forcing = rng.normal(size=n)
+    fm = N.build_feature_map(RbfKernel(sigma2), lm)
+    assert fm.m_eff == m and fm.condition < L.KSPACE_MAX_COND
+    E = L.gram_ext_device(fm, p, torch.as_tensor(pts, device="cuda"),
+                          torch.as_tensor(coef, device="cuda"),
+                          torch.as_tensor(forcing, device="cuda")).cpu().numpy()
+    G = O.rbf_block(sigma2, p, lm, pts).T.copy()
+    for k in range(1, p + 1):
+        G -= coef[k - 1][:, None] * O.rbf_block(sigma2, p - k, lm, pts).T
+    X = np.column_stack([G, -coef[p - 1], forcing])
+    K = X.T @ X
+    Wx = np.zeros((m + 2, m + 2))
+    Wx[:m, :m] = fm.d_W[:, :m].cpu().numpy()
+    Wx[m, m] = Wx[m + 1, m + 1] = 1.0
+    Eo = Wx.T @ K @ Wx
+    assert np.isfinite(E).all()
+    np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
+
+
 def test_solve_many_callables_match_array_batch():
     """Reference-style callables through solve_many (host sampling on the thread
     pool) give the same solutions as the array batch entry."""
