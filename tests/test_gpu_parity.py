@@ -278,6 +278,56 @@ def test_kspace_gram_coarse_uniform_grids(case):
     np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max())
 
 
+def test_kspace_gram_random_shapes():
+    """Kernel-space Gram against the oracle on 40 seeded random shapes: m in
+    71..256 (equidistant or jittered landmarks), p in {1, 2}, sigma 0.2..3
+    landmark spacings, n from 97 to 60000 rows, uniform grids (exp recurrence
+    where its range check allows it: h / sigma runs from 8e-4 to 4.7) and random
+    points (exp per entry).  Shapes outside the kernel-space gate (m_eff < m or
+    cond(Omega) > 1e6) are skipped; at least 30 must remain."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+
+    rng = np.random.default_rng(12345)
+    checked = 0
+    for case in range(40):
+        m, p = int(rng.integers(71, 257)), int(rng.integers(1, 3))
+        spacing = float(rng.uniform(0.05, 3.0))
+        sigma = float(rng.uniform(0.6, 3.0)) * spacing * rng.choice([1.0, 0.3])
+        n = int(rng.choice([97, 300, 1000, 5000, 20000, 60000]))
+        uniform = bool(rng.integers(0, 2))
+        lm = np.linspace(0.0, spacing * (m - 1), m)
+        if rng.integers(0, 2):
+            lm = np.sort(lm + rng.uniform(-0.2, 0.2, m) * spacing)
+        pts = (np.linspace(lm[0] - 0.3 * spacing, lm[-1] + 0.2 * spacing, n) if uniform
+               else np.sort(rng.uniform(lm[0], lm[-1], n)))
+        coef, forcing = rng.normal(size=(p, n)), rng.normal(size=n)
+        sigma2 = sigma * sigma
+        fm = N.build_feature_map(RbfKernel(sigma2), lm)
+        if fm.m_eff != m or fm.condition >= L.KSPACE_MAX_COND:
+            continue
+        E = L.gram_ext_device(fm, p, torch.as_tensor(pts, device="cuda"),
+                              torch.as_tensor(coef, device="cuda"),
+                              torch.as_tensor(forcing, device="cuda")).cpu().numpy()
+        G = O.rbf_block(sigma2, p, lm, pts).T.copy()
+        for k in range(1, p + 1):
+            G -= coef[k - 1][:, None] * O.rbf_block(sigma2, p - k, lm, pts).T
+        X = np.column_stack([G, -coef[p - 1], forcing])
+        K = X.T @ X
+        Wx = np.zeros((m + 2, m + 2))
+        Wx[:m, :m] = fm.d_W[:, :m].cpu().numpy()
+        Wx[m, m] = Wx[m + 1, m + 1] = 1.0
+        Eo = Wx.T @ K @ Wx
+        assert np.isfinite(E).all(), (case, m, p, n, uniform)
+        np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-11 * np.abs(Eo).max(),
+                                   err_msg=f"case {case}: m={m} p={p} n={n} uniform={uniform}")
+        checked += 1
+    assert checked >= 30
+
+
 def test_solve_many_callables_match_array_batch():
     """Reference-style callables through solve_many (host sampling on the thread
     pool) give the same solutions as the array batch entry."""
