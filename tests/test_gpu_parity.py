@@ -328,6 +328,51 @@ def test_kspace_gram_random_shapes():
     assert checked >= 30
 
 
+def test_fused_gram_random_shapes():
+    """Fused feature + Gram kernel (m_eff + 2 <= 72, configs 0/1) against the
+    oracle on 48 seeded random shapes: m 2..70, order 1..3, n from 3 to 20000
+    rows (uniform or random points, some outside the landmark span),
+    cond(Omega) up to ~1e6.  E = [D g r]^T [D g r] with D from the oracle's
+    rbf_block (kernel.py:75-92, linear.py:103-114) in the device's basis W."""
+    import torch
+
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200.kernel import RbfKernel
+
+    rng = np.random.default_rng(777)
+    checked = 0
+    for case in range(48):
+        m, p = int(rng.integers(2, 71)), int(rng.integers(1, 4))
+        spacing = float(rng.uniform(0.02, 1.0))
+        sigma = float(rng.uniform(0.4, 2.5)) * spacing
+        n = int(rng.choice([3, 9, 33, 100, 999, 4097, 20000]))
+        lm = np.linspace(0.0, spacing * (m - 1), m)
+        pts = (np.sort(rng.uniform(lm[0] - spacing, lm[-1] + spacing, n)) if rng.integers(0, 2)
+               else np.linspace(lm[0], lm[-1] + spacing, n))
+        coef, forcing = rng.normal(size=(p, n)), rng.normal(size=n)
+        sigma2 = sigma * sigma
+        fm = N.build_feature_map(RbfKernel(sigma2), lm)
+        me = fm.m_eff
+        if me + 2 > 72:
+            continue
+        E = L.gram_ext_device(fm, p, torch.as_tensor(pts, device="cuda"),
+                              torch.as_tensor(coef, device="cuda"),
+                              torch.as_tensor(forcing, device="cuda")).cpu().numpy()
+        W = fm.d_W[:, :me].cpu().numpy()
+        Psi = [O.rbf_block(sigma2, ell, lm, pts).T @ W for ell in range(p + 1)]
+        D = Psi[p].copy()
+        for k in range(1, p + 1):
+            D -= coef[k - 1][:, None] * Psi[p - k]
+        X = np.column_stack([D, -coef[p - 1], forcing])
+        Eo = X.T @ X
+        assert np.isfinite(E).all(), (case, m, p, n)
+        np.testing.assert_allclose(E, Eo, rtol=0, atol=1e-10 * np.abs(Eo).max(),
+                                   err_msg=f"case {case}: m={m} m_eff={me} p={p} n={n}")
+        checked += 1
+    assert checked >= 40
+
+
 def test_solve_many_callables_match_array_batch():
     """Reference-style callables through solve_many (host sampling on the thread
     pool) give the same solutions as the array batch entry."""
