@@ -373,6 +373,45 @@ def test_fused_gram_random_shapes():
     assert checked >= 40
 
 
+def test_batch_solver_random_shapes():
+    """LinearBatchSolver (batched Gram + KKT, config 2's path) on 16 seeded random
+    shapes -- m 8..70 (every m_eff class: the DMMA-blocked KKT for multiples of
+    8, the packed Cholesky otherwise, a dropped eigenpair), n 65..4096, B 1..150,
+    sigma 0.05..0.3, gamma 1e6..1e9: y_hat of the first, middle and last instance
+    within 1e-6 of the oracle restatement (observed <= 4e-10), same m_eff, info 0."""
+    from paper_2510_04094_b200 import batch as BT
+    from paper_2510_04094_b200 import linear as L
+    from paper_2510_04094_b200 import nystrom as N
+    from paper_2510_04094_b200 import workloads as W
+    from paper_2510_04094_b200.kernel import RbfKernel
+    from paper_2510_04094_b200.problems import ivp
+
+    rng = np.random.default_rng(2024)
+    for case in range(16):
+        m = int(rng.integers(8, 71))
+        n = int(rng.choice([65, 257, 1000, 2049, 4096]))
+        B = int(rng.choice([1, 3, 8, 17, 64, 150]))
+        sigma = float(rng.choice([0.05, 0.1, 0.15, 0.2, 0.3]))
+        gamma = float(rng.choice([1e6, 1e8, 1e9]))
+        cfg = W.scaled(W.CONFIGS[2], n=n, m=m, batch=B, sigma=sigma, gamma=gamma)
+        bt = W.linear_batch(cfg, seed=case)
+        fm = N.build_feature_map(RbfKernel(cfg.sigma2), bt.landmarks)
+        cond = ivp([(t, int(o), 0.0) for t, o in zip(bt.cond_points, bt.cond_orders)])
+        solver = BT.LinearBatchSolver(fm, bt.grid, cfg.gamma, cfg.order, cond, cfg.batch)
+        x, info = solver.solve(bt.coef, bt.forcing, bt.cond_values)
+        Y = L.predict_batch(fm, x, 0, bt.grid).cpu().numpy()
+        assert (info.cpu().numpy() == 0).all(), case
+        for b in sorted({0, B // 2, B - 1}):
+            ref = O.solve_linear_instance(cfg.order, list(bt.coef[b]), bt.forcing[b],
+                                          bt.instances[b].conditions(), bt.grid, cfg.gamma,
+                                          cfg.sigma2, cfg.m)
+            assert ref["m_eff"] == fm.m_eff, (case, ref["m_eff"], fm.m_eff)
+            yref = O.predict(cfg.sigma2, ref["landmarks"], ref["W"], ref["omega"], ref["bias"],
+                             0, bt.grid)
+            err = O.rel_l2(Y[b], yref)
+            assert err <= 1e-6, f"case {case} (m={m} n={n} B={B} sigma={sigma}): {err:.2e}"
+
+
 def test_solve_many_callables_match_array_batch():
     """Reference-style callables through solve_many (host sampling on the thread
     pool) give the same solutions as the array batch entry."""
